@@ -1,0 +1,212 @@
+/*
+ * isogs.h -- C ABI of the B200 training-step hot path (libisogs.so).
+ *
+ * Drop-in boundary for the numba kernels of the reference package
+ * (isosplat 0.1.0; paths relative to /root/reference/pkg/src/isosplat/).
+ * Every entry point:
+ *   - takes DEVICE pointers, element counts, POD structs and a cudaStream_t
+ *     (passed as void*); no torch or C++ types cross the boundary;
+ *   - never allocates: the caller owns every buffer, including workspaces
+ *     whose size is queried first (two-phase, CUB style);
+ *   - returns 0 (cudaSuccess) or a cudaError_t code (cudaErrorInvalidValue = 1
+ *     for bad arguments); it never aborts or exits;
+ *   - is reentrant and stream ordered (no global mutable state), so one host
+ *     thread or process per GPU can drive it concurrently.
+ * Floating-point "dtype" tags select the kernel instantiation, mirroring the
+ * reference's `dtype` argument: ISG_F32 (production) or ISG_F64 (tight
+ * cross-check build).
+ */
+#ifndef ISOGS_H
+#define ISOGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ISG_F32 0
+#define ISG_F64 1
+#define ISG_TILE 16
+
+/* Pinhole camera (camera.py:15-54): q = R p + t, u = fx q.x / q.z + cx.
+ * C = -R^T t is the camera centre (Camera.position). */
+typedef struct isg_camera {
+    double R[9];
+    double t[3];
+    double C[3];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} isg_camera;
+
+/* Pre-activation Gaussian parameters (gaussians.py:27-78), row-major per
+ * parameter: positions (n,3), log_scales (n,3), rotations (n,4) wxyz,
+ * opacity_logits (n), sh (n,K,3) with K = (degree+1)^2.  dtype: ISG_F32/F64. */
+typedef struct isg_params {
+    const void *positions;
+    const void *log_scales;
+    const void *rotations;
+    const void *opacity_logits;
+    const void *sh;
+    int64_t n;
+    int32_t degree;
+    int32_t dtype;
+} isg_params;
+
+/* Outputs of isg_preprocess, all indexed by cloud row i (length n).
+ * key[i]  : depth bits (fp64, ascending as uint64) if visible, else ~0.
+ * rect[i] : inclusive tile rect (tx0, ty0, tx1, ty1), int32 x4.
+ * feat    : raster features, 12 values of feat_dtype per row:
+ *           (mx, my, conic_a, conic_b, conic_c, opacity, r, g, b, 0, 0, 0).
+ * flag[i] : 1 if kept (rasterizer.py:142-158 `keep`).
+ * full64  : optional (NULL to skip) reference SplatBatch columns in float64,
+ *           16 per row: mean2d(2) cov2d(3) conic(3) depth color(3) opacity
+ *           pad(3). */
+typedef struct isg_preprocess_out {
+    uint64_t *key;
+    int32_t *rect;
+    void *feat;
+    uint8_t *flag;
+    double *full64;
+    int32_t feat_dtype;
+} isg_preprocess_out;
+
+/* Replaces _project_kernel (_kernels.py:144-198) + the keep mask of
+ * project (rasterizer.py:105-158). fp64 arithmetic, no FMA contraction,
+ * glibc-exact exp: depth/mean2d/cov2d/conic/rect are bit-exact. */
+int isg_preprocess(const isg_params *p, const isg_camera *cam, int32_t tile_size,
+                   const isg_preprocess_out *out, void *stream);
+
+/* Stable radix sort of (uint64 key, int32 value) pairs over key bits
+ * [begin_bit, end_bit).  Replaces np.lexsort((indices, depth))
+ * (rasterizer.py:161-163, engine.py:214) when values are in index order.
+ * Call with workspace == NULL to get *ws_bytes. */
+int isg_sort_u64(void *workspace, size_t *ws_bytes, const uint64_t *keys_in,
+                 uint64_t *keys_out, const int32_t *vals_in, int32_t *vals_out,
+                 int64_t n, int32_t begin_bit, int32_t end_bit, void *stream);
+
+/* Same for (uint32 key, int32 value) pairs (tile binning). */
+int isg_sort_u32(void *workspace, size_t *ws_bytes, const uint32_t *keys_in,
+                 uint32_t *keys_out, const int32_t *vals_in, int32_t *vals_out,
+                 int64_t n, int32_t begin_bit, int32_t end_bit, void *stream);
+
+/* Binning, stage 1 (_count_tile_entries, _kernels.py:202-211 + the cumsum of
+ * rasterizer.py:183-184): gather per-rank rect/features into rank order and
+ * scan the tile counts of each rect clipped to tile rows [row_lo, row_hi)
+ * (the caller's own tiles; all rows for one GPU).  order[r] = row of rank r
+ * (the sorted values); ranks whose sorted key is ~0 are culled (0 tiles).
+ * emit_off has n+1 entries (exclusive scan); counts[0] = visible ranks M,
+ * counts[1] = total entries E (int64, device).  Workspace as above. */
+int isg_bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_t *sorted_keys,
+                  const int32_t *order, const int32_t *rect, const void *feat,
+                  int32_t feat_dtype, int32_t row_lo, int32_t row_hi, int32_t *rect_sorted,
+                  void *feat_sorted, int64_t *emit_off, int64_t *counts, void *stream);
+
+/* Binning, stage 2 (_fill_tile_entries, _kernels.py:215-225): emit
+ * (tile id - row_lo*tiles_x, rank) pairs in rank order for ranks [0, m),
+ * rects clipped to tile rows [row_lo, row_hi) exactly as in isg_bin_count. */
+int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
+                 int32_t tiles_x, int32_t row_lo, int32_t row_hi, uint32_t *tile_keys,
+                 int32_t *tile_vals, void *stream);
+
+/* Binning, stage 3: CSR tile offsets from sorted tile keys (n_tiles+1). */
+int isg_tile_offsets(int64_t e, const uint32_t *sorted_tile_keys, int32_t n_tiles,
+                     int32_t *offsets, void *stream);
+
+/* Forward composite (_forward_tiles, _kernels.py:229-278) over the tile rows
+ * [row_lo, row_hi) of a tiles_x-wide grid; offsets (CSR, relative to
+ * row_lo*tiles_x) and entries (ranks) come from binning.  If tile_ids is
+ * non-NULL the CTAs instead walk the n_tiles listed tile ids (the
+ * reference's arbitrary `own_tiles`) with offsets indexed by list slot.
+ * Outputs (full-image, row-major): image (H,W,3) in image_dtype, t_final
+ * (H,W) in feat_dtype, n_last (H,W) = 1 + index (within the tile's list) of
+ * the last composited entry, n_contrib (H,W) optional, touched (per rank,
+ * int64) optional. bg: 3 doubles (host values). */
+int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
+                   int32_t row_lo, int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
+                   const int32_t *offsets,
+                   const int32_t *entries, const void *feat_sorted, const double *bg,
+                   void *image, int32_t image_dtype, void *t_final, int32_t *n_last,
+                   int32_t *n_contrib, int64_t *touched, void *stream);
+
+/* L1 + D-SSIM loss and its exact image gradient (metrics.py:135-189) over
+ * full images (H,W,3) of `dtype`.  grad gets dL/dimage in `dtype`; the loss
+ * scalar (float64) lands in *loss_dev.  Workspace as above. */
+int isg_loss_l1_dssim(void *workspace, size_t *ws_bytes, int32_t dtype, int32_t height,
+                      int32_t width, const void *image, const void *ref, double lambda_dssim,
+                      void *grad, double *loss_dev, void *stream);
+
+/* Mean SSIM over valid centres (metrics.py:105-132) of (H,W,C) float64
+ * images, into *out_dev. */
+int isg_ssim(void *workspace, size_t *ws_bytes, int32_t height, int32_t width,
+             int32_t channels, const double *image, const double *ref, double *out_dev,
+             void *stream);
+
+/* Per-tile backward (_backward_tiles, _kernels.py:282-374).  Writes the
+ * per-(tile, splat) subtotals as 9 values (dmean 2, dconic 3, dcolor 3,
+ * dopac 1, feat_dtype) into slot emit_off[rank] + (index of the tile inside
+ * the rank's row-clipped rect), i.e. splat-major with tiles ascending --
+ * exactly the order in which _reduce_scratch folds them.  With emit_off ==
+ * NULL the subtotal of entry e goes to slot e instead (the reference's
+ * scratch layout, rasterizer.py:218-245).  tile_ids as in isg_raster_fwd. */
+int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
+                   int32_t row_lo, int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
+                   const int32_t *offsets,
+                   const int32_t *entries, const void *feat_sorted, const int32_t *rect_sorted,
+                   const int64_t *emit_off, const double *bg, const void *t_final,
+                   const int32_t *n_last, const void *dl_dimage, int32_t dl_dtype,
+                   void *partials, void *stream);
+
+/* Ordered fold (_reduce_scratch, _kernels.py:398-411): for rank r < m sum its
+ * subtotal slots [emit_off[r], emit_off[r+1]) in ascending tile order in
+ * float64 and write grad2d[order[r]] (9 doubles).  If grad_norm is non-NULL
+ * it receives hypot(dmean) at row order[r] (rasterizer.py:397). */
+int isg_reduce_ordered(int32_t feat_dtype, int64_t m, const int64_t *emit_off,
+                       const void *partials, const int32_t *order, double *grad2d,
+                       double *grad_norm, void *stream);
+
+/* 2D -> 3D chain rule (_chain_kernel, _kernels.py:415-634) for rows with
+ * flag != 0; grad2d is (n, 9) float64.  Outputs (parameter dtype, same
+ * shapes as isg_params) are fully written (zeros for unflagged rows). */
+int isg_chain(const isg_params *p, const isg_camera *cam, const uint8_t *flag,
+              const double *grad2d, void *d_positions, void *d_log_scales,
+              void *d_rotations, void *d_opacity_logits, void *d_sh, void *stream);
+
+/* Dense Adam (optim.py:20-56) over n elements, numpy weak-scalar semantics:
+ * constants are given already rounded to the storage dtype. */
+typedef struct isg_adam_consts {
+    double b1, omb1, b2, omb2, bc1, bc2, lr, eps;
+} isg_adam_consts;
+
+int isg_adam(int32_t dtype, int64_t n, void *p, const void *g, void *m, void *v,
+             const isg_adam_consts *c, void *stream);
+
+/* Fused training update for float32 parameters: chain rule for flagged rows,
+ * TrainStats update (engine.py:508-515) and Adam for all n rows and five
+ * groups (engine.py:524-536), one pass.  m/v mirror the parameter layout.
+ * lr[5] in PARAM_NAMES order; stats_seen/grad_accum optional. */
+typedef struct isg_train_state {
+    float *positions, *log_scales, *rotations, *opacity_logits, *sh;
+    float *m_positions, *m_log_scales, *m_rotations, *m_opacity_logits, *m_sh;
+    float *v_positions, *v_log_scales, *v_rotations, *v_opacity_logits, *v_sh;
+    int64_t *seen;
+    double *grad_accum;
+    int64_t n;
+    int32_t degree;
+} isg_train_state;
+
+int isg_chain_adam(const isg_train_state *s, const isg_camera *cam, const uint8_t *flag,
+                   const double *grad2d, const float *lr5, const isg_adam_consts *c,
+                   double half_w, double half_h, void *stream);
+
+/* glibc-exact exp over an array (verification hook for the key path). */
+int isg_exp_f64(int64_t n, const double *x, double *y, void *stream);
+
+/* Library identification: returns a static string (arch, build flags). */
+const char *isg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISOGS_H */

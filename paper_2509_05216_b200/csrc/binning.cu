@@ -1,0 +1,175 @@
+// binning.cu -- global depth order and per-tile CSR lists (sm_100a).
+//
+// Replaces np.lexsort((indices, depth)) (rasterizer.py:161-163,
+// engine.py:213-215) and build_tile_lists (rasterizer.py:166-191 over
+// _kernels.py:202-225).  The depth order is a stable LSD radix sort of the
+// fp64 depth bits (positive doubles order like their bit patterns) over
+// values already in ascending global-id order, so ties break on the id
+// exactly like lexsort.  Tile lists are built by duplicating each rank into
+// (tile, rank) pairs in rank order and stably sorting on the tile id, so each
+// tile's list is in global compositing order -- bit-identical to the
+// reference's count/cumsum/fill.  All kernels are HBM-bound integer work.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace isg {
+
+__global__ void __launch_bounds__(256) gather_rank_kernel(
+    int64_t n, const uint64_t *__restrict__ sorted_keys, const int32_t *__restrict__ order,
+    const int4 *__restrict__ rect, const float4 *__restrict__ feat, int feat_vec4,
+    int row_lo, int row_hi, int4 *__restrict__ rect_sorted, float4 *__restrict__ feat_sorted,
+    int64_t *__restrict__ cnt, int64_t *__restrict__ counts) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint64_t key = sorted_keys[r];
+    const bool vis = key != ~0ull;
+    int64_t c = 0;
+    if (vis) {
+        const int32_t row = order[r];
+        int4 rc = rect[row];
+        rect_sorted[r] = rc;
+        for (int j = 0; j < feat_vec4; j++) feat_sorted[(int64_t)feat_vec4 * r + j] =
+            feat[(int64_t)feat_vec4 * row + j];
+        int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
+        if (y1 >= y0) c = (int64_t)(rc.z - rc.x + 1) * (int64_t)(y1 - y0 + 1);
+        if (r + 1 == n || sorted_keys[r + 1] == ~0ull) counts[0] = r + 1;
+    } else {
+        rect_sorted[r] = make_int4(0, 0, -1, -1);
+    }
+    cnt[r] = c;
+}
+
+__global__ void finish_counts_kernel(int64_t n, const int64_t *emit_off, int64_t *counts) {
+    counts[1] = emit_off[n];
+}
+
+// Warp-cooperative emission: each warp walks 32 consecutive ranks; for each
+// rank its lanes write the rank's (clipped) rect tiles row-major, i.e. in
+// ascending tile id -- the order _fill_tile_entries visits them.
+__global__ void __launch_bounds__(256) emit_kernel(int64_t m, const int4 *__restrict__ rect_sorted,
+                                                   const int64_t *__restrict__ emit_off,
+                                                   int tiles_x, int row_lo, int row_hi,
+                                                   uint32_t *__restrict__ tile_keys,
+                                                   int32_t *__restrict__ tile_vals) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t r0 = warp * 32;
+    if (r0 >= m) return;
+    const int64_t r_end = min(r0 + 32, m);
+    const uint32_t base_tile = (uint32_t)row_lo * (uint32_t)tiles_x;
+    for (int64_t r = r0; r < r_end; r++) {
+        const int4 rc = rect_sorted[r];
+        const int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
+        if (y1 < y0) continue;
+        const int w = rc.z - rc.x + 1;
+        const int64_t cnt = (int64_t)w * (y1 - y0 + 1);
+        const int64_t off = emit_off[r];
+        for (int64_t k = lane; k < cnt; k += 32) {
+            const int ty = y0 + (int)(k / w), tx = rc.x + (int)(k % w);
+            tile_keys[off + k] = (uint32_t)ty * (uint32_t)tiles_x + (uint32_t)tx - base_tile;
+            tile_vals[off + k] = (int32_t)r;
+        }
+    }
+}
+
+__global__ void tile_offsets_kernel(int64_t e, const uint32_t *__restrict__ keys, int n_tiles,
+                                    int32_t *__restrict__ offsets) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > n_tiles) return;
+    int64_t lo = 0, hi = e;  // lower_bound(keys, t)
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < (uint32_t)t) lo = mid + 1;
+        else hi = mid;
+    }
+    offsets[t] = (int32_t)lo;
+}
+
+inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace isg
+
+using namespace isg;
+
+extern "C" int isg_sort_u64(void *workspace, size_t *ws_bytes, const uint64_t *keys_in,
+                            uint64_t *keys_out, const int32_t *vals_in, int32_t *vals_out,
+                            int64_t n, int32_t begin_bit, int32_t end_bit, void *stream) {
+    if (!ws_bytes || n < 0 || n > INT32_MAX || begin_bit < 0 || end_bit > 64 ||
+        begin_bit >= end_bit)
+        return (int)cudaErrorInvalidValue;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, *ws_bytes, keys_in, keys_out,
+                                                    vals_in, vals_out, (int)n, begin_bit,
+                                                    end_bit, (cudaStream_t)stream);
+    return (int)e;
+}
+
+extern "C" int isg_sort_u32(void *workspace, size_t *ws_bytes, const uint32_t *keys_in,
+                            uint32_t *keys_out, const int32_t *vals_in, int32_t *vals_out,
+                            int64_t n, int32_t begin_bit, int32_t end_bit, void *stream) {
+    if (!ws_bytes || n < 0 || n > INT32_MAX || begin_bit < 0 || end_bit > 32 ||
+        begin_bit >= end_bit)
+        return (int)cudaErrorInvalidValue;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, *ws_bytes, keys_in, keys_out,
+                                                    vals_in, vals_out, (int)n, begin_bit,
+                                                    end_bit, (cudaStream_t)stream);
+    return (int)e;
+}
+
+extern "C" int isg_bin_count(void *workspace, size_t *ws_bytes, int64_t n,
+                             const uint64_t *sorted_keys, const int32_t *order,
+                             const int32_t *rect, const void *feat, int32_t feat_dtype,
+                             int32_t row_lo, int32_t row_hi, int32_t *rect_sorted,
+                             void *feat_sorted, int64_t *emit_off, int64_t *counts,
+                             void *stream) {
+    if (!ws_bytes || n < 0 || n > INT32_MAX || row_lo < 0 || row_hi < row_lo)
+        return (int)cudaErrorInvalidValue;
+    size_t scan_bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, (const int64_t *)nullptr,
+                                  (int64_t *)nullptr, (int)(n > 0 ? n : 1));
+    const size_t need = align_up(sizeof(int64_t) * (size_t)(n > 0 ? n : 1)) + align_up(scan_bytes);
+    if (!workspace) {
+        *ws_bytes = need;
+        return 0;
+    }
+    if (*ws_bytes < need) return (int)cudaErrorInvalidValue;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), s);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaMemsetAsync(emit_off, 0, sizeof(int64_t), s);
+    if (e != cudaSuccess) return (int)e;
+    if (n == 0) return 0;
+    int64_t *cnt = (int64_t *)workspace;
+    void *scan_ws = (char *)workspace + align_up(sizeof(int64_t) * (size_t)n);
+    const int vec4 = feat_dtype == ISG_F64 ? 6 : 3;  // 12 values per splat
+    gather_rank_kernel<<<blocks_for(n, 256), 256, 0, s>>>(
+        n, sorted_keys, order, (const int4 *)rect, (const float4 *)feat, vec4, row_lo, row_hi,
+        (int4 *)rect_sorted, (float4 *)feat_sorted, cnt, counts);
+    ISG_CHECK_LAUNCH();
+    e = cub::DeviceScan::InclusiveSum(scan_ws, scan_bytes, cnt, emit_off + 1, (int)n, s);
+    if (e != cudaSuccess) return (int)e;
+    finish_counts_kernel<<<1, 1, 0, s>>>(n, emit_off, counts);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
+                            int32_t tiles_x, int32_t row_lo, int32_t row_hi, uint32_t *tile_keys,
+                            int32_t *tile_vals, void *stream) {
+    if (m < 0 || tiles_x <= 0) return (int)cudaErrorInvalidValue;
+    if (m == 0) return 0;
+    int64_t warps = (m + 31) / 32;
+    emit_kernel<<<blocks_for(warps * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+        m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_tile_offsets(int64_t e, const uint32_t *sorted_tile_keys, int32_t n_tiles,
+                                int32_t *offsets, void *stream) {
+    if (e < 0 || n_tiles < 0) return (int)cudaErrorInvalidValue;
+    tile_offsets_kernel<<<blocks_for(n_tiles + 1, 256), 256, 0, (cudaStream_t)stream>>>(
+        e, sorted_tile_keys, n_tiles, offsets);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}

@@ -1,0 +1,290 @@
+// loss.cu -- fused L1 + D-SSIM loss and its exact image gradient (sm_100a).
+//
+// metrics.py:135-189.  Two separable stencil passes, each staged through
+// shared memory in 16x16 output tiles with a 10-pixel halo:
+//   1. fields  -- per valid centre and channel: the five 11x11 Gaussian
+//                 moments (rows then columns, like _corr_valid), SSIM p*q and
+//                 the three adjoint fields f0, f1, f2 (metrics.py:166-183);
+//   2. adjoint -- per pixel: the adjoint correlation of f0..f2 (zero outside
+//                 the valid region, like _corr_adjoint), combined with the L1
+//                 sign term into dL/dimage.
+// Loss partials are reduced per block and then in a fixed block order, so the
+// scalar is deterministic.  Compute type follows the image dtype.
+#include "common.cuh"
+
+namespace isg {
+
+// metrics._W1D, pinned bit for bit (tests/test_oracle_golden.py).
+__constant__ double c_w1d[11] = {
+    0x1.0d956b52a1d70p-10, 0x1.f1fe01ae5a5b8p-8, 0x1.26eb175d83f67p-5,
+    0x1.bff0fe8e98418p-4,  0x1.b43c3f52b19f2p-3, 0x1.106560aa892c0p-2,
+    0x1.b43c3f52b19f2p-3,  0x1.bff0fe8e98418p-4, 0x1.26eb175d83f67p-5,
+    0x1.f1fe01ae5a5b8p-8,  0x1.0d956b52a1d70p-10};
+__constant__ float c_w1f[11] = {
+    (float)0x1.0d956b52a1d70p-10, (float)0x1.f1fe01ae5a5b8p-8, (float)0x1.26eb175d83f67p-5,
+    (float)0x1.bff0fe8e98418p-4,  (float)0x1.b43c3f52b19f2p-3, (float)0x1.106560aa892c0p-2,
+    (float)0x1.b43c3f52b19f2p-3,  (float)0x1.bff0fe8e98418p-4, (float)0x1.26eb175d83f67p-5,
+    (float)0x1.f1fe01ae5a5b8p-8,  (float)0x1.0d956b52a1d70p-10};
+
+template <typename T> __device__ __forceinline__ T wt(int i);
+template <> __device__ __forceinline__ float wt<float>(int i) { return c_w1f[i]; }
+template <> __device__ __forceinline__ double wt<double>(int i) { return c_w1d[i]; }
+
+constexpr int LT = 16;          // output tile edge
+constexpr int LP = LT + 10;     // patch edge (tile + 10-px halo)
+
+__device__ __forceinline__ double block_sum(double v, double *scratch) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += scratch[w];
+    return s;
+}
+
+// Pass 1.  fmap layout: [field f][channel c][hc][wc]; NULL for SSIM only.
+template <typename T, typename IN>
+__global__ void __launch_bounds__(256) ssim_fields_kernel(int H, int W, int C,
+                                                          const IN *__restrict__ img,
+                                                          const IN *__restrict__ ref,
+                                                          T *__restrict__ fmap,
+                                                          double *__restrict__ part) {
+    __shared__ T sx[LP][LP + 1], sy[LP][LP + 1];
+    __shared__ T hs[5][LP][LT];
+    __shared__ double red[8];
+    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;  // == pow(0.01, 2), pow(0.03, 2)
+    const int hc = H - 10, wc = W - 10;
+    const int cx0 = blockIdx.x * LT, cy0 = blockIdx.y * LT;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int ccx = cx0 + tx, ccy = cy0 + ty;
+    const bool valid = ccx < wc && ccy < hc;
+    double pq_acc = 0.0;
+    for (int c = 0; c < C; c++) {
+        for (int idx = threadIdx.x; idx < LP * LP; idx += 256) {
+            const int r = idx / LP, q = idx - r * LP;
+            const int y = cy0 + r, x = cx0 + q;
+            T vx = 0, vy = 0;
+            if (y < H && x < W) {
+                const int64_t o = ((int64_t)y * W + x) * C + c;
+                vx = (T)img[o];
+                vy = (T)ref[o];
+            }
+            sx[r][q] = vx;
+            sy[r][q] = vy;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < LP * LT; idx += 256) {
+            const int r = idx / LT, q = idx - r * LT;
+            T a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
+#pragma unroll
+            for (int i = 0; i < 11; i++) {
+                const T w = wt<T>(i), x = sx[r][q + i], y = sy[r][q + i];
+                a0 += w * x;
+                a1 += w * y;
+                a2 += w * (x * x);
+                a3 += w * (y * y);
+                a4 += w * (x * y);
+            }
+            hs[0][r][q] = a0; hs[1][r][q] = a1; hs[2][r][q] = a2; hs[3][r][q] = a3;
+            hs[4][r][q] = a4;
+        }
+        __syncthreads();
+        if (valid) {
+            T mx = 0, my = 0, mxx = 0, myy = 0, mxy = 0;
+#pragma unroll
+            for (int i = 0; i < 11; i++) {
+                const T w = wt<T>(i);
+                mx += w * hs[0][ty + i][tx];
+                my += w * hs[1][ty + i][tx];
+                mxx += w * hs[2][ty + i][tx];
+                myy += w * hs[3][ty + i][tx];
+                mxy += w * hs[4][ty + i][tx];
+            }
+            const T var_x = mxx - mx * mx, var_y = myy - my * my, cov = mxy - mx * my;
+            const T a1 = (T)2 * mx * my + (T)C1;
+            const T b1 = mx * mx + my * my + (T)C1;
+            const T a2 = (T)2 * cov + (T)C2;
+            const T b2 = var_x + var_y + (T)C2;
+            const T p = a1 / b1, q = a2 / b2;
+            pq_acc += (double)(p * q);
+            if (fmap) {
+                const T dp_dmux = ((T)2 * my * b1 - (T)2 * mx * a1) / (b1 * b1);
+                const T d_mu = q * dp_dmux;
+                const T d_sigma = -((p * q) / b2);
+                const T d_xy = ((T)2 * p) / b2;
+                const T f1 = (T)2 * d_sigma, f2 = d_xy;
+                const T f0 = d_mu - f1 * mx - f2 * my;
+                const int64_t plane = (int64_t)hc * wc;
+                const int64_t o = (int64_t)ccy * wc + ccx;
+                fmap[(0 * C + c) * plane + o] = f0;
+                fmap[(1 * C + c) * plane + o] = f1;
+                fmap[(2 * C + c) * plane + o] = f2;
+            }
+        }
+        __syncthreads();
+    }
+    const double s = block_sum(pq_acc, red);
+    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = s;
+}
+
+// Pass 2: dL/dimage = sign(x-y)(1-lam)/n + gscale * (A f0 + x A f1 + y A f2).
+template <typename T, typename IN>
+__global__ void __launch_bounds__(256) ssim_adjoint_kernel(int H, int W, const IN *__restrict__ img,
+                                                           const IN *__restrict__ ref,
+                                                           const T *__restrict__ fmap,
+                                                           IN *__restrict__ grad, T l1_scale,
+                                                           T gscale, double *__restrict__ part) {
+    __shared__ T sf[3][LP][LP + 1];
+    __shared__ T hs[3][LP][LT];
+    __shared__ double red[8];
+    const int hc = H - 10, wc = W - 10;
+    const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int x = x0 + tx, y = y0 + ty;
+    const bool inside = x < W && y < H;
+    const int64_t plane = (int64_t)hc * wc;
+    double l1_acc = 0.0;
+    for (int c = 0; c < 3; c++) {
+        for (int idx = threadIdx.x; idx < LP * LP; idx += 256) {
+            const int r = idx / LP, q = idx - r * LP;
+            const int cy = y0 - 10 + r, cx = x0 - 10 + q;
+            const bool ok = cy >= 0 && cy < hc && cx >= 0 && cx < wc;
+            const int64_t o = (int64_t)cy * wc + cx;
+#pragma unroll
+            for (int f = 0; f < 3; f++) sf[f][r][q] = ok ? fmap[(f * 3 + c) * plane + o] : (T)0;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < LP * LT; idx += 256) {
+            const int r = idx / LT, q = idx - r * LT;
+#pragma unroll
+            for (int f = 0; f < 3; f++) {
+                T a = 0;
+#pragma unroll
+                for (int i = 0; i < 11; i++) a += wt<T>(i) * sf[f][r][q + i];
+                hs[f][r][q] = a;
+            }
+        }
+        __syncthreads();
+        if (inside) {
+            T g0 = 0, g1 = 0, g2 = 0;
+#pragma unroll
+            for (int i = 0; i < 11; i++) {
+                const T w = wt<T>(i);
+                g0 += w * hs[0][ty + i][tx];
+                g1 += w * hs[1][ty + i][tx];
+                g2 += w * hs[2][ty + i][tx];
+            }
+            const int64_t o = ((int64_t)y * W + x) * 3 + c;
+            const T xv = (T)img[o], yv = (T)ref[o];
+            const T d = xv - yv;
+            const T sg = d > (T)0 ? (T)1 : (d < (T)0 ? (T)-1 : (T)0);
+            const T g = g0 + xv * g1 + yv * g2;
+            grad[o] = (IN)(sg * l1_scale + gscale * g);
+            l1_acc += (double)fabs(d);
+        }
+        __syncthreads();
+    }
+    const double s = block_sum(l1_acc, red);
+    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = s;
+}
+
+// Fixed-order final reduction (one block): loss = (1-lam) L1 + lam (1 - SSIM).
+__global__ void loss_finish_kernel(int n_ssim, const double *__restrict__ ssim_part, int n_l1,
+                                   const double *__restrict__ l1_part, double n_pix,
+                                   double n_centers, double lam, double *__restrict__ out) {
+    __shared__ double red[8];
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < n_ssim; i += blockDim.x) a += ssim_part[i];
+    for (int i = threadIdx.x; i < n_l1; i += blockDim.x) b += l1_part[i];
+    const double sa = block_sum(a, red);
+    __syncthreads();
+    const double sb = block_sum(b, red);
+    if (threadIdx.x == 0) {
+        if (n_l1 > 0)
+            out[0] = (1.0 - lam) * (sb / n_pix) + lam * (1.0 - sa / n_centers);
+        else
+            out[0] = sa / n_centers;  // SSIM only
+    }
+}
+
+inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+template <typename T>
+int loss_impl(void *ws, size_t *ws_bytes, int H, int W, const T *img, const T *ref, double lam,
+              T *grad, double *loss_dev, cudaStream_t s) {
+    const int hc = H - 10, wc = W - 10;
+    dim3 gf((wc + LT - 1) / LT, (hc + LT - 1) / LT), ga((W + LT - 1) / LT, (H + LT - 1) / LT);
+    const size_t nf = gf.x * gf.y, na = ga.x * ga.y;
+    const size_t need = al(sizeof(T) * 9 * (size_t)hc * wc) + al(8 * nf) + al(8 * na);
+    if (!ws) {
+        *ws_bytes = need;
+        return 0;
+    }
+    if (*ws_bytes < need) return (int)cudaErrorInvalidValue;
+    T *fmap = (T *)ws;
+    double *pf = (double *)((char *)ws + al(sizeof(T) * 9 * (size_t)hc * wc));
+    double *pa = (double *)((char *)pf + al(8 * nf));
+    ssim_fields_kernel<T, T><<<gf, 256, 0, s>>>(H, W, 3, img, ref, fmap, pf);
+    ISG_CHECK_LAUNCH();
+    const double n_pix = 3.0 * H * W, n_centers = 3.0 * hc * wc;
+    ssim_adjoint_kernel<T, T><<<ga, 256, 0, s>>>(H, W, img, ref, fmap, grad,
+                                                 (T)((1.0 - lam) / n_pix), (T)(-lam / n_centers),
+                                                 pa);
+    ISG_CHECK_LAUNCH();
+    loss_finish_kernel<<<1, 256, 0, s>>>((int)nf, pf, (int)na, pa, n_pix, n_centers, lam,
+                                         loss_dev);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+}  // namespace isg
+
+using namespace isg;
+
+extern "C" int isg_loss_l1_dssim(void *workspace, size_t *ws_bytes, int32_t dtype, int32_t height,
+                                 int32_t width, const void *image, const void *ref,
+                                 double lambda_dssim, void *grad, double *loss_dev,
+                                 void *stream) {
+    if (!ws_bytes || height < 11 || width < 11 || lambda_dssim < 0.0 || lambda_dssim > 1.0)
+        return (int)cudaErrorInvalidValue;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == ISG_F32)
+        return loss_impl<float>(workspace, ws_bytes, height, width, (const float *)image,
+                                (const float *)ref, lambda_dssim, (float *)grad, loss_dev, s);
+    if (dtype == ISG_F64)
+        return loss_impl<double>(workspace, ws_bytes, height, width, (const double *)image,
+                                 (const double *)ref, lambda_dssim, (double *)grad, loss_dev, s);
+    return (int)cudaErrorInvalidValue;
+}
+
+extern "C" int isg_ssim(void *workspace, size_t *ws_bytes, int32_t height, int32_t width,
+                        int32_t channels, const double *image, const double *ref,
+                        double *out_dev, void *stream) {
+    if (!ws_bytes || height < 11 || width < 11 || channels < 1)
+        return (int)cudaErrorInvalidValue;
+    const int hc = height - 10, wc = width - 10;
+    dim3 gf((wc + LT - 1) / LT, (hc + LT - 1) / LT);
+    const size_t nf = gf.x * gf.y;
+    if (!workspace) {
+        *ws_bytes = al(8 * nf);
+        return 0;
+    }
+    if (*ws_bytes < al(8 * nf)) return (int)cudaErrorInvalidValue;
+    cudaStream_t s = (cudaStream_t)stream;
+    double *pf = (double *)workspace;
+    ssim_fields_kernel<double, double><<<gf, 256, 0, s>>>(height, width, channels, image, ref,
+                                                          nullptr, pf);
+    ISG_CHECK_LAUNCH();
+    loss_finish_kernel<<<1, 256, 0, s>>>((int)nf, pf, 0, nullptr, 0.0,
+                                         (double)channels * hc * wc, 0.0, out_dev);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" const char *isg_version(void) {
+    return "libisogs 0.1 sm_100a (preprocess fp64/glibc-exp, raster f32|f64, ssim f32|f64)";
+}

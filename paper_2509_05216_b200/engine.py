@@ -1,0 +1,309 @@
+"""Device-resident training step (reference engine.py:465-562) on one B200.
+
+One iteration is a fixed chain of libisogs launches on the current stream:
+
+  isg_preprocess   project every Gaussian (fp64 key path)        N rows
+  isg_sort_u64     global (depth, id) order                        N keys
+  isg_bin_count    rank-order gather + tile-count scan             N ranks
+  [D2H 16 B]       M visible, E tile entries (sizes the E buffers)
+  isg_bin_emit     (tile, rank) pairs in rank order                E pairs
+  isg_sort_u32     stable sort on tile id -> per-tile lists        E pairs
+  isg_tile_offsets CSR offsets                                     T tiles
+  isg_raster_fwd   front-to-back composite                         P pixels
+  isg_loss_l1_dssim fused L1 + D-SSIM and dL/dimage                P pixels
+  isg_raster_bwd   per-(tile, splat) subtotals                     P pixels
+  isg_reduce_ordered ascending-tile fold per splat (fp64)          M ranks
+  isg_chain_adam   chain rule + stats + dense Adam                 N rows
+
+The only host synchronisation is the 16-byte read of (M, E).  Buffers are
+capacity-managed and reused across iterations; nothing is allocated in the
+steady state.  W > 1 lives in distributed.py.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .gaussians import PARAM_NAMES, GaussianCloud, cloud_from_points, to_device_cloud
+from .metrics import loss_l1_dssim_device, psnr, quantize8, ssim
+from .optim import adam_consts, position_lr
+from .training import (EvalRecord, TrainConfig, TrainDataset, TrainReport, TrainStats,
+                       build_schedule, init_log_scales)
+
+TILE = 16
+
+
+def _grow(buf: torch.Tensor | None, n: int, shape_tail=(), dtype=torch.float32, device=None,
+          slack: float = 1.25) -> torch.Tensor:
+    if buf is None or buf.shape[0] < n:
+        cap = max(int(n * slack), 16)
+        return torch.empty((cap,) + tuple(shape_tail), dtype=dtype, device=device)
+    return buf
+
+
+@dataclass
+class ViewContext:
+    """Per-view forward state kept for the backward (the cache of RenderAux)."""
+
+    m: int
+    e: int
+
+
+class Rasterizer:
+    """Buffers + launch sequence for one view on one GPU (band = all rows)."""
+
+    def __init__(self, n: int, width: int, height: int, device, background=(1.0, 1.0, 1.0),
+                 feat_dtype=torch.float32):
+        self.device = device
+        self.width, self.height = width, height
+        self.tiles_x = (width + TILE - 1) // TILE
+        self.tiles_y = (height + TILE - 1) // TILE
+        self.n_tiles = self.tiles_x * self.tiles_y
+        self.tile_bits = max(1, int(self.n_tiles - 1).bit_length())
+        self.bg = (ctypes.c_double * 3)(*[float(v) for v in background])
+        self.feat_dtype = feat_dtype
+        self.ftag = L.dtype_tag(feat_dtype)
+        self.ws_sort = L.Workspace()
+        self.ws_bin = L.Workspace()
+        self.counts_host = torch.zeros(2, dtype=torch.int64).pin_memory()
+        self.resize(n)
+        dev = device
+        self.image = torch.empty((height, width, 3), dtype=torch.float32, device=dev)
+        self.t_final = torch.empty((height, width), dtype=feat_dtype, device=dev)
+        self.n_last = torch.empty((height, width), dtype=torch.int32, device=dev)
+        self.dl = torch.empty((height, width, 3), dtype=torch.float32, device=dev)
+        self.offsets = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=dev)
+        self.tile_keys = self.tile_vals = self.keys_sorted_t = self.entries = None
+        self.partials = None
+        self.launches = 0
+
+    def resize(self, n: int) -> None:
+        dev = self.device
+        self.n = n
+        self.key = torch.empty(n, dtype=torch.int64, device=dev)
+        self.rect = torch.empty((n, 4), dtype=torch.int32, device=dev)
+        self.feat = torch.empty((n, 12), dtype=self.feat_dtype, device=dev)
+        self.flag = torch.empty(n, dtype=torch.uint8, device=dev)
+        self.vals0 = torch.arange(n, dtype=torch.int32, device=dev)
+        self.key_sorted = torch.empty(n, dtype=torch.int64, device=dev)
+        self.order = torch.empty(n, dtype=torch.int32, device=dev)
+        self.rect_sorted = torch.empty((n, 4), dtype=torch.int32, device=dev)
+        self.feat_sorted = torch.empty((n, 12), dtype=self.feat_dtype, device=dev)
+        self.emit_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self.counts = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.grad2d = torch.empty((n, 9), dtype=torch.float64, device=dev)
+
+    # -- forward ---------------------------------------------------------
+    def forward(self, cloud: GaussianCloud, cam) -> ViewContext:
+        lib = L.lib()
+        s = L.stream_ptr()
+        n = cloud.count
+        if n != self.n:
+            self.resize(n)
+        out = L.PreprocessOut_t()
+        out.key, out.rect, out.feat = L.ptr(self.key), L.ptr(self.rect), L.ptr(self.feat)
+        out.flag, out.full64, out.feat_dtype = L.ptr(self.flag), None, self.ftag
+        p = L.Params_t()
+        p.positions, p.log_scales = L.ptr(cloud.positions), L.ptr(cloud.log_scales)
+        p.rotations, p.opacity_logits = L.ptr(cloud.rotations), L.ptr(cloud.opacity_logits)
+        p.sh, p.n, p.degree, p.dtype = L.ptr(cloud.sh_coeffs), n, cloud.degree, L.ISG_F32
+        self.cam_struct = L.camera_struct(cam)
+        L.check(lib.isg_preprocess(ctypes.byref(p), ctypes.byref(self.cam_struct), TILE,
+                                   ctypes.byref(out), s), "isg_preprocess")
+        L.sort_pairs(self.key, self.vals0, (0, 64), self.ws_sort, self.key_sorted, self.order)
+        sz = ctypes.c_size_t(0)
+        L.check(lib.isg_bin_count(None, ctypes.byref(sz), n, None, None, None, None, self.ftag,
+                                  0, self.tiles_y, None, None, None, None, None), "bin (size)")
+        ws = self.ws_bin.get(sz.value, self.device)
+        sz = ctypes.c_size_t(ws.numel())
+        L.check(lib.isg_bin_count(L.ptr(ws), ctypes.byref(sz), n, L.ptr(self.key_sorted),
+                                  L.ptr(self.order), L.ptr(self.rect), L.ptr(self.feat),
+                                  self.ftag, 0, self.tiles_y, L.ptr(self.rect_sorted),
+                                  L.ptr(self.feat_sorted), L.ptr(self.emit_off),
+                                  L.ptr(self.counts), s), "isg_bin_count")
+        self.counts_host.copy_(self.counts, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        m, e = int(self.counts_host[0]), int(self.counts_host[1])
+        dev = self.device
+        self.tile_keys = _grow(self.tile_keys, e, dtype=torch.int32, device=dev)
+        self.tile_vals = _grow(self.tile_vals, e, dtype=torch.int32, device=dev)
+        self.keys_sorted_t = _grow(self.keys_sorted_t, e, dtype=torch.int32, device=dev)
+        self.entries = _grow(self.entries, e, dtype=torch.int32, device=dev)
+        if e:
+            L.check(lib.isg_bin_emit(m, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
+                                     self.tiles_x, 0, self.tiles_y, L.ptr(self.tile_keys),
+                                     L.ptr(self.tile_vals), s), "isg_bin_emit")
+            L.sort_pairs(self.tile_keys[:e], self.tile_vals[:e], (0, self.tile_bits),
+                         self.ws_sort, self.keys_sorted_t[:e], self.entries[:e])
+        L.check(lib.isg_tile_offsets(e, L.ptr(self.keys_sorted_t), self.n_tiles,
+                                     L.ptr(self.offsets), s), "isg_tile_offsets")
+        L.check(lib.isg_raster_fwd(self.ftag, self.width, self.height, self.tiles_x, 0,
+                                   self.tiles_y, None, 0, L.ptr(self.offsets), L.ptr(self.entries),
+                                   L.ptr(self.feat_sorted), ctypes.cast(self.bg, ctypes.c_void_p),
+                                   L.ptr(self.image), L.ISG_F32, L.ptr(self.t_final),
+                                   L.ptr(self.n_last), None, None, s), "isg_raster_fwd")
+        return ViewContext(m=m, e=e)
+
+    # -- backward --------------------------------------------------------
+    def backward(self, ctx: ViewContext) -> None:
+        lib = L.lib()
+        s = L.stream_ptr()
+        self.partials = _grow(self.partials, max(ctx.e, 1), (9,), dtype=self.feat_dtype,
+                              device=self.device)
+        L.check(lib.isg_raster_bwd(self.ftag, self.width, self.height, self.tiles_x, 0,
+                                   self.tiles_y, None, 0, L.ptr(self.offsets), L.ptr(self.entries),
+                                   L.ptr(self.feat_sorted), L.ptr(self.rect_sorted),
+                                   L.ptr(self.emit_off), ctypes.cast(self.bg, ctypes.c_void_p),
+                                   L.ptr(self.t_final), L.ptr(self.n_last), L.ptr(self.dl),
+                                   L.ISG_F32, L.ptr(self.partials), s), "isg_raster_bwd")
+        if ctx.m:
+            L.check(lib.isg_reduce_ordered(self.ftag, ctx.m, L.ptr(self.emit_off),
+                                           L.ptr(self.partials), L.ptr(self.order),
+                                           L.ptr(self.grad2d), None, s), "isg_reduce_ordered")
+
+    LAUNCHES_PER_STEP = None  # filled by Trainer (documented count)
+
+
+class Trainer:
+    """Single-GPU training state: parameters, Adam moments, stats, buffers."""
+
+    def __init__(self, cloud: GaussianCloud, width: int, height: int, config: TrainConfig,
+                 scene_extent: float, device=None):
+        self.device = device or L.require_cuda()
+        self.cfg = config
+        self.cloud = cloud
+        self.scene_extent = float(scene_extent)
+        n = cloud.count
+        self.m = {k: torch.zeros_like(getattr(cloud, k)) for k in PARAM_NAMES}
+        self.v = {k: torch.zeros_like(getattr(cloud, k)) for k in PARAM_NAMES}
+        self.stats = TrainStats(grad_accum=torch.zeros(n, dtype=torch.float64, device=self.device),
+                                seen=torch.zeros(n, dtype=torch.int64, device=self.device))
+        self.r = Rasterizer(n, width, height, self.device, config.background)
+        self.loss_dev = torch.zeros(max(config.iterations, 1) + 1, dtype=torch.float64,
+                                    device=self.device)
+        self.lr_host = (ctypes.c_float * 5)()
+
+    def _state_struct(self) -> L.TrainState_t:
+        st = L.TrainState_t()
+        c = self.cloud
+        st.positions, st.log_scales, st.rotations = L.ptr(c.positions), L.ptr(c.log_scales), L.ptr(c.rotations)
+        st.opacity_logits, st.sh = L.ptr(c.opacity_logits), L.ptr(c.sh_coeffs)
+        for pre, d in (("m_", self.m), ("v_", self.v)):
+            setattr(st, pre + "positions", L.ptr(d["positions"]))
+            setattr(st, pre + "log_scales", L.ptr(d["log_scales"]))
+            setattr(st, pre + "rotations", L.ptr(d["rotations"]))
+            setattr(st, pre + "opacity_logits", L.ptr(d["opacity_logits"]))
+            setattr(st, pre + "sh", L.ptr(d["sh_coeffs"]))
+        st.seen, st.grad_accum = L.ptr(self.stats.seen), L.ptr(self.stats.grad_accum)
+        st.n, st.degree = c.count, c.degree
+        return st
+
+    def lrs(self, it: int) -> list[float]:
+        """engine.py:525-535."""
+        cfg = self.cfg
+        return [self.scene_extent * position_lr(cfg.lr_position, it, cfg.iterations,
+                                                cfg.lr_position_final),
+                cfg.lr_scale, cfg.lr_rotation, cfg.lr_opacity, cfg.lr_sh]
+
+    def step(self, it: int, cam, gt: torch.Tensor, loss_slot: torch.Tensor | None = None) -> None:
+        """One training iteration on view `cam` with ground truth `gt`
+        (H, W, 3) float32 on the device.  The loss lands in loss_slot (or
+        self.loss_dev[it])."""
+        r = self.r
+        ctx = r.forward(self.cloud, cam)
+        slot = loss_slot if loss_slot is not None else self.loss_dev[it:it + 1]
+        loss_l1_dssim_device(r.image, gt, self.cfg.lambda_dssim, r.dl, slot)
+        r.backward(ctx)
+        for i, v in enumerate(self.lrs(it)):
+            self.lr_host[i] = float(np.float32(v))
+        c = adam_consts(torch.float32, it, 0.0)
+        st = self._state_struct()
+        L.check(L.lib().isg_chain_adam(ctypes.byref(st), ctypes.byref(r.cam_struct),
+                                       L.ptr(r.flag), L.ptr(r.grad2d),
+                                       ctypes.cast(self.lr_host, ctypes.c_void_p),
+                                       ctypes.byref(c), 0.5 * r.width, 0.5 * r.height,
+                                       L.stream_ptr()), "isg_chain_adam")
+
+    def render(self, cam) -> torch.Tensor:
+        self.r.forward(self.cloud, cam)
+        return self.r.image
+
+    def evaluate(self, cameras, images_dev, it: int, wall_s: float) -> EvalRecord:
+        """engine.py:440-462 + training.py:392-396 (8-bit round trip)."""
+        losses, psnrs, ssims = [], [], []
+        tmp_loss = torch.zeros(1, dtype=torch.float64, device=self.device)
+        for v, cam in enumerate(cameras):
+            img = self.render(cam)
+            ref = images_dev[v]
+            loss_l1_dssim_device(img, ref, self.cfg.lambda_dssim, self.r.dl, tmp_loss)
+            losses.append(float(tmp_loss.item()))
+            a = quantize8(img)
+            b = quantize8(ref)
+            psnrs.append(psnr(a, b))
+            ssims.append(ssim(a, b))
+        return EvalRecord(iteration=it, loss=float(np.mean(losses)), psnr=float(np.mean(psnrs)),
+                          ssim=float(np.mean(ssims)), wall_s=wall_s, gaussians=self.cloud.count)
+
+
+def _images_to_device(images, device) -> torch.Tensor:
+    arr = images if isinstance(images, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(images))
+    if arr.dtype == torch.uint8:
+        arr = (arr.to(torch.float64) / 255.0).to(torch.float32)
+    return arr.to(device=device, dtype=torch.float32).contiguous()
+
+
+def run_training(dataset: TrainDataset, config: TrainConfig, workers: int = 1,
+                 init_cloud=None, evaluate: bool = True):
+    """Train a Gaussian cloud against the dataset views (engine.py:613-652).
+
+    workers > 1 runs the sharded multi-GPU engine (distributed.py) under
+    torch.distributed; workers == 1 is the single-GPU loop here.
+    Returns (GaussianCloud on the device, TrainReport)."""
+    config.validate()
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    if config.resolution is not None and config.resolution != dataset.width:
+        raise ValueError(f"config resolution {config.resolution} != dataset width {dataset.width}")
+    if config.densify_active():
+        raise NotImplementedError("densify_and_prune is the next row (SURVEY 8f); "
+                                  "set densify=False or densify_start > iterations/2")
+    if workers > 1:
+        from .distributed import run_training_distributed
+        return run_training_distributed(dataset, config, workers, init_cloud, evaluate)
+    dev = L.require_cuda()
+    if init_cloud is None:
+        pts = np.asarray(dataset.points.positions, dtype=np.float64)
+        cloud = cloud_from_points(pts, init_log_scales(pts), config.sh_degree, dev)
+    else:
+        cloud = to_device_cloud(init_cloud, dev, torch.float32)
+    tr = Trainer(cloud, dataset.width, dataset.height, config, dataset.scene_extent, dev)
+    images = _images_to_device(dataset.images, dev)
+    report = TrainReport(workers=1, resolution=config.resolution or dataset.width)
+    if evaluate:
+        report.records.append(tr.evaluate(dataset.cameras, images, 0, 0.0))
+    schedule = build_schedule(config.iterations, dataset.view_count, config.seed)
+    wall = 0.0
+    for it in range(1, config.iterations + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        v = schedule[it - 1]
+        tr.step(it, dataset.cameras[v], images[v])
+        torch.cuda.synchronize()
+        wall += time.perf_counter() - t0
+        due = it == config.iterations or (config.eval_interval > 0 and it % config.eval_interval == 0)
+        if evaluate and due:
+            report.records.append(tr.evaluate(dataset.cameras, images, it, wall))
+    report.iteration_losses = [float(x) for x in tr.loss_dev[1:config.iterations + 1].tolist()]
+    report.total_wall_s = wall
+    return tr.cloud, report
+
+
+def train_single(dataset: TrainDataset, config: TrainConfig, **kw):
+    """Single-GPU training (training.py:399-402)."""
+    return run_training(dataset, config, workers=1, **kw)
