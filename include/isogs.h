@@ -121,21 +121,25 @@ int isg_tile_offsets(int64_t e, const uint32_t *sorted_tile_keys, int32_t n_tile
  * reference's arbitrary `own_tiles`) with offsets indexed by list slot.
  * Outputs (full-image, row-major): image (H,W,3) in image_dtype, t_final
  * (H,W) in feat_dtype, n_last (H,W) = 1 + index (within the tile's list) of
- * the last composited entry, n_contrib (H,W) optional, touched (per rank,
- * int64) optional. bg: 3 doubles (host values). */
+ * the last composited entry, n_contrib (H,W) optional, n_iter (H,W) optional
+ * (entries iterated before the stop: the reference's loop trip count, for
+ * the roofline's pair counts), touched (per rank, int64) optional.
+ * bg: 3 doubles (host values). */
 int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
                    int32_t row_lo, int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
                    const int32_t *offsets,
                    const int32_t *entries, const void *feat_sorted, const double *bg,
                    void *image, int32_t image_dtype, void *t_final, int32_t *n_last,
-                   int32_t *n_contrib, int64_t *touched, void *stream);
+                   int32_t *n_contrib, int32_t *n_iter, int64_t *touched, void *stream);
 
 /* L1 + D-SSIM loss and its exact image gradient (metrics.py:135-189) over
- * full images (H,W,3) of `dtype`.  grad gets dL/dimage in `dtype`; the loss
- * scalar (float64) lands in *loss_dev.  Workspace as above. */
+ * full images (H,W,3) of `dtype`.  ref is `dtype`, or 8-bit codes k when
+ * ref_u8 != 0 (read as float(k / 255.0), exactly the reference's PNG load).
+ * grad gets dL/dimage in `dtype`; the loss scalar (float64) lands in
+ * *loss_dev.  Workspace as above. */
 int isg_loss_l1_dssim(void *workspace, size_t *ws_bytes, int32_t dtype, int32_t height,
-                      int32_t width, const void *image, const void *ref, double lambda_dssim,
-                      void *grad, double *loss_dev, void *stream);
+                      int32_t width, const void *image, const void *ref, int32_t ref_u8,
+                      double lambda_dssim, void *grad, double *loss_dev, void *stream);
 
 /* Mean SSIM over valid centres (metrics.py:105-132) of (H,W,C) float64
  * images, into *out_dev. */

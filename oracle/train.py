@@ -116,9 +116,11 @@ def evaluate(params, degree, cameras, images, cfg: Config, it: int) -> Record:
 
 
 def train_w1(images, cameras, init_params: dict, cfg: Config, extent: float | None = None,
-             evaluate_views: bool = True, max_iters: int | None = None) -> Result:
-    """engine.py:465-562 with W=1.  ``max_iters`` stops early (the schedule and
-    learning rates still follow cfg.iterations), used for bounded CPU samples."""
+             evaluate_views: bool = True, max_iters: int | None = None,
+             wall_budget_s: float | None = None) -> Result:
+    """engine.py:465-562 with W=1.  ``max_iters`` / ``wall_budget_s`` stop early
+    (the schedule and learning rates still follow cfg.iterations), used for
+    bounded CPU samples; per-iteration wall times land in Result.iter_times."""
     params = {k: np.array(init_params[k], dtype=np.float32, copy=True) for k in PARAM_NAMES}
     state = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}
     degree = cfg.sh_degree
@@ -129,6 +131,7 @@ def train_w1(images, cameras, init_params: dict, cfg: Config, extent: float | No
         extent = scene_extent(cameras)
     h, w = images.shape[1], images.shape[2]
     res = Result(params=params)
+    res.iter_times = []
     if evaluate_views:
         res.records.append(evaluate(params, degree, cameras, images, cfg, 0))
     schedule = build_schedule(cfg.iterations, len(cameras), cfg.seed)
@@ -161,11 +164,15 @@ def train_w1(images, cameras, init_params: dict, cfg: Config, extent: float | No
             "sh_coeffs": cfg.lr_sh,
         }
         O.adam_step(params, grads, state, it, lrs)
-        res.total_wall_s += time.perf_counter() - t0
+        dt = time.perf_counter() - t0
+        res.total_wall_s += dt
+        res.iter_times.append(dt)
         res.losses.append(float(loss))
         due = it == cfg.iterations or (cfg.eval_interval > 0 and it % cfg.eval_interval == 0)
         if evaluate_views and due:
             res.records.append(evaluate(params, degree, cameras, images, cfg, it))
+        if wall_budget_s is not None and res.total_wall_s >= wall_budget_s:
+            break
     res.seen = seen
     res.grad_accum = grad_accum
     return res

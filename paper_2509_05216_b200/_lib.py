@@ -72,8 +72,8 @@ SIGNATURES = {
     "isg_bin_emit": [_I64, _P, _P, _I32, _I32, _I32, _P, _P, _P],
     "isg_tile_offsets": [_I64, _P, _I32, _P, _P],
     "isg_raster_fwd": [_I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _I32,
-                       _P, _P, _P, _P, _P],
-    "isg_loss_l1_dssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _D, _P, _P, _P],
+                       _P, _P, _P, _P, _P, _P],
+    "isg_loss_l1_dssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _I32, _D, _P, _P, _P],
     "isg_ssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _P, _P],
     "isg_raster_bwd": [_I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P,
                        _P, _P, _P, _I32, _P, _P],

@@ -30,6 +30,15 @@ template <typename T> __device__ __forceinline__ T wt(int i);
 template <> __device__ __forceinline__ float wt<float>(int i) { return c_w1f[i]; }
 template <> __device__ __forceinline__ double wt<double>(int i) { return c_w1d[i]; }
 
+// Ground-truth sample: float/double as stored, or an 8-bit code k read as
+// float(k / 255.0) -- the value the reference's PNG load + astype produces.
+template <typename T, typename R>
+__device__ __forceinline__ T gt_val(R v) { return (T)v; }
+template <>
+__device__ __forceinline__ float gt_val<float, uint8_t>(uint8_t v) { return (float)((double)v / 255.0); }
+template <>
+__device__ __forceinline__ double gt_val<double, uint8_t>(uint8_t v) { return (double)v / 255.0; }
+
 constexpr int LT = 16;          // output tile edge
 constexpr int LP = LT + 10;     // patch edge (tile + 10-px halo)
 
@@ -47,10 +56,10 @@ __device__ __forceinline__ double block_sum(double v, double *scratch) {
 }
 
 // Pass 1.  fmap layout: [field f][channel c][hc][wc]; NULL for SSIM only.
-template <typename T, typename IN>
+template <typename T, typename IN, typename R>
 __global__ void __launch_bounds__(256) ssim_fields_kernel(int H, int W, int C,
                                                           const IN *__restrict__ img,
-                                                          const IN *__restrict__ ref,
+                                                          const R *__restrict__ ref,
                                                           T *__restrict__ fmap,
                                                           double *__restrict__ part) {
     __shared__ T sx[LP][LP + 1], sy[LP][LP + 1];
@@ -71,7 +80,7 @@ __global__ void __launch_bounds__(256) ssim_fields_kernel(int H, int W, int C,
             if (y < H && x < W) {
                 const int64_t o = ((int64_t)y * W + x) * C + c;
                 vx = (T)img[o];
-                vy = (T)ref[o];
+                vy = gt_val<T, R>(ref[o]);
             }
             sx[r][q] = vx;
             sy[r][q] = vy;
@@ -132,9 +141,9 @@ __global__ void __launch_bounds__(256) ssim_fields_kernel(int H, int W, int C,
 }
 
 // Pass 2: dL/dimage = sign(x-y)(1-lam)/n + gscale * (A f0 + x A f1 + y A f2).
-template <typename T, typename IN>
+template <typename T, typename IN, typename R>
 __global__ void __launch_bounds__(256) ssim_adjoint_kernel(int H, int W, const IN *__restrict__ img,
-                                                           const IN *__restrict__ ref,
+                                                           const R *__restrict__ ref,
                                                            const T *__restrict__ fmap,
                                                            IN *__restrict__ grad, T l1_scale,
                                                            T gscale, double *__restrict__ part) {
@@ -179,7 +188,7 @@ __global__ void __launch_bounds__(256) ssim_adjoint_kernel(int H, int W, const I
                 g2 += w * hs[2][ty + i][tx];
             }
             const int64_t o = ((int64_t)y * W + x) * 3 + c;
-            const T xv = (T)img[o], yv = (T)ref[o];
+            const T xv = (T)img[o], yv = gt_val<T, R>(ref[o]);
             const T d = xv - yv;
             const T sg = d > (T)0 ? (T)1 : (d < (T)0 ? (T)-1 : (T)0);
             const T g = g0 + xv * g1 + yv * g2;
@@ -213,8 +222,8 @@ __global__ void loss_finish_kernel(int n_ssim, const double *__restrict__ ssim_p
 
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-template <typename T>
-int loss_impl(void *ws, size_t *ws_bytes, int H, int W, const T *img, const T *ref, double lam,
+template <typename T, typename R>
+int loss_impl(void *ws, size_t *ws_bytes, int H, int W, const T *img, const R *ref, double lam,
               T *grad, double *loss_dev, cudaStream_t s) {
     const int hc = H - 10, wc = W - 10;
     dim3 gf((wc + LT - 1) / LT, (hc + LT - 1) / LT), ga((W + LT - 1) / LT, (H + LT - 1) / LT);
@@ -228,10 +237,10 @@ int loss_impl(void *ws, size_t *ws_bytes, int H, int W, const T *img, const T *r
     T *fmap = (T *)ws;
     double *pf = (double *)((char *)ws + al(sizeof(T) * 9 * (size_t)hc * wc));
     double *pa = (double *)((char *)pf + al(8 * nf));
-    ssim_fields_kernel<T, T><<<gf, 256, 0, s>>>(H, W, 3, img, ref, fmap, pf);
+    ssim_fields_kernel<T, T, R><<<gf, 256, 0, s>>>(H, W, 3, img, ref, fmap, pf);
     ISG_CHECK_LAUNCH();
     const double n_pix = 3.0 * H * W, n_centers = 3.0 * hc * wc;
-    ssim_adjoint_kernel<T, T><<<ga, 256, 0, s>>>(H, W, img, ref, fmap, grad,
+    ssim_adjoint_kernel<T, T, R><<<ga, 256, 0, s>>>(H, W, img, ref, fmap, grad,
                                                  (T)((1.0 - lam) / n_pix), (T)(-lam / n_centers),
                                                  pa);
     ISG_CHECK_LAUNCH();
@@ -247,17 +256,26 @@ using namespace isg;
 
 extern "C" int isg_loss_l1_dssim(void *workspace, size_t *ws_bytes, int32_t dtype, int32_t height,
                                  int32_t width, const void *image, const void *ref,
-                                 double lambda_dssim, void *grad, double *loss_dev,
-                                 void *stream) {
+                                 int32_t ref_u8, double lambda_dssim, void *grad,
+                                 double *loss_dev, void *stream) {
     if (!ws_bytes || height < 11 || width < 11 || lambda_dssim < 0.0 || lambda_dssim > 1.0)
         return (int)cudaErrorInvalidValue;
     cudaStream_t s = (cudaStream_t)stream;
-    if (dtype == ISG_F32)
-        return loss_impl<float>(workspace, ws_bytes, height, width, (const float *)image,
-                                (const float *)ref, lambda_dssim, (float *)grad, loss_dev, s);
-    if (dtype == ISG_F64)
-        return loss_impl<double>(workspace, ws_bytes, height, width, (const double *)image,
-                                 (const double *)ref, lambda_dssim, (double *)grad, loss_dev, s);
+    if (dtype == ISG_F32 && !ref_u8)
+        return loss_impl<float, float>(workspace, ws_bytes, height, width, (const float *)image,
+                                       (const float *)ref, lambda_dssim, (float *)grad, loss_dev, s);
+    if (dtype == ISG_F32 && ref_u8)
+        return loss_impl<float, uint8_t>(workspace, ws_bytes, height, width, (const float *)image,
+                                         (const uint8_t *)ref, lambda_dssim, (float *)grad,
+                                         loss_dev, s);
+    if (dtype == ISG_F64 && !ref_u8)
+        return loss_impl<double, double>(workspace, ws_bytes, height, width,
+                                         (const double *)image, (const double *)ref,
+                                         lambda_dssim, (double *)grad, loss_dev, s);
+    if (dtype == ISG_F64 && ref_u8)
+        return loss_impl<double, uint8_t>(workspace, ws_bytes, height, width,
+                                          (const double *)image, (const uint8_t *)ref,
+                                          lambda_dssim, (double *)grad, loss_dev, s);
     return (int)cudaErrorInvalidValue;
 }
 
@@ -276,7 +294,7 @@ extern "C" int isg_ssim(void *workspace, size_t *ws_bytes, int32_t height, int32
     if (*ws_bytes < al(8 * nf)) return (int)cudaErrorInvalidValue;
     cudaStream_t s = (cudaStream_t)stream;
     double *pf = (double *)workspace;
-    ssim_fields_kernel<double, double><<<gf, 256, 0, s>>>(height, width, channels, image, ref,
+    ssim_fields_kernel<double, double, double><<<gf, 256, 0, s>>>(height, width, channels, image, ref,
                                                           nullptr, pf);
     ISG_CHECK_LAUNCH();
     loss_finish_kernel<<<1, 256, 0, s>>>((int)nf, pf, 0, nullptr, 0.0,

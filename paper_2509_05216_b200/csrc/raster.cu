@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(THREADS) raster_fwd_kernel(
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
     const T *__restrict__ feat, T bg0, T bg1, T bg2, void *image, int image_f64,
     T *__restrict__ t_final, int32_t *__restrict__ n_last,
-    int32_t *__restrict__ n_contrib, int64_t *__restrict__ touched) {
+    int32_t *__restrict__ n_contrib, int32_t *__restrict__ n_iter,
+    int64_t *__restrict__ touched) {
     __shared__ T s_mx[FWD_BATCH], s_my[FWD_BATCH], s_a[FWD_BATCH], s_b[FWD_BATCH],
         s_c[FWD_BATCH], s_op[FWD_BATCH], s_thr[FWD_BATCH], s_r[FWD_BATCH], s_g[FWD_BATCH],
         s_bl[FWD_BATCH];
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(THREADS) raster_fwd_kernel(
     const int e0 = offsets[tl], e1 = offsets[tl + 1];
     const T fpx = (T)px, fpy = (T)py;
     T t = 1, cr = 0, cg = 0, cb = 0;
-    int count = 0, last = 0;
+    int count = 0, last = 0, iters = 0;
     bool done = !inside;
     for (int base = e0; base < e1; base += FWD_BATCH) {
         if (__syncthreads_count(done) == THREADS) break;
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(THREADS) raster_fwd_kernel(
                 const T test = t * ((T)1 - alpha);
                 if (test < (T)T_STOP) {
                     done = true;
+                    iters = base - e0 + j + 1;
                     break;
                 }
                 cr += s_r[j] * alpha * t;
@@ -162,6 +164,7 @@ __global__ void __launch_bounds__(THREADS) raster_fwd_kernel(
         t_final[pix] = t;
         n_last[pix] = last;
         if (n_contrib) n_contrib[pix] = count;
+        if (n_iter) n_iter[pix] = done ? iters : e1 - e0;
     }
 }
 
@@ -341,7 +344,8 @@ extern "C" int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height,
                               int32_t n_tile_ids, const int32_t *offsets,
                               const int32_t *entries, const void *feat_sorted, const double *bg,
                               void *image, int32_t image_dtype, void *t_final, int32_t *n_last,
-                              int32_t *n_contrib, int64_t *touched, void *stream) {
+                              int32_t *n_contrib, int32_t *n_iter, int64_t *touched,
+                              void *stream) {
     if (width <= 0 || height <= 0 || tiles_x <= 0 || row_lo < 0 || row_hi < row_lo || !bg ||
         !image || !t_final || !n_last || n_tile_ids < 0)
         return (int)cudaErrorInvalidValue;
@@ -354,21 +358,21 @@ extern "C" int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height,
             raster_fwd_kernel<float, true><<<n_tiles, THREADS, 0, s>>>(
                 width, height, tiles_x, row_lo, tile_ids, offsets, entries, (const float *)feat_sorted,
                 (float)bg[0], (float)bg[1], (float)bg[2], image, img64, (float *)t_final, n_last,
-                n_contrib, touched);
+                n_contrib, n_iter, touched);
         else
             raster_fwd_kernel<float, false><<<n_tiles, THREADS, 0, s>>>(
                 width, height, tiles_x, row_lo, tile_ids, offsets, entries, (const float *)feat_sorted,
                 (float)bg[0], (float)bg[1], (float)bg[2], image, img64, (float *)t_final, n_last,
-                n_contrib, touched);
+                n_contrib, n_iter, touched);
     } else if (feat_dtype == ISG_F64) {
         if (touched)
             raster_fwd_kernel<double, true><<<n_tiles, THREADS, 0, s>>>(
                 width, height, tiles_x, row_lo, tile_ids, offsets, entries, (const double *)feat_sorted,
-                bg[0], bg[1], bg[2], image, img64, (double *)t_final, n_last, n_contrib, touched);
+                bg[0], bg[1], bg[2], image, img64, (double *)t_final, n_last, n_contrib, n_iter, touched);
         else
             raster_fwd_kernel<double, false><<<n_tiles, THREADS, 0, s>>>(
                 width, height, tiles_x, row_lo, tile_ids, offsets, entries, (const double *)feat_sorted,
-                bg[0], bg[1], bg[2], image, img64, (double *)t_final, n_last, n_contrib, touched);
+                bg[0], bg[1], bg[2], image, img64, (double *)t_final, n_last, n_contrib, n_iter, touched);
     } else {
         return (int)cudaErrorInvalidValue;
     }

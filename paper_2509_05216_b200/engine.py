@@ -47,6 +47,31 @@ def _grow(buf: torch.Tensor | None, n: int, shape_tail=(), dtype=torch.float32, 
     return buf
 
 
+class PhaseTimer:
+    """CUDA events between launches on the current stream: phase name ->
+    device milliseconds (used by bench.py for the per-kernel roofline)."""
+
+    def __init__(self):
+        self.marks: list[tuple[str, torch.cuda.Event]] = []
+
+    def mark(self, name: str) -> None:
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.marks.append((name, e))
+
+    def phases(self) -> dict[str, float]:
+        torch.cuda.synchronize()
+        out: dict[str, float] = {}
+        for (_, a), (name, b) in zip(self.marks[:-1], self.marks[1:]):
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
+
+
+def _mark(timer, name):
+    if timer is not None:
+        timer.mark(name)
+
+
 @dataclass
 class ViewContext:
     """Per-view forward state kept for the backward (the cache of RenderAux)."""
@@ -81,7 +106,9 @@ class Rasterizer:
         self.offsets = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=dev)
         self.tile_keys = self.tile_vals = self.keys_sorted_t = self.entries = None
         self.partials = None
-        self.launches = 0
+        self.n_contrib_out = None  # set to (H, W) int32 tensors to count pairs
+        self.n_iter_out = None
+        self.timer: PhaseTimer | None = None
 
     def resize(self, n: int) -> None:
         dev = self.device
@@ -114,9 +141,13 @@ class Rasterizer:
         p.rotations, p.opacity_logits = L.ptr(cloud.rotations), L.ptr(cloud.opacity_logits)
         p.sh, p.n, p.degree, p.dtype = L.ptr(cloud.sh_coeffs), n, cloud.degree, L.ISG_F32
         self.cam_struct = L.camera_struct(cam)
+        tm = self.timer
+        _mark(tm, "begin")
         L.check(lib.isg_preprocess(ctypes.byref(p), ctypes.byref(self.cam_struct), TILE,
                                    ctypes.byref(out), s), "isg_preprocess")
+        _mark(tm, "preprocess")
         L.sort_pairs(self.key, self.vals0, (0, 64), self.ws_sort, self.key_sorted, self.order)
+        _mark(tm, "sort_depth")
         sz = ctypes.c_size_t(0)
         L.check(lib.isg_bin_count(None, ctypes.byref(sz), n, None, None, None, None, self.ftag,
                                   0, self.tiles_y, None, None, None, None, None), "bin (size)")
@@ -127,8 +158,10 @@ class Rasterizer:
                                   self.ftag, 0, self.tiles_y, L.ptr(self.rect_sorted),
                                   L.ptr(self.feat_sorted), L.ptr(self.emit_off),
                                   L.ptr(self.counts), s), "isg_bin_count")
+        _mark(tm, "bin_count")
         self.counts_host.copy_(self.counts, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        _mark(tm, "host_sync")
         m, e = int(self.counts_host[0]), int(self.counts_host[1])
         dev = self.device
         self.tile_keys = _grow(self.tile_keys, e, dtype=torch.int32, device=dev)
@@ -139,15 +172,20 @@ class Rasterizer:
             L.check(lib.isg_bin_emit(m, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
                                      self.tiles_x, 0, self.tiles_y, L.ptr(self.tile_keys),
                                      L.ptr(self.tile_vals), s), "isg_bin_emit")
+            _mark(tm, "bin_emit")
             L.sort_pairs(self.tile_keys[:e], self.tile_vals[:e], (0, self.tile_bits),
                          self.ws_sort, self.keys_sorted_t[:e], self.entries[:e])
+            _mark(tm, "sort_tiles")
         L.check(lib.isg_tile_offsets(e, L.ptr(self.keys_sorted_t), self.n_tiles,
                                      L.ptr(self.offsets), s), "isg_tile_offsets")
+        _mark(tm, "tile_offsets")
         L.check(lib.isg_raster_fwd(self.ftag, self.width, self.height, self.tiles_x, 0,
                                    self.tiles_y, None, 0, L.ptr(self.offsets), L.ptr(self.entries),
                                    L.ptr(self.feat_sorted), ctypes.cast(self.bg, ctypes.c_void_p),
                                    L.ptr(self.image), L.ISG_F32, L.ptr(self.t_final),
-                                   L.ptr(self.n_last), None, None, s), "isg_raster_fwd")
+                                   L.ptr(self.n_last), L.ptr(self.n_contrib_out),
+                                   L.ptr(self.n_iter_out), None, s), "isg_raster_fwd")
+        _mark(tm, "raster_fwd")
         return ViewContext(m=m, e=e)
 
     # -- backward --------------------------------------------------------
@@ -162,10 +200,12 @@ class Rasterizer:
                                    L.ptr(self.emit_off), ctypes.cast(self.bg, ctypes.c_void_p),
                                    L.ptr(self.t_final), L.ptr(self.n_last), L.ptr(self.dl),
                                    L.ISG_F32, L.ptr(self.partials), s), "isg_raster_bwd")
+        _mark(self.timer, "raster_bwd")
         if ctx.m:
             L.check(lib.isg_reduce_ordered(self.ftag, ctx.m, L.ptr(self.emit_off),
                                            L.ptr(self.partials), L.ptr(self.order),
                                            L.ptr(self.grad2d), None, s), "isg_reduce_ordered")
+        _mark(self.timer, "reduce")
 
     LAUNCHES_PER_STEP = None  # filled by Trainer (documented count)
 
@@ -219,6 +259,7 @@ class Trainer:
         ctx = r.forward(self.cloud, cam)
         slot = loss_slot if loss_slot is not None else self.loss_dev[it:it + 1]
         loss_l1_dssim_device(r.image, gt, self.cfg.lambda_dssim, r.dl, slot)
+        _mark(r.timer, "loss")
         r.backward(ctx)
         for i, v in enumerate(self.lrs(it)):
             self.lr_host[i] = float(np.float32(v))
@@ -229,6 +270,7 @@ class Trainer:
                                        ctypes.cast(self.lr_host, ctypes.c_void_p),
                                        ctypes.byref(c), 0.5 * r.width, 0.5 * r.height,
                                        L.stream_ptr()), "isg_chain_adam")
+        _mark(r.timer, "chain_adam")
 
     def render(self, cam) -> torch.Tensor:
         self.r.forward(self.cloud, cam)

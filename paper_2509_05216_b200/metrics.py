@@ -35,12 +35,15 @@ def loss_l1_dssim_device(img: torch.Tensor, ref: torch.Tensor, lambda_dssim: flo
     h, w = int(img.shape[0]), int(img.shape[1])
     sz = ctypes.c_size_t(0)
     tag = L.dtype_tag(img.dtype)
-    L.check(L.lib().isg_loss_l1_dssim(None, ctypes.byref(sz), tag, h, w, None, None,
+    u8 = 1 if ref.dtype == torch.uint8 else 0
+    if not u8 and ref.dtype != img.dtype:
+        raise ValueError("ref must match the image dtype or be uint8 codes")
+    L.check(L.lib().isg_loss_l1_dssim(None, ctypes.byref(sz), tag, h, w, None, None, u8,
                                       float(lambda_dssim), None, None, None), "loss (size)")
     buf = _WS.get(sz.value, img.device)
     sz = ctypes.c_size_t(buf.numel())
     L.check(L.lib().isg_loss_l1_dssim(L.ptr(buf), ctypes.byref(sz), tag, h, w, L.ptr(img),
-                                      L.ptr(ref), float(lambda_dssim), L.ptr(grad),
+                                      L.ptr(ref), u8, float(lambda_dssim), L.ptr(grad),
                                       L.ptr(loss_out), L.stream_ptr()), "isg_loss_l1_dssim")
 
 

@@ -265,7 +265,8 @@ def _raster_fwd(feat, offsets32, entries, width, height, tiles_x, tile_ids, bg, 
         L.dtype_tag(feat.dtype), width, height, tiles_x, 0, rows, L.ptr(tile_ids), n_ids,
         L.ptr(offsets32), L.ptr(entries) if entries.numel() else None, L.ptr(feat) if feat.numel() else None,
         ctypes.cast(bgc, ctypes.c_void_p), L.ptr(image), L.dtype_tag(image.dtype), L.ptr(t_final),
-        L.ptr(n_last), L.ptr(n_contrib), L.ptr(touched) if touched is not None and touched.numel() else None,
+        L.ptr(n_last), L.ptr(n_contrib), None,
+        L.ptr(touched) if touched is not None and touched.numel() else None,
         L.stream_ptr()), "isg_raster_fwd")
 
 

@@ -53,4 +53,4 @@ def test_entry_points_reject_bad_arguments_without_gpu():
     assert lib.isg_sort_u64(None, None, None, None, None, None, -1, 0, 64, None) == 1
     assert lib.isg_adam(7, 1, None, None, None, None, None, None) == 1
     sz = ctypes.c_size_t(0)
-    assert lib.isg_loss_l1_dssim(None, ctypes.byref(sz), 0, 5, 5, None, None, 0.2, None, None, None) == 1
+    assert lib.isg_loss_l1_dssim(None, ctypes.byref(sz), 0, 5, 5, None, None, 0, 0.2, None, None, None) == 1
