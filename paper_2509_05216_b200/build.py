@@ -27,7 +27,8 @@ SOURCES = {
     # file: extra flags
     "project.cu": ["-fmad=false"],
     "binning.cu": [],
-    "raster.cu": ["-fmad=false"],
+    "raster_f64.cu": ["-fmad=false"],
+    "raster_f32.cu": ["-ftz=true"],
     "loss.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1,0 +1,480 @@
+// raster_f32.cu -- production float32 tile rasteriser (sm_100a).
+//
+// _forward_tiles / _backward_tiles (_kernels.py:229-374) re-designed for the
+// B200 SM: one 128-thread CTA per 16x16 tile, two pixels per thread (rows r
+// and r+8 of the same column, so the x offset d0 is shared).  Each round
+// stages a batch of the tile's entries in shared memory; while staging, one
+// thread per entry runs an exact conservative tile test -- the maximum of the
+// Gaussian exponent over the tile's pixel-centre box -- and entries that
+// cannot reach alpha >= 1/255 at any pixel of the tile are dropped from the
+// batch (ballot + prefix compaction).  Dropping them changes no result: every
+// pixel would have skipped them (the margin covers the float rounding of the
+// per-pixel exponent).  Per pair the exponent is 4 explicit FMA/FMULs against
+// a per-splat log threshold; only pairs that can pass pay for the SFU ex2.
+//
+// All decisions (skip, 0.99 clamp, stop) come from pair_alpha(), written with
+// explicit rounding intrinsics so the forward and the backward kernels compute
+// bit-identical exponents and alphas and therefore the same contributor sets.
+//
+// The backward walks each pixel's contributors back to front (T recovered by
+// division from T_final), sums the two pixels of a thread in registers and
+// reduces the 9 gradient terms of an entry over the warp with a 12-shuffle
+// butterfly reduce-scatter; the 4 warp sums are folded in fixed order and
+// written as the entry's (tile, splat) subtotal.  Deterministic throughout.
+#include "common.cuh"
+#include "raster_f32.cuh"
+
+namespace isg {
+namespace f32 {
+
+constexpr int NT = 128;  // threads per tile (2 pixels each)
+constexpr int NW = NT / 32;
+constexpr int FB = 128;  // forward staging batch
+constexpr int BB = 32;   // backward staging batch
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ float ex2a(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float lg2a(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Staged entry: g = (mx, my, -a/2, -b), h = (-c/2, thr, opacity, 0),
+// c = (r, g, b, 0).  The scalings are exact (powers of two / sign).
+struct Staged {
+    float4 g, h, c;
+};
+
+// Exponent threshold below which opacity * exp(power) < 1/255 for certain:
+// -ln(255 o) minus a margin far above the ex2/lg2 approximation error.
+__device__ __forceinline__ float skip_thr(float op) {
+    if (!(op > 0.0f)) return 1.0f;
+    return __fsub_rn(__fmul_rn(lg2a(__fmul_rn(255.0f, op)), -LN2), 1e-3f);
+}
+
+__device__ __forceinline__ Staged stage(const float *__restrict__ feat, int rank) {
+    const float4 *f = reinterpret_cast<const float4 *>(feat) + 3 * (int64_t)rank;
+    const float4 x = __ldg(f), y = __ldg(f + 1), z = __ldg(f + 2);
+    // x = (mx, my, a, b), y = (c, op, r, g), z = (b_col, 0, 0, 0)
+    Staged s;
+    s.g = make_float4(x.x, x.y, -0.5f * x.z, -x.w);
+    s.h = make_float4(-0.5f * y.x, skip_thr(y.y), y.y, 0.0f);
+    s.c = make_float4(y.z, y.w, z.x, 0.0f);
+    return s;
+}
+
+// Per-pair alpha (0 when the pair is skipped) and the Gaussian weight g.
+__device__ __forceinline__ float pair_alpha(float d0, float d1, const float4 &g4, const float4 &h4,
+                                            float &gw) {
+    const float power = __fmaf_rn(d0, __fmaf_rn(g4.z, d0, __fmul_rn(g4.w, d1)),
+                                  __fmul_rn(__fmul_rn(h4.x, d1), d1));
+    if (power > 0.0f || power < h4.y) return 0.0f;
+    gw = ex2a(__fmul_rn(power, LOG2E));
+    const float a = fminf(__fmul_rn(h4.z, gw), 0.99f);
+    return a >= (1.0f / 255.0f) ? a : 0.0f;
+}
+
+// True when no pixel centre of the tile box [x0, x0+15] x [y0, y0+15] can
+// reach the skip threshold: the exact maximum exponent over the box (convex
+// quadratic: interior minimum or an edge minimum) is below thr by a margin
+// that bounds the float rounding of the per-pixel exponent.
+__device__ __forceinline__ bool tile_dead(const Staged &s, float x0, float y0) {
+    const float thr = s.h.y;
+    if (thr > 0.0f) return true;  // opacity < 1/255: every pair is skipped
+    const float a = -2.0f * s.g.z, b = -s.g.w, c = -2.0f * s.h.x;
+    const float lx = x0 - s.g.x, hx = lx + 15.0f, ly = y0 - s.g.y, hy = ly + 15.0f;
+    if (lx <= 0.0f && hx >= 0.0f && ly <= 0.0f && hy >= 0.0f) return false;
+    float q = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+        const float d0 = e ? hx : lx;
+        const float d1 = fminf(fmaxf(-b * d0 / c, ly), hy);
+        q = fminf(q, a * d0 * d0 + 2.0f * b * d0 * d1 + c * d1 * d1);
+        const float e1 = e ? hy : ly;
+        const float e0 = fminf(fmaxf(-b * e1 / a, lx), hx);
+        q = fminf(q, a * e0 * e0 + 2.0f * b * e0 * e1 + c * e1 * e1);
+    }
+    const float mdx = fmaxf(fabsf(lx), fabsf(hx)), mdy = fmaxf(fabsf(ly), fabsf(hy));
+    const float scale = a * mdx * mdx + 2.0f * fabsf(b) * mdx * mdy + c * mdy * mdy;
+    return -0.5f * q < thr - (1e-3f + 1e-5f * scale);
+}
+
+// ------------------------------------------------------------- forward ----
+template <bool TOUCH>
+__global__ void __launch_bounds__(NT) fwd_kernel(
+    int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
+    const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
+    const float *__restrict__ feat, float bg0, float bg1, float bg2, void *image, int image_f64,
+    float *__restrict__ t_final, int32_t *__restrict__ n_last, int32_t *__restrict__ n_contrib,
+    int32_t *__restrict__ n_iter, int64_t *__restrict__ touched) {
+    __shared__ float4 sg[FB], sh[FB], sc[FB];
+    __shared__ int sj[FB];
+    __shared__ int srank[TOUCH ? FB : 1];
+    __shared__ int wcount[NW];
+    const int tl = blockIdx.x;
+    const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
+    const int ty = tid / tiles_x, tx = tid - ty * tiles_x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int px = tx * 16 + (threadIdx.x & 15);
+    const int py0 = ty * 16 + (threadIdx.x >> 4), py1 = py0 + 8;
+    const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
+    const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
+    const float x0 = (float)(tx * 16), y0 = (float)(ty * 16);
+    const int e0 = offsets[tl], n_ent = offsets[tl + 1] - e0;
+    float t0 = 1.0f, r0 = 0.0f, g0 = 0.0f, b0 = 0.0f;
+    float t1 = 1.0f, r1 = 0.0f, g1 = 0.0f, b1 = 0.0f;
+    int last0 = 0, last1 = 0, cnt0 = 0, cnt1 = 0, it0 = 0, it1 = 0;
+    bool done0 = !in0, done1 = !in1;
+    for (int base = 0; base < n_ent; base += FB) {
+        if (__syncthreads_count(done0 && done1) == NT) break;
+        const int j = base + threadIdx.x;
+        bool live = false;
+        Staged st;
+        int rank = 0;
+        if (j < n_ent) {
+            rank = entries[e0 + j];
+            st = stage(feat, rank);
+            live = !tile_dead(st, x0, y0);
+        }
+        const unsigned bal = __ballot_sync(FULL, live);
+        if (lane == 0) wcount[warp] = __popc(bal);
+        __syncthreads();
+        int off = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) {
+            const int c = wcount[w];
+            off += w < warp ? c : 0;
+            total += c;
+        }
+        if (live) {
+            const int pos = off + __popc(bal & ((1u << lane) - 1u));
+            sg[pos] = st.g;
+            sh[pos] = st.h;
+            sc[pos] = st.c;
+            sj[pos] = j;
+            if (TOUCH) srank[pos] = rank;
+        }
+        __syncthreads();
+        for (int k = 0; k < total; k++) {
+            if (done0 && done1) break;
+            const float4 g4 = sg[k], h4 = sh[k];
+            const float d0 = fpx - g4.x;
+            if (!done0) {
+                float gw;
+                const float a = pair_alpha(d0, fpy0 - g4.y, g4, h4, gw);
+                if (a > 0.0f) {
+                    const float test = t0 * (1.0f - a);
+                    if (test < 1e-4f) {
+                        done0 = true;
+                        it0 = sj[k] + 1;
+                    } else {
+                        const float4 c = sc[k];
+                        const float w = a * t0;
+                        r0 = fmaf(c.x, w, r0);
+                        g0 = fmaf(c.y, w, g0);
+                        b0 = fmaf(c.z, w, b0);
+                        t0 = test;
+                        last0 = sj[k] + 1;
+                        cnt0++;
+                        if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[k]], 1ull);
+                    }
+                }
+            }
+            if (!done1) {
+                float gw;
+                const float a = pair_alpha(d0, fpy1 - g4.y, g4, h4, gw);
+                if (a > 0.0f) {
+                    const float test = t1 * (1.0f - a);
+                    if (test < 1e-4f) {
+                        done1 = true;
+                        it1 = sj[k] + 1;
+                    } else {
+                        const float4 c = sc[k];
+                        const float w = a * t1;
+                        r1 = fmaf(c.x, w, r1);
+                        g1 = fmaf(c.y, w, g1);
+                        b1 = fmaf(c.z, w, b1);
+                        t1 = test;
+                        last1 = sj[k] + 1;
+                        cnt1++;
+                        if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[k]], 1ull);
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        const bool in = p ? in1 : in0;
+        if (!in) continue;
+        const int py = p ? py1 : py0;
+        const float t = p ? t1 : t0;
+        const int64_t pix = (int64_t)py * W + px;
+        const float vr = fmaf(t, bg0, p ? r1 : r0), vg = fmaf(t, bg1, p ? g1 : g0),
+                    vb = fmaf(t, bg2, p ? b1 : b0);
+        if (image_f64) {
+            double *im = (double *)image + 3 * pix;
+            im[0] = vr;
+            im[1] = vg;
+            im[2] = vb;
+        } else {
+            float *im = (float *)image + 3 * pix;
+            im[0] = vr;
+            im[1] = vg;
+            im[2] = vb;
+        }
+        t_final[pix] = t;
+        n_last[pix] = p ? last1 : last0;
+        if (n_contrib) n_contrib[pix] = p ? cnt1 : cnt0;
+        if (n_iter) n_iter[pix] = (p ? done1 : done0) ? (p ? it1 : it0) : n_ent;
+    }
+}
+
+// ------------------------------------------------------------ backward ----
+// Butterfly reduce-scatter of 9 values over the warp (12 shuffles).  After it,
+// lane L with bits (b4,b3,b2,b1) holds the full sum of value
+// 5*b4 + 3*b3 + 2*b2 + b1 (see bfly_slot).
+__device__ __forceinline__ float bfly9(const float (&v)[9], int lane) {
+    const bool s4 = lane & 16, s3 = lane & 8, s2 = lane & 4, s1 = lane & 2;
+    float u[5];
+#pragma unroll
+    for (int i = 0; i < 5; i++) {
+        const float a = v[i], b = i + 5 < 9 ? v[i + 5] : 0.0f;
+        u[i] = (s4 ? b : a) + __shfl_xor_sync(FULL, s4 ? a : b, 16);
+    }
+    float w[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        const float a = u[i], b = i + 3 < 5 ? u[i + 3] : 0.0f;
+        w[i] = (s3 ? b : a) + __shfl_xor_sync(FULL, s3 ? a : b, 8);
+    }
+    float x[2];
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        const float a = w[i], b = i + 2 < 3 ? w[i + 2] : 0.0f;
+        x[i] = (s2 ? b : a) + __shfl_xor_sync(FULL, s2 ? a : b, 4);
+    }
+    float y = (s1 ? x[1] : x[0]) + __shfl_xor_sync(FULL, s1 ? x[0] : x[1], 2);
+    return y + __shfl_xor_sync(FULL, y, 1);
+}
+
+// Value index held by `lane` after bfly9, or -1 (pad / duplicate lane).
+__device__ __forceinline__ int bfly_slot(int lane) {
+    if (lane & 1) return -1;
+    const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
+    const int f = 5 * b4 + 3 * b3 + 2 * b2 + b1;
+    return ((2 * b2 + b1) < (b3 ? 2 : 3) && f < 9) ? f : -1;
+}
+
+// One contributing (pixel, entry) pair: accumulate its 9 gradient terms and
+// advance the pixel's back-to-front state (T, S).  _kernels.py:342-374.
+__device__ __forceinline__ void pair_grad(float a, float gw, float d0, float d1, const float4 &g4,
+                                          const float4 &h4, const float4 &c, float wr, float wg,
+                                          float wb, float &T, float &sr, float &sg, float &sb,
+                                          float (&v)[9]) {
+    const float inv = __frcp_rn(1.0f - a);
+    const float ti = T * inv;  // T before this splat
+    const float at = a * ti;
+    v[5] = fmaf(wr, at, v[5]);
+    v[6] = fmaf(wg, at, v[6]);
+    v[7] = fmaf(wb, at, v[7]);
+    const float dalpha = wr * (c.x * ti - sr * inv) + wg * (c.y * ti - sg * inv) +
+                         wb * (c.z * ti - sb * inv);
+    sr = fmaf(c.x, at, sr);
+    sg = fmaf(c.y, at, sg);
+    sb = fmaf(c.z, at, sb);
+    if (!(__fmul_rn(h4.z, gw) > 0.99f)) {  // clamped alpha: zero sub-gradient
+        v[8] = fmaf(dalpha, gw, v[8]);
+        const float dpower = dalpha * h4.z * gw;
+        // conic (a, b, c) = (-2 g4.z, -g4.w, -2 h4.x)
+        v[2] = fmaf(dpower, -0.5f * d0 * d0, v[2]);
+        v[3] = fmaf(dpower, -(d0 * d1), v[3]);
+        v[4] = fmaf(dpower, -0.5f * d1 * d1, v[4]);
+        v[0] = fmaf(dpower, -2.0f * g4.z * d0 - g4.w * d1, v[0]);
+        v[1] = fmaf(dpower, -g4.w * d0 - 2.0f * h4.x * d1, v[1]);
+    }
+    T = ti;
+}
+
+template <typename DL>
+__global__ void __launch_bounds__(NT) bwd_kernel(
+    int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
+    const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
+    const float *__restrict__ feat, const int4 *__restrict__ rect_sorted,
+    const int64_t *__restrict__ emit_off, float bg0, float bg1, float bg2,
+    const float *__restrict__ t_final, const int32_t *__restrict__ n_last,
+    const DL *__restrict__ dl, float *__restrict__ partials) {
+    __shared__ float4 sg[BB], sh[BB], sc[BB];
+    __shared__ int sj[BB];
+    __shared__ int64_t sslot[BB];
+    __shared__ float sred[NW][BB][9];
+    __shared__ int smax[NW];
+    __shared__ int stotal;
+    const int tl = blockIdx.x;
+    const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
+    const int ty = tid / tiles_x, tx = tid - ty * tiles_x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int px = tx * 16 + (threadIdx.x & 15);
+    const int py0 = ty * 16 + (threadIdx.x >> 4), py1 = py0 + 8;
+    const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
+    const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
+    const float x0 = (float)(tx * 16), y0 = (float)(ty * 16);
+    const int e0 = offsets[tl], n_ent = offsets[tl + 1] - e0;
+    const int my_slot = bfly_slot(lane);
+
+    int last0 = 0, last1 = 0;
+    float T0 = 0.0f, T1 = 0.0f, wr0 = 0, wg0 = 0, wb0 = 0, wr1 = 0, wg1 = 0, wb1 = 0;
+    if (in0) {
+        const int64_t pix = (int64_t)py0 * W + px;
+        last0 = n_last[pix];
+        T0 = t_final[pix];
+        wr0 = (float)dl[3 * pix];
+        wg0 = (float)dl[3 * pix + 1];
+        wb0 = (float)dl[3 * pix + 2];
+    }
+    if (in1) {
+        const int64_t pix = (int64_t)py1 * W + px;
+        last1 = n_last[pix];
+        T1 = t_final[pix];
+        wr1 = (float)dl[3 * pix];
+        wg1 = (float)dl[3 * pix + 1];
+        wb1 = (float)dl[3 * pix + 2];
+    }
+    float sr0 = T0 * bg0, sg0 = T0 * bg1, sb0 = T0 * bg2;
+    float sr1 = T1 * bg0, sg1 = T1 * bg1, sb1 = T1 * bg2;
+    int m = max(last0, last1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
+    if (lane == 0) smax[warp] = m;
+    __syncthreads();
+    int max_last = 0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) max_last = max(max_last, smax[w]);
+
+    for (int end = n_ent; end > 0; end -= BB) {
+        const int start = max(end - BB, 0);
+        __syncthreads();
+        if (warp == 0) {
+            const int j = start + lane;
+            bool live = false;
+            Staged st;
+            int64_t slot = 0;
+            if (j < end) {
+                const int rank = entries[e0 + j];
+                if (emit_off) {
+                    const int4 rc = rect_sorted[rank];
+                    slot = emit_off[rank] + (int64_t)(ty - max(rc.y, row_lo)) * (rc.z - rc.x + 1) +
+                           (tx - rc.x);
+                } else {
+                    slot = (int64_t)e0 + j;
+                }
+                if (j < max_last) {
+                    st = stage(feat, rank);
+                    live = !tile_dead(st, x0, y0);
+                }
+                if (!live) {
+                    float *dst = partials + 9 * slot;
+#pragma unroll
+                    for (int q = 0; q < 9; q++) dst[q] = 0.0f;
+                }
+            }
+            const unsigned bal = __ballot_sync(FULL, live);
+            if (live) {
+                const int pos = __popc(bal & ((1u << lane) - 1u));
+                sg[pos] = st.g;
+                sh[pos] = st.h;
+                sc[pos] = st.c;
+                sj[pos] = j;
+                sslot[pos] = slot;
+            }
+            if (lane == 0) stotal = __popc(bal);
+        }
+        __syncthreads();
+        const int total = stotal;
+        for (int k = total - 1; k >= 0; k--) {
+            const float4 g4 = sg[k], h4 = sh[k];
+            const int jj = sj[k];
+            float v[9];
+#pragma unroll
+            for (int q = 0; q < 9; q++) v[q] = 0.0f;
+            bool act = false;
+            const float d0 = fpx - g4.x;
+            if (jj < last0) {
+                float gw;
+                const float d1 = fpy0 - g4.y;
+                const float a = pair_alpha(d0, d1, g4, h4, gw);
+                if (a > 0.0f) {
+                    act = true;
+                    pair_grad(a, gw, d0, d1, g4, h4, sc[k], wr0, wg0, wb0, T0, sr0, sg0, sb0, v);
+                }
+            }
+            if (jj < last1) {
+                float gw;
+                const float d1 = fpy1 - g4.y;
+                const float a = pair_alpha(d0, d1, g4, h4, gw);
+                if (a > 0.0f) {
+                    act = true;
+                    pair_grad(a, gw, d0, d1, g4, h4, sc[k], wr1, wg1, wb1, T1, sr1, sg1, sb1, v);
+                }
+            }
+            float y = 0.0f;
+            if (__any_sync(FULL, act)) y = bfly9(v, lane);
+            if (my_slot >= 0) sred[warp][k][my_slot] = y;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < total * 9; idx += NT) {
+            const int k = idx / 9, q = idx - k * 9;
+            const float acc = ((sred[0][k][q] + sred[1][k][q]) + sred[2][k][q]) + sred[3][k][q];
+            partials[9 * sslot[k] + q] = acc;
+        }
+    }
+}
+
+}  // namespace f32
+
+void launch_raster_fwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
+                           const int32_t *tile_ids, const int32_t *offsets, const int32_t *entries,
+                           const float *feat, float bg0, float bg1, float bg2, void *image,
+                           int image_f64, float *t_final, int32_t *n_last, int32_t *n_contrib,
+                           int32_t *n_iter, int64_t *touched, cudaStream_t s) {
+    if (touched)
+        f32::fwd_kernel<true><<<n_tiles, f32::NT, 0, s>>>(
+            W, H, tiles_x, row_lo, tile_ids, offsets, entries, feat, bg0, bg1, bg2, image,
+            image_f64, t_final, n_last, n_contrib, n_iter, touched);
+    else
+        f32::fwd_kernel<false><<<n_tiles, f32::NT, 0, s>>>(
+            W, H, tiles_x, row_lo, tile_ids, offsets, entries, feat, bg0, bg1, bg2, image,
+            image_f64, t_final, n_last, n_contrib, n_iter, touched);
+}
+
+template <typename DL>
+void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
+                           const int32_t *tile_ids, const int32_t *offsets, const int32_t *entries,
+                           const float *feat, const int4 *rect_sorted, const int64_t *emit_off,
+                           float bg0, float bg1, float bg2, const float *t_final,
+                           const int32_t *n_last, const DL *dl, float *partials, cudaStream_t s) {
+    f32::bwd_kernel<DL><<<n_tiles, f32::NT, 0, s>>>(W, H, tiles_x, row_lo, tile_ids, offsets,
+                                                    entries, feat, rect_sorted, emit_off, bg0, bg1,
+                                                    bg2, t_final, n_last, dl, partials);
+}
+
+template void launch_raster_bwd_f32<float>(int, int, int, int, int, const int32_t *,
+                                           const int32_t *, const int32_t *, const float *,
+                                           const int4 *, const int64_t *, float, float, float,
+                                           const float *, const int32_t *, const float *, float *,
+                                           cudaStream_t);
+template void launch_raster_bwd_f32<double>(int, int, int, int, int, const int32_t *,
+                                            const int32_t *, const int32_t *, const float *,
+                                            const int4 *, const int64_t *, float, float, float,
+                                            const float *, const int32_t *, const double *,
+                                            float *, cudaStream_t);
+
+}  // namespace isg

@@ -1,4 +1,6 @@
-// raster.cu -- tile rasteriser forward/backward and the ordered fold (sm_100a).
+// raster_f64.cu -- float64 cross-check rasteriser, the ordered fold and the
+// raster C ABI (sm_100a).  The float32 production kernels live in
+// raster_f32.cu; this file keeps the reference-exact float64 instantiation.
 //
 // One CTA per 16x16 tile, one pixel per thread.  Each CTA walks its tile's
 // entry list (global compositing order) in batches staged through shared
@@ -21,6 +23,7 @@
 // per (tile, splat) -- the reference's scratch row -- into a splat-major slot
 // so the per-splat fold below reads them in ascending tile order.
 #include "common.cuh"
+#include "raster_f32.cuh"
 
 namespace isg {
 
@@ -354,16 +357,10 @@ extern "C" int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height,
     cudaStream_t s = (cudaStream_t)stream;
     const int img64 = image_dtype == ISG_F64 ? 1 : 0;
     if (feat_dtype == ISG_F32) {
-        if (touched)
-            raster_fwd_kernel<float, true><<<n_tiles, THREADS, 0, s>>>(
-                width, height, tiles_x, row_lo, tile_ids, offsets, entries, (const float *)feat_sorted,
-                (float)bg[0], (float)bg[1], (float)bg[2], image, img64, (float *)t_final, n_last,
-                n_contrib, n_iter, touched);
-        else
-            raster_fwd_kernel<float, false><<<n_tiles, THREADS, 0, s>>>(
-                width, height, tiles_x, row_lo, tile_ids, offsets, entries, (const float *)feat_sorted,
-                (float)bg[0], (float)bg[1], (float)bg[2], image, img64, (float *)t_final, n_last,
-                n_contrib, n_iter, touched);
+        launch_raster_fwd_f32(n_tiles, width, height, tiles_x, row_lo, tile_ids, offsets, entries,
+                              (const float *)feat_sorted, (float)bg[0], (float)bg[1],
+                              (float)bg[2], image, img64, (float *)t_final, n_last, n_contrib,
+                              n_iter, touched, s);
     } else if (feat_dtype == ISG_F64) {
         if (touched)
             raster_fwd_kernel<double, true><<<n_tiles, THREADS, 0, s>>>(
@@ -401,8 +398,18 @@ extern "C" int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height,
         (const T *)feat_sorted, rs,                                                           \
         emit_off, (T)bg[0], (T)bg[1], (T)bg[2], (const T *)t_final, n_last,                  \
         (const DL *)dl_dimage, (T *)partials)
-    if (feat_dtype == ISG_F32 && dl_dtype == ISG_F32) ISG_BWD(float, float);
-    else if (feat_dtype == ISG_F32 && dl_dtype == ISG_F64) ISG_BWD(float, double);
+    if (feat_dtype == ISG_F32 && dl_dtype == ISG_F32)
+        launch_raster_bwd_f32<float>(n_tiles, width, height, tiles_x, row_lo, tile_ids, offsets,
+                                     entries, (const float *)feat_sorted, rs, emit_off,
+                                     (float)bg[0], (float)bg[1], (float)bg[2],
+                                     (const float *)t_final, n_last, (const float *)dl_dimage,
+                                     (float *)partials, s);
+    else if (feat_dtype == ISG_F32 && dl_dtype == ISG_F64)
+        launch_raster_bwd_f32<double>(n_tiles, width, height, tiles_x, row_lo, tile_ids, offsets,
+                                      entries, (const float *)feat_sorted, rs, emit_off,
+                                      (float)bg[0], (float)bg[1], (float)bg[2],
+                                      (const float *)t_final, n_last, (const double *)dl_dimage,
+                                      (float *)partials, s);
     else if (feat_dtype == ISG_F64 && dl_dtype == ISG_F32) ISG_BWD(double, float);
     else if (feat_dtype == ISG_F64 && dl_dtype == ISG_F64) ISG_BWD(double, double);
     else return (int)cudaErrorInvalidValue;
