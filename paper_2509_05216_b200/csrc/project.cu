@@ -276,8 +276,13 @@ __global__ void __launch_bounds__(256) chain_kernel(isg_params p, Cam cam, const
     }
     for (int j = 0; j < 4; j++) drot[4 * i + j] = (P)g.rot[j];
     dlogit[i] = (P)g.logit;
-    const int k3 = p.degree >= 1 ? 12 : 3;
-    for (int j = 0; j < k3; j++) dsh[(int64_t)k3 * i + j] = (P)g.sh[j];
+    if (p.degree >= 1) {
+#pragma unroll
+        for (int j = 0; j < 12; j++) dsh[12 * i + j] = (P)g.sh[j];
+    } else {
+#pragma unroll
+        for (int j = 0; j < 3; j++) dsh[3 * i + j] = (P)g.sh[j];
+    }
 }
 
 struct AdamF {
@@ -302,8 +307,11 @@ __device__ __forceinline__ void adam_f32(float &p, float &m, float &v, float g, 
 }
 
 // Fused: chain (flagged rows) + TrainStats (engine.py:508-515) + dense Adam
-// over the five groups (engine.py:524-536, optim.py:20-56).
-__global__ void __launch_bounds__(256) chain_adam_kernel(isg_train_state s, Cam cam,
+// over the five groups (engine.py:524-536, optim.py:20-56).  K3 = 3 (SH
+// degree 0) or 12 (degree 1) keeps every index static (no local memory); the
+// launch bound caps registers at 128 so 4 CTAs of 128 threads stay resident.
+template <int K3>
+__global__ void __launch_bounds__(128, 4) chain_adam_kernel(isg_train_state s, Cam cam,
                                                          const uint8_t *flag,
                                                          const double *grad2d, float lr0,
                                                          float lr1, float lr2, float lr3,
@@ -347,9 +355,9 @@ __global__ void __launch_bounds__(256) chain_adam_kernel(isg_train_state s, Cam 
                  (float)g.rot[j], lr2, c);
     adam_f32(s.opacity_logits[i], s.m_opacity_logits[i], s.v_opacity_logits[i],
              (float)g.logit, lr3, c);
-    const int k3 = s.degree >= 1 ? 12 : 3;
-    for (int j = 0; j < k3; j++) {
-        int64_t o = (int64_t)k3 * i + j;
+#pragma unroll
+    for (int j = 0; j < K3; j++) {
+        const int64_t o = (int64_t)K3 * i + j;
         adam_f32(s.sh[o], s.m_sh[o], s.v_sh[o], (float)g.sh[j], lr4, c);
     }
 }
@@ -471,8 +479,12 @@ extern "C" int isg_chain_adam(const isg_train_state *st, const isg_camera *cam,
     AdamF a{(float)c->b1, (float)c->omb1, (float)c->b2, (float)c->omb2,
             (float)c->bc1, (float)c->bc2, (float)c->eps};
     cudaStream_t s = (cudaStream_t)stream;
-    chain_adam_kernel<<<blocks_for(st->n, 256), 256, 0, s>>>(
-        *st, k, flag, grad2d, lr5[0], lr5[1], lr5[2], lr5[3], lr5[4], a, half_w, half_h);
+    if (st->degree >= 1)
+        chain_adam_kernel<12><<<blocks_for(st->n, 128), 128, 0, s>>>(
+            *st, k, flag, grad2d, lr5[0], lr5[1], lr5[2], lr5[3], lr5[4], a, half_w, half_h);
+    else
+        chain_adam_kernel<3><<<blocks_for(st->n, 128), 128, 0, s>>>(
+            *st, k, flag, grad2d, lr5[0], lr5[1], lr5[2], lr5[3], lr5[4], a, half_w, half_h);
     ISG_CHECK_LAUNCH();
     return 0;
 }

@@ -82,15 +82,15 @@ __device__ __forceinline__ float pair_alpha(float d0, float d1, const float4 &g4
     return a >= (1.0f / 255.0f) ? a : 0.0f;
 }
 
-// True when no pixel centre of the tile box [x0, x0+15] x [y0, y0+15] can
+// True when no pixel centre of the box [x0, x0+edge] x [y0, y0+edge] can
 // reach the skip threshold: the exact maximum exponent over the box (convex
 // quadratic: interior minimum or an edge minimum) is below thr by a margin
 // that bounds the float rounding of the per-pixel exponent.
-__device__ __forceinline__ bool tile_dead(const Staged &s, float x0, float y0) {
+__device__ __forceinline__ bool box_dead(const Staged &s, float x0, float y0, float edge) {
     const float thr = s.h.y;
     if (thr > 0.0f) return true;  // opacity < 1/255: every pair is skipped
     const float a = -2.0f * s.g.z, b = -s.g.w, c = -2.0f * s.h.x;
-    const float lx = x0 - s.g.x, hx = lx + 15.0f, ly = y0 - s.g.y, hy = ly + 15.0f;
+    const float lx = x0 - s.g.x, hx = lx + edge, ly = y0 - s.g.y, hy = ly + edge;
     if (lx <= 0.0f && hx >= 0.0f && ly <= 0.0f && hy >= 0.0f) return false;
     float q = __int_as_float(0x7f800000);
 #pragma unroll
@@ -107,7 +107,20 @@ __device__ __forceinline__ bool tile_dead(const Staged &s, float x0, float y0) {
     return -0.5f * q < thr - (1e-3f + 1e-5f * scale);
 }
 
+// Reachability mask of one staged entry over the four 8x8 quadrants of the
+// tile (bit q = quadrant (q & 1, q >> 1)); 0 when the whole tile is dead.
+__device__ __forceinline__ unsigned quad_mask(const Staged &st, float x0, float y0) {
+    if (box_dead(st, x0, y0, 15.0f)) return 0u;
+    unsigned m = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+        if (!box_dead(st, x0 + 8.0f * (q & 1), y0 + 8.0f * (q >> 1), 7.0f)) m |= 1u << q;
+    return m;
+}
+
 // ------------------------------------------------------------- forward ----
+// Warp w renders quadrant (w & 1, w >> 1) of the tile: lane (lx, ly) owns
+// pixels (lx, ly) and (lx, ly + 4) of the 8x8 quadrant.
 template <bool TOUCH>
 __global__ void __launch_bounds__(NT) fwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
@@ -115,16 +128,18 @@ __global__ void __launch_bounds__(NT) fwd_kernel(
     const float *__restrict__ feat, float bg0, float bg1, float bg2, void *image, int image_f64,
     float *__restrict__ t_final, int32_t *__restrict__ n_last, int32_t *__restrict__ n_contrib,
     int32_t *__restrict__ n_iter, int64_t *__restrict__ touched) {
-    __shared__ float4 sg[FB], sh[FB], sc[FB];
+    __shared__ float4 sgh[FB][2];
+    __shared__ float4 scol[FB];
     __shared__ int sj[FB];
     __shared__ int srank[TOUCH ? FB : 1];
-    __shared__ int wcount[NW];
+    __shared__ unsigned char slist[NW][FB];
+    __shared__ int qcnt[NW][NW];
     const int tl = blockIdx.x;
     const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
     const int ty = tid / tiles_x, tx = tid - ty * tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int px = tx * 16 + (threadIdx.x & 15);
-    const int py0 = ty * 16 + (threadIdx.x >> 4), py1 = py0 + 8;
+    const int px = tx * 16 + (warp & 1) * 8 + (lane & 7);
+    const int py0 = ty * 16 + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
     const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
     const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
     const float x0 = (float)(tx * 16), y0 = (float)(ty * 16);
@@ -136,36 +151,40 @@ __global__ void __launch_bounds__(NT) fwd_kernel(
     for (int base = 0; base < n_ent; base += FB) {
         if (__syncthreads_count(done0 && done1) == NT) break;
         const int j = base + threadIdx.x;
-        bool live = false;
-        Staged st;
-        int rank = 0;
+        unsigned mask = 0u;
         if (j < n_ent) {
-            rank = entries[e0 + j];
-            st = stage(feat, rank);
-            live = !tile_dead(st, x0, y0);
+            const int rank = entries[e0 + j];
+            const Staged st = stage(feat, rank);
+            mask = quad_mask(st, x0, y0);
+            sgh[threadIdx.x][0] = st.g;
+            sgh[threadIdx.x][1] = st.h;
+            scol[threadIdx.x] = st.c;
+            sj[threadIdx.x] = j;
+            if (TOUCH) srank[threadIdx.x] = rank;
         }
-        const unsigned bal = __ballot_sync(FULL, live);
-        if (lane == 0) wcount[warp] = __popc(bal);
-        __syncthreads();
-        int off = 0, total = 0;
+        unsigned bal[NW];
 #pragma unroll
-        for (int w = 0; w < NW; w++) {
-            const int c = wcount[w];
-            off += w < warp ? c : 0;
-            total += c;
-        }
-        if (live) {
-            const int pos = off + __popc(bal & ((1u << lane) - 1u));
-            sg[pos] = st.g;
-            sh[pos] = st.h;
-            sc[pos] = st.c;
-            sj[pos] = j;
-            if (TOUCH) srank[pos] = rank;
+        for (int q = 0; q < NW; q++) {
+            bal[q] = __ballot_sync(FULL, (mask >> q) & 1u);
+            if (lane == 0) qcnt[q][warp] = __popc(bal[q]);
         }
         __syncthreads();
+        const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int q = 0; q < NW; q++) {
+            if ((mask >> q) & 1u) {
+                int off = 0;
+#pragma unroll
+                for (int w = 0; w < NW; w++) off += w < warp ? qcnt[q][w] : 0;
+                slist[q][off + __popc(bal[q] & lt)] = (unsigned char)threadIdx.x;
+            }
+        }
+        __syncthreads();
+        const int total = qcnt[warp][0] + qcnt[warp][1] + qcnt[warp][2] + qcnt[warp][3];
         for (int k = 0; k < total; k++) {
-            if (done0 && done1) break;
-            const float4 g4 = sg[k], h4 = sh[k];
+            if (__all_sync(FULL, done0 && done1)) break;
+            const int slot = slist[warp][k];
+            const float4 g4 = sgh[slot][0], h4 = sgh[slot][1];
             const float d0 = fpx - g4.x;
             if (!done0) {
                 float gw;
@@ -174,17 +193,17 @@ __global__ void __launch_bounds__(NT) fwd_kernel(
                     const float test = t0 * (1.0f - a);
                     if (test < 1e-4f) {
                         done0 = true;
-                        it0 = sj[k] + 1;
+                        it0 = sj[slot] + 1;
                     } else {
-                        const float4 c = sc[k];
+                        const float4 c = scol[slot];
                         const float w = a * t0;
                         r0 = fmaf(c.x, w, r0);
                         g0 = fmaf(c.y, w, g0);
                         b0 = fmaf(c.z, w, b0);
                         t0 = test;
-                        last0 = sj[k] + 1;
+                        last0 = sj[slot] + 1;
                         cnt0++;
-                        if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[k]], 1ull);
+                        if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
                     }
                 }
             }
@@ -195,17 +214,17 @@ __global__ void __launch_bounds__(NT) fwd_kernel(
                     const float test = t1 * (1.0f - a);
                     if (test < 1e-4f) {
                         done1 = true;
-                        it1 = sj[k] + 1;
+                        it1 = sj[slot] + 1;
                     } else {
-                        const float4 c = sc[k];
+                        const float4 c = scol[slot];
                         const float w = a * t1;
                         r1 = fmaf(c.x, w, r1);
                         g1 = fmaf(c.y, w, g1);
                         b1 = fmaf(c.z, w, b1);
                         t1 = test;
-                        last1 = sj[k] + 1;
+                        last1 = sj[slot] + 1;
                         cnt1++;
-                        if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[k]], 1ull);
+                        if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
                     }
                 }
             }
@@ -312,18 +331,21 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
     const int64_t *__restrict__ emit_off, float bg0, float bg1, float bg2,
     const float *__restrict__ t_final, const int32_t *__restrict__ n_last,
     const DL *__restrict__ dl, float *__restrict__ partials) {
-    __shared__ float4 sg[BB], sh[BB], sc[BB];
-    __shared__ int sj[BB];
-    __shared__ int64_t sslot[BB];
-    __shared__ float sred[NW][BB][9];
-    __shared__ int smax[NW];
-    __shared__ int stotal;
+    __shared__ float4 sgh[FB][2];
+    __shared__ float4 scol[FB];
+    __shared__ int sj[FB];
+    __shared__ int64_t sslot[FB];
+    __shared__ unsigned char smask[FB];
+    __shared__ unsigned char slist[NW][FB];
+    __shared__ int qcnt[NW][NW];
+    __shared__ float sred[NW][FB][9];
+    __shared__ int wmax[NW];
     const int tl = blockIdx.x;
     const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
     const int ty = tid / tiles_x, tx = tid - ty * tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int px = tx * 16 + (threadIdx.x & 15);
-    const int py0 = ty * 16 + (threadIdx.x >> 4), py1 = py0 + 8;
+    const int px = tx * 16 + (warp & 1) * 8 + (lane & 7);
+    const int py0 = ty * 16 + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
     const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
     const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
     const float x0 = (float)(tx * 16), y0 = (float)(ty * 16);
@@ -353,55 +375,71 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
     int m = max(last0, last1);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
-    if (lane == 0) smax[warp] = m;
+    if (lane == 0) wmax[warp] = m;
     __syncthreads();
     int max_last = 0;
 #pragma unroll
-    for (int w = 0; w < NW; w++) max_last = max(max_last, smax[w]);
+    for (int w = 0; w < NW; w++) max_last = max(max_last, wmax[w]);
 
-    for (int end = n_ent; end > 0; end -= BB) {
-        const int start = max(end - BB, 0);
+    // Batches [start, end) walked back to front; quadrant q only sees entries
+    // j < wmax[q] (no pixel of the quadrant composited anything later).
+    for (int end = n_ent; end > 0; end -= FB) {
+        const int start = max(end - FB, 0);
         __syncthreads();
-        if (warp == 0) {
-            const int j = start + lane;
-            bool live = false;
-            Staged st;
-            int64_t slot = 0;
-            if (j < end) {
-                const int rank = entries[e0 + j];
-                if (emit_off) {
-                    const int4 rc = rect_sorted[rank];
-                    slot = emit_off[rank] + (int64_t)(ty - max(rc.y, row_lo)) * (rc.z - rc.x + 1) +
-                           (tx - rc.x);
-                } else {
-                    slot = (int64_t)e0 + j;
-                }
-                if (j < max_last) {
-                    st = stage(feat, rank);
-                    live = !tile_dead(st, x0, y0);
-                }
-                if (!live) {
-                    float *dst = partials + 9 * slot;
+        const int j = start + (int)threadIdx.x;
+        unsigned mask = 0u;
+        if (j < end) {
+            const int rank = entries[e0 + j];
+            int64_t slot;
+            if (emit_off) {
+                const int4 rc = rect_sorted[rank];
+                slot = emit_off[rank] + (int64_t)(ty - max(rc.y, row_lo)) * (rc.z - rc.x + 1) +
+                       (tx - rc.x);
+            } else {
+                slot = (int64_t)e0 + j;
+            }
+            if (j < max_last) {
+                const Staged st = stage(feat, rank);
+                mask = quad_mask(st, x0, y0);
 #pragma unroll
-                    for (int q = 0; q < 9; q++) dst[q] = 0.0f;
-                }
+                for (int q = 0; q < NW; q++)
+                    if (j >= wmax[q]) mask &= ~(1u << q);
+                sgh[threadIdx.x][0] = st.g;
+                sgh[threadIdx.x][1] = st.h;
+                scol[threadIdx.x] = st.c;
             }
-            const unsigned bal = __ballot_sync(FULL, live);
-            if (live) {
-                const int pos = __popc(bal & ((1u << lane) - 1u));
-                sg[pos] = st.g;
-                sh[pos] = st.h;
-                sc[pos] = st.c;
-                sj[pos] = j;
-                sslot[pos] = slot;
+            sj[threadIdx.x] = j;
+            sslot[threadIdx.x] = slot;
+            if (mask == 0u) {
+                float *dst = partials + 9 * slot;
+#pragma unroll
+                for (int q = 0; q < 9; q++) dst[q] = 0.0f;
             }
-            if (lane == 0) stotal = __popc(bal);
+        }
+        smask[threadIdx.x] = (unsigned char)mask;
+        unsigned bal[NW];
+#pragma unroll
+        for (int q = 0; q < NW; q++) {
+            bal[q] = __ballot_sync(FULL, (mask >> q) & 1u);
+            if (lane == 0) qcnt[q][warp] = __popc(bal[q]);
         }
         __syncthreads();
-        const int total = stotal;
+        const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int q = 0; q < NW; q++) {
+            if ((mask >> q) & 1u) {
+                int off = 0;
+#pragma unroll
+                for (int w = 0; w < NW; w++) off += w < warp ? qcnt[q][w] : 0;
+                slist[q][off + __popc(bal[q] & lt)] = (unsigned char)threadIdx.x;
+            }
+        }
+        __syncthreads();
+        const int total = qcnt[warp][0] + qcnt[warp][1] + qcnt[warp][2] + qcnt[warp][3];
         for (int k = total - 1; k >= 0; k--) {
-            const float4 g4 = sg[k], h4 = sh[k];
-            const int jj = sj[k];
+            const int slot = slist[warp][k];
+            const float4 g4 = sgh[slot][0], h4 = sgh[slot][1];
+            const int jj = sj[slot];
             float v[9];
 #pragma unroll
             for (int q = 0; q < 9; q++) v[q] = 0.0f;
@@ -413,7 +451,7 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
                 const float a = pair_alpha(d0, d1, g4, h4, gw);
                 if (a > 0.0f) {
                     act = true;
-                    pair_grad(a, gw, d0, d1, g4, h4, sc[k], wr0, wg0, wb0, T0, sr0, sg0, sb0, v);
+                    pair_grad(a, gw, d0, d1, g4, h4, scol[slot], wr0, wg0, wb0, T0, sr0, sg0, sb0, v);
                 }
             }
             if (jj < last1) {
@@ -422,18 +460,24 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
                 const float a = pair_alpha(d0, d1, g4, h4, gw);
                 if (a > 0.0f) {
                     act = true;
-                    pair_grad(a, gw, d0, d1, g4, h4, sc[k], wr1, wg1, wb1, T1, sr1, sg1, sb1, v);
+                    pair_grad(a, gw, d0, d1, g4, h4, scol[slot], wr1, wg1, wb1, T1, sr1, sg1, sb1, v);
                 }
             }
             float y = 0.0f;
             if (__any_sync(FULL, act)) y = bfly9(v, lane);
-            if (my_slot >= 0) sred[warp][k][my_slot] = y;
+            if (my_slot >= 0) sred[warp][slot][my_slot] = y;
         }
         __syncthreads();
-        for (int idx = threadIdx.x; idx < total * 9; idx += NT) {
-            const int k = idx / 9, q = idx - k * 9;
-            const float acc = ((sred[0][k][q] + sred[1][k][q]) + sred[2][k][q]) + sred[3][k][q];
-            partials[9 * sslot[k] + q] = acc;
+        // fixed-order fold over the quadrants that saw the entry
+        for (int idx = threadIdx.x; idx < (end - start) * 9; idx += NT) {
+            const int s = idx / 9, q = idx - s * 9;
+            const unsigned mk = smask[s];
+            if (mk == 0u) continue;
+            float acc = 0.0f;
+#pragma unroll
+            for (int w = 0; w < NW; w++)
+                if ((mk >> w) & 1u) acc += sred[w][s][q];
+            partials[9 * sslot[s] + q] = acc;
         }
     }
 }
