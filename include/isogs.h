@@ -141,6 +141,27 @@ int isg_loss_l1_dssim(void *workspace, size_t *ws_bytes, int32_t dtype, int32_t 
                       int32_t width, const void *image, const void *ref, int32_t ref_u8,
                       double lambda_dssim, void *grad, double *loss_dev, void *stream);
 
+/* Block-partial array sizes of the loss (16x16 centre / pixel blocks over
+ * the full image). */
+int isg_loss_partials_size(int32_t height, int32_t width, int32_t *n_ssim, int32_t *n_l1);
+
+/* Loss and gradient for the pixel rows [row0, row1) of a band (row0 a
+ * multiple of 16; row1 a multiple of 16 or H).  image points at global row
+ * img_row0 and must cover rows [row0-16, row1+10) clipped to [0, H); ref is
+ * the full (H,W,3) ground truth.  grad receives rows [row0, row1) (pointer at
+ * row0).  The band's own 16x16 block partials are written into the
+ * full-image arrays part_ssim / part_l1 (other entries untouched), so
+ * summing the bands' arrays and calling isg_loss_finish gives exactly the
+ * single-band loss. */
+int isg_loss_rows(void *workspace, size_t *ws_bytes, int32_t dtype, int32_t height,
+                  int32_t width, int32_t row0, int32_t row1, const void *image, int32_t img_row0,
+                  const void *ref, int32_t ref_u8, double lambda_dssim, void *grad,
+                  double *part_ssim, double *part_l1, void *stream);
+
+/* Fixed-order final sum of the block partials into *loss_dev. */
+int isg_loss_finish(int32_t height, int32_t width, double lambda_dssim, const double *part_ssim,
+                    const double *part_l1, double *loss_dev, void *stream);
+
 /* Mean SSIM over valid centres (metrics.py:105-132) of (H,W,C) float64
  * images, into *out_dev. */
 int isg_ssim(void *workspace, size_t *ws_bytes, int32_t height, int32_t width,
@@ -163,12 +184,73 @@ int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t ti
                    void *partials, void *stream);
 
 /* Ordered fold (_reduce_scratch, _kernels.py:398-411): for rank r < m sum its
- * subtotal slots [emit_off[r], emit_off[r+1]) in ascending tile order in
- * float64 and write grad2d[order[r]] (9 doubles).  If grad_norm is non-NULL
- * it receives hypot(dmean) at row order[r] (rasterizer.py:397). */
+ * subtotal slots [emit_off[r], emit_off[r+1]) in float64 and write
+ * grad2d[order[r]] (9 doubles).  canon_rows <= 0: the reference's single-level
+ * fold in ascending tile order.  canon_rows > 0: the canonical two-level fold
+ * used by the training step -- tiles ascending inside each block of
+ * canon_rows tile rows, then block sums ascending -- whose grouping does not
+ * depend on the GPU count (needs rect_sorted and the band rows).  If
+ * grad_norm is non-NULL it receives hypot(dmean) at row order[r]
+ * (rasterizer.py:397). */
 int isg_reduce_ordered(int32_t feat_dtype, int64_t m, const int64_t *emit_off,
-                       const void *partials, const int32_t *order, double *grad2d,
+                       const void *partials, const int32_t *order, const int32_t *rect_sorted,
+                       int32_t row_lo, int32_t row_hi, int32_t canon_rows, double *grad2d,
                        double *grad_norm, void *stream);
+
+/* ---- multi-GPU data plane (distributed.py:127-226, engine.py:201-237,
+ * 499-507), row-band pixel partition.  band_rows / shard_start are HOST
+ * arrays of n+1 boundaries (n <= 64). ---- */
+
+/* Exclusive scan of n int64 counts: off[0..n], *total = off[n] (device). */
+int isg_scan_i64(void *workspace, size_t *ws_bytes, int64_t n, const int64_t *cnt, int64_t *off,
+                 int64_t *total, void *stream);
+
+/* Per visible shard row: number of bands its rect overlaps and the first one
+ * (_route_mask, _kernels.py:378-394, for row bands). */
+int isg_route_count(int64_t n, const uint8_t *flag, const int32_t *rect, const int32_t *band_rows,
+                    int32_t n_bands, int64_t *cnt, int32_t *dlo, void *stream);
+
+/* (band, row) pairs in row order at off[row] (then stably sorted by band). */
+int isg_route_emit(int64_t n, const int64_t *off, const int32_t *dlo, uint32_t *keys,
+                   int32_t *vals, void *stream);
+
+/* Pack the routed rows into 80-byte splat records (20 x int32): depth key,
+ * global id (id_base + row), rect, 12 raster features (float32). */
+int isg_route_gather(int64_t s, const int32_t *rows, const uint64_t *key, const int32_t *rect,
+                     const float *feat, int64_t id_base, int32_t *records, void *stream);
+
+/* Unpack received splat records into SoA arrays. */
+int isg_records_unpack(int64_t r, const int32_t *records, uint64_t *key, int32_t *gid,
+                       int32_t *rect, float *feat, void *stream);
+
+/* Number of canonical blocks (canon_rows tile rows) each rank's clipped rect
+ * spans inside [row_lo, row_hi). */
+int isg_block_count(int64_t m, const int32_t *rect_sorted, int32_t row_lo, int32_t row_hi,
+                    int32_t canon_rows, int64_t *nb, void *stream);
+
+/* Per rank: fold its subtotals per canonical block (float64) into records at
+ * rec_off[r] + b with the owner shard (of gid[order[r]]), owner-local row and
+ * the 9 block sums.  The owner's in-order sum of these records equals the
+ * canonical two-level fold of isg_reduce_ordered bit for bit. */
+int isg_block_fold(int32_t feat_dtype, int64_t m, const int64_t *emit_off, const void *partials,
+                   const int32_t *rect_sorted, int32_t row_lo, int32_t row_hi,
+                   int32_t canon_rows, const int64_t *rec_off, const int32_t *order,
+                   const int32_t *gid, const int64_t *shard_start, int32_t n_shards,
+                   uint32_t *rec_owner, int32_t *rec_row, double *rec_val, void *stream);
+
+/* Pack block records (in idx order) into 80-byte gradient records
+ * [row, 0, 9 doubles]. */
+int isg_grad_gather(int64_t s, const int32_t *idx, const int32_t *rec_row, const double *rec_val,
+                    int32_t *out, void *stream);
+
+/* Keys (owner-local rows) and identity values of received gradient records. */
+int isg_grad_rows(int64_t r, const int32_t *records, uint32_t *rows, int32_t *idx, void *stream);
+
+/* Owner fold (reduce_gradients_fused, distributed.py:178-226): per shard row
+ * the records seg_off[i]..seg_off[i+1] (perm into records, arrival order) are
+ * summed in float64 into grad2d[i]; rows without records are left untouched. */
+int isg_owner_fold(int64_t n_rows, const int32_t *seg_off, const int32_t *perm,
+                   const int32_t *records, double *grad2d, void *stream);
 
 /* 2D -> 3D chain rule (_chain_kernel, _kernels.py:415-634) for rows with
  * flag != 0; grad2d is (n, 9) float64.  Outputs (parameter dtype, same

@@ -77,7 +77,22 @@ SIGNATURES = {
     "isg_ssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _P, _P],
     "isg_raster_bwd": [_I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P,
                        _P, _P, _P, _I32, _P, _P],
-    "isg_reduce_ordered": [_I32, _I64, _P, _P, _P, _P, _P, _P],
+    "isg_reduce_ordered": [_I32, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P],
+    "isg_loss_partials_size": [_I32, _I32, _P, _P],
+    "isg_loss_rows": [_P, _SZ, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _I32, _D, _P, _P, _P,
+                      _P],
+    "isg_loss_finish": [_I32, _I32, _D, _P, _P, _P, _P],
+    "isg_scan_i64": [_P, _SZ, _I64, _P, _P, _P, _P],
+    "isg_route_count": [_I64, _P, _P, _P, _I32, _P, _P, _P],
+    "isg_route_emit": [_I64, _P, _P, _P, _P, _P],
+    "isg_route_gather": [_I64, _P, _P, _P, _P, _I64, _P, _P],
+    "isg_records_unpack": [_I64, _P, _P, _P, _P, _P, _P],
+    "isg_block_count": [_I64, _P, _I32, _I32, _I32, _P, _P],
+    "isg_block_fold": [_I32, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _I32, _P, _P,
+                       _P, _P],
+    "isg_grad_gather": [_I64, _P, _P, _P, _P, _P],
+    "isg_grad_rows": [_I64, _P, _P, _P, _P],
+    "isg_owner_fold": [_I64, _P, _P, _P, _P, _P],
     "isg_chain": [ctypes.POINTER(Params_t), ctypes.POINTER(Camera_t), _P, _P, _P, _P, _P, _P,
                   _P, _P],
     "isg_adam": [_I32, _I64, _P, _P, _P, _P, ctypes.POINTER(AdamConsts_t), _P],

@@ -30,6 +30,7 @@ SOURCES = {
     "raster_f64.cu": ["-fmad=false"],
     "raster_f32.cu": ["-ftz=true"],
     "loss.cu": [],
+    "dist.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -8,8 +8,12 @@
 //   2. adjoint -- per pixel: the adjoint correlation of f0..f2 (zero outside
 //                 the valid region, like _corr_adjoint), combined with the L1
 //                 sign term into dL/dimage.
-// Loss partials are reduced per block and then in a fixed block order, so the
-// scalar is deterministic.  Compute type follows the image dtype.
+// Both passes work on a band of image rows [row0, row1) (multiples of 16), so
+// a GPU that renders one row band computes its pixels' gradient from its band
+// plus a halo (16 rows above, 10 below).  Loss partials are written per 16x16
+// block into arrays indexed over the FULL image; every block is owned by
+// exactly one band, and the final sum runs over the full arrays in a fixed
+// order -- so the loss is identical for any band split.
 #include "common.cuh"
 
 namespace isg {
@@ -55,19 +59,22 @@ __device__ __forceinline__ double block_sum(double v, double *scratch) {
     return s;
 }
 
-// Pass 1.  fmap layout: [field f][channel c][hc][wc]; NULL for SSIM only.
+// Pass 1 over centre block rows by_base + blockIdx.y.  img/ref are indexed by
+// global row (img points at global row img_row0).  fmap (may be NULL) holds
+// centre rows from fmap_row0: layout [field][channel][rows][wc].  Partials are
+// written for centre blocks whose first row lies in [own0, own1).
 template <typename T, typename IN, typename R>
-__global__ void __launch_bounds__(256) ssim_fields_kernel(int H, int W, int C,
-                                                          const IN *__restrict__ img,
-                                                          const R *__restrict__ ref,
-                                                          T *__restrict__ fmap,
-                                                          double *__restrict__ part) {
+__global__ void __launch_bounds__(256) ssim_fields_kernel(
+    int H, int W, int C, const IN *__restrict__ img, int img_row0, const R *__restrict__ ref,
+    T *__restrict__ fmap, int fmap_row0, int fmap_rows, int by_base, int own0, int own1,
+    double *__restrict__ part) {
     __shared__ T sx[LP][LP + 1], sy[LP][LP + 1];
     __shared__ T hs[5][LP][LT];
     __shared__ double red[8];
     const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;  // == pow(0.01, 2), pow(0.03, 2)
     const int hc = H - 10, wc = W - 10;
-    const int cx0 = blockIdx.x * LT, cy0 = blockIdx.y * LT;
+    const int by = by_base + blockIdx.y;
+    const int cx0 = blockIdx.x * LT, cy0 = by * LT;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int ccx = cx0 + tx, ccy = cy0 + ty;
     const bool valid = ccx < wc && ccy < hc;
@@ -78,9 +85,8 @@ __global__ void __launch_bounds__(256) ssim_fields_kernel(int H, int W, int C,
             const int y = cy0 + r, x = cx0 + q;
             T vx = 0, vy = 0;
             if (y < H && x < W) {
-                const int64_t o = ((int64_t)y * W + x) * C + c;
-                vx = (T)img[o];
-                vy = gt_val<T, R>(ref[o]);
+                vx = (T)img[((int64_t)(y - img_row0) * W + x) * C + c];
+                vy = gt_val<T, R>(ref[((int64_t)y * W + x) * C + c]);
             }
             sx[r][q] = vx;
             sy[r][q] = vy;
@@ -127,8 +133,8 @@ __global__ void __launch_bounds__(256) ssim_fields_kernel(int H, int W, int C,
                 const T d_xy = ((T)2 * p) / b2;
                 const T f1 = (T)2 * d_sigma, f2 = d_xy;
                 const T f0 = d_mu - f1 * mx - f2 * my;
-                const int64_t plane = (int64_t)hc * wc;
-                const int64_t o = (int64_t)ccy * wc + ccx;
+                const int64_t plane = (int64_t)fmap_rows * wc;
+                const int64_t o = (int64_t)(ccy - fmap_row0) * wc + ccx;
                 fmap[(0 * C + c) * plane + o] = f0;
                 fmap[(1 * C + c) * plane + o] = f1;
                 fmap[(2 * C + c) * plane + o] = f2;
@@ -137,32 +143,34 @@ __global__ void __launch_bounds__(256) ssim_fields_kernel(int H, int W, int C,
         __syncthreads();
     }
     const double s = block_sum(pq_acc, red);
-    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = s;
+    if (threadIdx.x == 0 && cy0 >= own0 && cy0 < own1) part[by * gridDim.x + blockIdx.x] = s;
 }
 
-// Pass 2: dL/dimage = sign(x-y)(1-lam)/n + gscale * (A f0 + x A f1 + y A f2).
+// Pass 2 over pixel block rows by_base + blockIdx.y:
+// dL/dimage = sign(x-y)(1-lam)/n + gscale * (A f0 + x A f1 + y A f2).
+// grad is indexed by global row from grad_row0.
 template <typename T, typename IN, typename R>
-__global__ void __launch_bounds__(256) ssim_adjoint_kernel(int H, int W, const IN *__restrict__ img,
-                                                           const R *__restrict__ ref,
-                                                           const T *__restrict__ fmap,
-                                                           IN *__restrict__ grad, T l1_scale,
-                                                           T gscale, double *__restrict__ part) {
+__global__ void __launch_bounds__(256) ssim_adjoint_kernel(
+    int H, int W, const IN *__restrict__ img, int img_row0, const R *__restrict__ ref,
+    const T *__restrict__ fmap, int fmap_row0, int fmap_rows, IN *__restrict__ grad,
+    int grad_row0, int row1, int by_base, T l1_scale, T gscale, double *__restrict__ part) {
     __shared__ T sf[3][LP][LP + 1];
     __shared__ T hs[3][LP][LT];
     __shared__ double red[8];
     const int hc = H - 10, wc = W - 10;
-    const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
+    const int by = by_base + blockIdx.y;
+    const int x0 = blockIdx.x * LT, y0 = by * LT;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int x = x0 + tx, y = y0 + ty;
-    const bool inside = x < W && y < H;
-    const int64_t plane = (int64_t)hc * wc;
+    const bool inside = x < W && y < H && y < row1;
+    const int64_t plane = (int64_t)fmap_rows * wc;
     double l1_acc = 0.0;
     for (int c = 0; c < 3; c++) {
         for (int idx = threadIdx.x; idx < LP * LP; idx += 256) {
             const int r = idx / LP, q = idx - r * LP;
             const int cy = y0 - 10 + r, cx = x0 - 10 + q;
             const bool ok = cy >= 0 && cy < hc && cx >= 0 && cx < wc;
-            const int64_t o = (int64_t)cy * wc + cx;
+            const int64_t o = (int64_t)(cy - fmap_row0) * wc + cx;
 #pragma unroll
             for (int f = 0; f < 3; f++) sf[f][r][q] = ok ? fmap[(f * 3 + c) * plane + o] : (T)0;
         }
@@ -187,18 +195,18 @@ __global__ void __launch_bounds__(256) ssim_adjoint_kernel(int H, int W, const I
                 g1 += w * hs[1][ty + i][tx];
                 g2 += w * hs[2][ty + i][tx];
             }
-            const int64_t o = ((int64_t)y * W + x) * 3 + c;
-            const T xv = (T)img[o], yv = gt_val<T, R>(ref[o]);
+            const T xv = (T)img[((int64_t)(y - img_row0) * W + x) * 3 + c];
+            const T yv = gt_val<T, R>(ref[((int64_t)y * W + x) * 3 + c]);
             const T d = xv - yv;
             const T sg = d > (T)0 ? (T)1 : (d < (T)0 ? (T)-1 : (T)0);
             const T g = g0 + xv * g1 + yv * g2;
-            grad[o] = (IN)(sg * l1_scale + gscale * g);
+            grad[((int64_t)(y - grad_row0) * W + x) * 3 + c] = (IN)(sg * l1_scale + gscale * g);
             l1_acc += (double)fabs(d);
         }
         __syncthreads();
     }
     const double s = block_sum(l1_acc, red);
-    if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = s;
+    if (threadIdx.x == 0) part[by * gridDim.x + blockIdx.x] = s;
 }
 
 // Fixed-order final reduction (one block): loss = (1-lam) L1 + lam (1 - SSIM).
@@ -222,61 +230,144 @@ __global__ void loss_finish_kernel(int n_ssim, const double *__restrict__ ssim_p
 
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-template <typename T, typename R>
-int loss_impl(void *ws, size_t *ws_bytes, int H, int W, const T *img, const R *ref, double lam,
-              T *grad, double *loss_dev, cudaStream_t s) {
+struct LossGrid {
+    dim3 gf, ga;
+    int fby0, fby1;  // centre block rows computed (incl. the halo block above)
+    int aby0, aby1;  // pixel block rows
+    int fmap_row0, fmap_rows;
+};
+
+inline LossGrid loss_grid(int H, int W, int row0, int row1) {
+    LossGrid g;
     const int hc = H - 10, wc = W - 10;
-    dim3 gf((wc + LT - 1) / LT, (hc + LT - 1) / LT), ga((W + LT - 1) / LT, (H + LT - 1) / LT);
-    const size_t nf = gf.x * gf.y, na = ga.x * ga.y;
-    const size_t need = al(sizeof(T) * 9 * (size_t)hc * wc) + al(8 * nf) + al(8 * na);
+    const int nfy = (hc + LT - 1) / LT;
+    g.gf = dim3((wc + LT - 1) / LT, nfy);
+    g.ga = dim3((W + LT - 1) / LT, (H + LT - 1) / LT);
+    g.fby0 = row0 / LT > 0 ? row0 / LT - 1 : 0;
+    g.fby1 = (row1 + LT - 1) / LT < nfy ? (row1 + LT - 1) / LT : nfy;
+    if (g.fby1 < g.fby0) g.fby1 = g.fby0;
+    g.aby0 = row0 / LT;
+    g.aby1 = (row1 + LT - 1) / LT;
+    g.fmap_row0 = g.fby0 * LT;
+    g.fmap_rows = (g.fby1 - g.fby0) * LT;
+    return g;
+}
+
+template <typename T, typename R>
+int loss_rows_impl(void *ws, size_t *ws_bytes, int H, int W, int row0, int row1, const T *img,
+                   int img_row0, const R *ref, double lam, T *grad, double *part_ssim,
+                   double *part_l1, cudaStream_t s) {
+    const LossGrid g = loss_grid(H, W, row0, row1);
+    const int wc = W - 10;
+    const size_t need = al(sizeof(T) * 9 * (size_t)(g.fmap_rows > 0 ? g.fmap_rows : 1) * wc);
     if (!ws) {
         *ws_bytes = need;
         return 0;
     }
     if (*ws_bytes < need) return (int)cudaErrorInvalidValue;
     T *fmap = (T *)ws;
-    double *pf = (double *)((char *)ws + al(sizeof(T) * 9 * (size_t)hc * wc));
-    double *pa = (double *)((char *)pf + al(8 * nf));
-    ssim_fields_kernel<T, T, R><<<gf, 256, 0, s>>>(H, W, 3, img, ref, fmap, pf);
-    ISG_CHECK_LAUNCH();
-    const double n_pix = 3.0 * H * W, n_centers = 3.0 * hc * wc;
-    ssim_adjoint_kernel<T, T, R><<<ga, 256, 0, s>>>(H, W, img, ref, fmap, grad,
-                                                 (T)((1.0 - lam) / n_pix), (T)(-lam / n_centers),
-                                                 pa);
-    ISG_CHECK_LAUNCH();
-    loss_finish_kernel<<<1, 256, 0, s>>>((int)nf, pf, (int)na, pa, n_pix, n_centers, lam,
-                                         loss_dev);
-    ISG_CHECK_LAUNCH();
+    const double n_pix = 3.0 * H * W, n_centers = 3.0 * (H - 10) * (W - 10);
+    if (g.fby1 > g.fby0) {
+        dim3 grid(g.gf.x, g.fby1 - g.fby0);
+        ssim_fields_kernel<T, T, R><<<grid, 256, 0, s>>>(H, W, 3, img, img_row0, ref, fmap,
+                                                         g.fmap_row0, g.fmap_rows, g.fby0, row0,
+                                                         row1, part_ssim);
+        ISG_CHECK_LAUNCH();
+    }
+    if (g.aby1 > g.aby0) {
+        dim3 grid(g.ga.x, g.aby1 - g.aby0);
+        ssim_adjoint_kernel<T, T, R><<<grid, 256, 0, s>>>(
+            H, W, img, img_row0, ref, fmap, g.fmap_row0, g.fmap_rows, grad, row0, row1, g.aby0,
+            (T)((1.0 - lam) / n_pix), (T)(-lam / n_centers), part_l1);
+        ISG_CHECK_LAUNCH();
+    }
     return 0;
+}
+
+template <typename T>
+int loss_rows_dispatch(void *ws, size_t *ws_bytes, int H, int W, int row0, int row1,
+                       const void *img, int img_row0, const void *ref, int ref_u8, double lam,
+                       void *grad, double *ps, double *pl, cudaStream_t s) {
+    if (ref_u8)
+        return loss_rows_impl<T, uint8_t>(ws, ws_bytes, H, W, row0, row1, (const T *)img,
+                                          img_row0, (const uint8_t *)ref, lam, (T *)grad, ps, pl,
+                                          s);
+    return loss_rows_impl<T, T>(ws, ws_bytes, H, W, row0, row1, (const T *)img, img_row0,
+                                (const T *)ref, lam, (T *)grad, ps, pl, s);
 }
 
 }  // namespace isg
 
 using namespace isg;
 
+extern "C" int isg_loss_partials_size(int32_t height, int32_t width, int32_t *n_ssim,
+                                      int32_t *n_l1) {
+    if (height < 11 || width < 11 || !n_ssim || !n_l1) return (int)cudaErrorInvalidValue;
+    const LossGrid g = loss_grid(height, width, 0, height);
+    *n_ssim = (int32_t)(g.gf.x * g.gf.y);
+    *n_l1 = (int32_t)(g.ga.x * g.ga.y);
+    return 0;
+}
+
+extern "C" int isg_loss_rows(void *workspace, size_t *ws_bytes, int32_t dtype, int32_t height,
+                             int32_t width, int32_t row0, int32_t row1, const void *image,
+                             int32_t img_row0, const void *ref, int32_t ref_u8,
+                             double lambda_dssim, void *grad, double *part_ssim, double *part_l1,
+                             void *stream) {
+    if (!ws_bytes || height < 11 || width < 11 || lambda_dssim < 0.0 || lambda_dssim > 1.0 ||
+        row0 < 0 || row1 > height || row0 > row1 || row0 % LT != 0 ||
+        (row1 % LT != 0 && row1 != height))
+        return (int)cudaErrorInvalidValue;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == ISG_F32)
+        return loss_rows_dispatch<float>(workspace, ws_bytes, height, width, row0, row1, image,
+                                         img_row0, ref, ref_u8, lambda_dssim, grad, part_ssim,
+                                         part_l1, s);
+    if (dtype == ISG_F64)
+        return loss_rows_dispatch<double>(workspace, ws_bytes, height, width, row0, row1, image,
+                                          img_row0, ref, ref_u8, lambda_dssim, grad, part_ssim,
+                                          part_l1, s);
+    return (int)cudaErrorInvalidValue;
+}
+
+extern "C" int isg_loss_finish(int32_t height, int32_t width, double lambda_dssim,
+                               const double *part_ssim, const double *part_l1, double *loss_dev,
+                               void *stream) {
+    int32_t nf = 0, na = 0;
+    int e = isg_loss_partials_size(height, width, &nf, &na);
+    if (e) return e;
+    const double n_pix = 3.0 * height * width, n_centers = 3.0 * (height - 10) * (width - 10);
+    loss_finish_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(nf, part_ssim, na, part_l1, n_pix,
+                                                            n_centers, lambda_dssim, loss_dev);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+// Whole image: loss_rows(0, H) + finish, partial arrays in the workspace.
 extern "C" int isg_loss_l1_dssim(void *workspace, size_t *ws_bytes, int32_t dtype, int32_t height,
                                  int32_t width, const void *image, const void *ref,
                                  int32_t ref_u8, double lambda_dssim, void *grad,
                                  double *loss_dev, void *stream) {
     if (!ws_bytes || height < 11 || width < 11 || lambda_dssim < 0.0 || lambda_dssim > 1.0)
         return (int)cudaErrorInvalidValue;
-    cudaStream_t s = (cudaStream_t)stream;
-    if (dtype == ISG_F32 && !ref_u8)
-        return loss_impl<float, float>(workspace, ws_bytes, height, width, (const float *)image,
-                                       (const float *)ref, lambda_dssim, (float *)grad, loss_dev, s);
-    if (dtype == ISG_F32 && ref_u8)
-        return loss_impl<float, uint8_t>(workspace, ws_bytes, height, width, (const float *)image,
-                                         (const uint8_t *)ref, lambda_dssim, (float *)grad,
-                                         loss_dev, s);
-    if (dtype == ISG_F64 && !ref_u8)
-        return loss_impl<double, double>(workspace, ws_bytes, height, width,
-                                         (const double *)image, (const double *)ref,
-                                         lambda_dssim, (double *)grad, loss_dev, s);
-    if (dtype == ISG_F64 && ref_u8)
-        return loss_impl<double, uint8_t>(workspace, ws_bytes, height, width,
-                                          (const double *)image, (const uint8_t *)ref,
-                                          lambda_dssim, (double *)grad, loss_dev, s);
-    return (int)cudaErrorInvalidValue;
+    int32_t nf = 0, na = 0;
+    isg_loss_partials_size(height, width, &nf, &na);
+    size_t rows_bytes = 0;
+    int e = isg_loss_rows(nullptr, &rows_bytes, dtype, height, width, 0, height, nullptr, 0,
+                          nullptr, ref_u8, lambda_dssim, nullptr, nullptr, nullptr, nullptr);
+    if (e) return e;
+    const size_t need = al(rows_bytes) + al(8 * (size_t)nf) + al(8 * (size_t)na);
+    if (!workspace) {
+        *ws_bytes = need;
+        return 0;
+    }
+    if (*ws_bytes < need) return (int)cudaErrorInvalidValue;
+    double *ps = (double *)((char *)workspace + al(rows_bytes));
+    double *pl = (double *)((char *)ps + al(8 * (size_t)nf));
+    e = isg_loss_rows(workspace, &rows_bytes, dtype, height, width, 0, height, image, 0, ref,
+                      ref_u8, lambda_dssim, grad, ps, pl, stream);
+    if (e) return e;
+    return isg_loss_finish(height, width, lambda_dssim, ps, pl, loss_dev, stream);
 }
 
 extern "C" int isg_ssim(void *workspace, size_t *ws_bytes, int32_t height, int32_t width,
@@ -294,8 +385,8 @@ extern "C" int isg_ssim(void *workspace, size_t *ws_bytes, int32_t height, int32
     if (*ws_bytes < al(8 * nf)) return (int)cudaErrorInvalidValue;
     cudaStream_t s = (cudaStream_t)stream;
     double *pf = (double *)workspace;
-    ssim_fields_kernel<double, double, double><<<gf, 256, 0, s>>>(height, width, channels, image, ref,
-                                                          nullptr, pf);
+    ssim_fields_kernel<double, double, double><<<gf, 256, 0, s>>>(
+        height, width, channels, image, 0, ref, nullptr, 0, 0, 0, 0, height, pf);
     ISG_CHECK_LAUNCH();
     loss_finish_kernel<<<1, 256, 0, s>>>((int)nf, pf, 0, nullptr, 0.0,
                                          (double)channels * hc * wc, 0.0, out_dev);
@@ -304,5 +395,6 @@ extern "C" int isg_ssim(void *workspace, size_t *ws_bytes, int32_t height, int32
 }
 
 extern "C" const char *isg_version(void) {
-    return "libisogs 0.1 sm_100a (preprocess fp64/glibc-exp, raster f32|f64, ssim f32|f64)";
+    return "libisogs 0.2 sm_100a (preprocess fp64/glibc-exp, raster f32|f64, ssim f32|f64, "
+           "row-band data plane)";
 }

@@ -314,22 +314,42 @@ __global__ void __launch_bounds__(THREADS) raster_bwd_kernel(
 
 // ------------------------------------------------------------ fold ----------
 template <typename T>
-__global__ void __launch_bounds__(256) reduce_ordered_kernel(int64_t m,
-                                                             const int64_t *__restrict__ emit_off,
-                                                             const T *__restrict__ partials,
-                                                             const int32_t *__restrict__ order,
-                                                             double *__restrict__ grad2d,
-                                                             double *__restrict__ grad_norm) {
+__global__ void __launch_bounds__(256) reduce_ordered_kernel(
+    int64_t m, const int64_t *__restrict__ emit_off, const T *__restrict__ partials,
+    const int32_t *__restrict__ order, const int4 *__restrict__ rect_sorted, int row_lo,
+    int row_hi, int canon_rows, double *__restrict__ grad2d, double *__restrict__ grad_norm) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= m) return;
     double acc[9];
 #pragma unroll
     for (int k = 0; k < 9; k++) acc[k] = 0.0;
-    const int64_t p1 = emit_off[r + 1];
-    for (int64_t p = emit_off[r]; p < p1; p++) {
-        const T *src = partials + 9 * p;
+    const int64_t p0 = emit_off[r], p1 = emit_off[r + 1];
+    if (canon_rows <= 0) {
+        // the reference's single-level fold in ascending tile order
+        for (int64_t p = p0; p < p1; p++) {
+            const T *src = partials + 9 * p;
 #pragma unroll
-        for (int k = 0; k < 9; k++) acc[k] += (double)src[k];
+            for (int k = 0; k < 9; k++) acc[k] += (double)src[k];
+        }
+    } else if (p1 > p0) {
+        // canonical two-level fold: tiles ascending inside each block of
+        // canon_rows tile rows, block sums ascending (W-independent grouping)
+        const int4 rc = rect_sorted[r];
+        const int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
+        const int64_t w = rc.z - rc.x + 1;
+        for (int b = y0 / canon_rows; b <= y1 / canon_rows; b++) {
+            const int ys = max(y0, b * canon_rows), ye = min(y1, b * canon_rows + canon_rows - 1);
+            double bs[9];
+#pragma unroll
+            for (int k = 0; k < 9; k++) bs[k] = 0.0;
+            for (int64_t p = p0 + (ys - y0) * w; p < p0 + (ye - y0 + 1) * w; p++) {
+                const T *src = partials + 9 * p;
+#pragma unroll
+                for (int k = 0; k < 9; k++) bs[k] += (double)src[k];
+            }
+#pragma unroll
+            for (int k = 0; k < 9; k++) acc[k] += bs[k];
+        }
     }
     const int64_t row = order[r];
     double *dst = grad2d + 9 * row;
@@ -419,17 +439,22 @@ extern "C" int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height,
 }
 
 extern "C" int isg_reduce_ordered(int32_t feat_dtype, int64_t m, const int64_t *emit_off,
-                                  const void *partials, const int32_t *order, double *grad2d,
-                                  double *grad_norm, void *stream) {
-    if (m < 0) return (int)cudaErrorInvalidValue;
+                                  const void *partials, const int32_t *order,
+                                  const int32_t *rect_sorted, int32_t row_lo, int32_t row_hi,
+                                  int32_t canon_rows, double *grad2d, double *grad_norm,
+                                  void *stream) {
+    if (m < 0 || (canon_rows > 0 && !rect_sorted)) return (int)cudaErrorInvalidValue;
+    const int4 *rs = (const int4 *)rect_sorted;
     if (m == 0) return 0;
     cudaStream_t s = (cudaStream_t)stream;
     if (feat_dtype == ISG_F32)
         reduce_ordered_kernel<float><<<blocks_for(m, 256), 256, 0, s>>>(
-            m, emit_off, (const float *)partials, order, grad2d, grad_norm);
+            m, emit_off, (const float *)partials, order, rs, row_lo, row_hi, canon_rows, grad2d,
+            grad_norm);
     else if (feat_dtype == ISG_F64)
         reduce_ordered_kernel<double><<<blocks_for(m, 256), 256, 0, s>>>(
-            m, emit_off, (const double *)partials, order, grad2d, grad_norm);
+            m, emit_off, (const double *)partials, order, rs, row_lo, row_hi, canon_rows, grad2d,
+            grad_norm);
     else
         return (int)cudaErrorInvalidValue;
     ISG_CHECK_LAUNCH();

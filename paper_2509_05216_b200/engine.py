@@ -37,6 +37,11 @@ from .training import (EvalRecord, TrainConfig, TrainDataset, TrainReport, Train
                        build_schedule, init_log_scales)
 
 TILE = 16
+# Canonical fold grouping (tile rows per block): every per-splat gradient is
+# summed tiles-ascending inside 8-tile-row blocks, then block sums ascending.
+# Pixel bands of the multi-GPU step are unions of whole blocks, which makes
+# the result bitwise independent of the GPU count (see csrc/dist.cu).
+CANON_ROWS = 8
 
 
 def _grow(buf: torch.Tensor | None, n: int, shape_tail=(), dtype=torch.float32, device=None,
@@ -84,7 +89,8 @@ class Rasterizer:
     """Buffers + launch sequence for one view on one GPU (band = all rows)."""
 
     def __init__(self, n: int, width: int, height: int, device, background=(1.0, 1.0, 1.0),
-                 feat_dtype=torch.float32):
+                 feat_dtype=torch.float32, canon_rows: int = CANON_ROWS):
+        self.canon_rows = canon_rows
         self.device = device
         self.width, self.height = width, height
         self.tiles_x = (width + TILE - 1) // TILE
@@ -204,6 +210,8 @@ class Rasterizer:
         if ctx.m:
             L.check(lib.isg_reduce_ordered(self.ftag, ctx.m, L.ptr(self.emit_off),
                                            L.ptr(self.partials), L.ptr(self.order),
+                                           L.ptr(self.rect_sorted), 0, self.tiles_y,
+                                           self.canon_rows,
                                            L.ptr(self.grad2d), None, s), "isg_reduce_ordered")
         _mark(self.timer, "reduce")
 
@@ -214,7 +222,7 @@ class Trainer:
     """Single-GPU training state: parameters, Adam moments, stats, buffers."""
 
     def __init__(self, cloud: GaussianCloud, width: int, height: int, config: TrainConfig,
-                 scene_extent: float, device=None):
+                 scene_extent: float, device=None, canon_rows: int = CANON_ROWS):
         self.device = device or L.require_cuda()
         self.cfg = config
         self.cloud = cloud
@@ -224,7 +232,8 @@ class Trainer:
         self.v = {k: torch.zeros_like(getattr(cloud, k)) for k in PARAM_NAMES}
         self.stats = TrainStats(grad_accum=torch.zeros(n, dtype=torch.float64, device=self.device),
                                 seen=torch.zeros(n, dtype=torch.int64, device=self.device))
-        self.r = Rasterizer(n, width, height, self.device, config.background)
+        self.r = Rasterizer(n, width, height, self.device, config.background,
+                            canon_rows=canon_rows)
         self.loss_dev = torch.zeros(max(config.iterations, 1) + 1, dtype=torch.float64,
                                     device=self.device)
         self.lr_host = (ctypes.c_float * 5)()

@@ -345,8 +345,8 @@ def reduce_scratch(entries, scratch: dict, m: int) -> dict:
     order = torch.arange(m, dtype=torch.int32, device=dev)
     if m:
         L.check(L.lib().isg_reduce_ordered(L.ISG_F64, m, L.ptr(off), L.ptr(part) if part.numel() else None,
-                                           L.ptr(order), L.ptr(g2d), None, L.stream_ptr()),
-                "isg_reduce_ordered")
+                                           L.ptr(order), None, 0, 0, 0, L.ptr(g2d), None,
+                                           L.stream_ptr()), "isg_reduce_ordered")
     return {"dmean": g2d[:, 0:2], "dconic": g2d[:, 2:5], "dcolor": g2d[:, 5:8], "dopac": g2d[:, 8]}
 
 
@@ -450,7 +450,8 @@ def render_backward(cloud, cam, batch: SplatBatch, order, aux: RenderAux,
     if m:
         L.check(L.lib().isg_reduce_ordered(
             L.dtype_tag(feat.dtype), m, L.ptr(cache["emit_off"]), L.ptr(partials),
-            L.ptr(order.to(torch.int32)), L.ptr(g2d_b), L.ptr(gnorm), L.stream_ptr()),
+            L.ptr(order.to(torch.int32)), None, 0, 0, 0, L.ptr(g2d_b), L.ptr(gnorm),
+            L.stream_ptr()),
             "isg_reduce_ordered")
     aux.grad_norm.copy_(gnorm)
     c = cloud if isinstance(cloud, GaussianCloud) and cloud.positions.is_cuda else \

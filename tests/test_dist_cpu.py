@@ -1,0 +1,145 @@
+"""CPU tests of the multi-GPU host layer: partitions, routing, protocol
+checks and the collectives (TorchComm) with world_size 2 over gloo."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2509_05216_b200 import distributed as D
+
+
+def test_partition_gaussians_matches_reference_rules():
+    smap = D.partition_gaussians(10, 3)
+    assert smap.sizes == [4, 3, 3]
+    assert smap.starts == [0, 4, 7, 10]
+    np.testing.assert_array_equal(smap.lists[1], [4, 5, 6])
+    smap = D.partition_gaussians(4_000_000, 4)
+    assert smap.sizes == [1_000_000] * 4
+    with pytest.raises(ValueError):
+        D.partition_gaussians(5, 0)
+
+
+@pytest.mark.parametrize("workers", [1, 2, 3, 4, 8])
+def test_row_bands_are_unions_of_canonical_blocks(workers):
+    part = D.partition_pixels(2048, 2048, 16, workers)
+    assert part.band_rows[0] == 0 and part.band_rows[-1] == part.tiles_y
+    for w in range(workers):
+        assert part.band_rows[w] % part.canon_rows == 0
+        assert part.band_rows[w + 1] > part.band_rows[w]
+    a = part.assignment
+    assert a.shape == (128 * 128,)
+    assert (np.diff(a) >= 0).all()
+    assert sorted(set(a.tolist())) == list(range(workers))
+
+
+def test_row_bands_need_enough_blocks():
+    with pytest.raises(ValueError):
+        D.partition_pixels(64, 64, 16, 2)  # 4 tile rows = 1 block of 8
+    part = D.partition_pixels(64, 64, 16, 4, canon_rows=1)
+    assert part.band_rows == [0, 1, 2, 3, 4]
+
+
+def test_cost_weighted_bands():
+    part = D.partition_pixels(2048, 2048, 16, 2, weights=[10, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1,
+                                                          1, 1, 1, 1, 1])
+    assert part.band_rows[1] < 64  # the heavy first block pulls the cut up
+
+
+def test_route_rows_band_mask():
+    part = D.partition_pixels(64, 64, 16, 4, canon_rows=1)
+    tmin = np.array([[0, 0], [1, 1], [0, 3], [2, 0]])
+    tmax = np.array([[0, 0], [2, 2], [3, 3], [2, 3]])
+    mask = D.route_rows(tmin, tmax, part)
+    np.testing.assert_array_equal(mask, [[1, 0, 0, 0], [0, 1, 1, 0], [0, 0, 0, 1], [1, 1, 1, 1]])
+
+
+def test_estimate_min_workers():
+    assert D.estimate_min_workers(18_000_000, 11_200_000) == 2
+    with pytest.raises(ValueError):
+        D.estimate_min_workers(1, 0)
+
+
+def test_reduce_gradients_fused_protocol_errors():
+    smap = D.partition_gaussians(6, 2)
+    chunk = D.GradChunk(0, np.array([5]), np.zeros((1, 2)), np.zeros((1, 3)), np.zeros((1, 3)),
+                        np.zeros(1))
+    with pytest.raises(D.ProtocolError, match="duplicate message"):
+        D.reduce_gradients_fused([D.GradMessage(0, 0, []), D.GradMessage(0, 0, [])], smap)
+    with pytest.raises(D.ProtocolError, match="unknown destination"):
+        D.reduce_gradients_fused([D.GradMessage(0, 5, [chunk])], smap)
+
+
+# --------------------------------------------------------- gloo, world 2 --
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = D.TorchComm()
+        # all-to-all-v: rank r sends (r+1)*(d+1) rows to d, rows tagged (src, dst, k)
+        counts = [(rank + 1) * (d + 1) for d in range(world)]
+        rows = []
+        for d_ in range(world):
+            for k in range(counts[d_]):
+                rows.append([rank, d_, k] + [0] * 17)
+        send = torch.tensor(rows, dtype=torch.int32)
+        recv, rc = comm.alltoallv(send, counts)
+        exp = []
+        for src in range(world):
+            for k in range((src + 1) * (rank + 1)):
+                exp.append([src, rank, k] + [0] * 17)
+        ok_a2a = torch.equal(recv, torch.tensor(exp, dtype=torch.int32)) and \
+            rc == [(s + 1) * (rank + 1) for s in range(world)]
+        # halo: first 2 rows to prev, last 3 rows to next
+        band = torch.full((6, 4, 3), float(rank))
+        to_prev = band[:2] if rank > 0 else None
+        to_next = band[-3:] if rank + 1 < world else None
+        gp, gn = comm.halo(to_prev, to_next, (3, 4, 3) if rank > 0 else None,
+                           (2, 4, 3) if rank + 1 < world else None, torch.float32,
+                           torch.device("cpu"))
+        ok_halo = True
+        if rank > 0:
+            ok_halo &= gp.shape == (3, 4, 3) and bool((gp == rank - 1).all())
+        if rank + 1 < world:
+            ok_halo &= gn.shape == (2, 4, 3) and bool((gn == rank + 1).all())
+        # disjoint block partials + all-reduce sum is exact
+        parts = torch.zeros(8, dtype=torch.float64)
+        parts[rank * 4:(rank + 1) * 4] = torch.tensor([0.1, 1e-17, -3.0, 1e300]) * (rank + 1)
+        comm.allreduce_sum_(parts)
+        ref = torch.cat([torch.tensor([0.1, 1e-17, -3.0, 1e300]) * (r + 1) for r in range(world)])
+        ok_red = torch.equal(parts, ref)
+        q.put((rank, ok_a2a, ok_halo, ok_red))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_collectives_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, a2a, halo, red in results:
+        assert a2a, f"rank {rank} all-to-all-v"
+        assert halo, f"rank {rank} halo"
+        assert red, f"rank {rank} all-reduce"

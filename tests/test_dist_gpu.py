@@ -1,0 +1,76 @@
+"""Bitwise GPU-count invariance of the sharded step, on one B200.
+
+The multi-GPU step (paper_2509_05216_b200/distributed.py) is a sequence of
+per-rank phases separated by collectives.  Here W ranks' phases run in
+sequence on ONE GPU with the collectives replaced by in-process copies (no
+kernel ever waits on another rank), which exercises every data-plane kernel
+(route, pack/unpack, band binning, halo'd loss, per-block fold, owner fold)
+and must reproduce the single-GPU engine bit for bit -- the reference's
+headline property (tests/test_acceptance.py:101-123 of the reference)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from golden_io import cam_from, load
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup():
+    import paper_2509_05216_b200 as P
+    d = load("config1")
+    cams = []
+    for i in range(d["images_u8"].shape[0]):
+        c = cam_from(d, prefix=f"cam{i}_")
+        cams.append(P.Camera(c.rotation, c.translation, c.fx, c.fy, c.cx, c.cy, c.width, c.height))
+    gt = torch.from_numpy(d["images_u8"]).cuda()
+    cloud = P.cloud_from_points(d["points"], d["init_log_scales"])
+    return P, d, cams, gt, cloud
+
+
+def _run_single(P, cams, gt, cloud, iters, canon):
+    from paper_2509_05216_b200.engine import Trainer
+    cfg = P.TrainConfig(iterations=iters, densify=False)
+    tr = Trainer(cloud.copy(), cams[0].width, cams[0].height, cfg, 3.0, canon_rows=canon)
+    sched = P.build_schedule(iters, len(cams), 0)
+    for it in range(1, iters + 1):
+        tr.step(it, cams[sched[it - 1]], gt[sched[it - 1]])
+    torch.cuda.synchronize()
+    return tr.loss_dev[1:iters + 1].tolist(), tr.cloud
+
+
+def _run_emulated(P, cams, gt, cloud, iters, canon, workers):
+    from paper_2509_05216_b200 import distributed as D
+    cfg = P.TrainConfig(iterations=iters, densify=False)
+    ranks, smap, part = D.make_ranks(cloud.copy(), cams[0].width, cams[0].height, cfg, 3.0,
+                                     workers, torch.device("cuda", 0), canon_rows=canon)
+    sched = P.build_schedule(iters, len(cams), 0)
+    losses = []
+    for it in range(1, iters + 1):
+        loss = D.emulated_step(ranks, cams[sched[it - 1]], gt[sched[it - 1]], it)
+        losses.append(float(loss[0]))
+    torch.cuda.synchronize()
+    return losses, D.gather_cloud(ranks), part
+
+
+@pytest.mark.parametrize("workers", [1, 2, 3, 4])
+def test_sharded_step_bitwise_equals_single_gpu(workers):
+    P, d, cams, gt, cloud = _setup()
+    iters, canon = 4, 1
+    ref_losses, ref_cloud = _run_single(P, cams, gt, cloud, iters, canon)
+    losses, got, part = _run_emulated(P, cams, gt, cloud, iters, canon, workers)
+    assert len(part.band_rows) == workers + 1
+    assert losses == ref_losses, (losses, ref_losses)
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(got, k), getattr(ref_cloud, k)), k
+
+
+def test_sharded_losses_track_reference():
+    """The W=2 sharded run also tracks the reference's own loss trajectory."""
+    P, d, cams, gt, cloud = _setup()
+    losses, _, _ = _run_emulated(P, cams, gt, cloud, 10, 1, 2)
+    ref = np.array(d["losses"][:10])
+    assert np.max(np.abs(np.array(losses) - ref) / ref) <= 2e-3
