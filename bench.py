@@ -104,7 +104,7 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -210,7 +210,7 @@ def run_ours(args, world, rank, local):
     from paper_2509_05216_b200.training import TrainConfig, build_schedule
 
     dev = torch.device("cuda", local if world > 1 else 0)
-    if world > 1:
+    if world > 1 or args.dist:
         from paper_2509_05216_b200.distributed import bench_distributed
         return bench_distributed(args, world, rank, local)
     wl = S.make_workload(args.config, dev, log=log)
@@ -401,6 +401,8 @@ def main():
     ap.add_argument("--cpu-res", type=int, default=None)
     ap.add_argument("--cpu-views", type=int, default=4)
     ap.add_argument("--cpu-budget-s", type=float, default=150.0)
+    ap.add_argument("--dist", action="store_true",
+                    help="run the sharded engine even at N=1 (torchrun, world 1)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warm-up raised to the required minimum of 3")
@@ -411,7 +413,7 @@ def main():
         return run_reference(args, world, rank)
     world, rank, local = dist_setup(args)
     run_ours(args, world, rank, local)
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()

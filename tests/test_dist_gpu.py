@@ -34,7 +34,7 @@ def _setup():
 def _run_single(P, cams, gt, cloud, iters, canon):
     from paper_2509_05216_b200.engine import Trainer
     cfg = P.TrainConfig(iterations=iters, densify=False)
-    tr = Trainer(cloud.copy(), cams[0].width, cams[0].height, cfg, 3.0, canon_rows=canon)
+    tr = Trainer(cloud.copy(), cams[0].width, cams[0].height, cfg, _extent(cams), canon_rows=canon)
     sched = P.build_schedule(iters, len(cams), 0)
     for it in range(1, iters + 1):
         tr.step(it, cams[sched[it - 1]], gt[sched[it - 1]])
@@ -42,12 +42,12 @@ def _run_single(P, cams, gt, cloud, iters, canon):
     return tr.loss_dev[1:iters + 1].tolist(), tr.cloud
 
 
-def _run_emulated(P, cams, gt, cloud, iters, canon, workers):
+def _run_emulated(P, cams, gt, cloud, iters, canon, workers, total=None):
     from paper_2509_05216_b200 import distributed as D
-    cfg = P.TrainConfig(iterations=iters, densify=False)
-    ranks, smap, part = D.make_ranks(cloud.copy(), cams[0].width, cams[0].height, cfg, 3.0,
+    cfg = P.TrainConfig(iterations=total or iters, densify=False)
+    ranks, smap, part = D.make_ranks(cloud.copy(), cams[0].width, cams[0].height, cfg, _extent(cams),
                                      workers, torch.device("cuda", 0), canon_rows=canon)
-    sched = P.build_schedule(iters, len(cams), 0)
+    sched = P.build_schedule(total or iters, len(cams), 0)
     losses = []
     for it in range(1, iters + 1):
         loss = D.emulated_step(ranks, cams[sched[it - 1]], gt[sched[it - 1]], it)
@@ -71,6 +71,11 @@ def test_sharded_step_bitwise_equals_single_gpu(workers):
 def test_sharded_losses_track_reference():
     """The W=2 sharded run also tracks the reference's own loss trajectory."""
     P, d, cams, gt, cloud = _setup()
-    losses, _, _ = _run_emulated(P, cams, gt, cloud, 10, 1, 2)
+    losses, _, _ = _run_emulated(P, cams, gt, cloud, 10, 1, 2, total=100)
     ref = np.array(d["losses"][:10])
     assert np.max(np.abs(np.array(losses) - ref) / ref) <= 2e-3
+
+
+def _extent(cams):
+    from oracle import train as T
+    return T.scene_extent(cams)
