@@ -286,6 +286,20 @@ int isg_chain_adam(const isg_train_state *s, const isg_camera *cam, const uint8_
                    const double *grad2d, const float *lr5, const isg_adam_consts *c,
                    double half_w, double half_h, void *stream);
 
+/* Training-step split of isg_chain_adam: chain rule + TrainStats for float32
+ * parameters (grads written for every row, zeros when unflagged) ... */
+int isg_chain_train(const isg_params *p, const isg_camera *cam, const uint8_t *flag,
+                    const double *grad2d, float *d_positions, float *d_log_scales,
+                    float *d_rotations, float *d_opacity_logits, float *d_sh, int64_t *seen,
+                    double *grad_accum, double half_w, double half_h, void *stream);
+
+/* ... then dense float32 Adam over up to 8 groups in one launch (arrays of
+ * `count` host-side pointers / sizes / learning rates; constants as for
+ * isg_adam).  Bit-identical to isg_adam per element. */
+int isg_adam_groups(int32_t count, float *const *p, const float *const *g, float *const *m,
+                    float *const *v, const int64_t *n, const float *lr, const isg_adam_consts *c,
+                    void *stream);
+
 /* glibc-exact exp over an array (verification hook for the key path). */
 int isg_exp_f64(int64_t n, const double *x, double *y, void *stream);
 

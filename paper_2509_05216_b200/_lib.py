@@ -98,6 +98,9 @@ SIGNATURES = {
     "isg_adam": [_I32, _I64, _P, _P, _P, _P, ctypes.POINTER(AdamConsts_t), _P],
     "isg_chain_adam": [ctypes.POINTER(TrainState_t), ctypes.POINTER(Camera_t), _P, _P, _P,
                        ctypes.POINTER(AdamConsts_t), _D, _D, _P],
+    "isg_chain_train": [ctypes.POINTER(Params_t), ctypes.POINTER(Camera_t), _P, _P, _P, _P, _P,
+                        _P, _P, _P, _P, _D, _D, _P],
+    "isg_adam_groups": [_I32, _P, _P, _P, _P, _P, _P, ctypes.POINTER(AdamConsts_t), _P],
     "isg_exp_f64": [_I64, _P, _P, _P],
     "isg_version": [],
 }

@@ -44,32 +44,69 @@ __global__ void finish_counts_kernel(int64_t n, const int64_t *emit_off, int64_t
     counts[1] = emit_off[n];
 }
 
-// Warp-cooperative emission: each warp walks 32 consecutive ranks; for each
-// rank its lanes write the rank's (clipped) rect tiles row-major, i.e. in
-// ascending tile id -- the order _fill_tile_entries visits them.
+// Entry-parallel emission: each block takes chunks of EMIT_CHUNK consecutive
+// output slots, stages the emit offsets of the ranks covering the chunk in
+// shared memory and gives every slot its rank by binary search, so the
+// (tile, rank) pairs are written fully coalesced.  Within a rank the slots
+// walk the (clipped) rect row-major, i.e. in ascending tile id -- the order
+// _fill_tile_entries visits them.
+constexpr int EMIT_CHUNK = 2048;
+
+__device__ __forceinline__ int64_t owner_rank(const int64_t *__restrict__ off, int64_t lo,
+                                              int64_t hi, int64_t e) {
+    // largest r in [lo, hi] with off[r] <= e
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= e) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
 __global__ void __launch_bounds__(256) emit_kernel(int64_t m, const int4 *__restrict__ rect_sorted,
                                                    const int64_t *__restrict__ emit_off,
                                                    int tiles_x, int row_lo, int row_hi,
                                                    uint32_t *__restrict__ tile_keys,
                                                    int32_t *__restrict__ tile_vals) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t r0 = warp * 32;
-    if (r0 >= m) return;
-    const int64_t r_end = min(r0 + 32, m);
+    __shared__ int64_t s_off[EMIT_CHUNK + 1];
+    __shared__ int64_t s_r0;
+    const int64_t E = emit_off[m];
     const uint32_t base_tile = (uint32_t)row_lo * (uint32_t)tiles_x;
-    for (int64_t r = r0; r < r_end; r++) {
-        const int4 rc = rect_sorted[r];
-        const int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
-        if (y1 < y0) continue;
-        const int w = rc.z - rc.x + 1;
-        const int64_t cnt = (int64_t)w * (y1 - y0 + 1);
-        const int64_t off = emit_off[r];
-        for (int64_t k = lane; k < cnt; k += 32) {
-            const int ty = y0 + (int)(k / w), tx = rc.x + (int)(k % w);
-            tile_keys[off + k] = (uint32_t)ty * (uint32_t)tiles_x + (uint32_t)tx - base_tile;
-            tile_vals[off + k] = (int32_t)r;
+    for (int64_t c0 = (int64_t)blockIdx.x * EMIT_CHUNK; c0 < E;
+         c0 += (int64_t)gridDim.x * EMIT_CHUNK) {
+        if (threadIdx.x == 0) s_r0 = owner_rank(emit_off, 0, m - 1, c0);
+        __syncthreads();
+        const int64_t r0 = s_r0;
+        const int nr = (int)min((int64_t)EMIT_CHUNK + 1, m + 1 - r0);
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) s_off[i] = emit_off[r0 + i];
+        __syncthreads();
+        for (int t = threadIdx.x; t < EMIT_CHUNK; t += blockDim.x) {
+            const int64_t e = c0 + t;
+            if (e >= E) break;
+            int64_t r, base;
+            if (e < s_off[nr - 1] || r0 + nr - 1 == m) {
+                int lo = 0, hi = nr - 2;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_off[mid] <= e) lo = mid;
+                    else hi = mid - 1;
+                }
+                r = r0 + lo;
+                base = s_off[lo];
+            } else {  // more empty ranks than staged: fall back to global memory
+                r = owner_rank(emit_off, r0, m - 1, e);
+                base = emit_off[r];
+            }
+            const int4 rc = rect_sorted[r];
+            const int y0 = max(rc.y, row_lo);
+            const int w = rc.z - rc.x + 1;
+            const int k = (int)(e - base);
+            const int dy = k / w;
+            const int ty = y0 + dy, tx = rc.x + (k - dy * w);
+            tile_keys[e] = (uint32_t)ty * (uint32_t)tiles_x + (uint32_t)tx - base_tile;
+            tile_vals[e] = (int32_t)r;
         }
+        __syncthreads();
     }
 }
 
@@ -158,8 +195,11 @@ extern "C" int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t
                             int32_t *tile_vals, void *stream) {
     if (m < 0 || tiles_x <= 0) return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
-    int64_t warps = (m + 31) / 32;
-    emit_kernel<<<blocks_for(warps * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+    int sms = 148;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    emit_kernel<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(
         m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals);
     ISG_CHECK_LAUNCH();
     return 0;

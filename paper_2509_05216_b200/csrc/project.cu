@@ -362,6 +362,84 @@ __global__ void __launch_bounds__(128, 4) chain_adam_kernel(isg_train_state s, C
     }
 }
 
+// Chain rule + TrainStats for float32 parameters (training step, split from
+// Adam so each kernel keeps its occupancy): grads written for every row
+// (zeros for unflagged rows), stats for flagged rows.
+template <int K3>
+__global__ void __launch_bounds__(128) chain_train_kernel(isg_params p, Cam cam,
+                                                          const uint8_t *__restrict__ flag,
+                                                          const double *__restrict__ grad2d,
+                                                          float *dpos, float *dls, float *drot,
+                                                          float *dlogit, float *dsh,
+                                                          int64_t *seen, double *grad_accum,
+                                                          double half_w, double half_h) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    Grads g;
+    if (flag[i]) {
+        Row<float> row;
+        load_row<float>(p, i, row);
+        const double *g2 = grad2d + 9 * i;
+        chain_one<float>(row, p.degree, cam, g2, g);
+        if (seen) seen[i] += 1;
+        if (grad_accum) grad_accum[i] += hypot(g2[0] * half_w, g2[1] * half_h);
+    } else {
+        zero_grads(g);
+    }
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        dpos[3 * i + j] = (float)g.pos[j];
+        dls[3 * i + j] = (float)g.ls[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) drot[4 * i + j] = (float)g.rot[j];
+    dlogit[i] = (float)g.logit;
+#pragma unroll
+    for (int j = 0; j < K3; j++) dsh[(int64_t)K3 * i + j] = (float)g.sh[j];
+}
+
+// Dense Adam over up to 8 float32 groups in one launch, 4 elements per thread
+// (16-byte vector accesses), numpy operation order (no FMA).
+struct AdamGroups {
+    float *p[8];
+    const float *g[8];
+    float *m[8];
+    float *v[8];
+    float lr[8];
+    int64_t start[9];  // prefix of group sizes in float4 units
+    int64_t n[8];      // group sizes in floats
+    int count;
+};
+
+__global__ void __launch_bounds__(256) adam_groups_kernel(AdamGroups G, AdamF c) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= G.start[G.count]) return;
+    int k = 0;
+#pragma unroll
+    for (int j = 1; j < 8; j++)
+        if (j < G.count && q >= G.start[j]) k = j;
+    const int64_t e = 4 * (q - G.start[k]);
+    const int64_t n = G.n[k];
+    const float lr = G.lr[k];
+    if (e + 4 <= n && (((uintptr_t)G.p[k] | (uintptr_t)G.g[k] | (uintptr_t)G.m[k] |
+                        (uintptr_t)G.v[k]) & 15) == 0) {
+        float4 p = *reinterpret_cast<float4 *>(G.p[k] + e);
+        const float4 g = *reinterpret_cast<const float4 *>(G.g[k] + e);
+        float4 m = *reinterpret_cast<float4 *>(G.m[k] + e);
+        float4 v = *reinterpret_cast<float4 *>(G.v[k] + e);
+        adam_f32(p.x, m.x, v.x, g.x, lr, c);
+        adam_f32(p.y, m.y, v.y, g.y, lr, c);
+        adam_f32(p.z, m.z, v.z, g.z, lr, c);
+        adam_f32(p.w, m.w, v.w, g.w, lr, c);
+        *reinterpret_cast<float4 *>(G.p[k] + e) = p;
+        *reinterpret_cast<float4 *>(G.m[k] + e) = m;
+        *reinterpret_cast<float4 *>(G.v[k] + e) = v;
+    } else {
+        for (int64_t j = e; j < e + 4 && j < n; j++)
+            adam_f32(G.p[k][j], G.m[k][j], G.v[k][j], G.g[k][j], lr, c);
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) adam_kernel(int64_t n, T *p, const T *g, T *m, T *v, T b1,
                                                    T omb1, T b2, T omb2, T bc1, T bc2, T lr,
@@ -464,6 +542,60 @@ extern "C" int isg_adam(int32_t dtype, int64_t n, void *p, const void *g, void *
                                                  c->bc1, c->bc2, c->lr, c->eps);
     else
         return (int)cudaErrorInvalidValue;
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_chain_train(const isg_params *p, const isg_camera *cam, const uint8_t *flag,
+                               const double *grad2d, float *d_positions, float *d_log_scales,
+                               float *d_rotations, float *d_opacity_logits, float *d_sh,
+                               int64_t *seen, double *grad_accum, double half_w, double half_h,
+                               void *stream) {
+    if (!p || !cam || !flag || !grad2d || p->n < 0 || p->dtype != ISG_F32)
+        return (int)cudaErrorInvalidValue;
+    if (p->n == 0) return 0;
+    Cam c = to_cam(*cam);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p->degree >= 1)
+        chain_train_kernel<12><<<blocks_for(p->n, 128), 128, 0, s>>>(
+            *p, c, flag, grad2d, d_positions, d_log_scales, d_rotations, d_opacity_logits, d_sh,
+            seen, grad_accum, half_w, half_h);
+    else
+        chain_train_kernel<3><<<blocks_for(p->n, 128), 128, 0, s>>>(
+            *p, c, flag, grad2d, d_positions, d_log_scales, d_rotations, d_opacity_logits, d_sh,
+            seen, grad_accum, half_w, half_h);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_adam_groups(int32_t count, float *const *p, const float *const *g,
+                               float *const *m, float *const *v, const int64_t *n,
+                               const float *lr, const isg_adam_consts *c, void *stream) {
+    if (count < 1 || count > 8 || !c) return (int)cudaErrorInvalidValue;
+    AdamGroups G;
+    G.count = count;
+    G.start[0] = 0;
+    for (int k = 0; k < count; k++) {
+        G.p[k] = p[k];
+        G.g[k] = g[k];
+        G.m[k] = m[k];
+        G.v[k] = v[k];
+        G.lr[k] = lr[k];
+        G.n[k] = n[k];
+        G.start[k + 1] = G.start[k] + (n[k] + 3) / 4;
+    }
+    for (int k = count; k < 8; k++) {
+        G.p[k] = nullptr;
+        G.g[k] = nullptr;
+        G.m[k] = G.v[k] = nullptr;
+        G.lr[k] = 0.0f;
+        G.n[k] = 0;
+        G.start[k + 1] = G.start[count];
+    }
+    if (G.start[count] == 0) return 0;
+    AdamF a{(float)c->b1, (float)c->omb1, (float)c->b2, (float)c->omb2,
+            (float)c->bc1, (float)c->bc2, (float)c->eps};
+    adam_groups_kernel<<<blocks_for(G.start[count], 256), 256, 0, (cudaStream_t)stream>>>(G, a);
     ISG_CHECK_LAUNCH();
     return 0;
 }

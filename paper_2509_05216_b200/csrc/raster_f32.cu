@@ -71,11 +71,17 @@ __device__ __forceinline__ Staged stage(const float *__restrict__ feat, int rank
     return s;
 }
 
+// Column terms of the exponent shared by a thread's two pixels (same x):
+// power = A + d1 * (B + nc * d1) with A = na d0^2, B = nb d0.
+__device__ __forceinline__ void col_terms(float d0, const float4 &g4, float &A, float &B) {
+    A = __fmul_rn(__fmul_rn(g4.z, d0), d0);
+    B = __fmul_rn(g4.w, d0);
+}
+
 // Per-pair alpha (0 when the pair is skipped) and the Gaussian weight g.
-__device__ __forceinline__ float pair_alpha(float d0, float d1, const float4 &g4, const float4 &h4,
+__device__ __forceinline__ float pair_alpha(float d1, float A, float B, const float4 &h4,
                                             float &gw) {
-    const float power = __fmaf_rn(d0, __fmaf_rn(g4.z, d0, __fmul_rn(g4.w, d1)),
-                                  __fmul_rn(__fmul_rn(h4.x, d1), d1));
+    const float power = __fmaf_rn(d1, __fmaf_rn(h4.x, d1, B), A);
     if (power > 0.0f || power < h4.y) return 0.0f;
     gw = ex2a(__fmul_rn(power, LOG2E));
     const float a = fminf(__fmul_rn(h4.z, gw), 0.99f);
@@ -185,10 +191,11 @@ __global__ void __launch_bounds__(NT) fwd_kernel(
             if (__all_sync(FULL, done0 && done1)) break;
             const int slot = slist[warp][k];
             const float4 g4 = sgh[slot][0], h4 = sgh[slot][1];
-            const float d0 = fpx - g4.x;
+            float A, B;
+            col_terms(fpx - g4.x, g4, A, B);
             if (!done0) {
                 float gw;
-                const float a = pair_alpha(d0, fpy0 - g4.y, g4, h4, gw);
+                const float a = pair_alpha(fpy0 - g4.y, A, B, h4, gw);
                 if (a > 0.0f) {
                     const float test = t0 * (1.0f - a);
                     if (test < 1e-4f) {
@@ -209,7 +216,7 @@ __global__ void __launch_bounds__(NT) fwd_kernel(
             }
             if (!done1) {
                 float gw;
-                const float a = pair_alpha(d0, fpy1 - g4.y, g4, h4, gw);
+                const float a = pair_alpha(fpy1 - g4.y, A, B, h4, gw);
                 if (a > 0.0f) {
                     const float test = t1 * (1.0f - a);
                     if (test < 1e-4f) {
@@ -295,30 +302,59 @@ __device__ __forceinline__ int bfly_slot(int lane) {
 
 // One contributing (pixel, entry) pair: accumulate its 9 gradient terms and
 // advance the pixel's back-to-front state (T, S).  _kernels.py:342-374.
-__device__ __forceinline__ void pair_grad(float a, float gw, float d0, float d1, const float4 &g4,
-                                          const float4 &h4, const float4 &c, float wr, float wg,
-                                          float wb, float &T, float &sr, float &sg, float &sb,
-                                          float (&v)[9]) {
-    const float inv = __frcp_rn(1.0f - a);
+__device__ __forceinline__ float rcpa(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Per-entry quantities shared by a thread's two pixels (same column).
+struct EntryB {
+    float A, B;        // exponent column terms (col_terms)
+    float d0, q00;     // x offset, -d0^2/2
+    float P0, P1;      // a d0, b d0  (conic a = -2 g.z, b = -g.w, c = -2 h.x)
+    float b, c, op;
+    float4 col;
+};
+
+__device__ __forceinline__ EntryB entry_terms(float fpx, const float4 &g4, const float4 &h4,
+                                              const float4 &col) {
+    EntryB e;
+    e.d0 = fpx - g4.x;
+    col_terms(e.d0, g4, e.A, e.B);
+    e.q00 = -0.5f * e.d0 * e.d0;
+    e.b = -g4.w;
+    e.c = -2.0f * h4.x;
+    e.P0 = -2.0f * g4.z * e.d0;
+    e.P1 = e.b * e.d0;
+    e.op = h4.z;
+    e.col = col;
+    return e;
+}
+
+__device__ __forceinline__ void pair_grad(float a, float gw, float d1, const EntryB &e, float wr,
+                                          float wg, float wb, float &T, float &sr, float &sg,
+                                          float &sb, float (&v)[9]) {
+    const float inv = rcpa(1.0f - a);
     const float ti = T * inv;  // T before this splat
     const float at = a * ti;
     v[5] = fmaf(wr, at, v[5]);
     v[6] = fmaf(wg, at, v[6]);
     v[7] = fmaf(wb, at, v[7]);
-    const float dalpha = wr * (c.x * ti - sr * inv) + wg * (c.y * ti - sg * inv) +
-                         wb * (c.z * ti - sb * inv);
-    sr = fmaf(c.x, at, sr);
-    sg = fmaf(c.y, at, sg);
-    sb = fmaf(c.z, at, sb);
-    if (!(__fmul_rn(h4.z, gw) > 0.99f)) {  // clamped alpha: zero sub-gradient
-        v[8] = fmaf(dalpha, gw, v[8]);
-        const float dpower = dalpha * h4.z * gw;
-        // conic (a, b, c) = (-2 g4.z, -g4.w, -2 h4.x)
-        v[2] = fmaf(dpower, -0.5f * d0 * d0, v[2]);
-        v[3] = fmaf(dpower, -(d0 * d1), v[3]);
+    const float dalpha = wr * fmaf(e.col.x, ti, -sr * inv) + wg * fmaf(e.col.y, ti, -sg * inv) +
+                         wb * fmaf(e.col.z, ti, -sb * inv);
+    sr = fmaf(e.col.x, at, sr);
+    sg = fmaf(e.col.y, at, sg);
+    sb = fmaf(e.col.z, at, sb);
+    if (!(__fmul_rn(e.op, gw) > 0.99f)) {  // clamped alpha: zero sub-gradient
+        const float dg = dalpha * gw;
+        v[8] += dg;
+        const float dpower = dg * e.op;
+        v[2] = fmaf(dpower, e.q00, v[2]);
+        v[3] = fmaf(dpower, -(e.d0 * d1), v[3]);
         v[4] = fmaf(dpower, -0.5f * d1 * d1, v[4]);
-        v[0] = fmaf(dpower, -2.0f * g4.z * d0 - g4.w * d1, v[0]);
-        v[1] = fmaf(dpower, -g4.w * d0 - 2.0f * h4.x * d1, v[1]);
+        v[0] = fmaf(dpower, fmaf(e.b, d1, e.P0), v[0]);
+        v[1] = fmaf(dpower, fmaf(e.c, d1, e.P1), v[1]);
     }
     T = ti;
 }
@@ -444,23 +480,23 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
 #pragma unroll
             for (int q = 0; q < 9; q++) v[q] = 0.0f;
             bool act = false;
-            const float d0 = fpx - g4.x;
+            const EntryB e = entry_terms(fpx, g4, h4, scol[slot]);
             if (jj < last0) {
                 float gw;
                 const float d1 = fpy0 - g4.y;
-                const float a = pair_alpha(d0, d1, g4, h4, gw);
+                const float a = pair_alpha(d1, e.A, e.B, h4, gw);
                 if (a > 0.0f) {
                     act = true;
-                    pair_grad(a, gw, d0, d1, g4, h4, scol[slot], wr0, wg0, wb0, T0, sr0, sg0, sb0, v);
+                    pair_grad(a, gw, d1, e, wr0, wg0, wb0, T0, sr0, sg0, sb0, v);
                 }
             }
             if (jj < last1) {
                 float gw;
                 const float d1 = fpy1 - g4.y;
-                const float a = pair_alpha(d0, d1, g4, h4, gw);
+                const float a = pair_alpha(d1, e.A, e.B, h4, gw);
                 if (a > 0.0f) {
                     act = true;
-                    pair_grad(a, gw, d0, d1, g4, h4, scol[slot], wr1, wg1, wb1, T1, sr1, sg1, sb1, v);
+                    pair_grad(a, gw, d1, e, wr1, wg1, wb1, T1, sr1, sg1, sb1, v);
                 }
             }
             float y = 0.0f;

@@ -629,26 +629,11 @@ class RankStep:
         lrs = [self.scene_extent * position_lr(cfg.lr_position, it, cfg.iterations,
                                                cfg.lr_position_final),
                cfg.lr_scale, cfg.lr_rotation, cfg.lr_opacity, cfg.lr_sh]
-        for i, v in enumerate(lrs):
-            self.lr_host[i] = float(np.float32(v))
-        c = adam_consts(torch.float32, it, 0.0)
-        st = L.TrainState_t()
-        cl = self.cloud
-        st.positions, st.log_scales, st.rotations = L.ptr(cl.positions), L.ptr(cl.log_scales), L.ptr(cl.rotations)
-        st.opacity_logits, st.sh = L.ptr(cl.opacity_logits), L.ptr(cl.sh_coeffs)
-        for pre, dd in (("m_", self.m), ("v_", self.v)):
-            setattr(st, pre + "positions", L.ptr(dd["positions"]))
-            setattr(st, pre + "log_scales", L.ptr(dd["log_scales"]))
-            setattr(st, pre + "rotations", L.ptr(dd["rotations"]))
-            setattr(st, pre + "opacity_logits", L.ptr(dd["opacity_logits"]))
-            setattr(st, pre + "sh", L.ptr(dd["sh_coeffs"]))
-        st.seen, st.grad_accum = L.ptr(self.seen), L.ptr(self.grad_accum)
-        st.n, st.degree = self.n, cl.degree
-        L.check(L.lib().isg_chain_adam(ctypes.byref(st), ctypes.byref(self.cam_struct),
-                                       L.ptr(self.flag), L.ptr(self.grad2d),
-                                       ctypes.cast(self.lr_host, ctypes.c_void_p), ctypes.byref(c),
-                                       0.5 * self.W, 0.5 * self.H, L.stream_ptr()),
-                "isg_chain_adam")
+        from .engine import update_params
+        if getattr(self, "grads", None) is None:
+            self.grads = {k: torch.empty_like(v) for k, v in self.m.items()}
+        update_params(self.cloud, self.m, self.v, self.grads, self.seen, self.grad_accum,
+                      self.flag, self.grad2d, self.cam_struct, lrs, it, self.W, self.H)
 
 
 # ------------------------------------------------------------------ drivers --

@@ -218,6 +218,39 @@ class Rasterizer:
     LAUNCHES_PER_STEP = None  # filled by Trainer (documented count)
 
 
+def update_params(cloud: GaussianCloud, m: dict, v: dict, grads: dict, seen, grad_accum, flag,
+                  grad2d, cam_struct, lrs: list, it: int, width: int, height: int,
+                  timer=None) -> None:
+    """Chain rule + TrainStats (isg_chain_train), then dense Adam over the five
+    groups in one launch (isg_adam_groups): engine.py:508-536, optim.py:20-56."""
+    lib = L.lib()
+    s = L.stream_ptr()
+    p = L.Params_t()
+    p.positions, p.log_scales = L.ptr(cloud.positions), L.ptr(cloud.log_scales)
+    p.rotations, p.opacity_logits = L.ptr(cloud.rotations), L.ptr(cloud.opacity_logits)
+    p.sh, p.n, p.degree, p.dtype = L.ptr(cloud.sh_coeffs), cloud.count, cloud.degree, L.ISG_F32
+    if cloud.count == 0:
+        return
+    L.check(lib.isg_chain_train(ctypes.byref(p), ctypes.byref(cam_struct), L.ptr(flag),
+                                L.ptr(grad2d), L.ptr(grads["positions"]),
+                                L.ptr(grads["log_scales"]), L.ptr(grads["rotations"]),
+                                L.ptr(grads["opacity_logits"]), L.ptr(grads["sh_coeffs"]),
+                                L.ptr(seen), L.ptr(grad_accum), 0.5 * width, 0.5 * height, s),
+            "isg_chain_train")
+    _mark(timer, "chain")
+    P5 = ctypes.c_void_p * 5
+    pp = P5(*(L.ptr(getattr(cloud, k)) for k in PARAM_NAMES))
+    gg = P5(*(L.ptr(grads[k]) for k in PARAM_NAMES))
+    mm = P5(*(L.ptr(m[k]) for k in PARAM_NAMES))
+    vv = P5(*(L.ptr(v[k]) for k in PARAM_NAMES))
+    nn = (ctypes.c_int64 * 5)(*(getattr(cloud, k).numel() for k in PARAM_NAMES))
+    ll = (ctypes.c_float * 5)(*(float(np.float32(x)) for x in lrs))
+    c = adam_consts(torch.float32, it, 0.0)
+    L.check(lib.isg_adam_groups(5, pp, gg, mm, vv, nn, ll, ctypes.byref(c), s),
+            "isg_adam_groups")
+    _mark(timer, "adam")
+
+
 class Trainer:
     """Single-GPU training state: parameters, Adam moments, stats, buffers."""
 
@@ -237,6 +270,7 @@ class Trainer:
         self.loss_dev = torch.zeros(max(config.iterations, 1) + 1, dtype=torch.float64,
                                     device=self.device)
         self.lr_host = (ctypes.c_float * 5)()
+        self.grads = None
 
     def _state_struct(self) -> L.TrainState_t:
         st = L.TrainState_t()
@@ -270,16 +304,11 @@ class Trainer:
         loss_l1_dssim_device(r.image, gt, self.cfg.lambda_dssim, r.dl, slot)
         _mark(r.timer, "loss")
         r.backward(ctx)
-        for i, v in enumerate(self.lrs(it)):
-            self.lr_host[i] = float(np.float32(v))
-        c = adam_consts(torch.float32, it, 0.0)
-        st = self._state_struct()
-        L.check(L.lib().isg_chain_adam(ctypes.byref(st), ctypes.byref(r.cam_struct),
-                                       L.ptr(r.flag), L.ptr(r.grad2d),
-                                       ctypes.cast(self.lr_host, ctypes.c_void_p),
-                                       ctypes.byref(c), 0.5 * r.width, 0.5 * r.height,
-                                       L.stream_ptr()), "isg_chain_adam")
-        _mark(r.timer, "chain_adam")
+        if self.grads is None:
+            self.grads = {k: torch.empty_like(getattr(self.cloud, k)) for k in PARAM_NAMES}
+        update_params(self.cloud, self.m, self.v, self.grads, self.stats.seen,
+                      self.stats.grad_accum, r.flag, r.grad2d, r.cam_struct, self.lrs(it), it,
+                      r.width, r.height, r.timer)
 
     def render(self, cam) -> torch.Tensor:
         self.r.forward(self.cloud, cam)
