@@ -50,7 +50,36 @@ __global__ void finish_counts_kernel(int64_t n, const int64_t *emit_off, int64_t
 // (tile, rank) pairs are written fully coalesced.  Within a rank the slots
 // walk the (clipped) rect row-major, i.e. in ascending tile id -- the order
 // _fill_tile_entries visits them.
-constexpr int EMIT_CHUNK = 2048;
+constexpr int EMIT_CHUNK = 4096;
+
+// Block-cooperative search: largest r in [0, m-1] with off[r] <= e; each of
+// the 256 threads probes one point per round, narrowing the bracket 256x.
+__device__ __forceinline__ int64_t owner_rank_block(const int64_t *__restrict__ off, int64_t m,
+                                                    int64_t e) {
+    __shared__ int64_t s_lo, s_hi;
+    if (threadIdx.x == 0) {
+        s_lo = 0;
+        s_hi = m - 1;
+    }
+    __syncthreads();
+    while (true) {
+        const int64_t lo = s_lo, hi = s_hi;
+        if (hi <= lo) break;
+        const int64_t step = (hi - lo + blockDim.x) / blockDim.x;
+        const int64_t idx = lo + (int64_t)threadIdx.x * step;
+        const bool ok = idx <= hi && off[idx] <= e;
+        const int cnt = __syncthreads_count(ok);  // probes are monotone: a true prefix
+        if (threadIdx.x == 0) {
+            const int64_t nlo = lo + (int64_t)(cnt - 1) * step;
+            s_lo = nlo;
+            s_hi = min(hi, nlo + step - 1);
+        }
+        __syncthreads();
+    }
+    const int64_t r = s_lo;
+    __syncthreads();
+    return r;
+}
 
 __device__ __forceinline__ int64_t owner_rank(const int64_t *__restrict__ off, int64_t lo,
                                               int64_t hi, int64_t e) {
@@ -69,14 +98,11 @@ __global__ void __launch_bounds__(256) emit_kernel(int64_t m, const int4 *__rest
                                                    uint32_t *__restrict__ tile_keys,
                                                    int32_t *__restrict__ tile_vals) {
     __shared__ int64_t s_off[EMIT_CHUNK + 1];
-    __shared__ int64_t s_r0;
     const int64_t E = emit_off[m];
     const uint32_t base_tile = (uint32_t)row_lo * (uint32_t)tiles_x;
     for (int64_t c0 = (int64_t)blockIdx.x * EMIT_CHUNK; c0 < E;
          c0 += (int64_t)gridDim.x * EMIT_CHUNK) {
-        if (threadIdx.x == 0) s_r0 = owner_rank(emit_off, 0, m - 1, c0);
-        __syncthreads();
-        const int64_t r0 = s_r0;
+        const int64_t r0 = owner_rank_block(emit_off, m, c0);
         const int nr = (int)min((int64_t)EMIT_CHUNK + 1, m + 1 - r0);
         for (int i = threadIdx.x; i < nr; i += blockDim.x) s_off[i] = emit_off[r0 + i];
         __syncthreads();
@@ -199,7 +225,7 @@ extern "C" int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    emit_kernel<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(
+    emit_kernel<<<sms * 4, 256, 0, (cudaStream_t)stream>>>(
         m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals);
     ISG_CHECK_LAUNCH();
     return 0;
