@@ -44,95 +44,26 @@ __global__ void finish_counts_kernel(int64_t n, const int64_t *emit_off, int64_t
     counts[1] = emit_off[n];
 }
 
-// Entry-parallel emission: each block takes chunks of EMIT_CHUNK consecutive
-// output slots, stages the emit offsets of the ranks covering the chunk in
-// shared memory and gives every slot its rank by binary search, so the
-// (tile, rank) pairs are written fully coalesced.  Within a rank the slots
-// walk the (clipped) rect row-major, i.e. in ascending tile id -- the order
-// _fill_tile_entries visits them.
-constexpr int EMIT_CHUNK = 4096;
-
-// Block-cooperative search: largest r in [0, m-1] with off[r] <= e; each of
-// the 256 threads probes one point per round, narrowing the bracket 256x.
-__device__ __forceinline__ int64_t owner_rank_block(const int64_t *__restrict__ off, int64_t m,
-                                                    int64_t e) {
-    __shared__ int64_t s_lo, s_hi;
-    if (threadIdx.x == 0) {
-        s_lo = 0;
-        s_hi = m - 1;
-    }
-    __syncthreads();
-    while (true) {
-        const int64_t lo = s_lo, hi = s_hi;
-        if (hi <= lo) break;
-        const int64_t step = (hi - lo + blockDim.x) / blockDim.x;
-        const int64_t idx = lo + (int64_t)threadIdx.x * step;
-        const bool ok = idx <= hi && off[idx] <= e;
-        const int cnt = __syncthreads_count(ok);  // probes are monotone: a true prefix
-        if (threadIdx.x == 0) {
-            const int64_t nlo = lo + (int64_t)(cnt - 1) * step;
-            s_lo = nlo;
-            s_hi = min(hi, nlo + step - 1);
-        }
-        __syncthreads();
-    }
-    const int64_t r = s_lo;
-    __syncthreads();
-    return r;
-}
-
-__device__ __forceinline__ int64_t owner_rank(const int64_t *__restrict__ off, int64_t lo,
-                                              int64_t hi, int64_t e) {
-    // largest r in [lo, hi] with off[r] <= e
-    while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (off[mid] <= e) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
-
+// One thread per rank writes its (clipped) rect's tiles row-major, i.e. in
+// ascending tile id -- the order _fill_tile_entries visits them.  Adjacent
+// ranks own adjacent slot ranges, so a warp's stores stay clustered.
 __global__ void __launch_bounds__(256) emit_kernel(int64_t m, const int4 *__restrict__ rect_sorted,
                                                    const int64_t *__restrict__ emit_off,
                                                    int tiles_x, int row_lo, int row_hi,
                                                    uint32_t *__restrict__ tile_keys,
                                                    int32_t *__restrict__ tile_vals) {
-    __shared__ int64_t s_off[EMIT_CHUNK + 1];
-    const int64_t E = emit_off[m];
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const int4 rc = rect_sorted[r];
+    const int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
+    int64_t o = emit_off[r];
     const uint32_t base_tile = (uint32_t)row_lo * (uint32_t)tiles_x;
-    for (int64_t c0 = (int64_t)blockIdx.x * EMIT_CHUNK; c0 < E;
-         c0 += (int64_t)gridDim.x * EMIT_CHUNK) {
-        const int64_t r0 = owner_rank_block(emit_off, m, c0);
-        const int nr = (int)min((int64_t)EMIT_CHUNK + 1, m + 1 - r0);
-        for (int i = threadIdx.x; i < nr; i += blockDim.x) s_off[i] = emit_off[r0 + i];
-        __syncthreads();
-        for (int t = threadIdx.x; t < EMIT_CHUNK; t += blockDim.x) {
-            const int64_t e = c0 + t;
-            if (e >= E) break;
-            int64_t r, base;
-            if (e < s_off[nr - 1] || r0 + nr - 1 == m) {
-                int lo = 0, hi = nr - 2;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (s_off[mid] <= e) lo = mid;
-                    else hi = mid - 1;
-                }
-                r = r0 + lo;
-                base = s_off[lo];
-            } else {  // more empty ranks than staged: fall back to global memory
-                r = owner_rank(emit_off, r0, m - 1, e);
-                base = emit_off[r];
-            }
-            const int4 rc = rect_sorted[r];
-            const int y0 = max(rc.y, row_lo);
-            const int w = rc.z - rc.x + 1;
-            const int k = (int)(e - base);
-            const int dy = k / w;
-            const int ty = y0 + dy, tx = rc.x + (k - dy * w);
-            tile_keys[e] = (uint32_t)ty * (uint32_t)tiles_x + (uint32_t)tx - base_tile;
-            tile_vals[e] = (int32_t)r;
+    for (int ty = y0; ty <= y1; ty++) {
+        const uint32_t rowbase = (uint32_t)ty * (uint32_t)tiles_x - base_tile;
+        for (int tx = rc.x; tx <= rc.z; tx++, o++) {
+            tile_keys[o] = rowbase + (uint32_t)tx;
+            tile_vals[o] = (int32_t)r;
         }
-        __syncthreads();
     }
 }
 
@@ -221,11 +152,7 @@ extern "C" int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t
                             int32_t *tile_vals, void *stream) {
     if (m < 0 || tiles_x <= 0) return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
-    int sms = 148;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    emit_kernel<<<sms * 4, 256, 0, (cudaStream_t)stream>>>(
+    emit_kernel<<<blocks_for(m, 256), 256, 0, (cudaStream_t)stream>>>(
         m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals);
     ISG_CHECK_LAUNCH();
     return 0;

@@ -32,7 +32,7 @@ __device__ __forceinline__ void store_feat<double>(double *base, const double (&
 
 // _kernels.py:144-198 (+ the `keep` compaction flag of rasterizer.py:142-158).
 template <typename P, typename F>
-__global__ void __launch_bounds__(256) preprocess_kernel(isg_params p, Cam cam, int tile,
+__global__ void __launch_bounds__(128, 6) preprocess_kernel(isg_params p, Cam cam, int tile,
                                                          int tiles_x, int tiles_y, uint64_t *key,
                                                          int4 *rect, F *feat, uint8_t *flag,
                                                          double *full64) {
@@ -479,22 +479,22 @@ extern "C" int isg_preprocess(const isg_params *p, const isg_camera *cam, int32_
     int tiles_x = (cam->width + tile_size - 1) / tile_size;
     int tiles_y = (cam->height + tile_size - 1) / tile_size;
     cudaStream_t s = (cudaStream_t)stream;
-    dim3 grid(blocks_for(p->n, 256));
+    dim3 grid(blocks_for(p->n, 128));
     int4 *rect = reinterpret_cast<int4 *>(out->rect);
     if (p->dtype == ISG_F32 && out->feat_dtype == ISG_F32)
-        preprocess_kernel<float, float><<<grid, 256, 0, s>>>(*p, c, tile_size, tiles_x, tiles_y,
+        preprocess_kernel<float, float><<<grid, 128, 0, s>>>(*p, c, tile_size, tiles_x, tiles_y,
                                                              out->key, rect, (float *)out->feat,
                                                              out->flag, out->full64);
     else if (p->dtype == ISG_F32 && out->feat_dtype == ISG_F64)
-        preprocess_kernel<float, double><<<grid, 256, 0, s>>>(*p, c, tile_size, tiles_x, tiles_y,
+        preprocess_kernel<float, double><<<grid, 128, 0, s>>>(*p, c, tile_size, tiles_x, tiles_y,
                                                               out->key, rect, (double *)out->feat,
                                                               out->flag, out->full64);
     else if (p->dtype == ISG_F64 && out->feat_dtype == ISG_F32)
-        preprocess_kernel<double, float><<<grid, 256, 0, s>>>(*p, c, tile_size, tiles_x, tiles_y,
+        preprocess_kernel<double, float><<<grid, 128, 0, s>>>(*p, c, tile_size, tiles_x, tiles_y,
                                                               out->key, rect, (float *)out->feat,
                                                               out->flag, out->full64);
     else if (p->dtype == ISG_F64 && out->feat_dtype == ISG_F64)
-        preprocess_kernel<double, double><<<grid, 256, 0, s>>>(
+        preprocess_kernel<double, double><<<grid, 128, 0, s>>>(
             *p, c, tile_size, tiles_x, tiles_y, out->key, rect, (double *)out->feat, out->flag,
             out->full64);
     else

@@ -318,19 +318,13 @@ __global__ void __launch_bounds__(256) reduce_ordered_kernel(
     int64_t m, const int64_t *__restrict__ emit_off, const T *__restrict__ partials,
     const int32_t *__restrict__ order, const int4 *__restrict__ rect_sorted, int row_lo,
     int row_hi, int canon_rows, double *__restrict__ grad2d, double *__restrict__ grad_norm) {
-    // The block's 256 ranks own the contiguous slot range [P0, P1); it is
-    // staged through shared memory in coalesced chunks and every thread folds
-    // its own slots sequentially (the fold order never depends on chunking).
-    constexpr int CH = sizeof(T) == 4 ? 1024 : 512;
-    __shared__ T s_part[CH * 9];
-    const int64_t rb = (int64_t)blockIdx.x * blockDim.x;
-    const int64_t r = rb + threadIdx.x;
-    const bool valid = r < m;
-    const int64_t rend = min(rb + (int64_t)blockDim.x, m);
-    const int64_t P0 = emit_off[rb], P1 = emit_off[rend];
-    const int64_t p0 = valid ? emit_off[r] : 0, p1 = valid ? emit_off[r + 1] : 0;
+    // One thread per rank: its slots are contiguous and already in ascending
+    // tile order; they are folded sequentially (block sums when canon_rows > 0).
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    const int64_t p0 = emit_off[r], p1 = emit_off[r + 1];
     int y0 = 0, w = 1;
-    if (valid && canon_rows > 0 && p1 > p0) {
+    if (canon_rows > 0 && p1 > p0) {
         const int4 rc = rect_sorted[r];
         y0 = max(rc.y, row_lo);
         w = rc.z - rc.x + 1;
@@ -338,40 +332,25 @@ __global__ void __launch_bounds__(256) reduce_ordered_kernel(
     double acc[9], bs[9];
 #pragma unroll
     for (int k = 0; k < 9; k++) acc[k] = bs[k] = 0.0;
-    int cur = -1;  // canonical block of the slots in bs (single block if canon_rows <= 0)
-    for (int64_t c0 = P0; c0 < P1; c0 += CH) {
-        const int64_t c1 = min(c0 + CH, P1);
-        const T *src = partials + 9 * c0;
-        const int nval = (int)(9 * (c1 - c0));
-        for (int i = threadIdx.x; i < nval; i += blockDim.x) s_part[i] = src[i];
-        __syncthreads();
-        const int64_t a = max(p0, c0), b = min(p1, c1);
-        if (a < b) {
-            int rel = (int)(a - p0);
-            int dy = canon_rows > 0 ? rel / w : 0;
-            int dx = rel - dy * w;
-            for (int64_t p = a; p < b; p++) {
-                const int blk = canon_rows > 0 ? (y0 + dy) / canon_rows : 0;
-                if (blk != cur) {
+    int cur = -1, dy = 0, dx = 0;
+    for (int64_t p = p0; p < p1; p++) {
+        const int blk = canon_rows > 0 ? (y0 + dy) / canon_rows : 0;
+        if (blk != cur) {
 #pragma unroll
-                    for (int k = 0; k < 9; k++) {
-                        acc[k] += bs[k];
-                        bs[k] = 0.0;
-                    }
-                    cur = blk;
-                }
-                const T *v = s_part + 9 * (p - c0);
-#pragma unroll
-                for (int k = 0; k < 9; k++) bs[k] += (double)v[k];
-                if (++dx == w) {
-                    dx = 0;
-                    dy++;
-                }
+            for (int k = 0; k < 9; k++) {
+                acc[k] += bs[k];
+                bs[k] = 0.0;
             }
+            cur = blk;
         }
-        __syncthreads();
+        const T *v = partials + 9 * p;
+#pragma unroll
+        for (int k = 0; k < 9; k++) bs[k] += (double)__ldg(v + k);
+        if (++dx == w) {
+            dx = 0;
+            dy++;
+        }
     }
-    if (!valid) return;
 #pragma unroll
     for (int k = 0; k < 9; k++) acc[k] += bs[k];
     const int64_t row = order[r];
