@@ -12,7 +12,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libisogs.so")
+LIB_PATH = os.environ.get("ISOGS_LIB") or os.path.join(HERE, "_build", "libisogs.so")
 
 ISG_F32 = 0
 ISG_F64 = 1
