@@ -125,10 +125,37 @@ __device__ __forceinline__ unsigned quad_mask(const Staged &st, float x0, float 
 }
 
 // ------------------------------------------------------------- forward ----
+// Shared-memory accessors on 32-bit shared-window addresses, so the inner
+// loops carry one base register per array instead of re-deriving generic
+// addresses every iteration.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    // opaque copy: keeps the address in a register instead of letting the
+    // compiler re-derive the shared window base at every use
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return r;
+}
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int ldsu8(uint32_t a) {
+    unsigned short v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+    return (int)v;
+}
+
 // Warp w renders quadrant (w & 1, w >> 1) of the tile: lane (lx, ly) owns
-// pixels (lx, ly) and (lx, ly + 4) of the 8x8 quadrant.
+// pixels (lx, ly) and (lx, ly + 4) of the 8x8 quadrant.  The warp walks its
+// quadrant's culled entry list; "all pixels done" is tested every FCHK
+// entries (a finished pixel only skips work, so the late test changes no
+// result).
+constexpr int FCHK = 4;
+
 template <bool TOUCH>
-__global__ void __launch_bounds__(NT) fwd_kernel(
+__global__ void __launch_bounds__(NT, 6) fwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
     const float *__restrict__ feat, float bg0, float bg1, float bg2, void *image, int image_f64,
@@ -136,7 +163,6 @@ __global__ void __launch_bounds__(NT) fwd_kernel(
     int32_t *__restrict__ n_iter, int64_t *__restrict__ touched) {
     __shared__ float4 sgh[FB][2];
     __shared__ float4 scol[FB];
-    __shared__ int sj[FB];
     __shared__ int srank[TOUCH ? FB : 1];
     __shared__ unsigned char slist[NW][FB];
     __shared__ int qcnt[NW][NW];
@@ -150,6 +176,8 @@ __global__ void __launch_bounds__(NT) fwd_kernel(
     const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
     const float x0 = (float)(tx * 16), y0 = (float)(ty * 16);
     const int e0 = offsets[tl], n_ent = offsets[tl + 1] - e0;
+    const uint32_t a_gh = smem_addr(&sgh[0][0]), a_col = smem_addr(&scol[0]);
+    const uint32_t a_list = smem_addr(&slist[warp][0]);
     float t0 = 1.0f, r0 = 0.0f, g0 = 0.0f, b0 = 0.0f;
     float t1 = 1.0f, r1 = 0.0f, g1 = 0.0f, b1 = 0.0f;
     int last0 = 0, last1 = 0, cnt0 = 0, cnt1 = 0, it0 = 0, it1 = 0;
@@ -165,7 +193,6 @@ __global__ void __launch_bounds__(NT) fwd_kernel(
             sgh[threadIdx.x][0] = st.g;
             sgh[threadIdx.x][1] = st.h;
             scol[threadIdx.x] = st.c;
-            sj[threadIdx.x] = j;
             if (TOUCH) srank[threadIdx.x] = rank;
         }
         unsigned bal[NW];
@@ -187,51 +214,55 @@ __global__ void __launch_bounds__(NT) fwd_kernel(
         }
         __syncthreads();
         const int total = qcnt[warp][0] + qcnt[warp][1] + qcnt[warp][2] + qcnt[warp][3];
-        for (int k = 0; k < total; k++) {
+        for (int k0 = 0; k0 < total; k0 += FCHK) {
             if (__all_sync(FULL, done0 && done1)) break;
-            const int slot = slist[warp][k];
-            const float4 g4 = sgh[slot][0], h4 = sgh[slot][1];
-            float A, B;
-            col_terms(fpx - g4.x, g4, A, B);
-            if (!done0) {
-                float gw;
-                const float a = pair_alpha(fpy0 - g4.y, A, B, h4, gw);
-                if (a > 0.0f) {
-                    const float test = t0 * (1.0f - a);
-                    if (test < 1e-4f) {
-                        done0 = true;
-                        it0 = sj[slot] + 1;
-                    } else {
-                        const float4 c = scol[slot];
-                        const float w = a * t0;
-                        r0 = fmaf(c.x, w, r0);
-                        g0 = fmaf(c.y, w, g0);
-                        b0 = fmaf(c.z, w, b0);
-                        t0 = test;
-                        last0 = sj[slot] + 1;
-                        cnt0++;
-                        if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
+            const int kend = min(k0 + FCHK, total);
+            for (int k = k0; k < kend; k++) {
+                const int slot = ldsu8(a_list + k);
+                const uint32_t ag = a_gh + 32 * slot;
+                const float4 g4 = lds4(ag), h4 = lds4(ag + 16);
+                float A, B;
+                col_terms(fpx - g4.x, g4, A, B);
+                if (!done0) {
+                    float gw;
+                    const float a = pair_alpha(fpy0 - g4.y, A, B, h4, gw);
+                    if (a > 0.0f) {
+                        const float test = t0 * (1.0f - a);
+                        if (test < 1e-4f) {
+                            done0 = true;
+                            it0 = base + slot + 1;
+                        } else {
+                            const float4 c = lds4(a_col + 16 * slot);
+                            const float w = a * t0;
+                            r0 = fmaf(c.x, w, r0);
+                            g0 = fmaf(c.y, w, g0);
+                            b0 = fmaf(c.z, w, b0);
+                            t0 = test;
+                            last0 = base + slot + 1;
+                            cnt0++;
+                            if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
+                        }
                     }
                 }
-            }
-            if (!done1) {
-                float gw;
-                const float a = pair_alpha(fpy1 - g4.y, A, B, h4, gw);
-                if (a > 0.0f) {
-                    const float test = t1 * (1.0f - a);
-                    if (test < 1e-4f) {
-                        done1 = true;
-                        it1 = sj[slot] + 1;
-                    } else {
-                        const float4 c = scol[slot];
-                        const float w = a * t1;
-                        r1 = fmaf(c.x, w, r1);
-                        g1 = fmaf(c.y, w, g1);
-                        b1 = fmaf(c.z, w, b1);
-                        t1 = test;
-                        last1 = sj[slot] + 1;
-                        cnt1++;
-                        if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
+                if (!done1) {
+                    float gw;
+                    const float a = pair_alpha(fpy1 - g4.y, A, B, h4, gw);
+                    if (a > 0.0f) {
+                        const float test = t1 * (1.0f - a);
+                        if (test < 1e-4f) {
+                            done1 = true;
+                            it1 = base + slot + 1;
+                        } else {
+                            const float4 c = lds4(a_col + 16 * slot);
+                            const float w = a * t1;
+                            r1 = fmaf(c.x, w, r1);
+                            g1 = fmaf(c.y, w, g1);
+                            b1 = fmaf(c.z, w, b1);
+                            t1 = test;
+                            last1 = base + slot + 1;
+                            cnt1++;
+                            if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
+                        }
                     }
                 }
             }
@@ -369,7 +400,6 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
     const DL *__restrict__ dl, float *__restrict__ partials) {
     __shared__ float4 sgh[FB][2];
     __shared__ float4 scol[FB];
-    __shared__ int sj[FB];
     __shared__ int64_t sslot[FB];
     __shared__ unsigned char smask[FB];
     __shared__ unsigned char slist[NW][FB];
@@ -387,6 +417,8 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
     const float x0 = (float)(tx * 16), y0 = (float)(ty * 16);
     const int e0 = offsets[tl], n_ent = offsets[tl + 1] - e0;
     const int my_slot = bfly_slot(lane);
+    const uint32_t a_gh = smem_addr(&sgh[0][0]), a_col = smem_addr(&scol[0]);
+    const uint32_t a_list = smem_addr(&slist[warp][0]);
 
     int last0 = 0, last1 = 0;
     float T0 = 0.0f, T1 = 0.0f, wr0 = 0, wg0 = 0, wb0 = 0, wr1 = 0, wg1 = 0, wb1 = 0;
@@ -444,7 +476,6 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
                 sgh[threadIdx.x][1] = st.h;
                 scol[threadIdx.x] = st.c;
             }
-            sj[threadIdx.x] = j;
             sslot[threadIdx.x] = slot;
             if (mask == 0u) {
                 float *dst = partials + 9 * slot;
@@ -473,14 +504,15 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
         __syncthreads();
         const int total = qcnt[warp][0] + qcnt[warp][1] + qcnt[warp][2] + qcnt[warp][3];
         for (int k = total - 1; k >= 0; k--) {
-            const int slot = slist[warp][k];
-            const float4 g4 = sgh[slot][0], h4 = sgh[slot][1];
-            const int jj = sj[slot];
+            const int slot = ldsu8(a_list + k);
+            const uint32_t ag = a_gh + 32 * slot;
+            const float4 g4 = lds4(ag), h4 = lds4(ag + 16);
+            const int jj = start + slot;
             float v[9];
 #pragma unroll
             for (int q = 0; q < 9; q++) v[q] = 0.0f;
             bool act = false;
-            const EntryB e = entry_terms(fpx, g4, h4, scol[slot]);
+            const EntryB e = entry_terms(fpx, g4, h4, lds4(a_col + 16 * slot));
             if (jj < last0) {
                 float gw;
                 const float d1 = fpy0 - g4.y;
