@@ -340,54 +340,45 @@ __device__ __forceinline__ float rcpa(float x) {
 }
 
 // Per-entry quantities shared by a thread's two pixels (same column).
-struct EntryB {
-    float A, B;        // exponent column terms (col_terms)
-    float d0, q00;     // x offset, -d0^2/2
-    float P0, P1;      // a d0, b d0  (conic a = -2 g.z, b = -g.w, c = -2 h.x)
-    float b, c, op;
-    float4 col;
-};
-
-__device__ __forceinline__ EntryB entry_terms(float fpx, const float4 &g4, const float4 &h4,
-                                              const float4 &col) {
-    EntryB e;
-    e.d0 = fpx - g4.x;
-    col_terms(e.d0, g4, e.A, e.B);
-    e.q00 = -0.5f * e.d0 * e.d0;
-    e.b = -g4.w;
-    e.c = -2.0f * h4.x;
-    e.P0 = -2.0f * g4.z * e.d0;
-    e.P1 = e.b * e.d0;
-    e.op = h4.z;
-    e.col = col;
-    return e;
-}
-
-__device__ __forceinline__ void pair_grad(float a, float gw, float d1, const EntryB &e, float wr,
-                                          float wg, float wb, float &T, float &sr, float &sg,
-                                          float &sb, float (&v)[9]) {
+// Per pixel the backward keeps T and Q = sum_c dL/dC_c * S_c (the reference's
+// three running sums S_c only ever enter dalpha through this dot product), so
+//   dalpha = wc * T_before - Q / (1 - alpha),  Q += wc * alpha * T_before,
+// with wc = sum_c dL/dC_c * colour_c.  The conic and mean terms are moments
+// of dpower over the thread's pixels (s0 = sum dp, s1 = sum dp d1,
+// s2 = sum dp d1^2; d0 is shared), expanded once per entry by finish_terms.
+__device__ __forceinline__ void pair_grad(float a, float gw, float d1, float op, float wc, float wr,
+                                          float wg, float wb, float &T, float &Q, float (&v)[9],
+                                          float &s0, float &s1, float &s2) {
     const float inv = rcpa(1.0f - a);
     const float ti = T * inv;  // T before this splat
     const float at = a * ti;
     v[5] = fmaf(wr, at, v[5]);
     v[6] = fmaf(wg, at, v[6]);
     v[7] = fmaf(wb, at, v[7]);
-    const float dalpha = wr * fmaf(e.col.x, ti, -sr * inv) + wg * fmaf(e.col.y, ti, -sg * inv) +
-                         wb * fmaf(e.col.z, ti, -sb * inv);
-    sr = fmaf(e.col.x, at, sr);
-    sg = fmaf(e.col.y, at, sg);
-    sb = fmaf(e.col.z, at, sb);
-    if (!(__fmul_rn(e.op, gw) > 0.99f)) {  // clamped alpha: zero sub-gradient
+    const float dalpha = fmaf(wc, ti, -(Q * inv));
+    Q = fmaf(wc, at, Q);
+    if (!(__fmul_rn(op, gw) > 0.99f)) {  // clamped alpha: zero sub-gradient
         const float dg = dalpha * gw;
         v[8] += dg;
-        const float dpower = dg * e.op;
-        v[2] = fmaf(dpower, e.q00, v[2]);
-        v[3] = fmaf(dpower, -(e.d0 * d1), v[3]);
-        v[4] = fmaf(dpower, -0.5f * d1 * d1, v[4]);
-        v[0] = fmaf(dpower, fmaf(e.b, d1, e.P0), v[0]);
-        v[1] = fmaf(dpower, fmaf(e.c, d1, e.P1), v[1]);
+        const float dp = dg * op;
+        const float t = dp * d1;
+        s0 += dp;
+        s1 += t;
+        s2 = fmaf(t, d1, s2);
     }
     T = ti;
+}
+
+// v[0..4] from the dpower moments: dmean = dp (a d0 + b d1, b d0 + c d1),
+// dconic = dp (-d0^2/2, -d0 d1, -d1^2/2)  (_kernels.py:363-374).
+__device__ __forceinline__ void finish_terms(float d0, const float4 &g4, const float4 &h4,
+                                             float s0, float s1, float s2, float (&v)[9]) {
+    const float a = -2.0f * g4.z, b = -g4.w, c = -2.0f * h4.x;
+    v[0] = fmaf(b, s1, (a * d0) * s0);
+    v[1] = fmaf(c, s1, (b * d0) * s0);
+    v[2] = (-0.5f * d0) * d0 * s0;
+    v[3] = -d0 * s1;
+    v[4] = -0.5f * s2;
 }
 
 template <typename DL>
@@ -438,8 +429,9 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
         wg1 = (float)dl[3 * pix + 1];
         wb1 = (float)dl[3 * pix + 2];
     }
-    float sr0 = T0 * bg0, sg0 = T0 * bg1, sb0 = T0 * bg2;
-    float sr1 = T1 * bg0, sg1 = T1 * bg1, sb1 = T1 * bg2;
+    // Q = sum_c w_c S_c with S_c starting at T_final * bg_c
+    float Q0 = wr0 * (T0 * bg0) + wg0 * (T0 * bg1) + wb0 * (T0 * bg2);
+    float Q1 = wr1 * (T1 * bg0) + wg1 * (T1 * bg1) + wb1 * (T1 * bg2);
     int m = max(last0, last1);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
@@ -511,28 +503,31 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
             float v[9];
 #pragma unroll
             for (int q = 0; q < 9; q++) v[q] = 0.0f;
-            bool act = false;
-            const EntryB e = entry_terms(fpx, g4, h4, lds4(a_col + 16 * slot));
+            float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;
+            const float d0 = fpx - g4.x;
+            float A, B;
+            col_terms(d0, g4, A, B);
+            const float4 col = lds4(a_col + 16 * slot);
             if (jj < last0) {
                 float gw;
                 const float d1 = fpy0 - g4.y;
-                const float a = pair_alpha(d1, e.A, e.B, h4, gw);
+                const float a = pair_alpha(d1, A, B, h4, gw);
                 if (a > 0.0f) {
-                    act = true;
-                    pair_grad(a, gw, d1, e, wr0, wg0, wb0, T0, sr0, sg0, sb0, v);
+                    const float wc = fmaf(wb0, col.z, fmaf(wg0, col.y, wr0 * col.x));
+                    pair_grad(a, gw, d1, h4.z, wc, wr0, wg0, wb0, T0, Q0, v, s0, s1, s2);
                 }
             }
             if (jj < last1) {
                 float gw;
                 const float d1 = fpy1 - g4.y;
-                const float a = pair_alpha(d1, e.A, e.B, h4, gw);
+                const float a = pair_alpha(d1, A, B, h4, gw);
                 if (a > 0.0f) {
-                    act = true;
-                    pair_grad(a, gw, d1, e, wr1, wg1, wb1, T1, sr1, sg1, sb1, v);
+                    const float wc = fmaf(wb1, col.z, fmaf(wg1, col.y, wr1 * col.x));
+                    pair_grad(a, gw, d1, h4.z, wc, wr1, wg1, wb1, T1, Q1, v, s0, s1, s2);
                 }
             }
-            float y = 0.0f;
-            if (__any_sync(FULL, act)) y = bfly9(v, lane);
+            finish_terms(d0, g4, h4, s0, s1, s2, v);
+            const float y = bfly9(v, lane);
             if (my_slot >= 0) sred[warp][slot][my_slot] = y;
         }
         __syncthreads();
