@@ -345,7 +345,7 @@ __device__ __forceinline__ float rcpa(float x) {
 //   dalpha = wc * T_before - Q / (1 - alpha),  Q += wc * alpha * T_before,
 // with wc = sum_c dL/dC_c * colour_c.  The conic and mean terms are moments
 // of dpower over the thread's pixels (s0 = sum dp, s1 = sum dp d1,
-// s2 = sum dp d1^2; d0 is shared), expanded once per entry by finish_terms.
+// s2 = sum dp d1^2; d0 is shared), turned into linear moments by moment_terms.
 __device__ __forceinline__ void pair_grad(float a, float gw, float d1, float op, float wc, float wr,
                                           float wg, float wb, float &T, float &Q, float (&v)[9],
                                           float &s0, float &s1, float &s2) {
@@ -369,16 +369,20 @@ __device__ __forceinline__ void pair_grad(float a, float gw, float d1, float op,
     T = ti;
 }
 
-// v[0..4] from the dpower moments: dmean = dp (a d0 + b d1, b d0 + c d1),
-// dconic = dp (-d0^2/2, -d0 d1, -d1^2/2)  (_kernels.py:363-374).
-__device__ __forceinline__ void finish_terms(float d0, const float4 &g4, const float4 &h4,
-                                             float s0, float s1, float s2, float (&v)[9]) {
-    const float a = -2.0f * g4.z, b = -g4.w, c = -2.0f * h4.x;
-    v[0] = fmaf(b, s1, (a * d0) * s0);
-    v[1] = fmaf(c, s1, (b * d0) * s0);
-    v[2] = (-0.5f * d0) * d0 * s0;
-    v[3] = -d0 * s1;
-    v[4] = -0.5f * s2;
+// The conic and mean terms leave the warp as linear moments (summed over
+// lanes and quadrants like every other term):
+//   v0 = sum d0 dp, v1 = sum dp d1, v2 = sum d0^2 dp, v3 = sum d0 dp d1,
+//   v4 = sum dp d1^2
+// and are expanded once per (tile, entry) in the fold (_kernels.py:363-374):
+//   dmean = (a v0 + b v1, b v0 + c v1), dconic = (-v2/2, -v3, -v4/2).
+__device__ __forceinline__ void moment_terms(float d0, float s0, float s1, float s2,
+                                             float (&v)[9]) {
+    const float d0s0 = d0 * s0;
+    v[0] = d0s0;
+    v[1] = s1;
+    v[2] = d0 * d0s0;
+    v[3] = d0 * s1;
+    v[4] = s2;
 }
 
 template <typename DL>
@@ -526,21 +530,35 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
                     pair_grad(a, gw, d1, h4.z, wc, wr1, wg1, wb1, T1, Q1, v, s0, s1, s2);
                 }
             }
-            finish_terms(d0, g4, h4, s0, s1, s2, v);
+            moment_terms(d0, s0, s1, s2, v);
             const float y = bfly9(v, lane);
             if (my_slot >= 0) sred[warp][slot][my_slot] = y;
         }
         __syncthreads();
-        // fixed-order fold over the quadrants that saw the entry
-        for (int idx = threadIdx.x; idx < (end - start) * 9; idx += NT) {
-            const int s = idx / 9, q = idx - s * 9;
+        // fixed-order fold over the quadrants that saw the entry, then the
+        // moment expansion of the conic and mean terms
+        for (int s = threadIdx.x; s < end - start; s += NT) {
             const unsigned mk = smask[s];
             if (mk == 0u) continue;
-            float acc = 0.0f;
+            float acc[9];
+#pragma unroll
+            for (int q = 0; q < 9; q++) acc[q] = 0.0f;
 #pragma unroll
             for (int w = 0; w < NW; w++)
-                if ((mk >> w) & 1u) acc += sred[w][s][q];
-            partials[9 * sslot[s] + q] = acc;
+                if ((mk >> w) & 1u) {
+#pragma unroll
+                    for (int q = 0; q < 9; q++) acc[q] += sred[w][s][q];
+                }
+            const float4 g4 = sgh[s][0], h4 = sgh[s][1];
+            const float a = -2.0f * g4.z, b = -g4.w, c = -2.0f * h4.x;
+            float *dst = partials + 9 * sslot[s];
+            dst[0] = fmaf(a, acc[0], b * acc[1]);
+            dst[1] = fmaf(b, acc[0], c * acc[1]);
+            dst[2] = -0.5f * acc[2];
+            dst[3] = -acc[3];
+            dst[4] = -0.5f * acc[4];
+#pragma unroll
+            for (int q = 5; q < 9; q++) dst[q] = acc[q];
         }
     }
 }
