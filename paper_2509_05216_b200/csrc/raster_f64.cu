@@ -23,6 +23,7 @@
 // per (tile, splat) -- the reference's scratch row -- into a splat-major slot
 // so the per-splat fold below reads them in ascending tile order.
 #include "common.cuh"
+#include "fold.cuh"
 #include "raster_f32.cuh"
 
 namespace isg {
@@ -322,37 +323,8 @@ __global__ void __launch_bounds__(256) reduce_ordered_kernel(
     // tile order; they are folded sequentially (block sums when canon_rows > 0).
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= m) return;
-    const int64_t p0 = emit_off[r], p1 = emit_off[r + 1];
-    int y0 = 0, w = 1;
-    if (canon_rows > 0 && p1 > p0) {
-        const int4 rc = rect_sorted[r];
-        y0 = max(rc.y, row_lo);
-        w = rc.z - rc.x + 1;
-    }
-    double acc[9], bs[9];
-#pragma unroll
-    for (int k = 0; k < 9; k++) acc[k] = bs[k] = 0.0;
-    int cur = -1, dy = 0, dx = 0;
-    for (int64_t p = p0; p < p1; p++) {
-        const int blk = canon_rows > 0 ? (y0 + dy) / canon_rows : 0;
-        if (blk != cur) {
-#pragma unroll
-            for (int k = 0; k < 9; k++) {
-                acc[k] += bs[k];
-                bs[k] = 0.0;
-            }
-            cur = blk;
-        }
-        const T *v = partials + 9 * p;
-#pragma unroll
-        for (int k = 0; k < 9; k++) bs[k] += (double)__ldg(v + k);
-        if (++dx == w) {
-            dx = 0;
-            dy++;
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < 9; k++) acc[k] += bs[k];
+    double acc[9];
+    fold_rank<T>(partials, emit_off[r], emit_off[r + 1], rect_sorted, r, row_lo, canon_rows, acc);
     const int64_t row = order[r];
     double *dst = grad2d + 9 * row;
 #pragma unroll
