@@ -67,6 +67,50 @@ __global__ void __launch_bounds__(256) emit_kernel(int64_t m, const int4 *__rest
     }
 }
 
+// Entry-parallel emission: a block of EMIT_R consecutive ranks owns the
+// contiguous slot span [emit_off[r0], emit_off[r0 + EMIT_R]); the block
+// stages the ranks' offsets and clipped rects in shared memory and writes the
+// span with consecutive threads on consecutive slots (coalesced stores).  Each
+// slot finds its rank by binary search in the staged offsets; its tile is the
+// row-major position inside the rank's rect -- the same (tile, rank) pairs in
+// the same slots as emit_kernel.
+constexpr int EMIT_R = 256;
+
+__global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
+                                                        const int4 *__restrict__ rect_sorted,
+                                                        const int64_t *__restrict__ emit_off,
+                                                        int tiles_x, int row_lo, int row_hi,
+                                                        uint32_t *__restrict__ tile_keys,
+                                                        int32_t *__restrict__ tile_vals) {
+    __shared__ int64_t soff[EMIT_R + 1];
+    __shared__ int4 srect[EMIT_R];
+    const int64_t r0 = (int64_t)blockIdx.x * EMIT_R;
+    const int nr = (int)min((int64_t)EMIT_R, m - r0);
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) soff[i] = emit_off[r0 + i];
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+        int4 rc = rect_sorted[r0 + i];
+        rc.y = max(rc.y, row_lo);  // clipped rows, width in .w
+        rc.w = rc.z - rc.x + 1;
+        srect[i] = rc;
+    }
+    __syncthreads();
+    const int64_t s0 = soff[0], s1 = soff[nr];
+    const uint32_t base_tile = (uint32_t)row_lo * (uint32_t)tiles_x;
+    for (int64_t o = s0 + threadIdx.x; o < s1; o += blockDim.x) {
+        int lo = 0, hi = nr;  // last i with soff[i] <= o (ranks with no slots are skipped)
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (soff[mid] <= o) lo = mid;
+            else hi = mid;
+        }
+        const int4 rc = srect[lo];
+        const int k = (int)(o - soff[lo]);
+        const int dy = k / rc.w, dx = k - dy * rc.w;
+        tile_keys[o] = (uint32_t)(rc.y + dy) * (uint32_t)tiles_x - base_tile + (uint32_t)(rc.x + dx);
+        tile_vals[o] = (int32_t)(r0 + lo);
+    }
+}
+
 __global__ void tile_offsets_kernel(int64_t e, const uint32_t *__restrict__ keys, int n_tiles,
                                     int32_t *__restrict__ offsets) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -152,7 +196,7 @@ extern "C" int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t
                             int32_t *tile_vals, void *stream) {
     if (m < 0 || tiles_x <= 0) return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
-    emit_kernel<<<blocks_for(m, 256), 256, 0, (cudaStream_t)stream>>>(
+    emit_span_kernel<<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
         m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals);
     ISG_CHECK_LAUNCH();
     return 0;

@@ -12,22 +12,30 @@
 
 namespace isg {
 
-template <typename T>
-__device__ __forceinline__ void fold_rank(const T *__restrict__ partials, int64_t p0, int64_t p1,
-                                          const int4 *__restrict__ rect_sorted, int64_t r,
-                                          int row_lo, int canon_rows, double (&acc)[9]) {
-    int y0 = 0, w = 1;
-    if (canon_rows > 0 && p1 > p0) {
-        const int4 rc = rect_sorted[r];
-        y0 = max(rc.y, row_lo);
-        w = rc.z - rc.x + 1;
-    }
-    double bs[9];
+// Running state of one rank's fold; step() consumes the next slot's 9 terms.
+struct FoldState {
+    double acc[9], bs[9];
+    int y0, w, cur, dy, dx, canon;
+
+    __device__ __forceinline__ void init(const int4 *__restrict__ rect_sorted, int64_t r,
+                                         int64_t n_slots, int row_lo, int canon_rows) {
+        y0 = 0;
+        w = 1;
+        if (canon_rows > 0 && n_slots > 0) {
+            const int4 rc = rect_sorted[r];
+            y0 = max(rc.y, row_lo);
+            w = rc.z - rc.x + 1;
+        }
+        canon = canon_rows;
+        cur = -1;
+        dy = dx = 0;
 #pragma unroll
-    for (int k = 0; k < 9; k++) acc[k] = bs[k] = 0.0;
-    int cur = -1, dy = 0, dx = 0;
-    for (int64_t p = p0; p < p1; p++) {
-        const int blk = canon_rows > 0 ? (y0 + dy) / canon_rows : 0;
+        for (int k = 0; k < 9; k++) acc[k] = bs[k] = 0.0;
+    }
+
+    template <typename V>
+    __device__ __forceinline__ void step(const V *v) {
+        const int blk = canon > 0 ? (y0 + dy) / canon : 0;
         if (blk != cur) {
 #pragma unroll
             for (int k = 0; k < 9; k++) {
@@ -36,16 +44,30 @@ __device__ __forceinline__ void fold_rank(const T *__restrict__ partials, int64_
             }
             cur = blk;
         }
-        const T *v = partials + 9 * p;
 #pragma unroll
-        for (int k = 0; k < 9; k++) bs[k] += (double)__ldg(v + k);
+        for (int k = 0; k < 9; k++) bs[k] += (double)v[k];
         if (++dx == w) {
             dx = 0;
             dy++;
         }
     }
+
+    __device__ __forceinline__ void finish() {
 #pragma unroll
-    for (int k = 0; k < 9; k++) acc[k] += bs[k];
+        for (int k = 0; k < 9; k++) acc[k] += bs[k];
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ void fold_rank(const T *__restrict__ partials, int64_t p0, int64_t p1,
+                                          const int4 *__restrict__ rect_sorted, int64_t r,
+                                          int row_lo, int canon_rows, double (&acc)[9]) {
+    FoldState st;
+    st.init(rect_sorted, r, p1 - p0, row_lo, canon_rows);
+    for (int64_t p = p0; p < p1; p++) st.step(partials + 9 * p);
+    st.finish();
+#pragma unroll
+    for (int k = 0; k < 9; k++) acc[k] = st.acc[k];
 }
 
 }  // namespace isg

@@ -332,6 +332,50 @@ __global__ void __launch_bounds__(256) reduce_ordered_kernel(
     if (grad_norm) grad_norm[row] = hypot(acc[0], acc[1]);
 }
 
+// float32 subtotals: a block of 256 consecutive ranks owns one contiguous
+// span of slots (emit_off is monotone); the span is streamed through shared
+// memory in chunks with coalesced 16-byte loads and every thread folds its own
+// slots from there -- the same FoldState arithmetic as fold_rank.
+constexpr int RED_THREADS = 128;
+constexpr int RED_CHUNK = 1024;  // slots per chunk (36 KB): one chunk for most blocks
+
+__global__ void __launch_bounds__(RED_THREADS) reduce_ordered_f32_kernel(
+    int64_t m, const int64_t *__restrict__ emit_off, const float *__restrict__ partials,
+    const int32_t *__restrict__ order, const int4 *__restrict__ rect_sorted, int row_lo,
+    int canon_rows, double *__restrict__ grad2d, double *__restrict__ grad_norm) {
+    __shared__ __align__(16) float sbuf[RED_CHUNK * 9 + 4];
+    const int64_t r0 = (int64_t)blockIdx.x * RED_THREADS;
+    const int64_t r = r0 + threadIdx.x;
+    const bool live = r < m;
+    const int64_t span0 = emit_off[r0];
+    const int64_t span1 = emit_off[min(r0 + RED_THREADS, m)];
+    int64_t p = live ? emit_off[r] : 0;
+    const int64_t p1 = live ? emit_off[r + 1] : 0;
+    FoldState st;
+    st.init(rect_sorted, r, live ? p1 - p : 0, row_lo, canon_rows);
+    // chunk starts aligned to 4 slots so the float offset is a multiple of 4
+    for (int64_t c0 = span0 & ~3ll; c0 < span1; c0 += RED_CHUNK) {
+        const int64_t c1 = min(c0 + RED_CHUNK, span1);
+        const int64_t f0 = 9 * c0, nf = 9 * (c1 - c0);
+        const float4 *src = reinterpret_cast<const float4 *>(partials + f0);
+        const int n4 = (int)(nf >> 2);
+        __syncthreads();
+        for (int i = threadIdx.x; i < n4; i += RED_THREADS)
+            reinterpret_cast<float4 *>(sbuf)[i] = __ldg(src + i);
+        for (int i = 4 * n4 + threadIdx.x; i < nf; i += RED_THREADS) sbuf[i] = __ldg(partials + f0 + i);
+        __syncthreads();
+        const int64_t e = min(p1, c1);
+        for (; p < e; p++) st.step(sbuf + 9 * (p - c0));
+    }
+    if (!live) return;
+    st.finish();
+    const int64_t row = order[r];
+    double *dst = grad2d + 9 * row;
+#pragma unroll
+    for (int k = 0; k < 9; k++) dst[k] = st.acc[k];
+    if (grad_norm) grad_norm[row] = hypot(st.acc[0], st.acc[1]);
+}
+
 }  // namespace isg
 
 using namespace isg;
@@ -422,8 +466,8 @@ extern "C" int isg_reduce_ordered(int32_t feat_dtype, int64_t m, const int64_t *
     if (m == 0) return 0;
     cudaStream_t s = (cudaStream_t)stream;
     if (feat_dtype == ISG_F32)
-        reduce_ordered_kernel<float><<<blocks_for(m, 256), 256, 0, s>>>(
-            m, emit_off, (const float *)partials, order, rs, row_lo, row_hi, canon_rows, grad2d,
+        reduce_ordered_f32_kernel<<<blocks_for(m, RED_THREADS), RED_THREADS, 0, s>>>(
+            m, emit_off, (const float *)partials, order, rs, row_lo, canon_rows, grad2d,
             grad_norm);
     else if (feat_dtype == ISG_F64)
         reduce_ordered_kernel<double><<<blocks_for(m, 256), 256, 0, s>>>(
