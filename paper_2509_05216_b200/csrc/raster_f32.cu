@@ -29,8 +29,14 @@ namespace f32 {
 
 constexpr int NT = 128;  // threads per tile (2 pixels each)
 constexpr int NW = NT / 32;
-constexpr int FB = 128;  // forward staging batch
-constexpr int BB = 32;   // backward staging batch
+constexpr int FB = 128;  // staging batch (entries)
+#ifndef BWD_MINB
+#define BWD_MINB 8
+#endif
+#ifndef BWD_BATCH
+#define BWD_BATCH 128
+#endif
+constexpr int BB = BWD_BATCH;  // backward staging batch (entries)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 constexpr unsigned FULL = 0xffffffffu;
@@ -386,20 +392,20 @@ __device__ __forceinline__ void moment_terms(float d0, float s0, float s1, float
 }
 
 template <typename DL>
-__global__ void __launch_bounds__(NT) bwd_kernel(
+__global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
     const float *__restrict__ feat, const int4 *__restrict__ rect_sorted,
     const int64_t *__restrict__ emit_off, float bg0, float bg1, float bg2,
     const float *__restrict__ t_final, const int32_t *__restrict__ n_last,
     const DL *__restrict__ dl, float *__restrict__ partials) {
-    __shared__ float4 sgh[FB][2];
-    __shared__ float4 scol[FB];
-    __shared__ int64_t sslot[FB];
-    __shared__ unsigned char smask[FB];
-    __shared__ unsigned char slist[NW][FB];
+    __shared__ float4 sgh[BB][2];
+    __shared__ float4 scol[BB];
+    __shared__ int64_t sslot[BB];
+    __shared__ unsigned char smask[BB];
+    __shared__ unsigned char slist[NW][BB];
     __shared__ int qcnt[NW][NW];
-    __shared__ float sred[NW][FB][9];
+    __shared__ float sred[NW][BB][9];
     __shared__ int wmax[NW];
     const int tl = blockIdx.x;
     const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
@@ -447,8 +453,8 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
 
     // Batches [start, end) walked back to front; quadrant q only sees entries
     // j < wmax[q] (no pixel of the quadrant composited anything later).
-    for (int end = n_ent; end > 0; end -= FB) {
-        const int start = max(end - FB, 0);
+    for (int end = n_ent; end > 0; end -= BB) {
+        const int start = max(end - BB, 0);
         __syncthreads();
         const int j = start + (int)threadIdx.x;
         unsigned mask = 0u;
@@ -479,7 +485,7 @@ __global__ void __launch_bounds__(NT) bwd_kernel(
                 for (int q = 0; q < 9; q++) dst[q] = 0.0f;
             }
         }
-        smask[threadIdx.x] = (unsigned char)mask;
+        if (threadIdx.x < BB) smask[threadIdx.x] = (unsigned char)mask;
         unsigned bal[NW];
 #pragma unroll
         for (int q = 0; q < NW; q++) {
