@@ -8,6 +8,7 @@ include/isogs.h (libisogs.so, loaded by _lib.py); there is no CPU fallback.
 """
 
 from .camera import Camera, OrbitSpec, look_at, make_orbit
+from .densify import DensifyMapping, densify_and_prune
 from .gaussians import PARAM_NAMES, GaussianCloud, cloud_from_points, to_device_cloud
 from .metrics import loss_l1_dssim, psnr, quantize8, ssim
 from .optim import adam_init, adam_step, position_lr

@@ -310,6 +310,31 @@ class Trainer:
                       self.stats.grad_accum, r.flag, r.grad2d, r.cam_struct, self.lrs(it), it,
                       r.width, r.height, r.timer)
 
+    def densify_due(self, it: int) -> bool:
+        """engine.py:540-541."""
+        cfg = self.cfg
+        return (cfg.densify and cfg.densify_start <= it <= cfg.effective_densify_stop()
+                and it % cfg.densify_interval == 0)
+
+    def densify(self, it: int) -> None:
+        """Single-worker _densify_step (engine.py:307-382): densify_and_prune
+        with global ids = row indices, Adam moments of kept rows carried, new
+        rows cold, statistics restarted (a fresh _Shard)."""
+        from .densify import SPLIT_EXTENT_FRACTION, carry_moments, densify_and_prune
+        cfg = self.cfg
+        res = cfg.resolution if cfg.resolution is not None else self.r.width
+        grad_thr = cfg.effective_grad_threshold(res)
+        split_thr = (cfg.split_threshold if cfg.split_threshold is not None
+                     else SPLIT_EXTENT_FRACTION * self.scene_extent)
+        new, mapping = densify_and_prune(self.cloud, self.stats, cfg, it, grad_thr, split_thr)
+        self.m = carry_moments(self.m, mapping, new)
+        self.v = carry_moments(self.v, mapping, new)
+        self.cloud = new
+        n = new.count
+        self.stats = TrainStats(grad_accum=torch.zeros(n, dtype=torch.float64, device=self.device),
+                                seen=torch.zeros(n, dtype=torch.int64, device=self.device))
+        self.grads = None
+
     def render(self, cam) -> torch.Tensor:
         self.r.forward(self.cloud, cam)
         return self.r.image
@@ -350,10 +375,10 @@ def run_training(dataset: TrainDataset, config: TrainConfig, workers: int = 1,
         raise ValueError("workers must be >= 1")
     if config.resolution is not None and config.resolution != dataset.width:
         raise ValueError(f"config resolution {config.resolution} != dataset width {dataset.width}")
-    if config.densify_active():
-        raise NotImplementedError("densify_and_prune is the next row (SURVEY 8f); "
-                                  "set densify=False or densify_start > iterations/2")
     if workers > 1:
+        if config.densify_active():
+            raise NotImplementedError("densify/prune in the sharded engine is not implemented; "
+                                      "use workers=1 or densify=False")
         from .distributed import run_training_distributed
         return run_training_distributed(dataset, config, workers, init_cloud, evaluate)
     dev = L.require_cuda()
@@ -374,6 +399,8 @@ def run_training(dataset: TrainDataset, config: TrainConfig, workers: int = 1,
         t0 = time.perf_counter()
         v = schedule[it - 1]
         tr.step(it, dataset.cameras[v], images[v])
+        if tr.densify_due(it):
+            tr.densify(it)
         torch.cuda.synchronize()
         wall += time.perf_counter() - t0
         due = it == config.iterations or (config.eval_interval > 0 and it % config.eval_interval == 0)

@@ -2,8 +2,7 @@
 
 The hot-path fields and semantics of TrainConfig, TrainDataset, TrainStats,
 EvalRecord and TrainReport are kept verbatim so a reference user can switch.
-Densification (training.py:315-389) is the next §8(f) row and not part of
-this package yet: configs that would trigger it are rejected loudly.
+Densification (training.py:315-389) lives in densify.py.
 """
 
 from __future__ import annotations

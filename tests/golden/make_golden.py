@@ -159,7 +159,7 @@ def main():
     print("train_tiny losses", rep.iteration_losses)
 
 
-if __name__ == "__main__" and "--config1" not in sys.argv:
+if __name__ == "__main__" and "--config1" not in sys.argv and "--densify" not in sys.argv:
     main()
 
 
@@ -192,3 +192,59 @@ def config1():
 
 if __name__ == "__main__" and "--config1" in sys.argv:
     config1()
+
+
+def densify():
+    """densify_and_prune pinned on its own (training.py:315-389, clone + split
+    + prune with child sampling seeded by (seed, iteration, global id)), and a
+    short training run with densification active (engine.py:540-545)."""
+    from isosplat.training import TrainStats, densify_and_prune
+    grid = distance_field(24)
+    ds = build_dataset(grid, 8.0, views=8, resolution=48, max_points=600)
+    cloud = init_from_points(ds.points, degree=1)
+    n = cloud.count
+    rng = np.random.default_rng(21)
+    cloud.opacity_logits[rng.random(n) < 0.1] = -7.0           # prune candidates
+    cloud.log_scales += rng.normal(0.0, 0.3, cloud.log_scales.shape).astype(np.float32)
+    q = rng.standard_normal((n, 4)).astype(np.float32)
+    cloud.rotations[:] = q
+    stats = TrainStats(grad_accum=rng.exponential(1.0, n), seen=rng.integers(0, 6, n))
+    avg = stats.grad_accum / np.maximum(stats.seen, 1)
+    grad_thr = float(np.quantile(avg, 0.6))
+    max_scale = np.exp(cloud.log_scales.astype(np.float64)).max(axis=1)
+    split_thr = float(np.median(max_scale))
+    cfg = TrainConfig(seed=3, opacity_prune=0.005)
+    gids = (np.arange(n, dtype=np.int64) * 3 + 1)
+    new, mp = densify_and_prune(cloud, stats, cfg, 7, grad_threshold=grad_thr,
+                                split_threshold=split_thr, global_ids=gids)
+    out = {"seen": stats.seen, "grad_accum": stats.grad_accum, "grad_thr": grad_thr,
+           "split_thr": split_thr, "gids": gids, "seed": 3, "iteration": 7,
+           "kept": mp.kept, "cloned": mp.cloned, "split": mp.split, "pruned": mp.pruned}
+    out.update(cloud_dict(cloud, prefix="in_"))
+    out.update(cloud_dict(new, prefix="out_"))
+    np.savez_compressed(os.path.join(HERE, "densify.npz"), **out)
+    print("densify unit:", n, "->", new.count, "kept", mp.kept.size, "clone", mp.cloned.size,
+          "split", mp.split.size, "prune", mp.pruned.size)
+
+    cfg = TrainConfig(iterations=40, densify_start=10, densify_interval=10, densify_stop=30,
+                      eval_interval=20, seed=0)
+    cloud, rep = train_single(ds, cfg)
+    init = init_from_points(ds.points, degree=1)
+    out = {"images": ds.images, "points": ds.points.positions, "normals": ds.points.normals,
+           "losses": np.array(rep.iteration_losses),
+           "rec_iter": np.array([r.iteration for r in rep.records]),
+           "rec_psnr": np.array([r.psnr for r in rep.records]),
+           "rec_ssim": np.array([r.ssim for r in rep.records]),
+           "rec_gauss": np.array([r.gaussians for r in rep.records]),
+           "scene_extent": ds.scene_extent}
+    for i, c in enumerate(ds.cameras):
+        out.update(cam_dict(c, prefix=f"cam{i}_"))
+    out.update(cloud_dict(cloud, prefix="final_"))
+    out.update(cloud_dict(init, prefix="init_"))
+    np.savez_compressed(os.path.join(HERE, "train_densify.npz"), **out)
+    print("train_densify:", init.count, "->", cloud.count, "records",
+          [(r.iteration, r.gaussians, round(r.psnr, 3)) for r in rep.records])
+
+
+if __name__ == "__main__" and "--densify" in sys.argv:
+    densify()
