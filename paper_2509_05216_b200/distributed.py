@@ -636,6 +636,173 @@ class RankStep:
                       self.flag, self.grad2d, self.cam_struct, lrs, it, self.W, self.H)
 
 
+# ------------------------------------------------------- densify + rebalance --
+# _densify_step + _rebalance_step (engine.py:307-437), for contiguous shards:
+# every rank classifies its own rows (densify.classify on the rows' state,
+# children seeded by (seed, iteration, global id) with global id = shard
+# start + row), the per-rank class counts fix the single-worker new-id order
+# (all kept rows by ascending old id, then clones by parent, then the two
+# children of every split parent), the new id space is re-cut into balanced
+# contiguous shards, and rows move to their new owner with one all-to-all-v.
+# Kept rows carry their Adam moments; new rows start cold; the statistics of
+# every rank restart at zero.  The result is bitwise the single-GPU densify.
+
+def densify_local(rs: "RankStep", it: int, grad_threshold: float, split_threshold: float):
+    """Phase 1 on one rank: classify and build this rank's outgoing rows in
+    [kept, clones, children] order.  Returns (payload (R, F) float32 with the
+    23 parameter floats + m + v per row, counts (n_kept, n_clone, n_split))."""
+    from .densify import densify_and_prune
+    from .gaussians import PARAM_NAMES
+    from .training import TrainStats
+    ids = np.arange(rs.id_base, rs.id_base + rs.n, dtype=np.int64)
+    new, mp = densify_and_prune(rs.cloud, TrainStats(grad_accum=rs.grad_accum, seen=rs.seen),
+                                rs.cfg, it, grad_threshold, split_threshold, global_ids=ids)
+    nk, nc, ns = int(mp.kept.numel()), int(mp.cloned.numel()), int(mp.split.numel())
+    cols = []
+    for k in PARAM_NAMES:
+        t = getattr(new, k)
+        cols.append(t.reshape(t.shape[0], -1))
+    for st in (rs.m, rs.v):
+        for k in PARAM_NAMES:
+            t = getattr(new, k)
+            z = torch.zeros((t.shape[0], t[0].numel()), dtype=t.dtype, device=t.device)
+            if nk:
+                z[:nk] = st[k][mp.kept].reshape(nk, -1)
+            cols.append(z)
+    payload = torch.cat(cols, 1).contiguous()
+    return payload, (nk, nc, ns)
+
+
+def densify_targets(counts_all: list, rank: int, world: int):
+    """New global ids of rank `rank`'s outgoing rows (kept, clones, children
+    in order) from every rank's (kept, clone, split) counts, the new balanced
+    shard map, and the number of rows this rank sends to each destination."""
+    K = sum(c[0] for c in counts_all)
+    C = sum(c[1] for c in counts_all)
+    S = sum(c[2] for c in counts_all)
+    kb = sum(c[0] for c in counts_all[:rank])
+    cb = sum(c[1] for c in counts_all[:rank])
+    sb = sum(c[2] for c in counts_all[:rank])
+    nk, nc, ns = counts_all[rank]
+    new_ids = np.concatenate([kb + np.arange(nk), K + cb + np.arange(nc),
+                              K + C + 2 * sb + np.arange(2 * ns)]).astype(np.int64)
+    smap = partition_gaussians(K + C + 2 * S, world)
+    starts = np.asarray(smap.starts, dtype=np.int64)
+    # ids ascend inside the outgoing list, so destinations are contiguous runs
+    cuts = np.searchsorted(new_ids, starts, side="left")
+    send_counts = [int(cuts[d + 1] - cuts[d]) for d in range(world)]
+    return new_ids, smap, send_counts
+
+
+def _param_width(k: str, degree: int) -> int:
+    return {"positions": 3, "log_scales": 3, "rotations": 4, "opacity_logits": 1,
+            "sh_coeffs": 3 * (degree + 1) ** 2}[k]
+
+
+def assemble_rows(recv: torch.Tensor, recv_ids: torch.Tensor, smap: ShardMap,
+                  rank: int) -> torch.Tensor:
+    """The rows a rank received (any order) placed by their new global id:
+    row id - shard start is the new local row; every row arrives once."""
+    n_new = smap.sizes[rank]
+    if recv.shape[0] != n_new:
+        raise ProtocolError(f"rank {rank}: densify delivered {recv.shape[0]} rows, "
+                            f"expected {n_new}")
+    local = recv_ids.to(torch.int64) - smap.starts[rank]
+    if n_new and (int(local.min()) < 0 or int(local.max()) >= n_new
+                  or torch.unique(local).numel() != n_new):
+        raise ProtocolError(f"rank {rank}: densify rows do not tile the new shard")
+    rows = torch.empty_like(recv)
+    rows[local] = recv
+    return rows
+
+
+def unpack_rows(rows: torch.Tensor, degree: int) -> list:
+    """(params, m, v) dicts from the packed (R, 3 * 23) rows."""
+    from .gaussians import PARAM_NAMES
+    tails = {"positions": (3,), "log_scales": (3,), "rotations": (4,), "opacity_logits": (),
+             "sh_coeffs": ((degree + 1) ** 2, 3)}
+    n = rows.shape[0]
+    off = 0
+    groups = []
+    for _ in range(3):
+        g = {}
+        for k in PARAM_NAMES:
+            wd = _param_width(k, degree)
+            g[k] = rows[:, off:off + wd].reshape((n,) + tails[k]).contiguous()
+            off += wd
+        groups.append(g)
+    return groups
+
+
+def densify_exchange(rs, comm: "TorchComm", it: int, grad_threshold: float,
+                     split_threshold: float) -> tuple:
+    """Phases 1-3 over a process group: (this rank's new rows in new-id
+    order, the new shard map)."""
+    payload, counts = densify_local(rs, it, grad_threshold, split_threshold)
+    dev = payload.device
+    mine = torch.tensor(counts, dtype=torch.int64, device=dev)
+    allc = [torch.empty_like(mine) for _ in range(comm.world)]
+    comm.dist.all_gather(allc, mine, group=comm.group)
+    counts_all = [tuple(int(x) for x in c.tolist()) for c in allc]
+    new_ids, smap, send_counts = densify_targets(counts_all, comm.rank, comm.world)
+    recv, _ = comm.alltoallv(payload, send_counts)
+    recv_ids, _ = comm.alltoallv(torch.from_numpy(new_ids).to(dev), send_counts)
+    return assemble_rows(recv, recv_ids, smap, comm.rank), smap
+
+
+def _rank_from_rows(rs: "RankStep", rows: torch.Tensor, smap: ShardMap) -> "RankStep":
+    """New RankStep for this rank from its rows in new-id order."""
+    deg = rs.cloud.degree
+    groups = unpack_rows(rows, deg)
+    new = RankStep(rs.rank, rs.world, smap, rs.part, groups[0], deg, rs.cfg, rs.scene_extent,
+                   rs.dev, rs.cfg.background)
+    new.m, new.v = groups[1], groups[2]
+    return new
+
+
+def densify_thresholds(cfg, width: int, scene_extent: float) -> tuple:
+    from .densify import SPLIT_EXTENT_FRACTION
+    res = cfg.resolution if cfg.resolution is not None else width
+    return (cfg.effective_grad_threshold(res),
+            cfg.split_threshold if cfg.split_threshold is not None
+            else SPLIT_EXTENT_FRACTION * scene_extent)
+
+
+def densify_due(cfg, it: int) -> bool:
+    return (cfg.densify and cfg.densify_start <= it <= cfg.effective_densify_stop()
+            and it % cfg.densify_interval == 0)
+
+
+def comm_densify(rs: "RankStep", comm: "TorchComm", it: int) -> "RankStep":
+    """Densify + rebalance on this rank (multi-process): one all_gather of the
+    class counts, then two all-to-all-v (row payloads, new ids)."""
+    gt, st = densify_thresholds(rs.cfg, rs.W, rs.scene_extent)
+    rows, smap = densify_exchange(rs, comm, it, gt, st)
+    return _rank_from_rows(rs, rows, smap)
+
+
+def emulated_densify(ranks: list, it: int) -> list:
+    """The same three phases for W ranks in sequence on one GPU."""
+    W = len(ranks)
+    gt, st = densify_thresholds(ranks[0].cfg, ranks[0].W, ranks[0].scene_extent)
+    outs = [densify_local(r, it, gt, st) for r in ranks]
+    counts_all = [o[1] for o in outs]
+    plans = [densify_targets(counts_all, w, W) for w in range(W)]
+    smap = plans[0][1]
+    new_ranks = []
+    for dst in range(W):
+        parts, ids = [], []
+        for src in range(W):
+            sc = plans[src][2]
+            o = sum(sc[:dst])
+            parts.append(outs[src][0][o:o + sc[dst]])
+            ids.append(torch.from_numpy(plans[src][0][o:o + sc[dst]]))
+        rows = assemble_rows(torch.cat(parts, 0), torch.cat(ids, 0).to(ranks[dst].dev), smap,
+                             dst)
+        new_ranks.append(_rank_from_rows(ranks[dst], rows, smap))
+    return new_ranks
+
+
 # ------------------------------------------------------------------ drivers --
 
 def comm_step(rs: RankStep, comm: TorchComm, cam, gt: torch.Tensor, it: int) -> torch.Tensor:
@@ -748,6 +915,9 @@ def run_training_distributed(dataset, config, workers: int, init_cloud=None, eva
         v = schedule[it - 1]
         loss = comm_step(rs, comm, dataset.cameras[v], images[v], it)
         losses[it - 1] = loss[0]
+        if densify_due(config, it):
+            rs = comm_densify(rs, comm, it)
+            smap = partition_gaussians(sum(_all_sizes(rs, comm)), workers)
         torch.cuda.synchronize()
         wall += time.perf_counter() - t0
     # gather the shards on rank 0 (checkpoint gather, engine.py:564-590)
@@ -769,6 +939,13 @@ def run_training_distributed(dataset, config, workers: int, init_cloud=None, eva
         tr = Trainer(result, dataset.width, dataset.height, config, dataset.scene_extent, dev)
         report.records.append(tr.evaluate(dataset.cameras, images, config.iterations, wall))
     return result, report
+
+
+def _all_sizes(rs: "RankStep", comm: "TorchComm") -> list:
+    mine = torch.tensor([rs.n], dtype=torch.int64, device=rs.dev)
+    allc = [torch.empty_like(mine) for _ in range(comm.world)]
+    comm.dist.all_gather(allc, mine, group=comm.group)
+    return [int(c.item()) for c in allc]
 
 
 def bench_distributed(args, world: int, rank: int, local: int):

@@ -376,9 +376,6 @@ def run_training(dataset: TrainDataset, config: TrainConfig, workers: int = 1,
     if config.resolution is not None and config.resolution != dataset.width:
         raise ValueError(f"config resolution {config.resolution} != dataset width {dataset.width}")
     if workers > 1:
-        if config.densify_active():
-            raise NotImplementedError("densify/prune in the sharded engine is not implemented; "
-                                      "use workers=1 or densify=False")
         from .distributed import run_training_distributed
         return run_training_distributed(dataset, config, workers, init_cloud, evaluate)
     dev = L.require_cuda()

@@ -143,3 +143,84 @@ def test_collectives_world2_gloo():
         assert a2a, f"rank {rank} all-to-all-v"
         assert halo, f"rank {rank} halo"
         assert red, f"rank {rank} all-reduce"
+
+
+# ------------------------------------------- densify exchange, gloo world 2 --
+
+def _densify_inputs():
+    """Densify fixture cloud (reference make_golden.py --densify) with seeded
+    Adam moments; thresholds from the fixture."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from golden_io import cloud_from, load
+    from paper_2509_05216_b200.gaussians import PARAM_NAMES, GaussianCloud
+    d = load("densify")
+    src = cloud_from(d, "in_")
+    cloud = GaussianCloud(*(torch.from_numpy(np.ascontiguousarray(getattr(src, k)))
+                            for k in PARAM_NAMES), degree=int(src.degree))
+    g = torch.Generator().manual_seed(5)
+    m = {k: torch.randn(getattr(cloud, k).shape, generator=g) for k in PARAM_NAMES}
+    v = {k: torch.rand(getattr(cloud, k).shape, generator=g) for k in PARAM_NAMES}
+    return d, cloud, m, v
+
+
+def _densify_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from types import SimpleNamespace
+        import paper_2509_05216_b200 as P
+        from paper_2509_05216_b200.gaussians import PARAM_NAMES, GaussianCloud
+        d, cloud, m, v = _densify_inputs()
+        smap = D.partition_gaussians(cloud.count, world)
+        a, b = smap.starts[rank], smap.starts[rank + 1]
+        rs = SimpleNamespace(
+            cloud=GaussianCloud(*(getattr(cloud, k)[a:b].clone() for k in PARAM_NAMES),
+                                degree=cloud.degree),
+            m={k: m[k][a:b].clone() for k in PARAM_NAMES},
+            v={k: v[k][a:b].clone() for k in PARAM_NAMES},
+            seen=torch.from_numpy(d["seen"][a:b].copy()),
+            grad_accum=torch.from_numpy(d["grad_accum"][a:b].copy()),
+            cfg=P.TrainConfig(seed=int(d["seed"])), id_base=a, n=b - a)
+        rows, new_map = D.densify_exchange(rs, D.TorchComm(), int(d["iteration"]),
+                                           float(d["grad_thr"]), float(d["split_thr"]))
+        params, mm, vv = D.unpack_rows(rows, cloud.degree)
+        q.put((rank, {k: params[k].numpy() for k in PARAM_NAMES},
+               {k: mm[k].numpy() for k in PARAM_NAMES}, {k: vv[k].numpy() for k in PARAM_NAMES},
+               new_map.starts))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_densify_exchange_world2_gloo_equals_single():
+    """Sharded densify (local classify, global id reassignment, all-to-all-v to
+    the rebalanced contiguous shards) == one worker's densify, bit for bit."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200.densify import carry_moments
+    from paper_2509_05216_b200.gaussians import PARAM_NAMES
+    from paper_2509_05216_b200.training import TrainStats
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_densify_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = sorted([q.get(timeout=180) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    d, cloud, m, v = _densify_inputs()
+    stats = TrainStats(grad_accum=torch.from_numpy(d["grad_accum"]),
+                       seen=torch.from_numpy(d["seen"]))
+    new, mapping = P.densify_and_prune(cloud, stats, P.TrainConfig(seed=int(d["seed"])),
+                                       int(d["iteration"]), float(d["grad_thr"]),
+                                       float(d["split_thr"]))
+    m1, v1 = carry_moments(m, mapping, new), carry_moments(v, mapping, new)
+    starts = results[0][4]
+    assert starts[-1] == new.count and results[1][4] == starts
+    for rank, params, mm, vv, _ in results:
+        a, b = starts[rank], starts[rank + 1]
+        for k in PARAM_NAMES:
+            assert np.array_equal(params[k], getattr(new, k)[a:b].numpy()), (rank, k)
+            assert np.array_equal(mm[k], m1[k][a:b].numpy()), (rank, "m", k)
+            assert np.array_equal(vv[k], v1[k][a:b].numpy()), (rank, "v", k)

@@ -79,3 +79,41 @@ def test_sharded_losses_track_reference():
 def _extent(cams):
     from oracle import train as T
     return T.scene_extent(cams)
+
+
+def _run_single_densify(P, cams, gt, cloud, iters, canon, cfg):
+    from paper_2509_05216_b200.engine import Trainer
+    tr = Trainer(cloud.copy(), cams[0].width, cams[0].height, cfg, _extent(cams), canon_rows=canon)
+    sched = P.build_schedule(iters, len(cams), 0)
+    for it in range(1, iters + 1):
+        tr.step(it, cams[sched[it - 1]], gt[sched[it - 1]])
+        if tr.densify_due(it):
+            tr.densify(it)
+    torch.cuda.synchronize()
+    return tr.loss_dev[1:iters + 1].tolist(), tr.cloud
+
+
+@pytest.mark.parametrize("workers", [2, 3])
+def test_sharded_densify_bitwise_equals_single_gpu(workers):
+    """Densify + rebalance inside the sharded engine (emulated ranks) keeps
+    the run bitwise equal to the single-GPU engine across the event."""
+    from paper_2509_05216_b200 import distributed as D
+    P, d, cams, gt, cloud = _setup()
+    iters, canon = 5, 1
+    cfg = P.TrainConfig(iterations=iters, densify_start=2, densify_interval=2, densify_stop=4)
+    ref_losses, ref_cloud = _run_single_densify(P, cams, gt, cloud, iters, canon, cfg)
+    assert ref_cloud.count != cloud.count
+    ranks, smap, part = D.make_ranks(cloud.copy(), cams[0].width, cams[0].height, cfg,
+                                     _extent(cams), workers, torch.device("cuda", 0),
+                                     canon_rows=canon)
+    sched = P.build_schedule(iters, len(cams), 0)
+    losses = []
+    for it in range(1, iters + 1):
+        loss = D.emulated_step(ranks, cams[sched[it - 1]], gt[sched[it - 1]], it)
+        losses.append(float(loss[0]))
+        if D.densify_due(cfg, it):
+            ranks = D.emulated_densify(ranks, it)
+    got = D.gather_cloud(ranks)
+    assert losses == ref_losses, (losses, ref_losses)
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(got, k), getattr(ref_cloud, k)), k
