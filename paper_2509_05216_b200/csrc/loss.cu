@@ -46,6 +46,22 @@ __device__ __forceinline__ double gt_val<double, uint8_t>(uint8_t v) { return (d
 constexpr int LT = 16;          // output tile edge
 constexpr int LP = LT + 10;     // patch edge (tile + 10-px halo)
 
+// 8-bit ground truth: the 256 values float(k / 255.0) (gt_val) staged once per
+// block in shared memory, so a sample costs one shared load instead of a
+// float64 division.
+template <typename T, typename R>
+struct GtLut {
+    __device__ __forceinline__ void init(T *) const {}
+    __device__ __forceinline__ T operator()(const T *, R v) const { return gt_val<T, R>(v); }
+};
+template <typename T>
+struct GtLut<T, uint8_t> {
+    __device__ __forceinline__ void init(T *lut) const {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = gt_val<T, uint8_t>((uint8_t)i);
+    }
+    __device__ __forceinline__ T operator()(const T *lut, uint8_t v) const { return lut[v]; }
+};
+
 __device__ __forceinline__ double block_sum(double v, double *scratch) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -71,6 +87,9 @@ __global__ void __launch_bounds__(256) ssim_fields_kernel(
     __shared__ T sx[LP][LP + 1], sy[LP][LP + 1];
     __shared__ T hs[5][LP][LT];
     __shared__ double red[8];
+    __shared__ T lut[256];
+    const GtLut<T, R> gt;
+    gt.init(lut);
     const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;  // == pow(0.01, 2), pow(0.03, 2)
     const int hc = H - 10, wc = W - 10;
     const int by = by_base + blockIdx.y;
@@ -79,21 +98,22 @@ __global__ void __launch_bounds__(256) ssim_fields_kernel(
     const int ccx = cx0 + tx, ccy = cy0 + ty;
     const bool valid = ccx < wc && ccy < hc;
     double pq_acc = 0.0;
+    __syncthreads();
     for (int c = 0; c < C; c++) {
-        for (int idx = threadIdx.x; idx < LP * LP; idx += 256) {
-            const int r = idx / LP, q = idx - r * LP;
-            const int y = cy0 + r, x = cx0 + q;
-            T vx = 0, vy = 0;
-            if (y < H && x < W) {
-                vx = (T)img[((int64_t)(y - img_row0) * W + x) * C + c];
-                vy = gt_val<T, R>(ref[((int64_t)y * W + x) * C + c]);
+        for (int r = ty; r < LP; r += 16)
+            for (int q = tx; q < LP; q += 16) {
+                const int y = cy0 + r, x = cx0 + q;
+                T vx = 0, vy = 0;
+                if (y < H && x < W) {
+                    vx = (T)img[((int64_t)(y - img_row0) * W + x) * C + c];
+                    vy = gt(lut, ref[((int64_t)y * W + x) * C + c]);
+                }
+                sx[r][q] = vx;
+                sy[r][q] = vy;
             }
-            sx[r][q] = vx;
-            sy[r][q] = vy;
-        }
         __syncthreads();
-        for (int idx = threadIdx.x; idx < LP * LT; idx += 256) {
-            const int r = idx / LT, q = idx - r * LT;
+        for (int r = ty; r < LP; r += 16) {
+            const int q = tx;
             T a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
 #pragma unroll
             for (int i = 0; i < 11; i++) {
@@ -157,6 +177,9 @@ __global__ void __launch_bounds__(256) ssim_adjoint_kernel(
     __shared__ T sf[3][LP][LP + 1];
     __shared__ T hs[3][LP][LT];
     __shared__ double red[8];
+    __shared__ T lut[256];
+    const GtLut<T, R> gt;
+    gt.init(lut);
     const int hc = H - 10, wc = W - 10;
     const int by = by_base + blockIdx.y;
     const int x0 = blockIdx.x * LT, y0 = by * LT;
@@ -165,18 +188,19 @@ __global__ void __launch_bounds__(256) ssim_adjoint_kernel(
     const bool inside = x < W && y < H && y < row1;
     const int64_t plane = (int64_t)fmap_rows * wc;
     double l1_acc = 0.0;
+    __syncthreads();
     for (int c = 0; c < 3; c++) {
-        for (int idx = threadIdx.x; idx < LP * LP; idx += 256) {
-            const int r = idx / LP, q = idx - r * LP;
-            const int cy = y0 - 10 + r, cx = x0 - 10 + q;
-            const bool ok = cy >= 0 && cy < hc && cx >= 0 && cx < wc;
-            const int64_t o = (int64_t)(cy - fmap_row0) * wc + cx;
+        for (int r = ty; r < LP; r += 16)
+            for (int q = tx; q < LP; q += 16) {
+                const int cy = y0 - 10 + r, cx = x0 - 10 + q;
+                const bool ok = cy >= 0 && cy < hc && cx >= 0 && cx < wc;
+                const int64_t o = (int64_t)(cy - fmap_row0) * wc + cx;
 #pragma unroll
-            for (int f = 0; f < 3; f++) sf[f][r][q] = ok ? fmap[(f * 3 + c) * plane + o] : (T)0;
-        }
+                for (int f = 0; f < 3; f++) sf[f][r][q] = ok ? fmap[(f * 3 + c) * plane + o] : (T)0;
+            }
         __syncthreads();
-        for (int idx = threadIdx.x; idx < LP * LT; idx += 256) {
-            const int r = idx / LT, q = idx - r * LT;
+        for (int r = ty; r < LP; r += 16) {
+            const int q = tx;
 #pragma unroll
             for (int f = 0; f < 3; f++) {
                 T a = 0;
@@ -196,7 +220,7 @@ __global__ void __launch_bounds__(256) ssim_adjoint_kernel(
                 g2 += w * hs[2][ty + i][tx];
             }
             const T xv = (T)img[((int64_t)(y - img_row0) * W + x) * 3 + c];
-            const T yv = gt_val<T, R>(ref[((int64_t)y * W + x) * 3 + c]);
+            const T yv = gt(lut, ref[((int64_t)y * W + x) * 3 + c]);
             const T d = xv - yv;
             const T sg = d > (T)0 ? (T)1 : (d < (T)0 ? (T)-1 : (T)0);
             const T g = g0 + xv * g1 + yv * g2;

@@ -366,7 +366,10 @@ __global__ void __launch_bounds__(128, 4) chain_adam_kernel(isg_train_state s, C
 // Adam so each kernel keeps its occupancy): grads written for every row
 // (zeros for unflagged rows), stats for flagged rows.
 template <int K3>
-__global__ void __launch_bounds__(128, 4) chain_train_kernel(isg_params p, Cam cam,
+#ifndef CHAIN_MINB
+#define CHAIN_MINB 4
+#endif
+__global__ void __launch_bounds__(128, CHAIN_MINB) chain_train_kernel(isg_params p, Cam cam,
                                                           const uint8_t *__restrict__ flag,
                                                           const double *__restrict__ grad2d,
                                                           float *dpos, float *dls, float *drot,
