@@ -260,7 +260,7 @@ def run_ours(args, world, rank, local):
     tr.r.timer = None
     phases = {k: v / phase_steps for k, v in phases.items()}
     counts = pair_counts(tr, wl, schedule[iters - 1])
-    roof = roofline(phases, counts, n)
+    roof = roofline(phases, counts, n, args.config)
     log("[ours] phases (ms): " + ", ".join(f"{k} {v:.3f}" for k, v in phases.items()))
 
     # ---- end-to-end through the public API: GT H2D from pinned host + loss D2H
@@ -302,7 +302,7 @@ def pair_counts(tr, wl, view):
     return out
 
 
-def roofline(phases, c, n):
+def roofline(phases, c, n, config="config3"):
     """Dominant kernel's achieved rate vs its roofline (SURVEY.md 8d units).
 
     raster fwd: 13 I_f + 9 C flops; raster bwd: 13 I_b + 55 C flops (FP32 pipe);
@@ -319,9 +319,11 @@ def roofline(phases, c, n):
     if dom in flops:
         fp32 = fp32_peak()
         achieved = flops[dom] / (ms * 1e-3) / 1e12
+        traffic, tsrc = ncu_traffic(dom, config)
         return {"kernel": dom, "bound": "fp32", "achieved": achieved, "peak": fp32,
                 "unit": "TFLOP/s", "frac": achieved / fp32 if fp32 else None,
-                "traffic": None, "peak_source": "FP32 FFMA peak 148 SM x 128 lanes x 2 x max "
+                "traffic": traffic, "traffic_source": tsrc,
+                "peak_source": "FP32 FFMA peak 148 SM x 128 lanes x 2 x max "
                 "SM clock (no FP32 entry in MEASURED_PEAKS.json)",
                 "algorithmic": f"{flops[dom]:.4g} flops per launch (SURVEY 8d)"}
     b = bytes_.get(dom)
@@ -332,6 +334,18 @@ def roofline(phases, c, n):
     return {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
             "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
             "peak_source": src}
+
+
+def ncu_traffic(kernel: str, config: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu --set full capture (profiles/traffic_<config>.json),
+    or None when no capture of this kernel/config is committed."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"traffic_{config}.json")) as fh:
+            t = json.load(fh)[kernel]
+        return t["dram_bytes_read"] + t["dram_bytes_write"], t["source"]
+    except (OSError, KeyError, ValueError):
+        return None, None
 
 
 def fp32_peak():

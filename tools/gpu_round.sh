@@ -5,7 +5,7 @@
 mkdir -p gpurun_out
 KREGEX=${1:-"bwd_kernel|fwd_kernel"}
 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -x 2>&1 | tail -15
-python bench.py --steps 10 --warmup 3 --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.log
+python bench.py --steps 10 --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.log
 tail -4 gpurun_out/bench.log
 python -c "import json;d=json.load(open('gpurun_out/bench.json'));print('VALUE',d['value'],'ms',d['ms_per_step'],'e2e',d['e2e']['value']);print(d['phases_ms']);print(d['roofline']);print(d['cpu_baseline']);print(d['clocks'])"
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
