@@ -170,7 +170,8 @@ int isg_ssim(void *workspace, size_t *ws_bytes, int32_t height, int32_t width,
 
 /* Per-tile backward (_backward_tiles, _kernels.py:282-374).  Writes the
  * per-(tile, splat) subtotals as 9 values (dmean 2, dconic 3, dcolor 3,
- * dopac 1, feat_dtype) into slot emit_off[rank] + (index of the tile inside
+ * dopac 1, feat_dtype; float32 records are padded to a 12-float / 48-byte
+ * stride, float64 records are 9 doubles) into slot emit_off[rank] + (index of the tile inside
  * the rank's row-clipped rect), i.e. splat-major with tiles ascending --
  * exactly the order in which _reduce_scratch folds them.  With emit_off ==
  * NULL the subtotal of entry e goes to slot e instead (the reference's

@@ -25,6 +25,13 @@ constexpr double T_STOP = 1e-4;
 constexpr int TILE = 16;
 constexpr int FEAT = 12;  // raster features per splat (see isg_preprocess_out)
 
+// Floats / doubles per (tile, splat) gradient subtotal record: 9 values
+// (dmean 2, dconic 3, dcolor 3, dopac 1); float32 records are padded to 12
+// (48 B, three 16-byte stores, 16-byte aligned), float64 records are packed.
+template <typename T> constexpr int partial_stride();
+template <> constexpr int partial_stride<float>() { return 12; }
+template <> constexpr int partial_stride<double>() { return 9; }
+
 struct Cam {
     double R[9];
     double t[3];

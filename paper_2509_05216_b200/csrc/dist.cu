@@ -157,7 +157,7 @@ __global__ void block_fold_kernel(int64_t m, const int64_t *__restrict__ emit_of
 #pragma unroll
         for (int k = 0; k < 9; k++) bs[k] = 0.0;
         for (int64_t p = p0 + (ys - y0) * w; p < p0 + (ye - y0 + 1) * w; p++) {
-            const T *src = partials + 9 * p;
+            const T *src = partials + partial_stride<T>() * p;
 #pragma unroll
             for (int k = 0; k < 9; k++) bs[k] += (double)src[k];
         }

@@ -10,6 +10,8 @@
 #pragma once
 #include <stdint.h>
 
+#include "common.cuh"
+
 namespace isg {
 
 // Running state of one rank's fold; step() consumes the next slot's 9 terms.
@@ -64,7 +66,7 @@ __device__ __forceinline__ void fold_rank(const T *__restrict__ partials, int64_
                                           int row_lo, int canon_rows, double (&acc)[9]) {
     FoldState st;
     st.init(rect_sorted, r, p1 - p0, row_lo, canon_rows);
-    for (int64_t p = p0; p < p1; p++) st.step(partials + 9 * p);
+    for (int64_t p = p0; p < p1; p++) st.step(partials + partial_stride<T>() * p);
     st.finish();
 #pragma unroll
     for (int k = 0; k < 9; k++) acc[k] = st.acc[k];

@@ -29,6 +29,7 @@ namespace f32 {
 
 constexpr int NT = 128;  // threads per tile (2 pixels each)
 constexpr int NW = NT / 32;
+constexpr int PSTRIDE = partial_stride<float>();  // floats per subtotal record
 constexpr int FB = 128;  // staging batch (entries)
 #ifndef BWD_MINB
 #define BWD_MINB 8
@@ -480,9 +481,11 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
             }
             sslot[threadIdx.x] = slot;
             if (mask == 0u) {
-                float *dst = partials + 9 * slot;
-#pragma unroll
-                for (int q = 0; q < 9; q++) dst[q] = 0.0f;
+                float4 *dst = reinterpret_cast<float4 *>(partials + PSTRIDE * slot);
+                const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                dst[0] = z;
+                dst[1] = z;
+                dst[2] = z;
             }
         }
         if (threadIdx.x < BB) smask[threadIdx.x] = (unsigned char)mask;
@@ -557,14 +560,11 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
                 }
             const float4 g4 = sgh[s][0], h4 = sgh[s][1];
             const float a = -2.0f * g4.z, b = -g4.w, c = -2.0f * h4.x;
-            float *dst = partials + 9 * sslot[s];
-            dst[0] = fmaf(a, acc[0], b * acc[1]);
-            dst[1] = fmaf(b, acc[0], c * acc[1]);
-            dst[2] = -0.5f * acc[2];
-            dst[3] = -acc[3];
-            dst[4] = -0.5f * acc[4];
-#pragma unroll
-            for (int q = 5; q < 9; q++) dst[q] = acc[q];
+            float4 *dst = reinterpret_cast<float4 *>(partials + PSTRIDE * sslot[s]);
+            dst[0] = make_float4(fmaf(a, acc[0], b * acc[1]), fmaf(b, acc[0], c * acc[1]),
+                                 -0.5f * acc[2], -acc[3]);
+            dst[1] = make_float4(-0.5f * acc[4], acc[5], acc[6], acc[7]);
+            dst[2] = make_float4(acc[8], 0.0f, 0.0f, 0.0f);
         }
     }
 }

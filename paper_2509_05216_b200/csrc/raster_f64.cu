@@ -337,13 +337,14 @@ __global__ void __launch_bounds__(256) reduce_ordered_kernel(
 // memory in chunks with coalesced 16-byte loads and every thread folds its own
 // slots from there -- the same FoldState arithmetic as fold_rank.
 constexpr int RED_THREADS = 128;
-constexpr int RED_CHUNK = 1024;  // slots per chunk (36 KB): one chunk for most blocks
+constexpr int RED_CHUNK = 768;  // slots per chunk (36 KB): one chunk for most blocks
 
 __global__ void __launch_bounds__(RED_THREADS) reduce_ordered_f32_kernel(
     int64_t m, const int64_t *__restrict__ emit_off, const float *__restrict__ partials,
     const int32_t *__restrict__ order, const int4 *__restrict__ rect_sorted, int row_lo,
     int canon_rows, double *__restrict__ grad2d, double *__restrict__ grad_norm) {
-    __shared__ __align__(16) float sbuf[RED_CHUNK * 9 + 4];
+    constexpr int PS = partial_stride<float>();
+    __shared__ __align__(16) float sbuf[RED_CHUNK * PS];
     const int64_t r0 = (int64_t)blockIdx.x * RED_THREADS;
     const int64_t r = r0 + threadIdx.x;
     const bool live = r < m;
@@ -353,10 +354,10 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_ordered_f32_kernel(
     const int64_t p1 = live ? emit_off[r + 1] : 0;
     FoldState st;
     st.init(rect_sorted, r, live ? p1 - p : 0, row_lo, canon_rows);
-    // chunk starts aligned to 4 slots so the float offset is a multiple of 4
-    for (int64_t c0 = span0 & ~3ll; c0 < span1; c0 += RED_CHUNK) {
+    // 48-byte records: every chunk start is 16-byte aligned
+    for (int64_t c0 = span0; c0 < span1; c0 += RED_CHUNK) {
         const int64_t c1 = min(c0 + RED_CHUNK, span1);
-        const int64_t f0 = 9 * c0, nf = 9 * (c1 - c0);
+        const int64_t f0 = (int64_t)PS * c0, nf = (int64_t)PS * (c1 - c0);
         const float4 *src = reinterpret_cast<const float4 *>(partials + f0);
         const int n4 = (int)(nf >> 2);
         __syncthreads();
@@ -365,7 +366,7 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_ordered_f32_kernel(
         for (int i = 4 * n4 + threadIdx.x; i < nf; i += RED_THREADS) sbuf[i] = __ldg(partials + f0 + i);
         __syncthreads();
         const int64_t e = min(p1, c1);
-        for (; p < e; p++) st.step(sbuf + 9 * (p - c0));
+        for (; p < e; p++) st.step(sbuf + PS * (p - c0));
     }
     if (!live) return;
     st.finish();

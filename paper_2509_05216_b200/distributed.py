@@ -578,7 +578,7 @@ class RankStep:
     def phase_backward(self):
         lib, s, d = L.lib(), L.stream_ptr(), self.dev
         E, M = self.E, self.M
-        self.partials = torch.empty((max(E, 1), 9), dtype=torch.float32, device=d)
+        self.partials = torch.empty((max(E, 1), 12), dtype=torch.float32, device=d)
         W3 = self.W * 3
         if self.n_tiles:
             L.check(lib.isg_raster_bwd(

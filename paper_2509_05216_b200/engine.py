@@ -198,7 +198,9 @@ class Rasterizer:
     def backward(self, ctx: ViewContext) -> None:
         lib = L.lib()
         s = L.stream_ptr()
-        self.partials = _grow(self.partials, max(ctx.e, 1), (9,), dtype=self.feat_dtype,
+        # float32 records are padded to 12 floats (isogs.h: isg_raster_bwd)
+        rec = 12 if self.feat_dtype == torch.float32 else 9
+        self.partials = _grow(self.partials, max(ctx.e, 1), (rec,), dtype=self.feat_dtype,
                               device=self.device)
         L.check(lib.isg_raster_bwd(self.ftag, self.width, self.height, self.tiles_x, 0,
                                    self.tiles_y, None, 0, L.ptr(self.offsets), L.ptr(self.entries),

@@ -436,7 +436,8 @@ def render_backward(cloud, cam, batch: SplatBatch, order, aux: RenderAux,
     m = len(batch)
     feat = cache["feat"]
     e = int(cache["entries"].numel())
-    partials = torch.empty((max(e, 1), 9), dtype=feat.dtype, device=dev)
+    rec = 12 if feat.dtype == torch.float32 else 9  # padded float32 records (isogs.h)
+    partials = torch.empty((max(e, 1), rec), dtype=feat.dtype, device=dev)
     bgc = (ctypes.c_double * 3)(*cache["background"])
     if m:
         L.check(L.lib().isg_raster_bwd(
