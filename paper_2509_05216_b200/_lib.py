@@ -68,6 +68,7 @@ SIGNATURES = {
                        ctypes.POINTER(PreprocessOut_t), _P],
     "isg_sort_u64": [_P, _SZ, _P, _P, _P, _P, _I64, _I32, _I32, _P],
     "isg_sort_u32": [_P, _SZ, _P, _P, _P, _P, _I64, _I32, _I32, _P],
+    "isg_sort_depth": [_P, _SZ, _P, _P, _P, _P, _I64, _P],
     "isg_bin_count": [_P, _SZ, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P],
     "isg_bin_emit": [_I64, _P, _P, _I32, _I32, _I32, _P, _P, _P],
     "isg_tile_offsets": [_I64, _P, _I32, _P, _P],
@@ -182,6 +183,28 @@ class Workspace:
         if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
             self.buf = torch.empty(int(nbytes * 1.25) + 256, dtype=torch.uint8, device=device)
         return self.buf
+
+
+def sort_depth(keys: torch.Tensor, vals: torch.Tensor, ws: Workspace,
+               keys_out: torch.Tensor | None = None, vals_out: torch.Tensor | None = None):
+    """The global depth order: stable sort of (float64 depth bits, id) pairs
+    (isg_sort_depth; identical to a full 64-bit sort_pairs)."""
+    n = keys.numel()
+    if keys_out is None:
+        keys_out = torch.empty_like(keys)
+    if vals_out is None:
+        vals_out = torch.empty_like(vals)
+    if n == 0:
+        return keys_out, vals_out
+    L = lib()
+    sz = ctypes.c_size_t(0)
+    check(L.isg_sort_depth(None, ctypes.byref(sz), ptr(keys), ptr(keys_out), ptr(vals),
+                           ptr(vals_out), n, None), "sort_depth (size query)")
+    buf = ws.get(sz.value, keys.device)
+    sz = ctypes.c_size_t(buf.numel())
+    check(L.isg_sort_depth(ptr(buf), ctypes.byref(sz), ptr(keys), ptr(keys_out), ptr(vals),
+                           ptr(vals_out), n, stream_ptr()), "sort_depth")
+    return keys_out, vals_out
 
 
 def sort_pairs(keys: torch.Tensor, vals: torch.Tensor, bits: tuple[int, int],

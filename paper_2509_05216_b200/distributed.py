@@ -497,7 +497,7 @@ class RankStep:
         L.check(lib.isg_records_unpack(R, L.ptr(records), L.ptr(self.r_key), L.ptr(self.r_gid),
                                        L.ptr(self.r_rect), L.ptr(self.r_feat), s), "unpack")
         vals0 = torch.arange(max(R, 1), dtype=torch.int32, device=d)
-        self.key_sorted, self.order = L.sort_pairs(self.r_key[:R], vals0[:R], (0, 64), self.ws[0])
+        self.key_sorted, self.order = L.sort_depth(self.r_key[:R], vals0[:R], self.ws[0])
         self.rect_sorted = torch.empty((max(R, 1), 4), dtype=torch.int32, device=d)
         self.feat_sorted = torch.empty((max(R, 1), 12), dtype=torch.float32, device=d)
         self.emit_off = torch.empty(R + 1, dtype=torch.int64, device=d)

@@ -152,7 +152,7 @@ class Rasterizer:
         L.check(lib.isg_preprocess(ctypes.byref(p), ctypes.byref(self.cam_struct), TILE,
                                    ctypes.byref(out), s), "isg_preprocess")
         _mark(tm, "preprocess")
-        L.sort_pairs(self.key, self.vals0, (0, 64), self.ws_sort, self.key_sorted, self.order)
+        L.sort_depth(self.key, self.vals0, self.ws_sort, self.key_sorted, self.order)
         _mark(tm, "sort_depth")
         sz = ctypes.c_size_t(0)
         L.check(lib.isg_bin_count(None, ctypes.byref(sz), n, None, None, None, None, self.ftag,

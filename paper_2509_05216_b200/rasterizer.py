@@ -125,7 +125,7 @@ _WS = L.Workspace()
 
 def _stable_argsort_u64(keys: torch.Tensor) -> torch.Tensor:
     vals = torch.arange(keys.numel(), dtype=torch.int32, device=keys.device)
-    _, out = L.sort_pairs(keys.contiguous(), vals, (0, 64), _WS)
+    _, out = L.sort_depth(keys.contiguous(), vals, _WS)
     return out.to(torch.int64)
 
 

@@ -242,3 +242,25 @@ def test_backward_rejects_mismatched_context(P):
         P.render_backward(cloud, cam, batch, order, aux, np.ones((47, 48, 3)))
     with pytest.raises(ValueError):
         P.render_forward(batch, 47, 48)
+
+
+def test_sort_depth_equals_full_64bit_sort():
+    """isg_sort_depth (6 passes over the top 48 bits + run fix-up) is the
+    stable 64-bit sort: adversarial keys with long equal-top-48 runs, exact
+    duplicates and the culled ~0 tail."""
+    from paper_2509_05216_b200 import _lib as L
+    g = torch.Generator().manual_seed(3)
+    n = 200_000
+    base = torch.randint(0, 2**40, (n,), generator=g, dtype=torch.int64) << 20
+    base[: n // 2] = base[: n // 2] % (2**26 << 20)  # many shared top-48 prefixes
+    low = torch.randint(0, 2**16, (n,), generator=g, dtype=torch.int64)
+    low[::7] = 5  # duplicates
+    keys = (base | low)
+    keys[-1000:] = -1  # culled (~0)
+    keys[1000:3000] = keys[1000]  # a long run of identical keys
+    keys = keys.cuda()
+    vals = torch.arange(n, dtype=torch.int32, device="cuda")
+    ws1, ws2 = L.Workspace(), L.Workspace()
+    k1, v1 = L.sort_pairs(keys, vals, (0, 64), ws1)
+    k2, v2 = L.sort_depth(keys, vals, ws2)
+    assert torch.equal(k1, k2) and torch.equal(v1, v2)
