@@ -72,6 +72,9 @@ SIGNATURES = {
     "isg_bin_count": [_P, _SZ, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P],
     "isg_bin_emit": [_I64, _P, _P, _I32, _I32, _I32, _P, _P, _P],
     "isg_tile_offsets": [_I64, _P, _I32, _P, _P],
+    "isg_bin_emit16": [_I64, _P, _P, _I32, _I32, _I32, _P, _P, _P],
+    "isg_sort_u16": [_P, _SZ, _P, _P, _P, _P, _I64, _I32, _I32, _P],
+    "isg_tile_offsets16": [_I64, _P, _I32, _P, _P],
     "isg_raster_fwd": [_I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _I32,
                        _P, _P, _P, _P, _P, _P],
     "isg_loss_l1_dssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _I32, _D, _P, _P, _P],
@@ -219,7 +222,7 @@ def sort_pairs(keys: torch.Tensor, vals: torch.Tensor, bits: tuple[int, int],
     if n == 0:
         return keys_out, vals_out
     L = lib()
-    fn = L.isg_sort_u64 if keys.element_size() == 8 else L.isg_sort_u32
+    fn = {8: L.isg_sort_u64, 4: L.isg_sort_u32, 2: L.isg_sort_u16}[keys.element_size()]
     sz = ctypes.c_size_t(0)
     check(fn(None, ctypes.byref(sz), ptr(keys), ptr(keys_out), ptr(vals), ptr(vals_out), n,
              bits[0], bits[1], None), "sort (size query)")

@@ -44,29 +44,6 @@ __global__ void finish_counts_kernel(int64_t n, const int64_t *emit_off, int64_t
     counts[1] = emit_off[n];
 }
 
-// One thread per rank writes its (clipped) rect's tiles row-major, i.e. in
-// ascending tile id -- the order _fill_tile_entries visits them.  Adjacent
-// ranks own adjacent slot ranges, so a warp's stores stay clustered.
-__global__ void __launch_bounds__(256) emit_kernel(int64_t m, const int4 *__restrict__ rect_sorted,
-                                                   const int64_t *__restrict__ emit_off,
-                                                   int tiles_x, int row_lo, int row_hi,
-                                                   uint32_t *__restrict__ tile_keys,
-                                                   int32_t *__restrict__ tile_vals) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= m) return;
-    const int4 rc = rect_sorted[r];
-    const int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
-    int64_t o = emit_off[r];
-    const uint32_t base_tile = (uint32_t)row_lo * (uint32_t)tiles_x;
-    for (int ty = y0; ty <= y1; ty++) {
-        const uint32_t rowbase = (uint32_t)ty * (uint32_t)tiles_x - base_tile;
-        for (int tx = rc.x; tx <= rc.z; tx++, o++) {
-            tile_keys[o] = rowbase + (uint32_t)tx;
-            tile_vals[o] = (int32_t)r;
-        }
-    }
-}
-
 // Entry-parallel emission: a block of EMIT_R consecutive ranks owns the
 // contiguous slot span [emit_off[r0], emit_off[r0 + EMIT_R]); the block
 // stages the ranks' offsets and clipped rects in shared memory and writes the
@@ -76,11 +53,12 @@ __global__ void __launch_bounds__(256) emit_kernel(int64_t m, const int4 *__rest
 // the same slots as emit_kernel.
 constexpr int EMIT_R = 256;
 
+template <typename K>
 __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
                                                         const int4 *__restrict__ rect_sorted,
                                                         const int64_t *__restrict__ emit_off,
                                                         int tiles_x, int row_lo, int row_hi,
-                                                        uint32_t *__restrict__ tile_keys,
+                                                        K *__restrict__ tile_keys,
                                                         int32_t *__restrict__ tile_vals) {
     __shared__ int64_t soff[EMIT_R + 1];
     __shared__ int4 srect[EMIT_R];
@@ -106,19 +84,21 @@ __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
         const int4 rc = srect[lo];
         const int k = (int)(o - soff[lo]);
         const int dy = k / rc.w, dx = k - dy * rc.w;
-        tile_keys[o] = (uint32_t)(rc.y + dy) * (uint32_t)tiles_x - base_tile + (uint32_t)(rc.x + dx);
+        tile_keys[o] =
+            (K)((uint32_t)(rc.y + dy) * (uint32_t)tiles_x - base_tile + (uint32_t)(rc.x + dx));
         tile_vals[o] = (int32_t)(r0 + lo);
     }
 }
 
-__global__ void tile_offsets_kernel(int64_t e, const uint32_t *__restrict__ keys, int n_tiles,
+template <typename K>
+__global__ void tile_offsets_kernel(int64_t e, const K *__restrict__ keys, int n_tiles,
                                     int32_t *__restrict__ offsets) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t > n_tiles) return;
     int64_t lo = 0, hi = e;  // lower_bound(keys, t)
     while (lo < hi) {
         int64_t mid = (lo + hi) >> 1;
-        if (keys[mid] < (uint32_t)t) lo = mid + 1;
+        if ((uint32_t)keys[mid] < (uint32_t)t) lo = mid + 1;
         else hi = mid;
     }
     offsets[t] = (int32_t)lo;
@@ -250,8 +230,41 @@ extern "C" int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t
                             int32_t *tile_vals, void *stream) {
     if (m < 0 || tiles_x <= 0) return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
-    emit_span_kernel<<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
+    emit_span_kernel<uint32_t><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
         m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_bin_emit16(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
+                              int32_t tiles_x, int32_t row_lo, int32_t row_hi,
+                              uint16_t *tile_keys, int32_t *tile_vals, void *stream) {
+    if (m < 0 || tiles_x <= 0 || (int64_t)(row_hi - row_lo) * tiles_x > 65536)
+        return (int)cudaErrorInvalidValue;
+    if (m == 0) return 0;
+    emit_span_kernel<uint16_t><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
+        m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_sort_u16(void *workspace, size_t *ws_bytes, const uint16_t *keys_in,
+                            uint16_t *keys_out, const int32_t *vals_in, int32_t *vals_out,
+                            int64_t n, int32_t begin_bit, int32_t end_bit, void *stream) {
+    if (!ws_bytes || n < 0 || n > INT32_MAX || begin_bit < 0 || end_bit > 16 ||
+        begin_bit >= end_bit)
+        return (int)cudaErrorInvalidValue;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, *ws_bytes, keys_in, keys_out,
+                                                    vals_in, vals_out, (int)n, begin_bit,
+                                                    end_bit, (cudaStream_t)stream);
+    return (int)e;
+}
+
+extern "C" int isg_tile_offsets16(int64_t e, const uint16_t *sorted_tile_keys, int32_t n_tiles,
+                                  int32_t *offsets, void *stream) {
+    if (e < 0 || n_tiles < 0 || n_tiles > 65536) return (int)cudaErrorInvalidValue;
+    tile_offsets_kernel<uint16_t><<<blocks_for(n_tiles + 1, 256), 256, 0, (cudaStream_t)stream>>>(
+        e, sorted_tile_keys, n_tiles, offsets);
     ISG_CHECK_LAUNCH();
     return 0;
 }

@@ -170,20 +170,26 @@ class Rasterizer:
         _mark(tm, "host_sync")
         m, e = int(self.counts_host[0]), int(self.counts_host[1])
         dev = self.device
-        self.tile_keys = _grow(self.tile_keys, e, dtype=torch.int32, device=dev)
+        k16 = self.n_tiles <= 65536  # 2-byte tile keys: 25 % less sort traffic
+        kdt = torch.int16 if k16 else torch.int32
+        if self.tile_keys is None or self.tile_keys.dtype != kdt:
+            self.tile_keys = self.keys_sorted_t = None
+        self.tile_keys = _grow(self.tile_keys, e, dtype=kdt, device=dev)
         self.tile_vals = _grow(self.tile_vals, e, dtype=torch.int32, device=dev)
-        self.keys_sorted_t = _grow(self.keys_sorted_t, e, dtype=torch.int32, device=dev)
+        self.keys_sorted_t = _grow(self.keys_sorted_t, e, dtype=kdt, device=dev)
         self.entries = _grow(self.entries, e, dtype=torch.int32, device=dev)
+        emit = lib.isg_bin_emit16 if k16 else lib.isg_bin_emit
+        offs = lib.isg_tile_offsets16 if k16 else lib.isg_tile_offsets
         if e:
-            L.check(lib.isg_bin_emit(m, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
-                                     self.tiles_x, 0, self.tiles_y, L.ptr(self.tile_keys),
-                                     L.ptr(self.tile_vals), s), "isg_bin_emit")
+            L.check(emit(m, L.ptr(self.rect_sorted), L.ptr(self.emit_off), self.tiles_x, 0,
+                         self.tiles_y, L.ptr(self.tile_keys), L.ptr(self.tile_vals), s),
+                    "isg_bin_emit")
             _mark(tm, "bin_emit")
             L.sort_pairs(self.tile_keys[:e], self.tile_vals[:e], (0, self.tile_bits),
                          self.ws_sort, self.keys_sorted_t[:e], self.entries[:e])
             _mark(tm, "sort_tiles")
-        L.check(lib.isg_tile_offsets(e, L.ptr(self.keys_sorted_t), self.n_tiles,
-                                     L.ptr(self.offsets), s), "isg_tile_offsets")
+        L.check(offs(e, L.ptr(self.keys_sorted_t), self.n_tiles, L.ptr(self.offsets), s),
+                "isg_tile_offsets")
         _mark(tm, "tile_offsets")
         L.check(lib.isg_raster_fwd(self.ftag, self.width, self.height, self.tiles_x, 0,
                                    self.tiles_y, None, 0, L.ptr(self.offsets), L.ptr(self.entries),
