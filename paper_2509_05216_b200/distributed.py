@@ -513,16 +513,17 @@ class RankStep:
                                   L.ptr(self.counts), s), "isg_bin_count")
         M, E = self._sync_ints(self.counts)
         self.M, self.E = M, E
-        tk = torch.empty(max(E, 1), dtype=torch.int32, device=d)
+        k16 = self.n_tiles <= 65536  # 2-byte tile keys (see engine.Rasterizer.forward)
+        tk = torch.empty(max(E, 1), dtype=torch.int16 if k16 else torch.int32, device=d)
         tv = torch.empty(max(E, 1), dtype=torch.int32, device=d)
+        emit = lib.isg_bin_emit16 if k16 else lib.isg_bin_emit
+        offs = lib.isg_tile_offsets16 if k16 else lib.isg_tile_offsets
         if E:
-            L.check(lib.isg_bin_emit(M, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
-                                     self.tiles_x, self.trow0, self.trow1, L.ptr(tk), L.ptr(tv),
-                                     s), "isg_bin_emit")
+            L.check(emit(M, L.ptr(self.rect_sorted), L.ptr(self.emit_off), self.tiles_x,
+                         self.trow0, self.trow1, L.ptr(tk), L.ptr(tv), s), "isg_bin_emit")
             tk, tv = L.sort_pairs(tk[:E], tv[:E], (0, self.tile_bits), self.ws[0])
         self.entries = tv
-        L.check(lib.isg_tile_offsets(E, L.ptr(tk), self.n_tiles, L.ptr(self.offsets), s),
-                "isg_tile_offsets")
+        L.check(offs(E, L.ptr(tk), self.n_tiles, L.ptr(self.offsets), s), "isg_tile_offsets")
         W3 = self.W * 3
         if self.n_tiles:
             L.check(lib.isg_raster_fwd(
