@@ -95,6 +95,18 @@ __device__ __forceinline__ float pair_alpha(float d1, float A, float B, const fl
     return a >= (1.0f / 255.0f) ? a : 0.0f;
 }
 
+// pair_alpha without the early exit (ex2 always evaluated): the same bits for
+// every pair, so several pairs' alphas can be computed ahead of the
+// sequential compositing.
+__device__ __forceinline__ float pair_alpha_bl(float d1, float A, float B, const float4 &h4,
+                                               float &gw) {
+    const float power = __fmaf_rn(d1, __fmaf_rn(h4.x, d1, B), A);
+    gw = ex2a(__fmul_rn(power, LOG2E));
+    const float a = fminf(__fmul_rn(h4.z, gw), 0.99f);
+    const bool ok = !(power > 0.0f || power < h4.y) && a >= (1.0f / 255.0f);
+    return ok ? a : 0.0f;
+}
+
 // True when no pixel centre of the box [x0, x0+edge] x [y0, y0+edge] can
 // reach the skip threshold: the exact maximum exponent over the box (convex
 // quadratic: interior minimum or an edge minimum) is below thr by a margin
@@ -152,6 +164,32 @@ __device__ __forceinline__ int ldsu8(uint32_t a) {
     unsigned short v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
     return (int)v;
+}
+
+// Front-to-back compositing of one pair (_kernels.py:258-272): skipped when
+// the pixel is done or alpha is 0; stops (without compositing) when T would
+// drop below 1e-4.
+template <bool TOUCH>
+__device__ __forceinline__ void composite(float a, int slot, int base, uint32_t a_col,
+                                          int64_t *touched, const int *srank, bool &done,
+                                          int &it, float &t, float &r, float &g, float &b,
+                                          int &last, int &cnt) {
+    if (done || !(a > 0.0f)) return;
+    const float test = t * (1.0f - a);
+    if (test < 1e-4f) {
+        done = true;
+        it = base + slot + 1;
+        return;
+    }
+    const float4 c = lds4(a_col + 16 * slot);
+    const float w = a * t;
+    r = fmaf(c.x, w, r);
+    g = fmaf(c.y, w, g);
+    b = fmaf(c.z, w, b);
+    t = test;
+    last = base + slot + 1;
+    cnt++;
+    if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
 }
 
 // Warp w renders quadrant (w & 1, w >> 1) of the tile: lane (lx, ly) owns
@@ -224,54 +262,29 @@ __global__ void __launch_bounds__(NT, 6) fwd_kernel(
         for (int k0 = 0; k0 < total; k0 += FCHK) {
             if (__all_sync(FULL, done0 && done1)) break;
             const int kend = min(k0 + FCHK, total);
-            for (int k = k0; k < kend; k++) {
-                const int slot = ldsu8(a_list + k);
-                const uint32_t ag = a_gh + 32 * slot;
-                const float4 g4 = lds4(ag), h4 = lds4(ag + 16);
-                float A, B;
-                col_terms(fpx - g4.x, g4, A, B);
-                if (!done0) {
-                    float gw;
-                    const float a = pair_alpha(fpy0 - g4.y, A, B, h4, gw);
-                    if (a > 0.0f) {
-                        const float test = t0 * (1.0f - a);
-                        if (test < 1e-4f) {
-                            done0 = true;
-                            it0 = base + slot + 1;
-                        } else {
-                            const float4 c = lds4(a_col + 16 * slot);
-                            const float w = a * t0;
-                            r0 = fmaf(c.x, w, r0);
-                            g0 = fmaf(c.y, w, g0);
-                            b0 = fmaf(c.z, w, b0);
-                            t0 = test;
-                            last0 = base + slot + 1;
-                            cnt0++;
-                            if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
-                        }
-                    }
-                }
-                if (!done1) {
-                    float gw;
-                    const float a = pair_alpha(fpy1 - g4.y, A, B, h4, gw);
-                    if (a > 0.0f) {
-                        const float test = t1 * (1.0f - a);
-                        if (test < 1e-4f) {
-                            done1 = true;
-                            it1 = base + slot + 1;
-                        } else {
-                            const float4 c = lds4(a_col + 16 * slot);
-                            const float w = a * t1;
-                            r1 = fmaf(c.x, w, r1);
-                            g1 = fmaf(c.y, w, g1);
-                            b1 = fmaf(c.z, w, b1);
-                            t1 = test;
-                            last1 = base + slot + 1;
-                            cnt1++;
-                            if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
-                        }
-                    }
-                }
+            // two entries per step: the four pair alphas are independent and
+            // computed ahead; compositing stays in list order per pixel
+            for (int k = k0; k < kend; k += 2) {
+                const bool two = k + 1 < kend;
+                const int sa = ldsu8(a_list + k), sb = two ? ldsu8(a_list + k + 1) : sa;
+                const float4 ga = lds4(a_gh + 32 * sa), ha = lds4(a_gh + 32 * sa + 16);
+                const float4 gb = lds4(a_gh + 32 * sb), hb = lds4(a_gh + 32 * sb + 16);
+                float Aa, Ba, Ab, Bb;
+                col_terms(fpx - ga.x, ga, Aa, Ba);
+                col_terms(fpx - gb.x, gb, Ab, Bb);
+                float gw;
+                const float aa0 = pair_alpha_bl(fpy0 - ga.y, Aa, Ba, ha, gw);
+                const float aa1 = pair_alpha_bl(fpy1 - ga.y, Aa, Ba, ha, gw);
+                const float ab0 = two ? pair_alpha_bl(fpy0 - gb.y, Ab, Bb, hb, gw) : 0.0f;
+                const float ab1 = two ? pair_alpha_bl(fpy1 - gb.y, Ab, Bb, hb, gw) : 0.0f;
+                composite<TOUCH>(aa0, sa, base, a_col, touched, srank, done0, it0, t0, r0, g0, b0,
+                                 last0, cnt0);
+                composite<TOUCH>(aa1, sa, base, a_col, touched, srank, done1, it1, t1, r1, g1, b1,
+                                 last1, cnt1);
+                composite<TOUCH>(ab0, sb, base, a_col, touched, srank, done0, it0, t0, r0, g0, b0,
+                                 last0, cnt0);
+                composite<TOUCH>(ab1, sb, base, a_col, touched, srank, done1, it1, t1, r1, g1, b1,
+                                 last1, cnt1);
             }
         }
     }
