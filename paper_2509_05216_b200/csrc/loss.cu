@@ -234,13 +234,32 @@ __global__ void __launch_bounds__(256) ssim_adjoint_kernel(
 }
 
 // Fixed-order final reduction (one block): loss = (1-lam) L1 + lam (1 - SSIM).
-__global__ void loss_finish_kernel(int n_ssim, const double *__restrict__ ssim_part, int n_l1,
-                                   const double *__restrict__ l1_part, double n_pix,
-                                   double n_centers, double lam, double *__restrict__ out) {
-    __shared__ double red[8];
-    double a = 0.0, b = 0.0;
-    for (int i = threadIdx.x; i < n_ssim; i += blockDim.x) a += ssim_part[i];
-    for (int i = threadIdx.x; i < n_l1; i += blockDim.x) b += l1_part[i];
+// Each thread sums a strided subset in index order; the loads of a batch of
+// 8 are issued together so the loop is not one dependent load per element.
+constexpr int FINISH_THREADS = 1024;
+
+__device__ __forceinline__ double strided_sum(const double *__restrict__ x, int n) {
+    double a = 0.0;
+    for (int i0 = threadIdx.x; i0 < n; i0 += 8 * FINISH_THREADS) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int i = i0 + u * FINISH_THREADS;
+            v[u] = i < n ? x[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            if (i0 + u * FINISH_THREADS < n) a += v[u];
+    }
+    return a;
+}
+
+__global__ void __launch_bounds__(FINISH_THREADS) loss_finish_kernel(
+    int n_ssim, const double *__restrict__ ssim_part, int n_l1, const double *__restrict__ l1_part,
+    double n_pix, double n_centers, double lam, double *__restrict__ out) {
+    __shared__ double red[FINISH_THREADS / 32];
+    const double a = strided_sum(ssim_part, n_ssim);
+    const double b = strided_sum(l1_part, n_l1);
     const double sa = block_sum(a, red);
     __syncthreads();
     const double sb = block_sum(b, red);
@@ -361,7 +380,7 @@ extern "C" int isg_loss_finish(int32_t height, int32_t width, double lambda_dssi
     int e = isg_loss_partials_size(height, width, &nf, &na);
     if (e) return e;
     const double n_pix = 3.0 * height * width, n_centers = 3.0 * (height - 10) * (width - 10);
-    loss_finish_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(nf, part_ssim, na, part_l1, n_pix,
+    loss_finish_kernel<<<1, FINISH_THREADS, 0, (cudaStream_t)stream>>>(nf, part_ssim, na, part_l1, n_pix,
                                                             n_centers, lambda_dssim, loss_dev);
     ISG_CHECK_LAUNCH();
     return 0;
@@ -412,7 +431,7 @@ extern "C" int isg_ssim(void *workspace, size_t *ws_bytes, int32_t height, int32
     ssim_fields_kernel<double, double, double><<<gf, 256, 0, s>>>(
         height, width, channels, image, 0, ref, nullptr, 0, 0, 0, 0, height, pf);
     ISG_CHECK_LAUNCH();
-    loss_finish_kernel<<<1, 256, 0, s>>>((int)nf, pf, 0, nullptr, 0.0,
+    loss_finish_kernel<<<1, FINISH_THREADS, 0, s>>>((int)nf, pf, 0, nullptr, 0.0,
                                          (double)channels * hc * wc, 0.0, out_dev);
     ISG_CHECK_LAUNCH();
     return 0;
