@@ -9,7 +9,8 @@ include/isogs.h (libisogs.so, loaded by _lib.py); there is no CPU fallback.
 
 from .camera import Camera, OrbitSpec, look_at, make_orbit
 from .densify import DensifyMapping, densify_and_prune
-from .gaussians import PARAM_NAMES, GaussianCloud, cloud_from_points, to_device_cloud
+from .gaussians import (PARAM_NAMES, GaussianCloud, cloud_from_points, load_checkpoint,
+                        load_train_state, save_checkpoint, save_train_state, to_device_cloud)
 from .metrics import loss_l1_dssim, psnr, quantize8, ssim
 from .optim import adam_init, adam_step, position_lr
 from .rasterizer import (ParamGradients, ProjectedSplat, RenderAux, SplatBatch,

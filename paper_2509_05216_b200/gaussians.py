@@ -9,6 +9,7 @@ training (float64 accepted by the API for the tight cross-check build).
 from __future__ import annotations
 
 import math
+import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -16,6 +17,8 @@ import torch
 
 PARAM_NAMES = ("positions", "log_scales", "rotations", "opacity_logits", "sh_coeffs")
 _INIT_OPACITY_LOGIT = math.log(0.1 / 0.9)
+_CKPT_MAGIC = b"SSGC"  # gaussians.py:18-19
+_CKPT_VERSION = 1
 
 
 @dataclass
@@ -96,3 +99,74 @@ def cloud_from_points(points: np.ndarray, log_scales: np.ndarray, degree: int = 
         sh_coeffs=torch.from_numpy(np.zeros((n, k, 3), dtype=np.float32)),
         degree=degree)
     return to_device_cloud(host, device)
+
+
+def save_checkpoint(path: str, cloud) -> None:
+    """The reference's SSGC file (gaussians.py:194-204): magic, <IQI version /
+    count / degree, then the five parameter blocks as little-endian float32.
+    Accepts a device GaussianCloud or any object with the cloud attributes."""
+    n = int(cloud.positions.shape[0])
+    deg = int(cloud.degree)
+    with open(path, "wb") as fh:
+        fh.write(_CKPT_MAGIC)
+        fh.write(struct.pack("<IQI", _CKPT_VERSION, n, deg))
+        for k in PARAM_NAMES:
+            a = getattr(cloud, k)
+            a = a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+            fh.write(np.ascontiguousarray(a, dtype="<f4").tobytes())
+
+
+def load_checkpoint(path: str, device=None) -> GaussianCloud:
+    """Read an SSGC file (gaussians.py:206-235, same validation errors) into
+    a float32 device cloud."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if blob[:4] != _CKPT_MAGIC:
+        raise ValueError(f"{path}: bad magic {blob[:4]!r}, expected {_CKPT_MAGIC!r}")
+    version, n, degree = struct.unpack_from("<IQI", blob, 4)
+    if version != _CKPT_VERSION:
+        raise ValueError(f"{path}: unsupported version {version}")
+    k = (degree + 1) ** 2
+    counts = [n * 3, n * 3, n * 4, n, n * k * 3]
+    body = 4 + struct.calcsize("<IQI")
+    want = body + 4 * sum(counts)
+    if len(blob) != want:
+        raise ValueError(f"{path}: expected {want} bytes, got {len(blob)}")
+    flat = np.frombuffer(blob, dtype="<f4", offset=body)
+    shapes = [(n, 3), (n, 3), (n, 4), (n,), (n, k, 3)]
+    parts, at = [], 0
+    for c, shp in zip(counts, shapes):
+        parts.append(flat[at:at + c].reshape(shp).astype(np.float32))
+        at += c
+    host = GaussianCloud(*(torch.from_numpy(p_) for p_ in parts), degree=int(degree))
+    host.validate()
+    return to_device_cloud(host, device)
+
+
+def save_train_state(path: str, trainer, iteration: int) -> None:
+    """Resumable training state (an extension: the reference checkpoint holds
+    parameters only): the SSGC cloud plus Adam moments, TrainStats and the
+    iteration in `path + '.state.npz'`."""
+    save_checkpoint(path, trainer.cloud)
+    extra = {"iteration": np.array(iteration)}
+    for k in PARAM_NAMES:
+        extra["m_" + k] = trainer.m[k].cpu().numpy()
+        extra["v_" + k] = trainer.v[k].cpu().numpy()
+    extra["seen"] = trainer.stats.seen.cpu().numpy()
+    extra["grad_accum"] = trainer.stats.grad_accum.cpu().numpy()
+    np.savez(path + ".state.npz", **extra)
+
+
+def load_train_state(path: str, trainer) -> int:
+    """Restore a Trainer from save_train_state; returns the iteration."""
+    from .training import TrainStats
+    cloud = load_checkpoint(path, trainer.device)
+    z = np.load(path + ".state.npz")
+    dev = trainer.device
+    trainer.cloud = cloud
+    trainer.m = {k: torch.from_numpy(z["m_" + k]).to(dev) for k in PARAM_NAMES}
+    trainer.v = {k: torch.from_numpy(z["v_" + k]).to(dev) for k in PARAM_NAMES}
+    trainer.stats = TrainStats(grad_accum=torch.from_numpy(z["grad_accum"]).to(dev),
+                               seen=torch.from_numpy(z["seen"]).to(dev))
+    trainer.grads = None
+    return int(z["iteration"])

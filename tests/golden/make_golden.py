@@ -159,7 +159,7 @@ def main():
     print("train_tiny losses", rep.iteration_losses)
 
 
-if __name__ == "__main__" and "--config1" not in sys.argv and "--densify" not in sys.argv:
+if __name__ == "__main__" and not set(sys.argv) & {"--config1", "--densify", "--checkpoint"}:
     main()
 
 
@@ -248,3 +248,15 @@ def densify():
 
 if __name__ == "__main__" and "--densify" in sys.argv:
     densify()
+
+
+def checkpoint():
+    """SSGC checkpoint bytes (gaussians.py:194-204) of a seeded random cloud."""
+    from isosplat.gaussians import save_checkpoint
+    c = oracles.random_cloud(np.random.default_rng(31), 40)
+    save_checkpoint(os.path.join(HERE, "ckpt_random40.ssgc"), c)
+    np.savez_compressed(os.path.join(HERE, "ckpt_random40.npz"), **cloud_dict(c))
+
+
+if __name__ == "__main__" and "--checkpoint" in sys.argv:
+    checkpoint()

@@ -70,3 +70,35 @@ def test_config1_psnr_parity_and_determinism():
     assert np.max(np.abs(got - ref) / ref) <= 2e-3
     _, rep2 = P.train_single(ds, cfg, init_cloud=_init(d), evaluate=False)
     assert rep2.iteration_losses == rep.iteration_losses
+
+
+def test_resume_from_train_state_is_bitwise(tmp_path):
+    """save_train_state / load_train_state (SSGC cloud + Adam moments + stats)
+    resume a run bit for bit."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200.engine import Trainer
+    d = load("train_tiny")
+    ds = _dataset(d, "images", d["images"].shape[0])
+    cfg = P.TrainConfig(iterations=6, densify=False, seed=4)
+    gt = torch.from_numpy(np.ascontiguousarray(d["images"])).cuda()
+    sched = P.build_schedule(6, ds.view_count, 4)
+
+    def fresh():
+        return Trainer(P.to_device_cloud(_init(d, "init_")), ds.width, ds.height, cfg,
+                       ds.scene_extent)
+
+    a = fresh()
+    for it in range(1, 7):
+        a.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
+    b = fresh()
+    for it in range(1, 4):
+        b.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
+    path = str(tmp_path / "run.ssgc")
+    P.save_train_state(path, b, 3)
+    c = fresh()
+    start = P.load_train_state(path, c)
+    assert start == 3
+    for it in range(start + 1, 7):
+        c.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(a.cloud, k), getattr(c.cloud, k)), k
