@@ -163,8 +163,7 @@ def cpu_workload(args):
     n, periods, mp, res, nv = S.CONFIGS[name]
     res_s = args.cpu_res or res
     pos, normals = S.gyroid_points(n, periods, mp)
-    from paper_2509_05216_b200.training import init_log_scales
-    ls = init_log_scales(pos)
+    ls = _host_log_scales(pos)
     cams = S.orbit(n, nv, res_s)
     # GT: target-cloud renders would need the GPU; the CPU arm trains against a
     # flat mid-grey target of the same shape (the work per step does not
@@ -177,6 +176,18 @@ def cpu_workload(args):
     return ({"points": pos, "log_scales": ls, "data": "synthetic gyroid isosurface",
              "config": workload_config(name, pos.shape[0], res_s, nv),
              "sample": sample}, cams, imgs)
+
+
+def _host_log_scales(points):
+    """Scale seeding for the CPU arm's inputs (the reference's exact 3-NN mean
+    distance, gaussians.py:124-191) on the host (scipy kd-tree), so no GPU
+    kernel touches the reference arm."""
+    import numpy as np
+    from scipy.spatial import cKDTree
+    pts = np.asarray(points, dtype=np.float64)
+    d, _ = cKDTree(pts).query(pts, k=4, workers=-1)
+    dist = np.maximum(np.asarray(d[:, 1:], dtype=np.float64).mean(axis=1), 1e-7)
+    return np.repeat(np.log(dist)[:, None], 3, axis=1).astype(np.float32)
 
 
 def workload_config(name, n, res, views):

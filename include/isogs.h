@@ -327,6 +327,16 @@ int isg_exp_f64(int64_t n, const double *x, double *y, void *stream);
 /* Library identification: returns a static string (arch, build flags). */
 const char *isg_version(void);
 
+/* Exact mean distance to the k (<= 8) nearest neighbours of every point
+ * over the reference's bucket grid (_mean_knn_distance_grid,
+ * gaussians.py:143-162; _knn_mean_grid, _kernels.py:636-708): points (n,3)
+ * float64 row-major; lo (3 host doubles), cell and the grid dims gx, gy, gz
+ * as the reference computes them on the host.  Bit-exact.  Two-phase
+ * workspace (workspace == NULL: size query). */
+int isg_knn_mean_grid(void *workspace, size_t *ws_bytes, const double *points, int64_t n,
+                      int32_t k, const double *lo, double cell, int64_t gx, int64_t gy,
+                      int64_t gz, double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

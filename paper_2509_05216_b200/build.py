@@ -31,6 +31,7 @@ SOURCES = {
     "raster_f32.cu": ["-ftz=true"],
     "loss.cu": [],
     "dist.cu": [],
+    "knn.cu": ["-fmad=false"],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

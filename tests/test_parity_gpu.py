@@ -264,3 +264,14 @@ def test_sort_depth_equals_full_64bit_sort():
     k1, v1 = L.sort_pairs(keys, vals, (0, 64), ws1)
     k2, v2 = L.sort_depth(keys, vals, ws2)
     assert torch.equal(k1, k2) and torch.equal(v1, v2)
+
+
+def test_gpu_knn_init_matches_reference_bitwise():
+    """init_log_scales on the GPU (isg_knn_mean_grid) reproduces the
+    reference's init_from_points log-scales bit for bit (config 1: 20000
+    points, the reference's grid path)."""
+    from paper_2509_05216_b200.training import init_log_scales
+    d = load("config1")
+    got = init_log_scales(d["points"])
+    assert got.dtype == np.float32 and got.shape == d["init_log_scales"].shape
+    assert np.array_equal(got, d["init_log_scales"])
