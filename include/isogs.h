@@ -111,6 +111,11 @@ int isg_bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_t *
                   int32_t feat_dtype, int32_t row_lo, int32_t row_hi, int32_t *rect_sorted,
                   void *feat_sorted, int64_t *emit_off, int64_t *counts, void *stream);
 
+/* Row -> rank inverse of the depth order: rank_of[order[r]] = r for
+ * visible ranks (sorted key != ~0), -1 for culled rows.  n <= INT32_MAX. */
+int isg_rank_of(int64_t n, const uint64_t *sorted_keys, const int32_t *order, int32_t *rank_of,
+                void *stream);
+
 /* Binning, stage 2 (_fill_tile_entries, _kernels.py:215-225): emit
  * (tile id - row_lo*tiles_x, rank) pairs in rank order for ranks [0, m),
  * rects clipped to tile rows [row_lo, row_hi) exactly as in isg_bin_count. */
@@ -212,7 +217,9 @@ int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t ti
  * canon_rows tile rows, then block sums ascending -- whose grouping does not
  * depend on the GPU count (needs rect_sorted and the band rows).  If
  * grad_norm is non-NULL it receives hypot(dmean) at row order[r]
- * (rasterizer.py:397). */
+ * (rasterizer.py:397).  order == NULL writes grad2d in rank order (row r =
+ * rank r) instead of at row order[r]: coalesced, for consumers indexed
+ * through isg_rank_of. */
 int isg_reduce_ordered(int32_t feat_dtype, int64_t m, const int64_t *emit_off,
                        const void *partials, const int32_t *order, const int32_t *rect_sorted,
                        int32_t row_lo, int32_t row_hi, int32_t canon_rows, double *grad2d,
@@ -313,6 +320,15 @@ int isg_chain_train(const isg_params *p, const isg_camera *cam, const uint8_t *f
                     const double *grad2d, float *d_positions, float *d_log_scales,
                     float *d_rotations, float *d_opacity_logits, float *d_sh, int64_t *seen,
                     double *grad_accum, double half_w, double half_h, void *stream);
+
+/* isg_chain_train over a rank-ordered grad2d (isg_reduce_ordered with
+ * order == NULL): row i reads the 2-D gradients of rank rank_of[i]
+ * (isg_rank_of); rows with rank -1 are not visible (zero gradients). */
+int isg_chain_train_ranked(const isg_params *p, const isg_camera *cam, const int32_t *rank_of,
+                           const double *grad2d_ranked, float *d_positions, float *d_log_scales,
+                           float *d_rotations, float *d_opacity_logits, float *d_sh,
+                           int64_t *seen, double *grad_accum, double half_w, double half_h,
+                           void *stream);
 
 /* ... then dense float32 Adam over up to 8 groups in one launch (arrays of
  * `count` host-side pointers / sizes / learning rates; constants as for

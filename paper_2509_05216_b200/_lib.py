@@ -71,6 +71,7 @@ SIGNATURES = {
     "isg_sort_depth": [_P, _SZ, _P, _P, _P, _P, _I64, _P],
     "isg_bin_count": [_P, _SZ, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P],
     "isg_bin_emit": [_I64, _P, _P, _I32, _I32, _I32, _P, _P, _P],
+    "isg_rank_of": [_I64, _P, _P, _P, _P],
     "isg_tile_offsets": [_I64, _P, _I32, _P, _P],
     "isg_bin_emit16": [_I64, _P, _P, _I32, _I32, _I32, _P, _P, _P],
     "isg_sort_u16": [_P, _SZ, _P, _P, _P, _P, _I64, _I32, _I32, _P],
@@ -104,6 +105,8 @@ SIGNATURES = {
                        ctypes.POINTER(AdamConsts_t), _D, _D, _P],
     "isg_chain_train": [ctypes.POINTER(Params_t), ctypes.POINTER(Camera_t), _P, _P, _P, _P, _P,
                         _P, _P, _P, _P, _D, _D, _P],
+    "isg_chain_train_ranked": [ctypes.POINTER(Params_t), ctypes.POINTER(Camera_t), _P, _P, _P,
+                               _P, _P, _P, _P, _P, _P, _D, _D, _P],
     "isg_adam_groups": [_I32, _P, _P, _P, _P, _P, _P, ctypes.POINTER(AdamConsts_t), _P],
     "isg_exp_f64": [_I64, _P, _P, _P],
     "isg_knn_mean_grid": [_P, _SZ, _P, _I64, _I32, _P, _D, _I64, _I64, _I64, _P, _P],

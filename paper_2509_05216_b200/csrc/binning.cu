@@ -225,6 +225,31 @@ extern "C" int isg_bin_count(void *workspace, size_t *ws_bytes, int64_t n,
     return 0;
 }
 
+namespace isg {
+// rank_of[order[r]] = r for visible ranks (sorted key != ~0), -1 otherwise:
+// the row -> rank inverse that lets row-parallel kernels read rank-ordered
+// per-splat data.  order is a permutation, so every row is written.
+__global__ void __launch_bounds__(256) rank_of_kernel(int64_t n,
+                                                      const uint64_t *__restrict__ sorted_keys,
+                                                      const int32_t *__restrict__ order,
+                                                      int32_t *__restrict__ rank_of) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    rank_of[order[r]] = sorted_keys[r] != ~0ull ? (int32_t)r : -1;
+}
+}  // namespace isg
+
+extern "C" int isg_rank_of(int64_t n, const uint64_t *sorted_keys, const int32_t *order,
+                           int32_t *rank_of, void *stream) {
+    if (n < 0 || n > INT32_MAX || (n > 0 && (!sorted_keys || !order || !rank_of)))
+        return (int)cudaErrorInvalidValue;
+    if (n == 0) return 0;
+    rank_of_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, sorted_keys, order,
+                                                                        rank_of);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
 extern "C" int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
                             int32_t tiles_x, int32_t row_lo, int32_t row_hi, uint32_t *tile_keys,
                             int32_t *tile_vals, void *stream) {

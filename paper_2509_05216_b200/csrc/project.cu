@@ -371,6 +371,7 @@ template <int K3>
 #endif
 __global__ void __launch_bounds__(128, CHAIN_MINB) chain_train_kernel(isg_params p, Cam cam,
                                                           const uint8_t *__restrict__ flag,
+                                                          const int32_t *__restrict__ rank_of,
                                                           const double *__restrict__ grad2d,
                                                           float *dpos, float *dls, float *drot,
                                                           float *dlogit, float *dsh,
@@ -379,10 +380,12 @@ __global__ void __launch_bounds__(128, CHAIN_MINB) chain_train_kernel(isg_params
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
     Grads g;
-    if (flag[i]) {
+    // rank_of: rank-ordered grad2d (row i -> its rank, -1 = not visible)
+    const int64_t gi = rank_of ? (int64_t)rank_of[i] : (flag[i] ? i : -1);
+    if (gi >= 0) {
         Row<float> row;
         load_row<float>(p, i, row);
-        const double *g2 = grad2d + 9 * i;
+        const double *g2 = grad2d + 9 * gi;
         chain_one<float>(row, p.degree, cam, g2, g);
         if (seen) seen[i] += 1;
         if (grad_accum) grad_accum[i] += hypot(g2[0] * half_w, g2[1] * half_h);
@@ -549,24 +552,53 @@ extern "C" int isg_adam(int32_t dtype, int64_t n, void *p, const void *g, void *
     return 0;
 }
 
+static int chain_train_launch(const isg_params *p, const isg_camera *cam, const uint8_t *flag,
+                              const int32_t *rank_of, const double *grad2d, float *d_positions,
+                              float *d_log_scales, float *d_rotations, float *d_opacity_logits,
+                              float *d_sh, int64_t *seen, double *grad_accum, double half_w,
+                              double half_h, void *stream);
+
 extern "C" int isg_chain_train(const isg_params *p, const isg_camera *cam, const uint8_t *flag,
                                const double *grad2d, float *d_positions, float *d_log_scales,
                                float *d_rotations, float *d_opacity_logits, float *d_sh,
                                int64_t *seen, double *grad_accum, double half_w, double half_h,
                                void *stream) {
-    if (!p || !cam || !flag || !grad2d || p->n < 0 || p->dtype != ISG_F32)
+    if (!flag) return (int)cudaErrorInvalidValue;
+    return chain_train_launch(p, cam, flag, nullptr, grad2d, d_positions, d_log_scales,
+                              d_rotations, d_opacity_logits, d_sh, seen, grad_accum, half_w,
+                              half_h, stream);
+}
+
+extern "C" int isg_chain_train_ranked(const isg_params *p, const isg_camera *cam,
+                                      const int32_t *rank_of, const double *grad2d_ranked,
+                                      float *d_positions, float *d_log_scales,
+                                      float *d_rotations, float *d_opacity_logits, float *d_sh,
+                                      int64_t *seen, double *grad_accum, double half_w,
+                                      double half_h, void *stream) {
+    if (!rank_of) return (int)cudaErrorInvalidValue;
+    return chain_train_launch(p, cam, nullptr, rank_of, grad2d_ranked, d_positions,
+                              d_log_scales, d_rotations, d_opacity_logits, d_sh, seen, grad_accum,
+                              half_w, half_h, stream);
+}
+
+static int chain_train_launch(const isg_params *p, const isg_camera *cam, const uint8_t *flag,
+                              const int32_t *rank_of, const double *grad2d, float *d_positions,
+                              float *d_log_scales, float *d_rotations, float *d_opacity_logits,
+                              float *d_sh, int64_t *seen, double *grad_accum, double half_w,
+                              double half_h, void *stream) {
+    if (!p || !cam || !grad2d || p->n < 0 || p->dtype != ISG_F32)
         return (int)cudaErrorInvalidValue;
     if (p->n == 0) return 0;
     Cam c = to_cam(*cam);
     cudaStream_t s = (cudaStream_t)stream;
     if (p->degree >= 1)
         chain_train_kernel<12><<<blocks_for(p->n, 128), 128, 0, s>>>(
-            *p, c, flag, grad2d, d_positions, d_log_scales, d_rotations, d_opacity_logits, d_sh,
-            seen, grad_accum, half_w, half_h);
+            *p, c, flag, rank_of, grad2d, d_positions, d_log_scales, d_rotations,
+            d_opacity_logits, d_sh, seen, grad_accum, half_w, half_h);
     else
         chain_train_kernel<3><<<blocks_for(p->n, 128), 128, 0, s>>>(
-            *p, c, flag, grad2d, d_positions, d_log_scales, d_rotations, d_opacity_logits, d_sh,
-            seen, grad_accum, half_w, half_h);
+            *p, c, flag, rank_of, grad2d, d_positions, d_log_scales, d_rotations,
+            d_opacity_logits, d_sh, seen, grad_accum, half_w, half_h);
     ISG_CHECK_LAUNCH();
     return 0;
 }

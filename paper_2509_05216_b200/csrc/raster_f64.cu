@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(256) reduce_ordered_kernel(
     if (r >= m) return;
     double acc[9];
     fold_rank<T>(partials, emit_off[r], emit_off[r + 1], rect_sorted, r, row_lo, canon_rows, acc);
-    const int64_t row = order[r];
+    const int64_t row = order ? (int64_t)order[r] : r;
     double *dst = grad2d + 9 * row;
 #pragma unroll
     for (int k = 0; k < 9; k++) dst[k] = acc[k];
@@ -370,7 +370,10 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_ordered_f32_kernel(
     }
     if (!live) return;
     st.finish();
-    const int64_t row = order[r];
+    // order == NULL: rank-ordered output (coalesced; row-parallel consumers
+    // find their rank through isg_rank_of).  Row-ordered writes of 72-byte
+    // records scatter partial sectors over HBM.
+    const int64_t row = order ? (int64_t)order[r] : r;
     double *dst = grad2d + 9 * row;
 #pragma unroll
     for (int k = 0; k < 9; k++) dst[k] = st.acc[k];

@@ -115,6 +115,9 @@ class Rasterizer:
         self.n_contrib_out = None  # set to (H, W) int32 tensors to count pairs
         self.n_iter_out = None
         self.timer: PhaseTimer | None = None
+        # training step: grad2d in rank order (coalesced fold output), read by
+        # the chain through rank_of (isg_chain_train_ranked)
+        self.ranked_grads = False
 
     def resize(self, n: int) -> None:
         dev = self.device
@@ -129,6 +132,7 @@ class Rasterizer:
         self.rect_sorted = torch.empty((n, 4), dtype=torch.int32, device=dev)
         self.feat_sorted = torch.empty((n, 12), dtype=self.feat_dtype, device=dev)
         self.emit_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self.rank_of = torch.empty(n, dtype=torch.int32, device=dev)
         self.counts = torch.zeros(2, dtype=torch.int64, device=dev)
         self.grad2d = torch.empty((n, 9), dtype=torch.float64, device=dev)
 
@@ -164,6 +168,9 @@ class Rasterizer:
                                   self.ftag, 0, self.tiles_y, L.ptr(self.rect_sorted),
                                   L.ptr(self.feat_sorted), L.ptr(self.emit_off),
                                   L.ptr(self.counts), s), "isg_bin_count")
+        if self.ranked_grads:
+            L.check(lib.isg_rank_of(n, L.ptr(self.key_sorted), L.ptr(self.order),
+                                    L.ptr(self.rank_of), s), "isg_rank_of")
         _mark(tm, "bin_count")
         self.counts_host.copy_(self.counts, non_blocking=True)
         torch.cuda.current_stream().synchronize()
@@ -217,7 +224,8 @@ class Rasterizer:
         _mark(self.timer, "raster_bwd")
         if ctx.m:
             L.check(lib.isg_reduce_ordered(self.ftag, ctx.m, L.ptr(self.emit_off),
-                                           L.ptr(self.partials), L.ptr(self.order),
+                                           L.ptr(self.partials),
+                                           None if self.ranked_grads else L.ptr(self.order),
                                            L.ptr(self.rect_sorted), 0, self.tiles_y,
                                            self.canon_rows,
                                            L.ptr(self.grad2d), None, s), "isg_reduce_ordered")
@@ -228,7 +236,7 @@ class Rasterizer:
 
 def update_params(cloud: GaussianCloud, m: dict, v: dict, grads: dict, seen, grad_accum, flag,
                   grad2d, cam_struct, lrs: list, it: int, width: int, height: int,
-                  timer=None) -> None:
+                  timer=None, rank_of=None) -> None:
     """Chain rule + TrainStats (isg_chain_train), then dense Adam over the five
     groups in one launch (isg_adam_groups): engine.py:508-536, optim.py:20-56."""
     lib = L.lib()
@@ -239,12 +247,19 @@ def update_params(cloud: GaussianCloud, m: dict, v: dict, grads: dict, seen, gra
     p.sh, p.n, p.degree, p.dtype = L.ptr(cloud.sh_coeffs), cloud.count, cloud.degree, L.ISG_F32
     if cloud.count == 0:
         return
-    L.check(lib.isg_chain_train(ctypes.byref(p), ctypes.byref(cam_struct), L.ptr(flag),
-                                L.ptr(grad2d), L.ptr(grads["positions"]),
-                                L.ptr(grads["log_scales"]), L.ptr(grads["rotations"]),
-                                L.ptr(grads["opacity_logits"]), L.ptr(grads["sh_coeffs"]),
-                                L.ptr(seen), L.ptr(grad_accum), 0.5 * width, 0.5 * height, s),
-            "isg_chain_train")
+    if rank_of is not None:
+        L.check(lib.isg_chain_train_ranked(
+            ctypes.byref(p), ctypes.byref(cam_struct), L.ptr(rank_of), L.ptr(grad2d),
+            L.ptr(grads["positions"]), L.ptr(grads["log_scales"]), L.ptr(grads["rotations"]),
+            L.ptr(grads["opacity_logits"]), L.ptr(grads["sh_coeffs"]), L.ptr(seen),
+            L.ptr(grad_accum), 0.5 * width, 0.5 * height, s), "isg_chain_train_ranked")
+    else:
+        L.check(lib.isg_chain_train(ctypes.byref(p), ctypes.byref(cam_struct), L.ptr(flag),
+                                    L.ptr(grad2d), L.ptr(grads["positions"]),
+                                    L.ptr(grads["log_scales"]), L.ptr(grads["rotations"]),
+                                    L.ptr(grads["opacity_logits"]), L.ptr(grads["sh_coeffs"]),
+                                    L.ptr(seen), L.ptr(grad_accum), 0.5 * width, 0.5 * height,
+                                    s), "isg_chain_train")
     _mark(timer, "chain")
     P5 = ctypes.c_void_p * 5
     pp = P5(*(L.ptr(getattr(cloud, k)) for k in PARAM_NAMES))
@@ -275,6 +290,7 @@ class Trainer:
                                 seen=torch.zeros(n, dtype=torch.int64, device=self.device))
         self.r = Rasterizer(n, width, height, self.device, config.background,
                             canon_rows=canon_rows)
+        self.r.ranked_grads = True
         self.loss_dev = torch.zeros(max(config.iterations, 1) + 1, dtype=torch.float64,
                                     device=self.device)
         self.lr_host = (ctypes.c_float * 5)()
@@ -316,7 +332,7 @@ class Trainer:
             self.grads = {k: torch.empty_like(getattr(self.cloud, k)) for k in PARAM_NAMES}
         update_params(self.cloud, self.m, self.v, self.grads, self.stats.seen,
                       self.stats.grad_accum, r.flag, r.grad2d, r.cam_struct, self.lrs(it), it,
-                      r.width, r.height, r.timer)
+                      r.width, r.height, r.timer, rank_of=r.rank_of)
 
     def densify_due(self, it: int) -> bool:
         """engine.py:540-541."""

@@ -21,7 +21,7 @@ def declared_symbols() -> list[str]:
 
 def test_header_declares_entry_points():
     syms = declared_symbols()
-    for s in ("isg_knn_mean_grid", "isg_preprocess", "isg_sort_u64", "isg_sort_depth", "isg_sort_u16", "isg_bin_emit16",
+    for s in ("isg_knn_mean_grid", "isg_rank_of", "isg_chain_train_ranked", "isg_preprocess", "isg_sort_u64", "isg_sort_depth", "isg_sort_u16", "isg_bin_emit16",
               "isg_tile_offsets16", "isg_bin_count", "isg_bin_emit",
               "isg_raster_fwd", "isg_loss_l1_dssim", "isg_raster_bwd", "isg_reduce_ordered",
               "isg_chain", "isg_adam", "isg_chain_adam"):
