@@ -32,6 +32,7 @@ SOURCES = {
     "loss.cu": [],
     "dist.cu": [],
     "knn.cu": ["-fmad=false"],
+    "chain_f32.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -557,6 +557,12 @@ static int chain_train_launch(const isg_params *p, const isg_camera *cam, const 
                               float *d_log_scales, float *d_rotations, float *d_opacity_logits,
                               float *d_sh, int64_t *seen, double *grad_accum, double half_w,
                               double half_h, void *stream);
+namespace isg {
+void launch_chain_train_f32(const isg_params &p, const Cam &cam, const uint8_t *flag,
+                            const int32_t *rank_of, const double *grad2d, float *dpos,
+                            float *dls, float *drot, float *dlogit, float *dsh, int64_t *seen,
+                            double *grad_accum, double half_w, double half_h, cudaStream_t s);
+}
 
 extern "C" int isg_chain_train(const isg_params *p, const isg_camera *cam, const uint8_t *flag,
                                const double *grad2d, float *d_positions, float *d_log_scales,
@@ -591,14 +597,9 @@ static int chain_train_launch(const isg_params *p, const isg_camera *cam, const 
     if (p->n == 0) return 0;
     Cam c = to_cam(*cam);
     cudaStream_t s = (cudaStream_t)stream;
-    if (p->degree >= 1)
-        chain_train_kernel<12><<<blocks_for(p->n, 128), 128, 0, s>>>(
-            *p, c, flag, rank_of, grad2d, d_positions, d_log_scales, d_rotations,
-            d_opacity_logits, d_sh, seen, grad_accum, half_w, half_h);
-    else
-        chain_train_kernel<3><<<blocks_for(p->n, 128), 128, 0, s>>>(
-            *p, c, flag, rank_of, grad2d, d_positions, d_log_scales, d_rotations,
-            d_opacity_logits, d_sh, seen, grad_accum, half_w, half_h);
+    // float32 chain (chain_f32.cu): the training step's gradients are float32
+    launch_chain_train_f32(*p, c, flag, rank_of, grad2d, d_positions, d_log_scales, d_rotations,
+                           d_opacity_logits, d_sh, seen, grad_accum, half_w, half_h, s);
     ISG_CHECK_LAUNCH();
     return 0;
 }
