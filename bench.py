@@ -280,9 +280,11 @@ def run_ours(args, world, rank, local):
     # ---- CPU baseline: the reference path (oracle port) on this host
     cpu = None if args.no_cpu_baseline else cpu_baseline(wl, args)
 
-    launches_per_step = 12  # our kernels: preprocess, gather, count-finish, emit,
-    #   tile-offsets, raster_fwd, ssim fields, ssim adjoint, loss finish,
-    #   raster_bwd, reduce, chain_adam (CUB sort/scan passes not counted)
+    # our kernels per step (CUB sort/scan passes not counted): preprocess,
+    # depth_tie_fix, gather_rank, finish_counts, rank_of, emit_span,
+    # tile_offsets, raster fwd, ssim_fields, ssim_adjoint, loss_finish,
+    # raster bwd, ordered fold, chain (f32), Adam groups
+    launches_per_step = 15
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
