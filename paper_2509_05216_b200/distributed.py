@@ -806,19 +806,31 @@ def emulated_densify(ranks: list, it: int) -> list:
 
 # ------------------------------------------------------------------ drivers --
 
-def comm_step(rs: RankStep, comm: TorchComm, cam, gt: torch.Tensor, it: int) -> torch.Tensor:
-    """One iteration on this rank (multi-process, one GPU per rank)."""
+def comm_step(rs: RankStep, comm: TorchComm, cam, gt: torch.Tensor, it: int,
+              timer=None) -> torch.Tensor:
+    """One iteration on this rank (multi-process, one GPU per rank).  timer:
+    optional engine.PhaseTimer (CUDA events between the phases)."""
+    from .engine import _mark
+    _mark(timer, "begin")
     rec, cnt = rs.phase_project(cam)
+    _mark(timer, "project_route")
     rrec, _ = comm.alltoallv(rec, cnt)
+    _mark(timer, "a2a_splats")
     to_prev, to_next = rs.phase_render(rrec)
+    _mark(timer, "bin_render")
     sp, sn = rs.halo_shapes()
     got_prev, got_next = comm.halo(to_prev, to_next, sp, sn, torch.float32, rs.dev)
+    _mark(timer, "halo")
     parts = rs.phase_loss(got_prev, got_next, gt)
     comm.allreduce_sum_(parts)
     loss = rs.finish_loss()
+    _mark(timer, "loss_allreduce")
     grec, gcnt = rs.phase_backward()
+    _mark(timer, "backward_blockfold")
     rg, _ = comm.alltoallv(grec, gcnt)
+    _mark(timer, "a2a_grads")
     rs.phase_update(rg, it)
+    _mark(timer, "owner_fold_chain_adam")
     return loss
 
 
@@ -960,6 +972,10 @@ def bench_distributed(args, world: int, rank: int, local: int):
     from .training import TrainConfig, TrainDataset, PointCloud, build_schedule
     dev = torch.device("cuda", local)
     comm = TorchComm()
+    # torchrun pins OMP_NUM_THREADS=1; the host side of the step (collective
+    # bookkeeping between the device phases) runs measurably slower that way
+    import os
+    torch.set_num_threads(max(1, (os.cpu_count() or 1) // max(world, 1)))
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
     wl = S.make_workload(args.config, dev, log=log)
     n = wl.points.shape[0]
@@ -992,6 +1008,13 @@ def bench_distributed(args, world: int, rank: int, local: int):
     ms = torch.tensor([start.elapsed_time(stop)], dtype=torch.float64, device=dev)
     comm.max_(ms)
     ms_per_step = float(ms[0]) / args.steps
+    # per-phase device times of one more step (untimed), rank 0's view
+    from .engine import PhaseTimer
+    timer = PhaseTimer()
+    v = schedule[iters - 1]
+    comm_step(rs, comm, wl.cameras[v], wl.images_u8[v], iters, timer=timer)
+    phases = {k: round(x, 4) for k, x in timer.phases().items()}
+    log("[dist] phases (ms): " + ", ".join(f"{k} {x:.3f}" for k, x in phases.items()))
     # end to end: GT H2D from pinned host memory + loss D2H per step
     host = torch.empty(wl.images_u8.shape[1:], dtype=torch.uint8).pin_memory()
     gt = torch.empty_like(wl.images_u8[0])
@@ -1026,5 +1049,6 @@ def bench_distributed(args, world: int, rank: int, local: int):
             "clocks": clk.summary(), "gpu_launches": 22 * args.steps,
             "roofline": None, "cpu_baseline": None,
             "partition": {"bands_tile_rows": part.band_rows, "shard_sizes": smap.sizes},
+            "phases_ms": phases,
         }
         print(json.dumps(line), flush=True)
