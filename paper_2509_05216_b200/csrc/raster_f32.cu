@@ -160,25 +160,36 @@ __device__ __forceinline__ float4 lds4(uint32_t a) {
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
     return v;
 }
+__device__ __forceinline__ void sts(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
 __device__ __forceinline__ int ldsu8(uint32_t a) {
     unsigned short v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
     return (int)v;
 }
 
+// Forward kernel modes: TOUCH counts per-splat touches (the reference's
+// `touched`), STATS records n_contrib / n_iter (bench statistics only).
+constexpr int F_TOUCH = 1, F_STATS = 2;
+#define FINF __int_as_float(0x7f800000)
+
 // Front-to-back compositing of one pair (_kernels.py:258-272): skipped when
-// the pixel is done or alpha is 0; stops (without compositing) when T would
-// drop below 1e-4.
-template <bool TOUCH>
+// alpha is 0; stops (without compositing) when T would drop below 1e-4.  A
+// finished pixel moves its row coordinate to +inf, so every later exponent is
+// -inf and every later alpha 0 (c > 0 for every staged conic): no done flag is
+// carried.  CHECK re-tests that sentinel for an alpha computed before the
+// pixel finished (the second entry of a step).
+template <int MODE, bool CHECK>
 __device__ __forceinline__ void composite(float a, int slot, int base, uint32_t a_col,
-                                          int64_t *touched, const int *srank, bool &done,
+                                          int64_t *touched, const int *srank, float &fpy,
                                           int &it, float &t, float &r, float &g, float &b,
                                           int &last, int &cnt) {
-    if (done || !(a > 0.0f)) return;
+    if (!(a > 0.0f) || (CHECK && fpy == FINF)) return;
     const float test = t * (1.0f - a);
     if (test < 1e-4f) {
-        done = true;
-        it = base + slot + 1;
+        fpy = FINF;
+        if (MODE & F_STATS) it = base + slot + 1;
         return;
     }
     const float4 c = lds4(a_col + 16 * slot);
@@ -188,8 +199,8 @@ __device__ __forceinline__ void composite(float a, int slot, int base, uint32_t 
     b = fmaf(c.z, w, b);
     t = test;
     last = base + slot + 1;
-    cnt++;
-    if (TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
+    if (MODE & F_STATS) cnt++;
+    if (MODE & F_TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
 }
 
 // Warp w renders quadrant (w & 1, w >> 1) of the tile: lane (lx, ly) owns
@@ -199,13 +210,14 @@ __device__ __forceinline__ void composite(float a, int slot, int base, uint32_t 
 // result).
 constexpr int FCHK = 4;
 
-template <bool TOUCH>
+template <int MODE>
 __global__ void __launch_bounds__(NT, 6) fwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
     const float *__restrict__ feat, float bg0, float bg1, float bg2, void *image, int image_f64,
     float *__restrict__ t_final, int32_t *__restrict__ n_last, int32_t *__restrict__ n_contrib,
     int32_t *__restrict__ n_iter, int64_t *__restrict__ touched) {
+    constexpr bool TOUCH = MODE & F_TOUCH;
     __shared__ float4 sgh[FB][2];
     __shared__ float4 scol[FB];
     __shared__ int srank[TOUCH ? FB : 1];
@@ -218,7 +230,8 @@ __global__ void __launch_bounds__(NT, 6) fwd_kernel(
     const int px = tx * 16 + (warp & 1) * 8 + (lane & 7);
     const int py0 = ty * 16 + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
     const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
-    const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
+    const float fpx = (float)px;
+    float fpy0 = in0 ? (float)py0 : FINF, fpy1 = in1 ? (float)py1 : FINF;
     const float x0 = (float)(tx * 16), y0 = (float)(ty * 16);
     const int e0 = offsets[tl], n_ent = offsets[tl + 1] - e0;
     const uint32_t a_gh = smem_addr(&sgh[0][0]), a_col = smem_addr(&scol[0]);
@@ -226,9 +239,8 @@ __global__ void __launch_bounds__(NT, 6) fwd_kernel(
     float t0 = 1.0f, r0 = 0.0f, g0 = 0.0f, b0 = 0.0f;
     float t1 = 1.0f, r1 = 0.0f, g1 = 0.0f, b1 = 0.0f;
     int last0 = 0, last1 = 0, cnt0 = 0, cnt1 = 0, it0 = 0, it1 = 0;
-    bool done0 = !in0, done1 = !in1;
     for (int base = 0; base < n_ent; base += FB) {
-        if (__syncthreads_count(done0 && done1) == NT) break;
+        if (__syncthreads_count(fpy0 == FINF && fpy1 == FINF) == NT) break;
         const int j = base + threadIdx.x;
         unsigned mask = 0u;
         if (j < n_ent) {
@@ -260,7 +272,7 @@ __global__ void __launch_bounds__(NT, 6) fwd_kernel(
         __syncthreads();
         const int total = qcnt[warp][0] + qcnt[warp][1] + qcnt[warp][2] + qcnt[warp][3];
         for (int k0 = 0; k0 < total; k0 += FCHK) {
-            if (__all_sync(FULL, done0 && done1)) break;
+            if (__all_sync(FULL, fpy0 == FINF && fpy1 == FINF)) break;
             const int kend = min(k0 + FCHK, total);
             // two entries per step: the four pair alphas are independent and
             // computed ahead; compositing stays in list order per pixel
@@ -277,14 +289,14 @@ __global__ void __launch_bounds__(NT, 6) fwd_kernel(
                 const float aa1 = pair_alpha_bl(fpy1 - ga.y, Aa, Ba, ha, gw);
                 const float ab0 = two ? pair_alpha_bl(fpy0 - gb.y, Ab, Bb, hb, gw) : 0.0f;
                 const float ab1 = two ? pair_alpha_bl(fpy1 - gb.y, Ab, Bb, hb, gw) : 0.0f;
-                composite<TOUCH>(aa0, sa, base, a_col, touched, srank, done0, it0, t0, r0, g0, b0,
-                                 last0, cnt0);
-                composite<TOUCH>(aa1, sa, base, a_col, touched, srank, done1, it1, t1, r1, g1, b1,
-                                 last1, cnt1);
-                composite<TOUCH>(ab0, sb, base, a_col, touched, srank, done0, it0, t0, r0, g0, b0,
-                                 last0, cnt0);
-                composite<TOUCH>(ab1, sb, base, a_col, touched, srank, done1, it1, t1, r1, g1, b1,
-                                 last1, cnt1);
+                composite<MODE, false>(aa0, sa, base, a_col, touched, srank, fpy0, it0, t0, r0,
+                                       g0, b0, last0, cnt0);
+                composite<MODE, false>(aa1, sa, base, a_col, touched, srank, fpy1, it1, t1, r1,
+                                       g1, b1, last1, cnt1);
+                composite<MODE, true>(ab0, sb, base, a_col, touched, srank, fpy0, it0, t0, r0,
+                                      g0, b0, last0, cnt0);
+                composite<MODE, true>(ab1, sb, base, a_col, touched, srank, fpy1, it1, t1, r1,
+                                      g1, b1, last1, cnt1);
             }
         }
     }
@@ -310,8 +322,10 @@ __global__ void __launch_bounds__(NT, 6) fwd_kernel(
         }
         t_final[pix] = t;
         n_last[pix] = p ? last1 : last0;
-        if (n_contrib) n_contrib[pix] = p ? cnt1 : cnt0;
-        if (n_iter) n_iter[pix] = (p ? done1 : done0) ? (p ? it1 : it0) : n_ent;
+        if (MODE & F_STATS) {
+            if (n_contrib) n_contrib[pix] = p ? cnt1 : cnt0;
+            if (n_iter) n_iter[pix] = (p ? fpy1 : fpy0) == FINF ? (p ? it1 : it0) : n_ent;
+        }
     }
 }
 
@@ -434,6 +448,8 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
     const int my_slot = bfly_slot(lane);
     const uint32_t a_gh = smem_addr(&sgh[0][0]), a_col = smem_addr(&scol[0]);
     const uint32_t a_list = smem_addr(&slist[warp][0]);
+    // this lane's column of sred[warp][.][.] (lanes without a slot never store)
+    const uint32_t a_red = smem_addr(&sred[warp][0][0]) + 4u * (uint32_t)max(my_slot, 0);
 
     int last0 = 0, last1 = 0;
     float T0 = 0.0f, T1 = 0.0f, wr0 = 0, wg0 = 0, wb0 = 0, wr1 = 0, wg1 = 0, wb1 = 0;
@@ -554,7 +570,7 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
             }
             moment_terms(d0, s0, s1, s2, v);
             const float y = bfly9(v, lane);
-            if (my_slot >= 0) sred[warp][slot][my_slot] = y;
+            if (my_slot >= 0) sts(a_red + 36u * (uint32_t)slot, y);
         }
         __syncthreads();
         // fixed-order fold over the quadrants that saw the entry, then the
@@ -589,14 +605,19 @@ void launch_raster_fwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
                            const float *feat, float bg0, float bg1, float bg2, void *image,
                            int image_f64, float *t_final, int32_t *n_last, int32_t *n_contrib,
                            int32_t *n_iter, int64_t *touched, cudaStream_t s) {
-    if (touched)
-        f32::fwd_kernel<true><<<n_tiles, f32::NT, 0, s>>>(
-            W, H, tiles_x, row_lo, tile_ids, offsets, entries, feat, bg0, bg1, bg2, image,
-            image_f64, t_final, n_last, n_contrib, n_iter, touched);
-    else
-        f32::fwd_kernel<false><<<n_tiles, f32::NT, 0, s>>>(
-            W, H, tiles_x, row_lo, tile_ids, offsets, entries, feat, bg0, bg1, bg2, image,
-            image_f64, t_final, n_last, n_contrib, n_iter, touched);
+    const int mode = (touched ? f32::F_TOUCH : 0) | (n_contrib || n_iter ? f32::F_STATS : 0);
+#define ISG_FWD(M)                                                                               \
+    f32::fwd_kernel<M><<<n_tiles, f32::NT, 0, s>>>(W, H, tiles_x, row_lo, tile_ids, offsets,     \
+                                                   entries, feat, bg0, bg1, bg2, image,          \
+                                                   image_f64, t_final, n_last, n_contrib, n_iter, \
+                                                   touched)
+    switch (mode) {
+        case 0: ISG_FWD(0); break;
+        case 1: ISG_FWD(1); break;
+        case 2: ISG_FWD(2); break;
+        default: ISG_FWD(3); break;
+    }
+#undef ISG_FWD
 }
 
 template <typename DL>
