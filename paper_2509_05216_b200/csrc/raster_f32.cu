@@ -55,7 +55,8 @@ __device__ __forceinline__ float lg2a(float x) {
 }
 
 // Staged entry: g = (mx, my, -a/2, -b), h = (-c/2, thr, opacity, 0),
-// c = (r, g, b, 0).  The scalings are exact (powers of two / sign).
+// c = (r, g, b, 0).  The scalings are exact (powers of two / sign).  box_dead
+// reads this form; the inner loops read the base-2 form of to_log2().
 struct Staged {
     float4 g, h, c;
 };
@@ -78,19 +79,32 @@ __device__ __forceinline__ Staged stage(const float *__restrict__ feat, int rank
     return s;
 }
 
+// The quadratic-form coefficients and the threshold in base-2 units
+// (multiplied by log2 e once per staged entry), so a pair's exponent feeds
+// ex2 directly: power2 = log2(e) * power.
+__device__ __forceinline__ void to_log2(Staged &s) {
+    s.g.z = __fmul_rn(s.g.z, LOG2E);
+    s.g.w = __fmul_rn(s.g.w, LOG2E);
+    s.h.x = __fmul_rn(s.h.x, LOG2E);
+    s.h.y = __fmul_rn(s.h.y, LOG2E);
+}
+
 // Column terms of the exponent shared by a thread's two pixels (same x):
-// power = A + d1 * (B + nc * d1) with A = na d0^2, B = nb d0.
+// power2 = A + d1 * (B + nc * d1) with A = na d0^2, B = nb d0 (base 2).
 __device__ __forceinline__ void col_terms(float d0, const float4 &g4, float &A, float &B) {
     A = __fmul_rn(__fmul_rn(g4.z, d0), d0);
     B = __fmul_rn(g4.w, d0);
 }
 
 // Per-pair alpha (0 when the pair is skipped) and the Gaussian weight g.
+// The threshold test is an early exit only: a pair below it also fails
+// alpha >= 1/255 (the margin dominates the ex2/lg2 error), so pair_alpha and
+// pair_alpha_bl make identical decisions.
 __device__ __forceinline__ float pair_alpha(float d1, float A, float B, const float4 &h4,
                                             float &gw) {
     const float power = __fmaf_rn(d1, __fmaf_rn(h4.x, d1, B), A);
     if (power > 0.0f || power < h4.y) return 0.0f;
-    gw = ex2a(__fmul_rn(power, LOG2E));
+    gw = ex2a(power);
     const float a = fminf(__fmul_rn(h4.z, gw), 0.99f);
     return a >= (1.0f / 255.0f) ? a : 0.0f;
 }
@@ -101,10 +115,9 @@ __device__ __forceinline__ float pair_alpha(float d1, float A, float B, const fl
 __device__ __forceinline__ float pair_alpha_bl(float d1, float A, float B, const float4 &h4,
                                                float &gw) {
     const float power = __fmaf_rn(d1, __fmaf_rn(h4.x, d1, B), A);
-    gw = ex2a(__fmul_rn(power, LOG2E));
+    gw = ex2a(power);
     const float a = fminf(__fmul_rn(h4.z, gw), 0.99f);
-    const bool ok = !(power > 0.0f || power < h4.y) && a >= (1.0f / 255.0f);
-    return ok ? a : 0.0f;
+    return (power > 0.0f || !(a >= (1.0f / 255.0f))) ? 0.0f : a;
 }
 
 // True when no pixel centre of the box [x0, x0+edge] x [y0, y0+edge] can
@@ -245,8 +258,9 @@ __global__ void __launch_bounds__(NT, 6) fwd_kernel(
         unsigned mask = 0u;
         if (j < n_ent) {
             const int rank = entries[e0 + j];
-            const Staged st = stage(feat, rank);
+            Staged st = stage(feat, rank);
             mask = quad_mask(st, x0, y0);
+            to_log2(st);
             sgh[threadIdx.x][0] = st.g;
             sgh[threadIdx.x][1] = st.h;
             scol[threadIdx.x] = st.c;
@@ -499,11 +513,12 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
                 slot = (int64_t)e0 + j;
             }
             if (j < max_last) {
-                const Staged st = stage(feat, rank);
+                Staged st = stage(feat, rank);
                 mask = quad_mask(st, x0, y0);
 #pragma unroll
                 for (int q = 0; q < NW; q++)
                     if (j >= wmax[q]) mask &= ~(1u << q);
+                to_log2(st);
                 sgh[threadIdx.x][0] = st.g;
                 sgh[threadIdx.x][1] = st.h;
                 scol[threadIdx.x] = st.c;
@@ -587,11 +602,13 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
 #pragma unroll
                     for (int q = 0; q < 9; q++) acc[q] += sred[w][s][q];
                 }
+            // staged coefficients are in base 2: a = -2 ln2 g.z, b = -ln2 g.w,
+            // c = -2 ln2 h.x
             const float4 g4 = sgh[s][0], h4 = sgh[s][1];
             const float a = -2.0f * g4.z, b = -g4.w, c = -2.0f * h4.x;
             float4 *dst = reinterpret_cast<float4 *>(partials + PSTRIDE * sslot[s]);
-            dst[0] = make_float4(fmaf(a, acc[0], b * acc[1]), fmaf(b, acc[0], c * acc[1]),
-                                 -0.5f * acc[2], -acc[3]);
+            dst[0] = make_float4(LN2 * fmaf(a, acc[0], b * acc[1]),
+                                 LN2 * fmaf(b, acc[0], c * acc[1]), -0.5f * acc[2], -acc[3]);
             dst[1] = make_float4(-0.5f * acc[4], acc[5], acc[6], acc[7]);
             dst[2] = make_float4(acc[8], 0.0f, 0.0f, 0.0f);
         }
