@@ -216,6 +216,26 @@ __device__ __forceinline__ void composite(float a, int slot, int base, uint32_t 
     if (MODE & F_TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
 }
 
+// composite() without branches, for the training launch (no touch / stats
+// counters): the same decisions and the same bits (a pair that does not
+// composite adds c * 0 to the colour sums, which is exact for finite c).
+// jn = the entry's list index + 1.
+template <bool CHECK>
+__device__ __forceinline__ void composite_bf(float a, const float4 &c, int jn, float &fpy,
+                                             float &t, float &r, float &g, float &b, int &last) {
+    const bool on = a > 0.0f && !(CHECK && fpy == FINF);
+    const float test = t * (1.0f - a);
+    const bool stop = test < 1e-4f;
+    const bool comp = on && !stop;
+    const float w = comp ? a * t : 0.0f;
+    r = fmaf(c.x, w, r);
+    g = fmaf(c.y, w, g);
+    b = fmaf(c.z, w, b);
+    t = comp ? test : t;
+    last = comp ? jn : last;
+    fpy = (on && stop) ? FINF : fpy;
+}
+
 // Warp w renders quadrant (w & 1, w >> 1) of the tile: lane (lx, ly) owns
 // pixels (lx, ly) and (lx, ly + 4) of the 8x8 quadrant.  The warp walks its
 // quadrant's culled entry list; "all pixels done" is tested every FCHK
@@ -303,14 +323,23 @@ __global__ void __launch_bounds__(NT, 6) fwd_kernel(
                 const float aa1 = pair_alpha_bl(fpy1 - ga.y, Aa, Ba, ha, gw);
                 const float ab0 = two ? pair_alpha_bl(fpy0 - gb.y, Ab, Bb, hb, gw) : 0.0f;
                 const float ab1 = two ? pair_alpha_bl(fpy1 - gb.y, Ab, Bb, hb, gw) : 0.0f;
-                composite<MODE, false>(aa0, sa, base, a_col, touched, srank, fpy0, it0, t0, r0,
-                                       g0, b0, last0, cnt0);
-                composite<MODE, false>(aa1, sa, base, a_col, touched, srank, fpy1, it1, t1, r1,
-                                       g1, b1, last1, cnt1);
-                composite<MODE, true>(ab0, sb, base, a_col, touched, srank, fpy0, it0, t0, r0,
-                                      g0, b0, last0, cnt0);
-                composite<MODE, true>(ab1, sb, base, a_col, touched, srank, fpy1, it1, t1, r1,
-                                      g1, b1, last1, cnt1);
+                if (MODE == 0) {
+                    const float4 ca = lds4(a_col + 16 * sa), cb = lds4(a_col + 16 * sb);
+                    const int ja = base + sa + 1, jb = base + sb + 1;
+                    composite_bf<false>(aa0, ca, ja, fpy0, t0, r0, g0, b0, last0);
+                    composite_bf<false>(aa1, ca, ja, fpy1, t1, r1, g1, b1, last1);
+                    composite_bf<true>(ab0, cb, jb, fpy0, t0, r0, g0, b0, last0);
+                    composite_bf<true>(ab1, cb, jb, fpy1, t1, r1, g1, b1, last1);
+                } else {
+                    composite<MODE, false>(aa0, sa, base, a_col, touched, srank, fpy0, it0, t0,
+                                           r0, g0, b0, last0, cnt0);
+                    composite<MODE, false>(aa1, sa, base, a_col, touched, srank, fpy1, it1, t1,
+                                           r1, g1, b1, last1, cnt1);
+                    composite<MODE, true>(ab0, sb, base, a_col, touched, srank, fpy0, it0, t0,
+                                          r0, g0, b0, last0, cnt0);
+                    composite<MODE, true>(ab1, sb, base, a_col, touched, srank, fpy1, it1, t1,
+                                          r1, g1, b1, last1, cnt1);
+                }
             }
         }
     }
