@@ -237,25 +237,30 @@ __device__ __forceinline__ void composite_bf(float a, const float4 &c, int jn, f
 }
 
 // Warp w renders quadrant (w & 1, w >> 1) of the tile: lane (lx, ly) owns
-// pixels (lx, ly) and (lx, ly + 4) of the 8x8 quadrant.  The warp walks its
-// quadrant's culled entry list; "all pixels done" is tested every FCHK
-// entries (a finished pixel only skips work, so the late test changes no
-// result).
+// pixels (lx, ly) and (lx, ly + 4) of the 8x8 quadrant.  The four warps run
+// independently (no block barrier): each walks the tile's entry list in
+// batches of 32, stages one entry per lane in its own shared slice, keeps the
+// entries that can reach its quadrant (box_dead over the 8x8 pixel box) and
+// composites them.  "All pixels done" is tested every FCHK entries (a
+// finished pixel only skips work, so the late test changes no result).
 constexpr int FCHK = 4;
+constexpr int WB = 32;  // per-warp staging batch
 
+#ifndef FWD_MINB
+#define FWD_MINB 6
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(NT, 6) fwd_kernel(
+__global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
     const float *__restrict__ feat, float bg0, float bg1, float bg2, void *image, int image_f64,
     float *__restrict__ t_final, int32_t *__restrict__ n_last, int32_t *__restrict__ n_contrib,
     int32_t *__restrict__ n_iter, int64_t *__restrict__ touched) {
     constexpr bool TOUCH = MODE & F_TOUCH;
-    __shared__ float4 sgh[FB][2];
-    __shared__ float4 scol[FB];
-    __shared__ int srank[TOUCH ? FB : 1];
-    __shared__ unsigned char slist[NW][FB];
-    __shared__ int qcnt[NW][NW];
+    __shared__ float4 sgh_all[NW][WB][2];
+    __shared__ float4 scol_all[NW][WB];
+    __shared__ int srank_all[NW][TOUCH ? WB : 1];
+    __shared__ unsigned char slist_all[NW][WB];
     const int tl = blockIdx.x;
     const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
     const int ty = tid / tiles_x, tx = tid - ty * tiles_x;
@@ -265,48 +270,37 @@ __global__ void __launch_bounds__(NT, 6) fwd_kernel(
     const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
     const float fpx = (float)px;
     float fpy0 = in0 ? (float)py0 : FINF, fpy1 = in1 ? (float)py1 : FINF;
-    const float x0 = (float)(tx * 16), y0 = (float)(ty * 16);
+    const float qx0 = (float)(tx * 16 + (warp & 1) * 8), qy0 = (float)(ty * 16 + (warp >> 1) * 8);
     const int e0 = offsets[tl], n_ent = offsets[tl + 1] - e0;
+    float4(&sgh)[WB][2] = sgh_all[warp];
+    float4(&scol)[WB] = scol_all[warp];
+    int *srank = srank_all[warp];
     const uint32_t a_gh = smem_addr(&sgh[0][0]), a_col = smem_addr(&scol[0]);
-    const uint32_t a_list = smem_addr(&slist[warp][0]);
+    const uint32_t a_list = smem_addr(&slist_all[warp][0]);
+    const unsigned lt = (1u << lane) - 1u;
     float t0 = 1.0f, r0 = 0.0f, g0 = 0.0f, b0 = 0.0f;
     float t1 = 1.0f, r1 = 0.0f, g1 = 0.0f, b1 = 0.0f;
     int last0 = 0, last1 = 0, cnt0 = 0, cnt1 = 0, it0 = 0, it1 = 0;
-    for (int base = 0; base < n_ent; base += FB) {
-        if (__syncthreads_count(fpy0 == FINF && fpy1 == FINF) == NT) break;
-        const int j = base + threadIdx.x;
-        unsigned mask = 0u;
+    for (int base = 0; base < n_ent; base += WB) {
+        if (__all_sync(FULL, fpy0 == FINF && fpy1 == FINF)) break;
+        const int j = base + lane;
+        bool alive = false;
         if (j < n_ent) {
             const int rank = entries[e0 + j];
             Staged st = stage(feat, rank);
-            mask = quad_mask(st, x0, y0);
+            alive = !box_dead(st, qx0, qy0, 7.0f);
             to_log2(st);
-            sgh[threadIdx.x][0] = st.g;
-            sgh[threadIdx.x][1] = st.h;
-            scol[threadIdx.x] = st.c;
-            if (TOUCH) srank[threadIdx.x] = rank;
+            sgh[lane][0] = st.g;
+            sgh[lane][1] = st.h;
+            scol[lane] = st.c;
+            if (TOUCH) srank[lane] = rank;
         }
-        unsigned bal[NW];
-#pragma unroll
-        for (int q = 0; q < NW; q++) {
-            bal[q] = __ballot_sync(FULL, (mask >> q) & 1u);
-            if (lane == 0) qcnt[q][warp] = __popc(bal[q]);
-        }
-        __syncthreads();
-        const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-        for (int q = 0; q < NW; q++) {
-            if ((mask >> q) & 1u) {
-                int off = 0;
-#pragma unroll
-                for (int w = 0; w < NW; w++) off += w < warp ? qcnt[q][w] : 0;
-                slist[q][off + __popc(bal[q] & lt)] = (unsigned char)threadIdx.x;
-            }
-        }
-        __syncthreads();
-        const int total = qcnt[warp][0] + qcnt[warp][1] + qcnt[warp][2] + qcnt[warp][3];
+        const unsigned bal = __ballot_sync(FULL, alive);
+        if (alive) slist_all[warp][__popc(bal & lt)] = (unsigned char)lane;
+        __syncwarp();
+        const int total = __popc(bal);
         for (int k0 = 0; k0 < total; k0 += FCHK) {
-            if (__all_sync(FULL, fpy0 == FINF && fpy1 == FINF)) break;
+            if (k0 && __all_sync(FULL, fpy0 == FINF && fpy1 == FINF)) break;
             const int kend = min(k0 + FCHK, total);
             // two entries per step: the four pair alphas are independent and
             // computed ahead; compositing stays in list order per pixel
@@ -342,6 +336,7 @@ __global__ void __launch_bounds__(NT, 6) fwd_kernel(
                 }
             }
         }
+        __syncwarp();  // the slice is restaged next batch
     }
 #pragma unroll
     for (int p = 0; p < 2; p++) {
@@ -462,6 +457,27 @@ __device__ __forceinline__ void moment_terms(float d0, float s0, float s1, float
     v[4] = s2;
 }
 
+// The four quadrant warps run independently here too.  Each walks the tile's
+// entry list back to front in batches of WB, stages the batch in its own
+// shared slice, keeps the entries that reach its quadrant (and lie before its
+// last contributor) and leaves one 9-value warp sum per kept entry in a ring
+// of RING batch slots.  The last warp to finish a batch (shared-memory arrival
+// counter) folds it: per entry, the quadrants that kept it in fixed order
+// 0..3, then the moment expansion, one padded record per (tile, entry).  A
+// warp may run up to RING-1 batches ahead of the slowest one; it waits only
+// when its ring slot has not been folded yet.
+#ifndef BWD_RING
+#define BWD_RING 4
+#endif
+constexpr int RING = BWD_RING;
+
+#ifndef BWD_SLEEP
+#define BWD_SLEEP 256
+#endif
+__device__ __forceinline__ int ld_volatile(const int *p) {
+    return *reinterpret_cast<const volatile int *>(p);
+}
+
 template <typename DL>
 __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
@@ -470,14 +486,13 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
     const int64_t *__restrict__ emit_off, float bg0, float bg1, float bg2,
     const float *__restrict__ t_final, const int32_t *__restrict__ n_last,
     const DL *__restrict__ dl, float *__restrict__ partials) {
-    __shared__ float4 sgh[BB][2];
-    __shared__ float4 scol[BB];
-    __shared__ int64_t sslot[BB];
-    __shared__ unsigned char smask[BB];
-    __shared__ unsigned char slist[NW][BB];
-    __shared__ int qcnt[NW][NW];
-    __shared__ float sred[NW][BB][9];
-    __shared__ int wmax[NW];
+    __shared__ float4 sgh_all[NW][WB][2];
+    __shared__ float4 scol_all[NW][WB];
+    __shared__ unsigned char slist_all[NW][WB];
+    __shared__ float sred[RING][NW][WB][9];
+    __shared__ unsigned spres[RING][NW];
+    __shared__ int sarrive[RING];
+    __shared__ int sfolded[RING];
     const int tl = blockIdx.x;
     const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
     const int ty = tid / tiles_x, tx = tid - ty * tiles_x;
@@ -486,13 +501,18 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
     const int py0 = ty * 16 + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
     const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
     const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
-    const float x0 = (float)(tx * 16), y0 = (float)(ty * 16);
+    const float qx0 = (float)(tx * 16 + (warp & 1) * 8), qy0 = (float)(ty * 16 + (warp >> 1) * 8);
     const int e0 = offsets[tl], n_ent = offsets[tl + 1] - e0;
     const int my_slot = bfly_slot(lane);
+    float4(&sgh)[WB][2] = sgh_all[warp];
+    float4(&scol)[WB] = scol_all[warp];
     const uint32_t a_gh = smem_addr(&sgh[0][0]), a_col = smem_addr(&scol[0]);
-    const uint32_t a_list = smem_addr(&slist[warp][0]);
-    // this lane's column of sred[warp][.][.] (lanes without a slot never store)
-    const uint32_t a_red = smem_addr(&sred[warp][0][0]) + 4u * (uint32_t)max(my_slot, 0);
+    const uint32_t a_list = smem_addr(&slist_all[warp][0]);
+    const unsigned lt = (1u << lane) - 1u;
+    if (threadIdx.x < RING) {
+        sarrive[threadIdx.x] = 0;
+        sfolded[threadIdx.x] = (int)threadIdx.x - RING;  // slot r is free for batch r
+    }
 
     int last0 = 0, last1 = 0;
     float T0 = 0.0f, T1 = 0.0f, wr0 = 0, wg0 = 0, wb0 = 0, wr1 = 0, wg1 = 0, wb1 = 0;
@@ -515,73 +535,33 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
     // Q = sum_c w_c S_c with S_c starting at T_final * bg_c
     float Q0 = wr0 * (T0 * bg0) + wg0 * (T0 * bg1) + wb0 * (T0 * bg2);
     float Q1 = wr1 * (T1 * bg0) + wg1 * (T1 * bg1) + wb1 * (T1 * bg2);
-    int m = max(last0, last1);
+    int wm = max(last0, last1);  // this quadrant composited nothing at j >= wm
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULL, m, o));
-    if (lane == 0) wmax[warp] = m;
-    __syncthreads();
-    int max_last = 0;
-#pragma unroll
-    for (int w = 0; w < NW; w++) max_last = max(max_last, wmax[w]);
+    for (int o = 16; o > 0; o >>= 1) wm = max(wm, __shfl_xor_sync(FULL, wm, o));
+    __syncthreads();  // ring state initialised
 
-    // Batches [start, end) walked back to front; quadrant q only sees entries
-    // j < wmax[q] (no pixel of the quadrant composited anything later).
-    for (int end = n_ent; end > 0; end -= BB) {
-        const int start = max(end - BB, 0);
-        __syncthreads();
-        const int j = start + (int)threadIdx.x;
-        unsigned mask = 0u;
-        if (j < end) {
-            const int rank = entries[e0 + j];
-            int64_t slot;
-            if (emit_off) {
-                const int4 rc = rect_sorted[rank];
-                slot = emit_off[rank] + (int64_t)(ty - max(rc.y, row_lo)) * (rc.z - rc.x + 1) +
-                       (tx - rc.x);
-            } else {
-                slot = (int64_t)e0 + j;
-            }
-            if (j < max_last) {
-                Staged st = stage(feat, rank);
-                mask = quad_mask(st, x0, y0);
-#pragma unroll
-                for (int q = 0; q < NW; q++)
-                    if (j >= wmax[q]) mask &= ~(1u << q);
-                to_log2(st);
-                sgh[threadIdx.x][0] = st.g;
-                sgh[threadIdx.x][1] = st.h;
-                scol[threadIdx.x] = st.c;
-            }
-            sslot[threadIdx.x] = slot;
-            if (mask == 0u) {
-                float4 *dst = reinterpret_cast<float4 *>(partials + PSTRIDE * slot);
-                const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                dst[0] = z;
-                dst[1] = z;
-                dst[2] = z;
-            }
+    const int n_b = (n_ent + WB - 1) / WB;
+    for (int bi = 0; bi < n_b; bi++) {
+        const int end = n_ent - bi * WB, start = max(end - WB, 0);
+        const int rs = bi % RING;
+        if (lane == 0)
+            while (ld_volatile(&sfolded[rs]) != bi - RING) __nanosleep(BWD_SLEEP);
+        __syncwarp();
+        const int j = start + lane;
+        bool alive = false;
+        if (j < end && j < wm) {
+            Staged st = stage(feat, entries[e0 + j]);
+            alive = !box_dead(st, qx0, qy0, 7.0f);
+            to_log2(st);
+            sgh[lane][0] = st.g;
+            sgh[lane][1] = st.h;
+            scol[lane] = st.c;
         }
-        if (threadIdx.x < BB) smask[threadIdx.x] = (unsigned char)mask;
-        unsigned bal[NW];
-#pragma unroll
-        for (int q = 0; q < NW; q++) {
-            bal[q] = __ballot_sync(FULL, (mask >> q) & 1u);
-            if (lane == 0) qcnt[q][warp] = __popc(bal[q]);
-        }
-        __syncthreads();
-        const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-        for (int q = 0; q < NW; q++) {
-            if ((mask >> q) & 1u) {
-                int off = 0;
-#pragma unroll
-                for (int w = 0; w < NW; w++) off += w < warp ? qcnt[q][w] : 0;
-                slist[q][off + __popc(bal[q] & lt)] = (unsigned char)threadIdx.x;
-            }
-        }
-        __syncthreads();
-        const int total = qcnt[warp][0] + qcnt[warp][1] + qcnt[warp][2] + qcnt[warp][3];
-        for (int k = total - 1; k >= 0; k--) {
+        const unsigned bal = __ballot_sync(FULL, alive);
+        if (alive) slist_all[warp][__popc(bal & lt)] = (unsigned char)lane;
+        __syncwarp();
+        const uint32_t a_red = smem_addr(&sred[rs][warp][0][0]) + 4u * (uint32_t)max(my_slot, 0);
+        for (int k = __popc(bal) - 1; k >= 0; k--) {
             const int slot = ldsu8(a_list + k);
             const uint32_t ag = a_gh + 32 * slot;
             const float4 g4 = lds4(ag), h4 = lds4(ag + 16);
@@ -616,31 +596,62 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
             const float y = bfly9(v, lane);
             if (my_slot >= 0) sts(a_red + 36u * (uint32_t)slot, y);
         }
-        __syncthreads();
-        // fixed-order fold over the quadrants that saw the entry, then the
-        // moment expansion of the conic and mean terms
-        for (int s = threadIdx.x; s < end - start; s += NT) {
-            const unsigned mk = smask[s];
-            if (mk == 0u) continue;
-            float acc[9];
-#pragma unroll
-            for (int q = 0; q < 9; q++) acc[q] = 0.0f;
-#pragma unroll
-            for (int w = 0; w < NW; w++)
-                if ((mk >> w) & 1u) {
-#pragma unroll
-                    for (int q = 0; q < 9; q++) acc[q] += sred[w][s][q];
+        // publish this warp's sums for the batch; the last warp to arrive folds
+        if (lane == 0) spres[rs][warp] = bal;
+        __threadfence_block();
+        __syncwarp();
+        int prev = 0;
+        if (lane == 0) prev = atomicAdd(&sarrive[rs], 1);
+        prev = __shfl_sync(FULL, prev, 0);
+        if (prev == NW - 1) {
+            __threadfence_block();
+            const int jf = start + lane;
+            if (jf < end) {
+                const int rank = entries[e0 + jf];
+                int64_t slot;
+                if (emit_off) {
+                    const int4 rc = rect_sorted[rank];
+                    slot = emit_off[rank] + (int64_t)(ty - max(rc.y, row_lo)) * (rc.z - rc.x + 1) +
+                           (tx - rc.x);
+                } else {
+                    slot = (int64_t)e0 + jf;
                 }
-            // staged coefficients are in base 2: a = -2 ln2 g.z, b = -ln2 g.w,
-            // c = -2 ln2 h.x
-            const float4 g4 = sgh[s][0], h4 = sgh[s][1];
-            const float a = -2.0f * g4.z, b = -g4.w, c = -2.0f * h4.x;
-            float4 *dst = reinterpret_cast<float4 *>(partials + PSTRIDE * sslot[s]);
-            dst[0] = make_float4(LN2 * fmaf(a, acc[0], b * acc[1]),
-                                 LN2 * fmaf(b, acc[0], c * acc[1]), -0.5f * acc[2], -acc[3]);
-            dst[1] = make_float4(-0.5f * acc[4], acc[5], acc[6], acc[7]);
-            dst[2] = make_float4(acc[8], 0.0f, 0.0f, 0.0f);
+                float4 *dst = reinterpret_cast<float4 *>(partials + PSTRIDE * slot);
+                unsigned pm = 0u;
+#pragma unroll
+                for (int w = 0; w < NW; w++) pm |= ((spres[rs][w] >> lane) & 1u) << w;
+                if (pm == 0u) {
+                    const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    dst[0] = z;
+                    dst[1] = z;
+                    dst[2] = z;
+                } else {
+                    float acc[9];
+#pragma unroll
+                    for (int q = 0; q < 9; q++) acc[q] = 0.0f;
+#pragma unroll
+                    for (int w = 0; w < NW; w++)
+                        if ((pm >> w) & 1u) {
+#pragma unroll
+                            for (int q = 0; q < 9; q++) acc[q] += sred[rs][w][lane][q];
+                        }
+                    // the conic (a, b, c) of the entry, as preprocessed
+                    const float4 f0 = __ldg(reinterpret_cast<const float4 *>(feat) + 3 * (int64_t)rank);
+                    const float ca = f0.z, cb = f0.w, cc = __ldg(feat + 12 * (int64_t)rank + 4);
+                    dst[0] = make_float4(fmaf(ca, acc[0], cb * acc[1]), fmaf(cb, acc[0], cc * acc[1]),
+                                         -0.5f * acc[2], -acc[3]);
+                    dst[1] = make_float4(-0.5f * acc[4], acc[5], acc[6], acc[7]);
+                    dst[2] = make_float4(acc[8], 0.0f, 0.0f, 0.0f);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                sarrive[rs] = 0;
+                __threadfence_block();
+                *reinterpret_cast<volatile int *>(&sfolded[rs]) = bi;
+            }
         }
+        __syncwarp();  // the slice is restaged next batch
     }
 }
 
