@@ -1,7 +1,7 @@
 // loss.cu -- fused L1 + D-SSIM loss and its exact image gradient (sm_100a).
 //
 // metrics.py:135-189.  Two separable stencil passes, each staged through
-// shared memory in 16x16 output tiles with a 10-pixel halo:
+// shared memory in 16x64 output tiles with a 10-pixel halo:
 //   1. fields  -- per valid centre and channel: the five 11x11 Gaussian
 //                 moments (rows then columns, like _corr_valid), SSIM p*q and
 //                 the three adjoint fields f0, f1, f2 (metrics.py:166-183);
@@ -75,162 +75,274 @@ __device__ __forceinline__ double block_sum(double v, double *scratch) {
     return s;
 }
 
+// Both passes run on 16-row x 64-column output tiles (LT x FW) with the
+// 10-pixel halo staged in shared memory (dynamic, FPH x FPW per plane).  The
+// separable 11-tap correlations are register-tiled: the horizontal pass gives
+// each of 208 threads one patch row and HK = 8 consecutive outputs (18 loads
+// feed 88 taps), the vertical pass gives each of 256 threads one column and
+// VK = 4 consecutive rows.  Every output still sums its taps in ascending
+// order, exactly as _corr_valid / _corr_adjoint do.  Partials stay per 16x16
+// block (4 per tile, each reduced in a fixed order), so the loss is
+// independent of the row-band split.
+constexpr int FW = 64;          // output tile width
+constexpr int FPW = FW + 10;    // patch width
+constexpr int FPH = LT + 10;    // patch height
+constexpr int HK = 8;           // horizontal outputs per thread
+constexpr int VK = 4;           // vertical outputs per thread
+constexpr int HTASKS = FPH * (FW / HK);  // 208
+constexpr int LTHREADS = 256;
+static_assert(LTHREADS == FW * (LT / VK), "vertical pass covers the tile");
+
+// Sum of a double over the 16 lanes of each half warp, then over the 4
+// row-runs of a 16x16 sub-block in fixed order; returns the sub-block sum
+// for threads 0..3 (sub-block = threadIdx.x).
+__device__ __forceinline__ double subblock_sum(double v, double *red /* [4][4] */) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int col = threadIdx.x & (FW - 1), rr = threadIdx.x / FW;
+    if ((threadIdx.x & 15) == 0) red[rr * 4 + (col >> 4)] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x < 4)
+        for (int r = 0; r < LT / VK; r++) s += red[r * 4 + threadIdx.x];
+    return s;
+}
+
 // Pass 1 over centre block rows by_base + blockIdx.y.  img/ref are indexed by
 // global row (img points at global row img_row0).  fmap (may be NULL) holds
 // centre rows from fmap_row0: layout [field][channel][rows][wc].  Partials are
-// written for centre blocks whose first row lies in [own0, own1).
+// written for centre blocks whose first row lies in [own0, own1), indexed by
+// 16x16 centre block over the full image.
 template <typename T, typename IN, typename R>
-__global__ void __launch_bounds__(256) ssim_fields_kernel(
+__global__ void __launch_bounds__(LTHREADS) ssim_fields_kernel(
     int H, int W, int C, const IN *__restrict__ img, int img_row0, const R *__restrict__ ref,
     T *__restrict__ fmap, int fmap_row0, int fmap_rows, int by_base, int own0, int own1,
     double *__restrict__ part) {
-    __shared__ T sx[LP][LP + 1], sy[LP][LP + 1];
-    __shared__ T hs[5][LP][LT];
-    __shared__ double red[8];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T(*sx)[FPW] = reinterpret_cast<T(*)[FPW]>(smem_raw);
+    T(*sy)[FPW] = sx + FPH;
+    T(*hs)[FPH][FW] = reinterpret_cast<T(*)[FPH][FW]>(sy + FPH);  // [5]
+    __shared__ double red[16];
     __shared__ T lut[256];
     const GtLut<T, R> gt;
     gt.init(lut);
     const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;  // == pow(0.01, 2), pow(0.03, 2)
     const int hc = H - 10, wc = W - 10;
     const int by = by_base + blockIdx.y;
-    const int cx0 = blockIdx.x * LT, cy0 = by * LT;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int ccx = cx0 + tx, ccy = cy0 + ty;
-    const bool valid = ccx < wc && ccy < hc;
+    const int cx0 = blockIdx.x * FW, cy0 = by * LT;
+    const int col = threadIdx.x & (FW - 1), rr = threadIdx.x / FW;
+    const int ccx = cx0 + col;
+    const int hr = threadIdx.x >> 3, hu = threadIdx.x & 7;  // horizontal task
     double pq_acc = 0.0;
     __syncthreads();
     for (int c = 0; c < C; c++) {
-        for (int r = ty; r < LP; r += 16)
-            for (int q = tx; q < LP; q += 16) {
-                const int y = cy0 + r, x = cx0 + q;
-                T vx = 0, vy = 0;
-                if (y < H && x < W) {
-                    vx = (T)img[((int64_t)(y - img_row0) * W + x) * C + c];
-                    vy = gt(lut, ref[((int64_t)y * W + x) * C + c]);
-                }
-                sx[r][q] = vx;
-                sy[r][q] = vy;
+        for (int i = threadIdx.x; i < FPH * FPW; i += LTHREADS) {
+            const int r = i / FPW, q = i - r * FPW;
+            const int y = cy0 + r, x = cx0 + q;
+            T vx = 0, vy = 0;
+            if (y < H && x < W) {
+                vx = (T)img[((int64_t)(y - img_row0) * W + x) * C + c];
+                vy = gt(lut, ref[((int64_t)y * W + x) * C + c]);
             }
-        __syncthreads();
-        for (int r = ty; r < LP; r += 16) {
-            const int q = tx;
-            T a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0;
-#pragma unroll
-            for (int i = 0; i < 11; i++) {
-                const T w = wt<T>(i), x = sx[r][q + i], y = sy[r][q + i];
-                a0 += w * x;
-                a1 += w * y;
-                a2 += w * (x * x);
-                a3 += w * (y * y);
-                a4 += w * (x * y);
-            }
-            hs[0][r][q] = a0; hs[1][r][q] = a1; hs[2][r][q] = a2; hs[3][r][q] = a3;
-            hs[4][r][q] = a4;
+            sx[r][q] = vx;
+            sy[r][q] = vy;
         }
         __syncthreads();
-        if (valid) {
-            T mx = 0, my = 0, mxx = 0, myy = 0, mxy = 0;
+        if (threadIdx.x < HTASKS) {
+            T a[5][HK];
 #pragma unroll
-            for (int i = 0; i < 11; i++) {
-                const T w = wt<T>(i);
-                mx += w * hs[0][ty + i][tx];
-                my += w * hs[1][ty + i][tx];
-                mxx += w * hs[2][ty + i][tx];
-                myy += w * hs[3][ty + i][tx];
-                mxy += w * hs[4][ty + i][tx];
+            for (int o = 0; o < HK; o++)
+#pragma unroll
+                for (int f = 0; f < 5; f++) a[f][o] = 0;
+#pragma unroll
+            for (int i = 0; i < HK + 10; i++) {
+                const T x = sx[hr][hu * HK + i], y = sy[hr][hu * HK + i];
+                const T xx = x * x, yy = y * y, xy = x * y;
+#pragma unroll
+                for (int o = 0; o < HK; o++) {
+                    const int t = i - o;
+                    if (t >= 0 && t < 11) {
+                        const T w = wt<T>(t);
+                        a[0][o] += w * x;
+                        a[1][o] += w * y;
+                        a[2][o] += w * xx;
+                        a[3][o] += w * yy;
+                        a[4][o] += w * xy;
+                    }
+                }
             }
-            const T var_x = mxx - mx * mx, var_y = myy - my * my, cov = mxy - mx * my;
-            const T a1 = (T)2 * mx * my + (T)C1;
-            const T b1 = mx * mx + my * my + (T)C1;
-            const T a2 = (T)2 * cov + (T)C2;
-            const T b2 = var_x + var_y + (T)C2;
-            const T p = a1 / b1, q = a2 / b2;
-            pq_acc += (double)(p * q);
-            if (fmap) {
-                const T dp_dmux = ((T)2 * my * b1 - (T)2 * mx * a1) / (b1 * b1);
-                const T d_mu = q * dp_dmux;
-                const T d_sigma = -((p * q) / b2);
-                const T d_xy = ((T)2 * p) / b2;
-                const T f1 = (T)2 * d_sigma, f2 = d_xy;
-                const T f0 = d_mu - f1 * mx - f2 * my;
-                const int64_t plane = (int64_t)fmap_rows * wc;
-                const int64_t o = (int64_t)(ccy - fmap_row0) * wc + ccx;
-                fmap[(0 * C + c) * plane + o] = f0;
-                fmap[(1 * C + c) * plane + o] = f1;
-                fmap[(2 * C + c) * plane + o] = f2;
+#pragma unroll
+            for (int f = 0; f < 5; f++)
+#pragma unroll
+                for (int o = 0; o < HK; o++) hs[f][hr][hu * HK + o] = a[f][o];
+        }
+        __syncthreads();
+        {
+            T m[5][VK];
+#pragma unroll
+            for (int k = 0; k < VK; k++)
+#pragma unroll
+                for (int f = 0; f < 5; f++) m[f][k] = 0;
+#pragma unroll
+            for (int t = 0; t < VK + 10; t++) {
+                T h[5];
+#pragma unroll
+                for (int f = 0; f < 5; f++) h[f] = hs[f][rr * VK + t][col];
+#pragma unroll
+                for (int k = 0; k < VK; k++) {
+                    const int i = t - k;
+                    if (i >= 0 && i < 11) {
+                        const T w = wt<T>(i);
+#pragma unroll
+                        for (int f = 0; f < 5; f++) m[f][k] += w * h[f];
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < VK; k++) {
+                const int ccy = cy0 + rr * VK + k;
+                if (ccx < wc && ccy < hc) {
+                    const T mx = m[0][k], my = m[1][k], mxx = m[2][k], myy = m[3][k],
+                            mxy = m[4][k];
+                    const T var_x = mxx - mx * mx, var_y = myy - my * my, cov = mxy - mx * my;
+                    const T a1 = (T)2 * mx * my + (T)C1;
+                    const T b1 = mx * mx + my * my + (T)C1;
+                    const T a2 = (T)2 * cov + (T)C2;
+                    const T b2 = var_x + var_y + (T)C2;
+                    const T p = a1 / b1, q = a2 / b2;
+                    pq_acc += (double)(p * q);
+                    if (fmap) {
+                        const T dp_dmux = ((T)2 * my * b1 - (T)2 * mx * a1) / (b1 * b1);
+                        const T d_mu = q * dp_dmux;
+                        const T d_sigma = -((p * q) / b2);
+                        const T d_xy = ((T)2 * p) / b2;
+                        const T f1 = (T)2 * d_sigma, f2 = d_xy;
+                        const T f0 = d_mu - f1 * mx - f2 * my;
+                        const int64_t plane = (int64_t)fmap_rows * wc;
+                        const int64_t o = (int64_t)(ccy - fmap_row0) * wc + ccx;
+                        fmap[(0 * C + c) * plane + o] = f0;
+                        fmap[(1 * C + c) * plane + o] = f1;
+                        fmap[(2 * C + c) * plane + o] = f2;
+                    }
+                }
             }
         }
         __syncthreads();
     }
-    const double s = block_sum(pq_acc, red);
-    if (threadIdx.x == 0 && cy0 >= own0 && cy0 < own1) part[by * gridDim.x + blockIdx.x] = s;
+    const double s = subblock_sum(pq_acc, red);
+    const int nbx = (wc + LT - 1) / LT, bx = blockIdx.x * (FW / LT) + (int)threadIdx.x;
+    if (threadIdx.x < FW / LT && bx < nbx && cy0 >= own0 && cy0 < own1) part[by * nbx + bx] = s;
 }
 
 // Pass 2 over pixel block rows by_base + blockIdx.y:
 // dL/dimage = sign(x-y)(1-lam)/n + gscale * (A f0 + x A f1 + y A f2).
 // grad is indexed by global row from grad_row0.
 template <typename T, typename IN, typename R>
-__global__ void __launch_bounds__(256) ssim_adjoint_kernel(
+__global__ void __launch_bounds__(LTHREADS) ssim_adjoint_kernel(
     int H, int W, const IN *__restrict__ img, int img_row0, const R *__restrict__ ref,
     const T *__restrict__ fmap, int fmap_row0, int fmap_rows, IN *__restrict__ grad,
     int grad_row0, int row1, int by_base, T l1_scale, T gscale, double *__restrict__ part) {
-    __shared__ T sf[3][LP][LP + 1];
-    __shared__ T hs[3][LP][LT];
-    __shared__ double red[8];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T(*sf)[FPH][FPW] = reinterpret_cast<T(*)[FPH][FPW]>(smem_raw);            // [3]
+    T(*hs)[FPH][FW] = reinterpret_cast<T(*)[FPH][FW]>(sf + 3);                // [3]
+    __shared__ double red[16];
     __shared__ T lut[256];
     const GtLut<T, R> gt;
     gt.init(lut);
     const int hc = H - 10, wc = W - 10;
     const int by = by_base + blockIdx.y;
-    const int x0 = blockIdx.x * LT, y0 = by * LT;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int x = x0 + tx, y = y0 + ty;
-    const bool inside = x < W && y < H && y < row1;
+    const int x0 = blockIdx.x * FW, y0 = by * LT;
+    const int col = threadIdx.x & (FW - 1), rr = threadIdx.x / FW;
+    const int x = x0 + col;
+    const int hr = threadIdx.x >> 3, hu = threadIdx.x & 7;
     const int64_t plane = (int64_t)fmap_rows * wc;
     double l1_acc = 0.0;
     __syncthreads();
     for (int c = 0; c < 3; c++) {
-        for (int r = ty; r < LP; r += 16)
-            for (int q = tx; q < LP; q += 16) {
-                const int cy = y0 - 10 + r, cx = x0 - 10 + q;
-                const bool ok = cy >= 0 && cy < hc && cx >= 0 && cx < wc;
-                const int64_t o = (int64_t)(cy - fmap_row0) * wc + cx;
+        for (int i = threadIdx.x; i < FPH * FPW; i += LTHREADS) {
+            const int r = i / FPW, q = i - r * FPW;
+            const int cy = y0 - 10 + r, cx = x0 - 10 + q;
+            const bool ok = cy >= 0 && cy < hc && cx >= 0 && cx < wc;
+            const int64_t o = (int64_t)(cy - fmap_row0) * wc + cx;
 #pragma unroll
-                for (int f = 0; f < 3; f++) sf[f][r][q] = ok ? fmap[(f * 3 + c) * plane + o] : (T)0;
-            }
+            for (int f = 0; f < 3; f++) sf[f][r][q] = ok ? fmap[(f * 3 + c) * plane + o] : (T)0;
+        }
         __syncthreads();
-        for (int r = ty; r < LP; r += 16) {
-            const int q = tx;
+        if (threadIdx.x < HTASKS) {
 #pragma unroll
             for (int f = 0; f < 3; f++) {
-                T a = 0;
+                T a[HK];
 #pragma unroll
-                for (int i = 0; i < 11; i++) a += wt<T>(i) * sf[f][r][q + i];
-                hs[f][r][q] = a;
+                for (int o = 0; o < HK; o++) a[o] = 0;
+#pragma unroll
+                for (int i = 0; i < HK + 10; i++) {
+                    const T v = sf[f][hr][hu * HK + i];
+#pragma unroll
+                    for (int o = 0; o < HK; o++) {
+                        const int t = i - o;
+                        if (t >= 0 && t < 11) a[o] += wt<T>(t) * v;
+                    }
+                }
+#pragma unroll
+                for (int o = 0; o < HK; o++) hs[f][hr][hu * HK + o] = a[o];
             }
         }
         __syncthreads();
-        if (inside) {
-            T g0 = 0, g1 = 0, g2 = 0;
+        {
+            T g[3][VK];
 #pragma unroll
-            for (int i = 0; i < 11; i++) {
-                const T w = wt<T>(i);
-                g0 += w * hs[0][ty + i][tx];
-                g1 += w * hs[1][ty + i][tx];
-                g2 += w * hs[2][ty + i][tx];
+            for (int k = 0; k < VK; k++) g[0][k] = g[1][k] = g[2][k] = 0;
+#pragma unroll
+            for (int t = 0; t < VK + 10; t++) {
+                const T h0 = hs[0][rr * VK + t][col], h1 = hs[1][rr * VK + t][col],
+                        h2 = hs[2][rr * VK + t][col];
+#pragma unroll
+                for (int k = 0; k < VK; k++) {
+                    const int i = t - k;
+                    if (i >= 0 && i < 11) {
+                        const T w = wt<T>(i);
+                        g[0][k] += w * h0;
+                        g[1][k] += w * h1;
+                        g[2][k] += w * h2;
+                    }
+                }
             }
-            const T xv = (T)img[((int64_t)(y - img_row0) * W + x) * 3 + c];
-            const T yv = gt(lut, ref[((int64_t)y * W + x) * 3 + c]);
-            const T d = xv - yv;
-            const T sg = d > (T)0 ? (T)1 : (d < (T)0 ? (T)-1 : (T)0);
-            const T g = g0 + xv * g1 + yv * g2;
-            grad[((int64_t)(y - grad_row0) * W + x) * 3 + c] = (IN)(sg * l1_scale + gscale * g);
-            l1_acc += (double)fabs(d);
+#pragma unroll
+            for (int k = 0; k < VK; k++) {
+                const int y = y0 + rr * VK + k;
+                if (x < W && y < H && y < row1) {
+                    const T xv = (T)img[((int64_t)(y - img_row0) * W + x) * 3 + c];
+                    const T yv = gt(lut, ref[((int64_t)y * W + x) * 3 + c]);
+                    const T d = xv - yv;
+                    const T sg = d > (T)0 ? (T)1 : (d < (T)0 ? (T)-1 : (T)0);
+                    const T gg = g[0][k] + xv * g[1][k] + yv * g[2][k];
+                    grad[((int64_t)(y - grad_row0) * W + x) * 3 + c] = (IN)(sg * l1_scale + gscale * gg);
+                    l1_acc += (double)fabs(d);
+                }
+            }
         }
         __syncthreads();
     }
-    const double s = block_sum(l1_acc, red);
-    if (threadIdx.x == 0) part[by * gridDim.x + blockIdx.x] = s;
+    const double s = subblock_sum(l1_acc, red);
+    const int nbx = (W + LT - 1) / LT, bx = blockIdx.x * (FW / LT) + (int)threadIdx.x;
+    if (threadIdx.x < FW / LT && bx < nbx) part[by * nbx + bx] = s;
+}
+
+template <typename T>
+constexpr size_t fields_smem() { return sizeof(T) * (2 * FPH * FPW + 5 * FPH * FW); }
+template <typename T>
+constexpr size_t adjoint_smem() { return sizeof(T) * (3 * FPH * FPW + 3 * FPH * FW); }
+
+// Opt the kernels into their dynamic shared memory once per process.
+template <typename T, typename IN, typename R>
+inline void loss_smem_optin() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(ssim_fields_kernel<T, IN, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)fields_smem<T>());
+    cudaFuncSetAttribute(ssim_adjoint_kernel<T, IN, R>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adjoint_smem<T>());
+    done = true;
 }
 
 // Fixed-order final reduction (one block): loss = (1-lam) L1 + lam (1 - SSIM).
@@ -284,7 +396,7 @@ inline LossGrid loss_grid(int H, int W, int row0, int row1) {
     LossGrid g;
     const int hc = H - 10, wc = W - 10;
     const int nfy = (hc + LT - 1) / LT;
-    g.gf = dim3((wc + LT - 1) / LT, nfy);
+    g.gf = dim3((wc + LT - 1) / LT, nfy);          // 16x16 partial blocks
     g.ga = dim3((W + LT - 1) / LT, (H + LT - 1) / LT);
     g.fby0 = row0 / LT > 0 ? row0 / LT - 1 : 0;
     g.fby1 = (row1 + LT - 1) / LT < nfy ? (row1 + LT - 1) / LT : nfy;
@@ -310,16 +422,17 @@ int loss_rows_impl(void *ws, size_t *ws_bytes, int H, int W, int row0, int row1,
     if (*ws_bytes < need) return (int)cudaErrorInvalidValue;
     T *fmap = (T *)ws;
     const double n_pix = 3.0 * H * W, n_centers = 3.0 * (H - 10) * (W - 10);
+    loss_smem_optin<T, T, R>();
     if (g.fby1 > g.fby0) {
-        dim3 grid(g.gf.x, g.fby1 - g.fby0);
-        ssim_fields_kernel<T, T, R><<<grid, 256, 0, s>>>(H, W, 3, img, img_row0, ref, fmap,
-                                                         g.fmap_row0, g.fmap_rows, g.fby0, row0,
-                                                         row1, part_ssim);
+        dim3 grid((wc + FW - 1) / FW, g.fby1 - g.fby0);
+        ssim_fields_kernel<T, T, R><<<grid, LTHREADS, fields_smem<T>(), s>>>(
+            H, W, 3, img, img_row0, ref, fmap, g.fmap_row0, g.fmap_rows, g.fby0, row0, row1,
+            part_ssim);
         ISG_CHECK_LAUNCH();
     }
     if (g.aby1 > g.aby0) {
-        dim3 grid(g.ga.x, g.aby1 - g.aby0);
-        ssim_adjoint_kernel<T, T, R><<<grid, 256, 0, s>>>(
+        dim3 grid((W + FW - 1) / FW, g.aby1 - g.aby0);
+        ssim_adjoint_kernel<T, T, R><<<grid, LTHREADS, adjoint_smem<T>(), s>>>(
             H, W, img, img_row0, ref, fmap, g.fmap_row0, g.fmap_rows, grad, row0, row1, g.aby0,
             (T)((1.0 - lam) / n_pix), (T)(-lam / n_centers), part_l1);
         ISG_CHECK_LAUNCH();
@@ -428,7 +541,9 @@ extern "C" int isg_ssim(void *workspace, size_t *ws_bytes, int32_t height, int32
     if (*ws_bytes < al(8 * nf)) return (int)cudaErrorInvalidValue;
     cudaStream_t s = (cudaStream_t)stream;
     double *pf = (double *)workspace;
-    ssim_fields_kernel<double, double, double><<<gf, 256, 0, s>>>(
+    loss_smem_optin<double, double, double>();
+    dim3 grid((wc + FW - 1) / FW, gf.y);
+    ssim_fields_kernel<double, double, double><<<grid, LTHREADS, fields_smem<double>(), s>>>(
         height, width, channels, image, 0, ref, nullptr, 0, 0, 0, 0, height, pf);
     ISG_CHECK_LAUNCH();
     loss_finish_kernel<<<1, FINISH_THREADS, 0, s>>>((int)nf, pf, 0, nullptr, 0.0,
