@@ -90,6 +90,8 @@ constexpr int FPH = LT + 10;    // patch height
 constexpr int HK = 8;           // horizontal outputs per thread
 constexpr int VK = 4;           // vertical outputs per thread
 constexpr int HTASKS = FPH * (FW / HK);  // 208
+constexpr int PR = (FPH + 7) / 8;          // patch rows per warp (8 warps)
+constexpr int PC = (FPW + 31) / 32;        // patch columns per lane
 constexpr int LTHREADS = 256;
 static_assert(LTHREADS == FW * (LT / VK), "vertical pass covers the tile");
 
@@ -114,7 +116,7 @@ __device__ __forceinline__ double subblock_sum(double v, double *red /* [4][4] *
 // written for centre blocks whose first row lies in [own0, own1), indexed by
 // 16x16 centre block over the full image.
 template <typename T, typename IN, typename R>
-__global__ void __launch_bounds__(LTHREADS) ssim_fields_kernel(
+__global__ void __launch_bounds__(LTHREADS, 3) ssim_fields_kernel(
     int H, int W, int C, const IN *__restrict__ img, int img_row0, const R *__restrict__ ref,
     T *__restrict__ fmap, int fmap_row0, int fmap_rows, int by_base, int own0, int own1,
     double *__restrict__ part) {
@@ -133,19 +135,34 @@ __global__ void __launch_bounds__(LTHREADS) ssim_fields_kernel(
     const int col = threadIdx.x & (FW - 1), rr = threadIdx.x / FW;
     const int ccx = cx0 + col;
     const int hr = threadIdx.x >> 3, hu = threadIdx.x & 7;  // horizontal task
+    const int lwarp = threadIdx.x >> 5, llane = threadIdx.x & 31;
     double pq_acc = 0.0;
     __syncthreads();
     for (int c = 0; c < C; c++) {
-        for (int i = threadIdx.x; i < FPH * FPW; i += LTHREADS) {
-            const int r = i / FPW, q = i - r * FPW;
-            const int y = cy0 + r, x = cx0 + q;
-            T vx = 0, vy = 0;
-            if (y < H && x < W) {
-                vx = (T)img[((int64_t)(y - img_row0) * W + x) * C + c];
-                vy = gt(lut, ref[((int64_t)y * W + x) * C + c]);
+        {
+            // warp w stages patch rows w, w+8, ..; a row's loads are issued
+            // before its stores
+#pragma unroll 2
+            for (int i = 0; i < PR; i++) {
+                IN vx[PC];
+                R vy[PC];
+                const int r = lwarp + 8 * i, y = cy0 + r;
+#pragma unroll
+                for (int k = 0; k < PC; k++) {
+                    const int q = llane + 32 * k, x = cx0 + q;
+                    const bool ok = r < FPH && q < FPW && y < H && x < W;
+                    vx[k] = ok ? img[((int64_t)(y - img_row0) * W + x) * C + c] : (IN)0;
+                    vy[k] = ok ? ref[((int64_t)y * W + x) * C + c] : (R)0;
+                }
+#pragma unroll
+                for (int k = 0; k < PC; k++) {
+                    const int q = llane + 32 * k;
+                    if (r < FPH && q < FPW) {
+                        sx[r][q] = (T)vx[k];
+                        sy[r][q] = gt(lut, vy[k]);
+                    }
+                }
             }
-            sx[r][q] = vx;
-            sy[r][q] = vy;
         }
         __syncthreads();
         if (threadIdx.x < HTASKS) {
@@ -209,13 +226,14 @@ __global__ void __launch_bounds__(LTHREADS) ssim_fields_kernel(
                     const T b1 = mx * mx + my * my + (T)C1;
                     const T a2 = (T)2 * cov + (T)C2;
                     const T b2 = var_x + var_y + (T)C2;
-                    const T p = a1 / b1, q = a2 / b2;
+                    const T rb1 = (T)1 / b1, rb2 = (T)1 / b2;
+                    const T p = a1 * rb1, q = a2 * rb2;
                     pq_acc += (double)(p * q);
                     if (fmap) {
-                        const T dp_dmux = ((T)2 * my * b1 - (T)2 * mx * a1) / (b1 * b1);
+                        const T dp_dmux = ((T)2 * my * b1 - (T)2 * mx * a1) * (rb1 * rb1);
                         const T d_mu = q * dp_dmux;
-                        const T d_sigma = -((p * q) / b2);
-                        const T d_xy = ((T)2 * p) / b2;
+                        const T d_sigma = -((p * q) * rb2);
+                        const T d_xy = ((T)2 * p) * rb2;
                         const T f1 = (T)2 * d_sigma, f2 = d_xy;
                         const T f0 = d_mu - f1 * mx - f2 * my;
                         const int64_t plane = (int64_t)fmap_rows * wc;
@@ -238,7 +256,7 @@ __global__ void __launch_bounds__(LTHREADS) ssim_fields_kernel(
 // dL/dimage = sign(x-y)(1-lam)/n + gscale * (A f0 + x A f1 + y A f2).
 // grad is indexed by global row from grad_row0.
 template <typename T, typename IN, typename R>
-__global__ void __launch_bounds__(LTHREADS) ssim_adjoint_kernel(
+__global__ void __launch_bounds__(LTHREADS, 4) ssim_adjoint_kernel(
     int H, int W, const IN *__restrict__ img, int img_row0, const R *__restrict__ ref,
     const T *__restrict__ fmap, int fmap_row0, int fmap_rows, IN *__restrict__ grad,
     int grad_row0, int row1, int by_base, T l1_scale, T gscale, double *__restrict__ part) {
@@ -255,17 +273,41 @@ __global__ void __launch_bounds__(LTHREADS) ssim_adjoint_kernel(
     const int col = threadIdx.x & (FW - 1), rr = threadIdx.x / FW;
     const int x = x0 + col;
     const int hr = threadIdx.x >> 3, hu = threadIdx.x & 7;
+    const int lwarp = threadIdx.x >> 5, llane = threadIdx.x & 31;
     const int64_t plane = (int64_t)fmap_rows * wc;
     double l1_acc = 0.0;
     __syncthreads();
     for (int c = 0; c < 3; c++) {
-        for (int i = threadIdx.x; i < FPH * FPW; i += LTHREADS) {
-            const int r = i / FPW, q = i - r * FPW;
-            const int cy = y0 - 10 + r, cx = x0 - 10 + q;
-            const bool ok = cy >= 0 && cy < hc && cx >= 0 && cx < wc;
-            const int64_t o = (int64_t)(cy - fmap_row0) * wc + cx;
+        // this thread's pixels' image / ground-truth samples, loaded early
+        IN xin[VK];
+        R yin[VK];
 #pragma unroll
-            for (int f = 0; f < 3; f++) sf[f][r][q] = ok ? fmap[(f * 3 + c) * plane + o] : (T)0;
+        for (int k = 0; k < VK; k++) {
+            const int y = y0 + rr * VK + k;
+            const bool ok = x < W && y < H && y < row1;
+            xin[k] = ok ? img[((int64_t)(y - img_row0) * W + x) * 3 + c] : (IN)0;
+            yin[k] = ok ? ref[((int64_t)y * W + x) * 3 + c] : (R)0;
+        }
+#pragma unroll 2
+        for (int i = 0; i < PR; i++) {
+            T v[3][PC];
+            const int r = lwarp + 8 * i, cy = y0 - 10 + r;
+#pragma unroll
+            for (int k = 0; k < PC; k++) {
+                const int q = llane + 32 * k, cx = x0 - 10 + q;
+                const bool ok = r < FPH && q < FPW && cy >= 0 && cy < hc && cx >= 0 && cx < wc;
+                const int64_t o = (int64_t)(cy - fmap_row0) * wc + cx;
+#pragma unroll
+                for (int f = 0; f < 3; f++) v[f][k] = ok ? fmap[(f * 3 + c) * plane + o] : (T)0;
+            }
+#pragma unroll
+            for (int k = 0; k < PC; k++) {
+                const int q = llane + 32 * k;
+                if (r < FPH && q < FPW) {
+#pragma unroll
+                    for (int f = 0; f < 3; f++) sf[f][r][q] = v[f][k];
+                }
+            }
         }
         __syncthreads();
         if (threadIdx.x < HTASKS) {
@@ -311,8 +353,8 @@ __global__ void __launch_bounds__(LTHREADS) ssim_adjoint_kernel(
             for (int k = 0; k < VK; k++) {
                 const int y = y0 + rr * VK + k;
                 if (x < W && y < H && y < row1) {
-                    const T xv = (T)img[((int64_t)(y - img_row0) * W + x) * 3 + c];
-                    const T yv = gt(lut, ref[((int64_t)y * W + x) * 3 + c]);
+                    const T xv = (T)xin[k];
+                    const T yv = gt(lut, yin[k]);
                     const T d = xv - yv;
                     const T sg = d > (T)0 ? (T)1 : (d < (T)0 ? (T)-1 : (T)0);
                     const T gg = g[0][k] + xv * g[1][k] + yv * g[2][k];
