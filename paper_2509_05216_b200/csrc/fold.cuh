@@ -17,40 +17,43 @@ namespace isg {
 // Running state of one rank's fold; step() consumes the next slot's 9 terms.
 struct FoldState {
     double acc[9], bs[9];
-    int y0, w, cur, dy, dx, canon;
+    int y, w, dx, canon;
+    bool flush;
 
     __device__ __forceinline__ void init(const int4 *__restrict__ rect_sorted, int64_t r,
                                          int64_t n_slots, int row_lo, int canon_rows) {
-        y0 = 0;
+        y = 0;
         w = 1;
         if (canon_rows > 0 && n_slots > 0) {
             const int4 rc = rect_sorted[r];
-            y0 = max(rc.y, row_lo);
+            y = max(rc.y, row_lo);
             w = rc.z - rc.x + 1;
         }
         canon = canon_rows;
-        cur = -1;
-        dy = dx = 0;
+        dx = 0;
+        flush = false;
 #pragma unroll
         for (int k = 0; k < 9; k++) acc[k] = bs[k] = 0.0;
     }
 
+    // Block sums close where a new tile row starts a new canon block (the
+    // only place the block index (row / canon) can change).
     template <typename V>
     __device__ __forceinline__ void step(const V *v) {
-        const int blk = canon > 0 ? (y0 + dy) / canon : 0;
-        if (blk != cur) {
+        if (flush) {
 #pragma unroll
             for (int k = 0; k < 9; k++) {
                 acc[k] += bs[k];
                 bs[k] = 0.0;
             }
-            cur = blk;
+            flush = false;
         }
 #pragma unroll
         for (int k = 0; k < 9; k++) bs[k] += (double)v[k];
         if (++dx == w) {
             dx = 0;
-            dy++;
+            y++;
+            flush = canon > 0 && y % canon == 0;
         }
     }
 

@@ -332,41 +332,93 @@ __global__ void __launch_bounds__(256) reduce_ordered_kernel(
     if (grad_norm) grad_norm[row] = hypot(acc[0], acc[1]);
 }
 
-// float32 subtotals: a block of 256 consecutive ranks owns one contiguous
-// span of slots (emit_off is monotone); the span is streamed through shared
-// memory in chunks with coalesced 16-byte loads and every thread folds its own
-// slots from there -- the same FoldState arithmetic as fold_rank.
-constexpr int RED_THREADS = 128;
-constexpr int RED_CHUNK = 768;  // slots per chunk (36 KB): one chunk for most blocks
+// float32 subtotals: every warp folds 32 consecutive ranks, whose slots form
+// one contiguous span (emit_off is monotone).  The span streams through two
+// per-warp shared buffers with TMA bulk copies (cp.async.bulk, completion on
+// an mbarrier): chunk k+1 lands while the lanes fold chunk k, each lane its
+// own slots -- the same FoldState arithmetic as fold_rank.  No block barriers.
+constexpr int RED_WARPS = 4;
+constexpr int RED_THREADS = 32 * RED_WARPS;
+#ifndef RED_SLOTS_N
+#define RED_SLOTS_N 96
+#endif
+constexpr int RED_SLOTS = RED_SLOTS_N;  // slots per chunk (4.5 KB)
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes,
+                                          uint64_t *bar) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"((unsigned)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(b), "r"(parity)
+            : "memory");
+    }
+}
 
 __global__ void __launch_bounds__(RED_THREADS) reduce_ordered_f32_kernel(
     int64_t m, const int64_t *__restrict__ emit_off, const float *__restrict__ partials,
     const int32_t *__restrict__ order, const int4 *__restrict__ rect_sorted, int row_lo,
     int canon_rows, double *__restrict__ grad2d, double *__restrict__ grad_norm) {
     constexpr int PS = partial_stride<float>();
-    __shared__ __align__(16) float sbuf[RED_CHUNK * PS];
-    const int64_t r0 = (int64_t)blockIdx.x * RED_THREADS;
-    const int64_t r = r0 + threadIdx.x;
+    __shared__ __align__(128) float sbuf[RED_WARPS][2][RED_SLOTS * PS];
+    __shared__ __align__(8) uint64_t sbar[RED_WARPS][2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r0 = ((int64_t)blockIdx.x * RED_WARPS + warp) * 32;
+    if (r0 >= m) return;
+    const int64_t r = r0 + lane;
     const bool live = r < m;
     const int64_t span0 = emit_off[r0];
-    const int64_t span1 = emit_off[min(r0 + RED_THREADS, m)];
+    const int64_t span1 = emit_off[min(r0 + 32, m)];
     int64_t p = live ? emit_off[r] : 0;
     const int64_t p1 = live ? emit_off[r + 1] : 0;
     FoldState st;
     st.init(rect_sorted, r, live ? p1 - p : 0, row_lo, canon_rows);
-    // 48-byte records: every chunk start is 16-byte aligned
-    for (int64_t c0 = span0; c0 < span1; c0 += RED_CHUNK) {
-        const int64_t c1 = min(c0 + RED_CHUNK, span1);
-        const int64_t f0 = (int64_t)PS * c0, nf = (int64_t)PS * (c1 - c0);
-        const float4 *src = reinterpret_cast<const float4 *>(partials + f0);
-        const int n4 = (int)(nf >> 2);
-        __syncthreads();
-        for (int i = threadIdx.x; i < n4; i += RED_THREADS)
-            reinterpret_cast<float4 *>(sbuf)[i] = __ldg(src + i);
-        for (int i = 4 * n4 + threadIdx.x; i < nf; i += RED_THREADS) sbuf[i] = __ldg(partials + f0 + i);
-        __syncthreads();
-        const int64_t e = min(p1, c1);
-        for (; p < e; p++) st.step(sbuf + PS * (p - c0));
+    const int nch = (int)((span1 - span0 + RED_SLOTS - 1) / RED_SLOTS);
+    float(*buf)[RED_SLOTS * PS] = sbuf[warp];
+    uint64_t *bar = sbar[warp];
+    auto issue = [&](int k) {
+        const int64_t c0 = span0 + (int64_t)k * RED_SLOTS;
+        const unsigned n = (unsigned)min((int64_t)RED_SLOTS, span1 - c0);
+        bulk_load(buf[k & 1], partials + PS * c0, n * PS * (unsigned)sizeof(float), &bar[k & 1]);
+    };
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (nch > 0) issue(0);
+        if (nch > 1) issue(1);
+    }
+    __syncwarp();
+    for (int k = 0; k < nch; k++) {
+        mbar_wait(&bar[k & 1], (unsigned)((k >> 1) & 1));
+        const int64_t c0 = span0 + (int64_t)k * RED_SLOTS;
+        const int64_t e = min(p1, c0 + RED_SLOTS);
+        const float *b = buf[k & 1];
+        for (; p < e; p++) st.step(b + PS * (p - c0));
+        __syncwarp();
+        if (lane == 0 && k + 2 < nch) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(k + 2);
+        }
     }
     if (!live) return;
     st.finish();
