@@ -289,7 +289,7 @@ def run_ours(args, world, rank, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic gyroid isosurface; GT rendered from a target cloud (8-bit codes)",
+        "data": "synthetic gyroid isosurface; GT = quantize8(raycast_isosurface) on the GPU (the reference dataset recipe, 8-bit codes)",
         "config": workload_config(args.config, n, res, len(wl.cameras)),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "gpu_launches": launches_per_step * args.steps,

@@ -353,6 +353,41 @@ int isg_knn_mean_grid(void *workspace, size_t *ws_bytes, const double *points, i
                       int32_t k, const double *lo, double cell, int64_t gx, int64_t gy,
                       int64_t gz, double *out, void *stream);
 
+/* ---- dataset generation (next row of SURVEY 8f: volume.py, raycast.py) ----
+ * Volumes are float64 (nz, ny, nx) x-fastest on the device; dims = (nx, ny,
+ * nz), spacing and origin are 3 HOST values each (VolumeGrid, volume.py:25-62).
+ * float64, reference statement order, no FMA contraction: bit-identical. */
+
+/* raycast_isosurface (raycast.py:99-262): first-hit march at `step`, bisection
+ * refine, headlight Lambertian shading.  image (H,W,3) float64 and/or codes
+ * (H,W,3) uint8 = quantize8 (images.py:9-16); either may be NULL.  albedo and
+ * background are 3 host doubles. */
+int isg_raycast(const double *data, const int32_t *dims, const double *spacing,
+                const double *origin, double isovalue, const isg_camera *cam, double step,
+                int32_t refine_steps, const double *albedo, const double *background,
+                double *image, uint8_t *codes, void *stream);
+
+/* _axis_crossings (volume.py:197-226), step 1: linear indices (C order over
+ * edge starts of the strided sub-lattice) of the edges along data axis
+ * axis_data (2 = x, 1 = y, 0 = z) whose ends straddle isovalue; *count
+ * (device) receives their number.  idx_out must hold every edge of the axis.
+ * Two-phase workspace. */
+int isg_iso_edges(void *workspace, size_t *ws_bytes, const double *data, const int32_t *dims,
+                  int32_t stride, int32_t axis_data, double isovalue, int64_t *idx_out,
+                  int64_t *count, void *stream);
+
+/* Step 2: the crossing points (n,3) float64 of n selected edges. */
+int isg_iso_edge_points(const double *data, const int32_t *dims, const double *spacing,
+                        const double *origin, int32_t stride, int32_t axis_data,
+                        double isovalue, int64_t n, const int64_t *idx, double *positions,
+                        void *stream);
+
+/* Unit normals (gradient_central + normalisation, volume.py:146-174,
+ * 270-275) at n points (n,3) float64. */
+int isg_iso_normals(const double *data, const int32_t *dims, const double *spacing,
+                    const double *origin, int64_t n, const double *positions, double *normals,
+                    void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,7 @@ SOURCES = {
     "dist.cu": [],
     "knn.cu": ["-fmad=false"],
     "chain_f32.cu": [],
+    "volume.cu": ["-fmad=false"],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -1,20 +1,17 @@
-"""Synthetic isosurface workloads of BASELINE.json's named shapes.
+"""Synthetic isosurface workloads of BASELINE.json's named shapes, built with
+the reference's own dataset recipe (tests/conftest.py:35-44 build_dataset):
 
-Dataset generation is outside the hot path (volume.py,
-raycast.py are out of scope), so this module only builds inputs of the right
-shape for bench.py and the tests:
-
-* points: edge crossings of a gyroid field sin x cos y + sin y cos z +
-  sin z cos x on an n^3 lattice with coordinate i*2*pi*periods/(n-1), the
-  reference's extract_isosurface_points recipe (volume.py:229-276: x, then y,
-  then z edges in C order, seeded subsample re-sorted into extraction order);
+* volume: the gyroid sin x cos y + sin y cos z + sin z cos x on an n^3
+  lattice with coordinate i*2*pi*periods/(n-1) (volume.gyroid_grid);
+* points: extract_isosurface_points (volume.py:229-276) on the GPU
+  (volume.py here, bit-exact), seeded subsample to max_points;
 * cameras: the reference orbit (inward fibonacci sphere, radius 1.5 x half
   diagonal, 60 deg fov; tests/conftest.py:25-32);
-* ground truth: NOT the reference's raycaster (2.4 s per 2K view on a CPU
-  core).  Each view is rendered by this package's forward rasteriser from a
-  target cloud (opacity 0.9, headlight-like view-dependent albedo shading
-  from the analytic normals) and stored as 8-bit codes like the reference's
-  PNG views.
+* ground truth: quantize8(raycast_isosurface(...)) (raycast.py:223-262) on the
+  GPU, stored as the 8-bit codes a PNG view holds.
+
+gyroid_points is the host (numpy) restatement of the same extraction, used
+by bench.py's CPU arm so that no GPU kernel touches the reference arm.
 """
 
 from __future__ import annotations
@@ -85,28 +82,6 @@ def orbit(n: int, count: int, resolution: int):
                                 width=resolution, height=resolution))
 
 
-def target_cloud(points: np.ndarray, normals: np.ndarray, log_scales: np.ndarray, device,
-                 albedo=(0.87, 0.80, 0.66)):
-    """The ground-truth generator cloud: opacity 0.9 and colour
-    albedo * (0.55 + 0.4 n.d) expressed exactly in SH degree 1."""
-    from .gaussians import GaussianCloud
-    n = points.shape[0]
-    c0, c1 = 0.28209479177387814, 0.4886025119029199
-    a = np.asarray(albedo)
-    sh = np.zeros((n, 4, 3))
-    sh[:, 0, :] = (a[None, :] * 0.55 - 0.5) / c0
-    k = 0.4 * a[None, :] / c1
-    sh[:, 1, :] = -k * normals[:, 1:2]
-    sh[:, 2, :] = k * normals[:, 2:3]
-    sh[:, 3, :] = -k * normals[:, 0:1]
-    rot = np.zeros((n, 4), dtype=np.float32)
-    rot[:, 0] = 1.0
-    f = lambda v: torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32)).to(device)
-    return GaussianCloud(positions=f(points), log_scales=f(log_scales), rotations=f(rot),
-                         opacity_logits=f(np.full(n, math.log(0.9 / 0.1))), sh_coeffs=f(sh),
-                         degree=1)
-
-
 @dataclass
 class Workload:
     name: str
@@ -121,27 +96,28 @@ class Workload:
 def make_workload(name: str, device, views: int | None = None, max_points: int | None = None,
                   resolution: int | None = None, log=print) -> Workload:
     import time
-    from .engine import Rasterizer
     from .training import init_log_scales
     n, periods, mp, res, nv = CONFIGS[name]
     mp = max_points or mp
     res = resolution or res
     nv = views or nv
+    from . import volume as V
     t0 = time.time()
-    pos, normals = gyroid_points(n, periods, mp)
+    grid = V.gyroid_grid(n, periods)
+    pc = V.extract_isosurface_points(grid, 0.0, max_points=mp, seed=0)
+    pos, normals = pc.positions, pc.normals
     t1 = time.time()
     ls = init_log_scales(pos)
     t2 = time.time()
     cams = orbit(n, nv, res)
-    tgt = target_cloud(pos, normals, ls, device)
-    r = Rasterizer(tgt.count, res, res, device)
+    data = grid.device_data(device)
+    grid = V.VolumeGrid(grid.dims, grid.spacing, grid.origin, data)
     imgs = torch.empty((nv, res, res, 3), dtype=torch.uint8, device=device)
     for v, cam in enumerate(cams):
-        r.forward(tgt, cam)
-        imgs[v] = torch.round(torch.clamp(r.image, 0.0, 1.0) * 255.0).to(torch.uint8)
+        imgs[v] = V.raycast_isosurface(grid, 0.0, cam, codes=True)
     torch.cuda.synchronize()
     t3 = time.time()
     log(f"[workload {name}] {pos.shape[0]} points ({t1 - t0:.1f}s), kNN scales ({t2 - t1:.1f}s), "
-        f"{nv} GT views at {res}^2 ({t3 - t2:.1f}s)")
-    del r, tgt
+        f"{nv} raycast GT views at {res}^2 ({t3 - t2:.1f}s)")
+    del grid, data
     return Workload(name, pos, normals, ls, cams, imgs, res)

@@ -159,7 +159,8 @@ def main():
     print("train_tiny losses", rep.iteration_losses)
 
 
-if __name__ == "__main__" and not set(sys.argv) & {"--config1", "--densify", "--checkpoint"}:
+if __name__ == "__main__" and not set(sys.argv) & {"--config1", "--densify", "--checkpoint",
+                                                  "--volume"}:
     main()
 
 
@@ -260,3 +261,48 @@ def checkpoint():
 
 if __name__ == "__main__" and "--checkpoint" in sys.argv:
     checkpoint()
+
+
+def volume():
+    """Dataset generation (volume.py, raycast.py): point extraction (plain,
+    strided + subsampled) and raycast views of a small gyroid and sphere."""
+    from isosplat.raycast import raycast_isosurface
+    from isosplat.volume import VolumeGrid, extract_isosurface_points
+    out = {}
+    n, periods = 28, 2.0
+    s = 2.0 * np.pi * periods / (n - 1)
+    ax = np.arange(n, dtype=np.float64) * s
+    sx, cx = np.sin(ax), np.cos(ax)
+    data = (sx[None, None, :] * cx[None, :, None] + sx[None, :, None] * cx[:, None, None]
+            + sx[:, None, None] * cx[None, None, :])
+    gyr = VolumeGrid(dims=(n, n, n), spacing=(1.0, 1.0, 1.0), origin=(0.0, 0.0, 0.0), data=data)
+    # anisotropic spacing / offset origin on the sphere
+    sph0 = distance_field(20)
+    sph = VolumeGrid(dims=sph0.dims, spacing=(0.5, 0.75, 1.0), origin=(-1.0, 2.0, 0.5),
+                     data=sph0.data)
+    for tag, grid, iso in (("gyr", gyr, 0.0), ("sph", sph, 6.0)):
+        out[tag + "_data"] = grid.data
+        out[tag + "_spacing"] = np.asarray(grid.spacing)
+        out[tag + "_origin"] = np.asarray(grid.origin)
+        out[tag + "_iso"] = np.array(iso)
+        pc = extract_isosurface_points(grid, iso)
+        out[tag + "_pos"], out[tag + "_nrm"] = pc.positions, pc.normals
+        pc2 = extract_isosurface_points(grid, iso, stride=2, max_points=150, seed=3)
+        out[tag + "_pos_s2"], out[tag + "_nrm_s2"] = pc2.positions, pc2.normals
+        lo = np.asarray(grid.world_min)
+        hi = np.asarray(grid.world_max)
+        spec = OrbitSpec(count=3, center=tuple((lo + hi) / 2.0),
+                         radius=1.5 * float(np.linalg.norm(hi - lo) / 2.0), width=40, height=34)
+        for i, cam in enumerate(make_orbit(spec)):
+            out.update(cam_dict(cam, f"{tag}_cam{i}_"))
+            out[f"{tag}_img{i}"] = raycast_isosurface(grid, iso, cam)
+    # a camera inside the volume and a coarse step with few refinements
+    cam = make_orbit(OrbitSpec(count=2, center=(13.5, 13.5, 13.5), radius=6.0, width=24,
+                               height=24))[1]
+    out.update(cam_dict(cam, "gyr_in_"))
+    out["gyr_in_img"] = raycast_isosurface(gyr, 0.0, cam, step_scale=1.5, refine_steps=3)
+    np.savez_compressed(os.path.join(HERE, "volume.npz"), **out)
+
+
+if __name__ == "__main__" and "--volume" in sys.argv:
+    volume()

@@ -24,7 +24,8 @@ def test_header_declares_entry_points():
     for s in ("isg_knn_mean_grid", "isg_rank_of", "isg_chain_train_ranked", "isg_preprocess", "isg_sort_u64", "isg_sort_depth", "isg_sort_u16", "isg_bin_emit16",
               "isg_tile_offsets16", "isg_bin_count", "isg_bin_emit",
               "isg_raster_fwd", "isg_loss_l1_dssim", "isg_raster_bwd", "isg_reduce_ordered",
-              "isg_chain", "isg_adam", "isg_chain_adam"):
+              "isg_chain", "isg_adam", "isg_chain_adam", "isg_raycast", "isg_iso_edges",
+              "isg_iso_edge_points", "isg_iso_normals"):
         assert s in syms
 
 
@@ -55,3 +56,8 @@ def test_entry_points_reject_bad_arguments_without_gpu():
     assert lib.isg_adam(7, 1, None, None, None, None, None, None) == 1
     sz = ctypes.c_size_t(0)
     assert lib.isg_loss_l1_dssim(None, ctypes.byref(sz), 0, 5, 5, None, None, 0, 0.2, None, None, None) == 1
+    dims = (ctypes.c_int32 * 3)(4, 4, 4)
+    assert lib.isg_iso_edges(None, ctypes.byref(sz), None, ctypes.cast(dims, ctypes.c_void_p),
+                             0, 2, 0.0, None, None, None) == 1  # stride 0
+    assert lib.isg_raycast(None, None, None, None, 0.0, None, 0.5, 8, None, None, None, None,
+                           None) == 1
