@@ -229,11 +229,12 @@ def run_ours(args, world, rank, local):
     res = wl.resolution
     cloud = P.cloud_from_points(wl.points, wl.log_scales, 1, dev)
     iters = args.warmup + args.steps
-    cfg = TrainConfig(iterations=max(iters, 1), densify=False, eval_interval=0)
+    total = iters + (args.warm_iters + args.steps if args.warm_iters > 0 else 0)
+    cfg = TrainConfig(iterations=max(total, 1), densify=False, eval_interval=0)
     scene_extent = P.TrainDataset(wl.cameras, np.zeros((len(wl.cameras), 1, 1, 3)),
                                   P.PointCloud(wl.points, wl.normals)).scene_extent
     tr = Trainer(cloud, res, res, cfg, scene_extent, dev)
-    schedule = build_schedule(iters, len(wl.cameras), 0)
+    schedule = build_schedule(total, len(wl.cameras), 0)
     # warm-up
     for it in range(1, args.warmup + 1):
         v = schedule[it - 1]
@@ -277,6 +278,9 @@ def run_ours(args, world, rank, local):
     # ---- end-to-end through the public API: GT H2D from pinned host + loss D2H
     e2e = end_to_end(tr, wl, schedule, args)
 
+    # ---- second regime: the same step after more training
+    warm = warm_regime(tr, wl, schedule, args) if args.warm_iters > 0 else None
+
     # ---- CPU baseline: the reference path (oracle port) on this host
     cpu = None if args.no_cpu_baseline else cpu_baseline(wl, args)
 
@@ -295,6 +299,7 @@ def run_ours(args, world, rank, local):
         "gpu_launches": launches_per_step * args.steps,
         "phases_ms": {k: round(v, 4) for k, v in phases.items()},
         "pairs": counts,
+        "warm": warm,
     }
     print(json.dumps(line), flush=True)
 
@@ -397,6 +402,34 @@ def end_to_end(tr, wl, schedule, args):
             "d2h_bytes_per_step": 8, "ms_per_step": ms}
 
 
+def warm_regime(tr, wl, schedule, args):
+    """SURVEY 8d's post-warm-up regime: args.warm_iters more (untimed)
+    training iterations of the same trainer (no densification, N fixed), then
+    K device-timed steps like the headline.  Opacities have grown, so pixels
+    saturate and stop earlier; the pair counts say by how much."""
+    import torch
+    base = args.warmup + args.steps
+    for it in range(base + 1, base + args.warm_iters + 1):
+        v = schedule[it - 1]
+        tr.step(it, wl.cameras[v], wl.images_u8[v])
+    first = base + args.warm_iters + 1
+    stream = torch.cuda.current_stream()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for it in range(first, first + args.steps):
+        v = schedule[it - 1]
+        tr.step(it, wl.cameras[v], wl.images_u8[v])
+    stop.record(stream)
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(stop) / args.steps
+    last = first + args.steps - 1
+    loss = float(tr.loss_dev[last])
+    log(f"[ours] warm regime after {first - 1} iterations: {ms:.3f} ms/step, loss {loss:.4f}")
+    return {"after_iterations": first - 1, "ms_per_step": ms, "value": 1000.0 / ms,
+            "unit": UNIT, "loss": loss, "pairs": pair_counts(tr, wl, schedule[last - 1])}
+
+
 def cpu_baseline(wl, args):
     """The oracle port of the reference path on this host's cores: one full
     training iteration of the same workload (bounded sample)."""
@@ -428,6 +461,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="config3", choices=["config2", "config3", "config4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--warm-iters", type=int, default=500,
+                    help="also time the post-warm-up regime after this many more "
+                         "iterations (0: skip)")
     ap.add_argument("--cpu-res", type=int, default=None)
     ap.add_argument("--cpu-views", type=int, default=4)
     ap.add_argument("--cpu-budget-s", type=float, default=150.0)

@@ -8,7 +8,7 @@ python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -x 2>&1 | tai
 python bench.py --steps 10 --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.log
 tail -4 gpurun_out/bench.log
 python -c "import json;d=json.load(open('gpurun_out/bench.json'));print('VALUE',d['value'],'ms',d['ms_per_step'],'e2e',d['e2e']['value']);print(d['phases_ms']);print(d['roofline']);print(d['cpu_baseline']);print(d['clocks'])"
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --warm-iters 0"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off \
     --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
