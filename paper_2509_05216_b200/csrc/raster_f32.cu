@@ -32,7 +32,7 @@ constexpr int NW = NT / 32;
 constexpr int PSTRIDE = partial_stride<float>();  // floats per subtotal record
 constexpr int FB = 128;  // staging batch (entries)
 #ifndef BWD_MINB
-#define BWD_MINB 8
+#define BWD_MINB 12
 #endif
 #ifndef BWD_BATCH
 #define BWD_BATCH 128
@@ -124,11 +124,12 @@ __device__ __forceinline__ float pair_alpha_bl(float d1, float A, float B, const
 // reach the skip threshold: the exact maximum exponent over the box (convex
 // quadratic: interior minimum or an edge minimum) is below thr by a margin
 // that bounds the float rounding of the per-pixel exponent.
-__device__ __forceinline__ bool box_dead(const Staged &s, float x0, float y0, float edge) {
+__device__ __forceinline__ bool box_dead(const Staged &s, float x0, float y0, float ex,
+                                         float ey) {
     const float thr = s.h.y;
     if (thr > 0.0f) return true;  // opacity < 1/255: every pair is skipped
     const float a = -2.0f * s.g.z, b = -s.g.w, c = -2.0f * s.h.x;
-    const float lx = x0 - s.g.x, hx = lx + edge, ly = y0 - s.g.y, hy = ly + edge;
+    const float lx = x0 - s.g.x, hx = lx + ex, ly = y0 - s.g.y, hy = ly + ey;
     if (lx <= 0.0f && hx >= 0.0f && ly <= 0.0f && hy >= 0.0f) return false;
     float q = __int_as_float(0x7f800000);
 #pragma unroll
@@ -143,6 +144,10 @@ __device__ __forceinline__ bool box_dead(const Staged &s, float x0, float y0, fl
     const float mdx = fmaxf(fabsf(lx), fabsf(hx)), mdy = fmaxf(fabsf(ly), fabsf(hy));
     const float scale = a * mdx * mdx + 2.0f * fabsf(b) * mdx * mdy + c * mdy * mdy;
     return -0.5f * q < thr - (1e-3f + 1e-5f * scale);
+}
+
+__device__ __forceinline__ bool box_dead(const Staged &s, float x0, float y0, float edge) {
+    return box_dead(s, x0, y0, edge, edge);
 }
 
 // Reachability mask of one staged entry over the four 8x8 quadrants of the
@@ -457,17 +462,20 @@ __device__ __forceinline__ void moment_terms(float d0, float s0, float s1, float
     v[4] = s2;
 }
 
-// The four quadrant warps run independently here too.  Each walks the tile's
-// entry list back to front in batches of WB, stages the batch in its own
-// shared slice, keeps the entries that reach its quadrant (and lie before its
-// last contributor) and leaves one 9-value warp sum per kept entry in a ring
-// of RING batch slots.  The last warp to finish a batch (shared-memory arrival
-// counter) folds it: per entry, the quadrants that kept it in fixed order
-// 0..3, then the moment expansion, one padded record per (tile, entry).  A
-// warp may run up to RING-1 batches ahead of the slowest one; it waits only
-// when its ring slot has not been folded yet.
+// Backward: one 64-thread CTA per tile, one warp per 16x8 half (four pixels
+// per thread: column lane & 15, rows (lane >> 4) + {0, 2, 4, 6}), so the
+// 9-value butterfly per entry is amortised over 128 pixels; the coarser cull
+// box costs fewer instructions than the halved reductions save.  The two
+// warps run independently.  Each walks the tile's entry list back to front in
+// batches of WB, stages the batch in its own shared slice, keeps the entries
+// that reach its half (and lie before its last contributor) and leaves one
+// 9-value warp sum per kept entry in a ring of RING batch slots.  The last
+// warp to finish a batch (shared-memory arrival counter) folds it: per entry,
+// the halves that kept it in fixed order, then the moment expansion, one
+// padded record per (tile, entry).  A warp may run up to RING-1 batches ahead
+// of the other; it waits only when its ring slot has not been folded yet.
 #ifndef BWD_RING
-#define BWD_RING 4
+#define BWD_RING 3
 #endif
 constexpr int RING = BWD_RING;
 
@@ -478,30 +486,33 @@ __device__ __forceinline__ int ld_volatile(const int *p) {
     return *reinterpret_cast<const volatile int *>(p);
 }
 
+constexpr int BNT = 64;  // backward threads per tile (two 16x8 halves)
+
 template <typename DL>
-__global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
+__global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
     const float *__restrict__ feat, const int4 *__restrict__ rect_sorted,
     const int64_t *__restrict__ emit_off, float bg0, float bg1, float bg2,
     const float *__restrict__ t_final, const int32_t *__restrict__ n_last,
     const DL *__restrict__ dl, float *__restrict__ partials) {
-    __shared__ float4 sgh_all[NW][WB][2];
-    __shared__ float4 scol_all[NW][WB];
-    __shared__ unsigned char slist_all[NW][WB];
-    __shared__ float sred[RING][NW][WB][9];
-    __shared__ unsigned spres[RING][NW];
+    constexpr int NH = BNT / 32;  // warps per tile: one per 16x8 half
+    __shared__ float4 sgh_all[NH][WB][2];
+    __shared__ float4 scol_all[NH][WB];
+    __shared__ unsigned char slist_all[NH][WB];
+    __shared__ float sred[RING][NH][WB][9];
+    __shared__ unsigned spres[RING][NH];
     __shared__ int sarrive[RING];
     __shared__ int sfolded[RING];
     const int tl = blockIdx.x;
     const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
     const int ty = tid / tiles_x, tx = tid - ty * tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int px = tx * 16 + (warp & 1) * 8 + (lane & 7);
-    const int py0 = ty * 16 + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
-    const bool in0 = px < W && py0 < H, in1 = px < W && py1 < H;
-    const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
-    const float qx0 = (float)(tx * 16 + (warp & 1) * 8), qy0 = (float)(ty * 16 + (warp >> 1) * 8);
+    // lane (col, rg) owns column col and rows rg + {0, 2, 4, 6} of its half
+    const int px = tx * 16 + (lane & 15);
+    const int pyb = ty * 16 + warp * 8 + (lane >> 4);
+    const float fpx = (float)px;
+    const float qx0 = (float)(tx * 16), qy0 = (float)(ty * 16 + warp * 8);
     const int e0 = offsets[tl], n_ent = offsets[tl + 1] - e0;
     const int my_slot = bfly_slot(lane);
     float4(&sgh)[WB][2] = sgh_all[warp];
@@ -514,28 +525,26 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
         sfolded[threadIdx.x] = (int)threadIdx.x - RING;  // slot r is free for batch r
     }
 
-    int last0 = 0, last1 = 0;
-    float T0 = 0.0f, T1 = 0.0f, wr0 = 0, wg0 = 0, wb0 = 0, wr1 = 0, wg1 = 0, wb1 = 0;
-    if (in0) {
-        const int64_t pix = (int64_t)py0 * W + px;
-        last0 = n_last[pix];
-        T0 = t_final[pix];
-        wr0 = (float)dl[3 * pix];
-        wg0 = (float)dl[3 * pix + 1];
-        wb0 = (float)dl[3 * pix + 2];
+    int last[4];
+    float T[4], Q[4], wr[4], wg[4], wb[4], fpy[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int py = pyb + 2 * q;
+        fpy[q] = (float)py;
+        last[q] = 0;
+        T[q] = wr[q] = wg[q] = wb[q] = 0.0f;
+        if (px < W && py < H) {
+            const int64_t pix = (int64_t)py * W + px;
+            last[q] = n_last[pix];
+            T[q] = t_final[pix];
+            wr[q] = (float)dl[3 * pix];
+            wg[q] = (float)dl[3 * pix + 1];
+            wb[q] = (float)dl[3 * pix + 2];
+        }
+        // Q = sum_c w_c S_c with S_c starting at T_final * bg_c
+        Q[q] = wr[q] * (T[q] * bg0) + wg[q] * (T[q] * bg1) + wb[q] * (T[q] * bg2);
     }
-    if (in1) {
-        const int64_t pix = (int64_t)py1 * W + px;
-        last1 = n_last[pix];
-        T1 = t_final[pix];
-        wr1 = (float)dl[3 * pix];
-        wg1 = (float)dl[3 * pix + 1];
-        wb1 = (float)dl[3 * pix + 2];
-    }
-    // Q = sum_c w_c S_c with S_c starting at T_final * bg_c
-    float Q0 = wr0 * (T0 * bg0) + wg0 * (T0 * bg1) + wb0 * (T0 * bg2);
-    float Q1 = wr1 * (T1 * bg0) + wg1 * (T1 * bg1) + wb1 * (T1 * bg2);
-    int wm = max(last0, last1);  // this quadrant composited nothing at j >= wm
+    int wm = max(max(last[0], last[1]), max(last[2], last[3]));  // nothing composited at j >= wm
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wm = max(wm, __shfl_xor_sync(FULL, wm, o));
     __syncthreads();  // ring state initialised
@@ -551,7 +560,7 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
         bool alive = false;
         if (j < end && j < wm) {
             Staged st = stage(feat, entries[e0 + j]);
-            alive = !box_dead(st, qx0, qy0, 7.0f);
+            alive = !box_dead(st, qx0, qy0, 15.0f, 7.0f);
             to_log2(st);
             sgh[lane][0] = st.g;
             sgh[lane][1] = st.h;
@@ -574,22 +583,17 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
             float A, B;
             col_terms(d0, g4, A, B);
             const float4 col = lds4(a_col + 16 * slot);
-            if (jj < last0) {
-                float gw;
-                const float d1 = fpy0 - g4.y;
-                const float a = pair_alpha(d1, A, B, h4, gw);
-                if (a > 0.0f) {
-                    const float wc = fmaf(wb0, col.z, fmaf(wg0, col.y, wr0 * col.x));
-                    pair_grad(a, gw, d1, h4.z, wc, wr0, wg0, wb0, T0, Q0, v, s0, s1, s2);
-                }
-            }
-            if (jj < last1) {
-                float gw;
-                const float d1 = fpy1 - g4.y;
-                const float a = pair_alpha(d1, A, B, h4, gw);
-                if (a > 0.0f) {
-                    const float wc = fmaf(wb1, col.z, fmaf(wg1, col.y, wr1 * col.x));
-                    pair_grad(a, gw, d1, h4.z, wc, wr1, wg1, wb1, T1, Q1, v, s0, s1, s2);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                if (jj < last[q]) {
+                    float gw;
+                    const float d1 = fpy[q] - g4.y;
+                    const float a = pair_alpha(d1, A, B, h4, gw);
+                    if (a > 0.0f) {
+                        const float wc = fmaf(wb[q], col.z, fmaf(wg[q], col.y, wr[q] * col.x));
+                        pair_grad(a, gw, d1, h4.z, wc, wr[q], wg[q], wb[q], T[q], Q[q], v, s0,
+                                  s1, s2);
+                    }
                 }
             }
             moment_terms(d0, s0, s1, s2, v);
@@ -603,7 +607,7 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
         int prev = 0;
         if (lane == 0) prev = atomicAdd(&sarrive[rs], 1);
         prev = __shfl_sync(FULL, prev, 0);
-        if (prev == NW - 1) {
+        if (prev == NH - 1) {
             __threadfence_block();
             const int jf = start + lane;
             if (jf < end) {
@@ -619,7 +623,7 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
                 float4 *dst = reinterpret_cast<float4 *>(partials + PSTRIDE * slot);
                 unsigned pm = 0u;
 #pragma unroll
-                for (int w = 0; w < NW; w++) pm |= ((spres[rs][w] >> lane) & 1u) << w;
+                for (int w = 0; w < NH; w++) pm |= ((spres[rs][w] >> lane) & 1u) << w;
                 if (pm == 0u) {
                     const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                     dst[0] = z;
@@ -630,7 +634,7 @@ __global__ void __launch_bounds__(NT, BWD_MINB) bwd_kernel(
 #pragma unroll
                     for (int q = 0; q < 9; q++) acc[q] = 0.0f;
 #pragma unroll
-                    for (int w = 0; w < NW; w++)
+                    for (int w = 0; w < NH; w++)
                         if ((pm >> w) & 1u) {
 #pragma unroll
                             for (int q = 0; q < 9; q++) acc[q] += sred[rs][w][lane][q];
@@ -683,7 +687,7 @@ void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
                            const float *feat, const int4 *rect_sorted, const int64_t *emit_off,
                            float bg0, float bg1, float bg2, const float *t_final,
                            const int32_t *n_last, const DL *dl, float *partials, cudaStream_t s) {
-    f32::bwd_kernel<DL><<<n_tiles, f32::NT, 0, s>>>(W, H, tiles_x, row_lo, tile_ids, offsets,
+    f32::bwd_kernel<DL><<<n_tiles, f32::BNT, 0, s>>>(W, H, tiles_x, row_lo, tile_ids, offsets,
                                                     entries, feat, rect_sorted, emit_off, bg0, bg1,
                                                     bg2, t_final, n_last, dl, partials);
 }
