@@ -7,8 +7,11 @@
 
 namespace isg {
 
+#ifndef CHAINF_MINB
+#define CHAINF_MINB 8
+#endif
 template <int K3>
-__global__ void __launch_bounds__(128, 5) chain_train_f32_kernel(
+__global__ void __launch_bounds__(128, CHAINF_MINB) chain_train_f32_kernel(
     isg_params p, CamF cam, const uint8_t *__restrict__ flag, const int32_t *__restrict__ rank_of,
     const double *__restrict__ grad2d, float *dpos, float *dls, float *drot, float *dlogit,
     float *dsh, int64_t *seen, double *grad_accum, double half_w, double half_h) {
