@@ -209,6 +209,30 @@ int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t ti
                    const int32_t *n_last, const void *dl_dimage, int32_t dl_dtype,
                    void *partials, void *stream);
 
+/* float32 raster pair with contribution masks: the forward also writes, per
+ * (tile, 8x8 quadrant, batch of 32 consecutive list entries), a 32-bit mask
+ * of the entries some pixel of the quadrant composited; the backward given
+ * the same array stages only those entries (the others have all-zero
+ * subtotals, written as zeros).  Results equal isg_raster_fwd / isg_raster_bwd
+ * with feat_dtype ISG_F32.  contrib_mask holds isg_contrib_mask_words(E,
+ * n_tiles) uint32 words for a launch over n_tiles tiles with E list entries;
+ * it needs no initialisation.  The two calls must see the same tiles,
+ * offsets and n_last. */
+int64_t isg_contrib_mask_words(int64_t n_entries, int32_t n_tiles);
+int isg_raster_fwd_masked(int32_t width, int32_t height, int32_t tiles_x, int32_t row_lo,
+                          int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
+                          const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
+                          const double *bg, void *image, int32_t image_dtype, void *t_final,
+                          int32_t *n_last, int32_t *n_contrib, int32_t *n_iter, int64_t *touched,
+                          uint32_t *contrib_mask, void *stream);
+int isg_raster_bwd_masked(int32_t width, int32_t height, int32_t tiles_x, int32_t row_lo,
+                          int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
+                          const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
+                          const int32_t *rect_sorted, const int64_t *emit_off, const double *bg,
+                          const void *t_final, const int32_t *n_last, const void *dl_dimage,
+                          int32_t dl_dtype, void *partials, const uint32_t *contrib_mask,
+                          void *stream);
+
 /* Ordered fold (_reduce_scratch, _kernels.py:398-411): for rank r < m sum its
  * subtotal slots [emit_off[r], emit_off[r+1]) in float64 and write
  * grad2d[order[r]] (9 doubles).  canon_rows <= 0: the reference's single-level

@@ -78,6 +78,11 @@ SIGNATURES = {
     "isg_tile_offsets16": [_I64, _P, _I32, _P, _P],
     "isg_raster_fwd": [_I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _I32,
                        _P, _P, _P, _P, _P, _P],
+    "isg_raster_fwd_masked": [_I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _I32,
+                              _P, _P, _P, _P, _P, _P, _P],
+    "isg_raster_bwd_masked": [_I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P,
+                              _P, _P, _P, _I32, _P, _P, _P],
+    "isg_contrib_mask_words": [_I64, _I32],
     "isg_loss_l1_dssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _I32, _D, _P, _P, _P],
     "isg_ssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _P, _P],
     "isg_raster_bwd": [_I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P,
@@ -118,6 +123,9 @@ SIGNATURES = {
 }
 
 
+RET_I64 = ("isg_contrib_mask_words",)
+
+
 def lib():
     """Load libisogs.so (building it first if the sources are newer)."""
     global _lib
@@ -129,7 +137,8 @@ def lib():
         for name, args in SIGNATURES.items():
             fn = getattr(L, name)
             fn.argtypes = args
-            fn.restype = ctypes.c_char_p if name == "isg_version" else ctypes.c_int
+            fn.restype = (ctypes.c_char_p if name == "isg_version" else
+                          ctypes.c_int64 if name in RET_I64 else ctypes.c_int)
         _lib = L
     return _lib
 

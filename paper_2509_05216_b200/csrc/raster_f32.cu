@@ -96,16 +96,16 @@ __device__ __forceinline__ void col_terms(float d0, const float4 &g4, float &A, 
     B = __fmul_rn(g4.w, d0);
 }
 
-// Per-pair alpha (0 when the pair is skipped) and the Gaussian weight g.
-// The threshold test is an early exit only: a pair below it also fails
-// alpha >= 1/255 (the margin dominates the ex2/lg2 error), so pair_alpha and
-// pair_alpha_bl make identical decisions.
+// Per-pair alpha (0 when the pair is skipped) and the unclamped product
+// o * g.  The threshold test is an early exit only: a pair below it also
+// fails alpha >= 1/255 (the margin dominates the ex2/lg2 error), so
+// pair_alpha and pair_alpha_bl make identical decisions.
 __device__ __forceinline__ float pair_alpha(float d1, float A, float B, const float4 &h4,
-                                            float &gw) {
+                                            float &og) {
     const float power = __fmaf_rn(d1, __fmaf_rn(h4.x, d1, B), A);
     if (power > 0.0f || power < h4.y) return 0.0f;
-    gw = ex2a(power);
-    const float a = fminf(__fmul_rn(h4.z, gw), 0.99f);
+    og = __fmul_rn(h4.z, ex2a(power));
+    const float a = fminf(og, 0.99f);
     return a >= (1.0f / 255.0f) ? a : 0.0f;
 }
 
@@ -202,7 +202,7 @@ template <int MODE, bool CHECK>
 __device__ __forceinline__ void composite(float a, int slot, int base, uint32_t a_col,
                                           int64_t *touched, const int *srank, float &fpy,
                                           int &it, float &t, float &r, float &g, float &b,
-                                          int &last, int &cnt) {
+                                          int &last, int &cnt, unsigned &cm) {
     if (!(a > 0.0f) || (CHECK && fpy == FINF)) return;
     const float test = t * (1.0f - a);
     if (test < 1e-4f) {
@@ -217,6 +217,7 @@ __device__ __forceinline__ void composite(float a, int slot, int base, uint32_t 
     b = fmaf(c.z, w, b);
     t = test;
     last = base + slot + 1;
+    cm |= 1u << slot;
     if (MODE & F_STATS) cnt++;
     if (MODE & F_TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
 }
@@ -226,7 +227,7 @@ __device__ __forceinline__ void composite(float a, int slot, int base, uint32_t 
 // composite adds c * 0 to the colour sums, which is exact for finite c).
 // jn = the entry's list index + 1.
 template <bool CHECK>
-__device__ __forceinline__ void composite_bf(float a, const float4 &c, int jn, float &fpy,
+__device__ __forceinline__ bool composite_bf(float a, const float4 &c, int jn, float &fpy,
                                              float &t, float &r, float &g, float &b, int &last) {
     const bool on = a > 0.0f && !(CHECK && fpy == FINF);
     const float test = t * (1.0f - a);
@@ -239,6 +240,7 @@ __device__ __forceinline__ void composite_bf(float a, const float4 &c, int jn, f
     t = comp ? test : t;
     last = comp ? jn : last;
     fpy = (on && stop) ? FINF : fpy;
+    return comp;
 }
 
 // Warp w renders quadrant (w & 1, w >> 1) of the tile: lane (lx, ly) owns
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
     const float *__restrict__ feat, float bg0, float bg1, float bg2, void *image, int image_f64,
     float *__restrict__ t_final, int32_t *__restrict__ n_last, int32_t *__restrict__ n_contrib,
-    int32_t *__restrict__ n_iter, int64_t *__restrict__ touched) {
+    int32_t *__restrict__ n_iter, int64_t *__restrict__ touched, uint32_t *__restrict__ cmask) {
     constexpr bool TOUCH = MODE & F_TOUCH;
     __shared__ float4 sgh_all[NW][WB][2];
     __shared__ float4 scol_all[NW][WB];
@@ -304,6 +306,7 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
         if (alive) slist_all[warp][__popc(bal & lt)] = (unsigned char)lane;
         __syncwarp();
         const int total = __popc(bal);
+        unsigned cm = 0u;  // batch slots this lane's pixels composited
         for (int k0 = 0; k0 < total; k0 += FCHK) {
             if (k0 && __all_sync(FULL, fpy0 == FINF && fpy1 == FINF)) break;
             const int kend = min(k0 + FCHK, total);
@@ -325,21 +328,29 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
                 if (MODE == 0) {
                     const float4 ca = lds4(a_col + 16 * sa), cb = lds4(a_col + 16 * sb);
                     const int ja = base + sa + 1, jb = base + sb + 1;
-                    composite_bf<false>(aa0, ca, ja, fpy0, t0, r0, g0, b0, last0);
-                    composite_bf<false>(aa1, ca, ja, fpy1, t1, r1, g1, b1, last1);
-                    composite_bf<true>(ab0, cb, jb, fpy0, t0, r0, g0, b0, last0);
-                    composite_bf<true>(ab1, cb, jb, fpy1, t1, r1, g1, b1, last1);
+                    const bool ca0 = composite_bf<false>(aa0, ca, ja, fpy0, t0, r0, g0, b0, last0);
+                    const bool ca1 = composite_bf<false>(aa1, ca, ja, fpy1, t1, r1, g1, b1, last1);
+                    const bool cb0 = composite_bf<true>(ab0, cb, jb, fpy0, t0, r0, g0, b0, last0);
+                    const bool cb1 = composite_bf<true>(ab1, cb, jb, fpy1, t1, r1, g1, b1, last1);
+                    if (ca0 || ca1) cm |= 1u << sa;
+                    if (cb0 || cb1) cm |= 1u << sb;
                 } else {
                     composite<MODE, false>(aa0, sa, base, a_col, touched, srank, fpy0, it0, t0,
-                                           r0, g0, b0, last0, cnt0);
+                                           r0, g0, b0, last0, cnt0, cm);
                     composite<MODE, false>(aa1, sa, base, a_col, touched, srank, fpy1, it1, t1,
-                                           r1, g1, b1, last1, cnt1);
+                                           r1, g1, b1, last1, cnt1, cm);
                     composite<MODE, true>(ab0, sb, base, a_col, touched, srank, fpy0, it0, t0,
-                                          r0, g0, b0, last0, cnt0);
+                                          r0, g0, b0, last0, cnt0, cm);
                     composite<MODE, true>(ab1, sb, base, a_col, touched, srank, fpy1, it1, t1,
-                                          r1, g1, b1, last1, cnt1);
+                                          r1, g1, b1, last1, cnt1, cm);
                 }
             }
+        }
+        // contribution mask of this (tile, quadrant, batch) for the backward:
+        // bit s = batch slot s was composited by some pixel of the quadrant
+        if (cmask) {
+            cm = __reduce_or_sync(FULL, cm);
+            if (lane == 0) cmask[4 * ((int64_t)(e0 >> 5) + tl + (base >> 5)) + warp] = cm;
         }
         __syncwarp();  // the slice is restaged next batch
     }
@@ -416,14 +427,16 @@ __device__ __forceinline__ float rcpa(float x) {
     return y;
 }
 
-// Per-entry quantities shared by a thread's two pixels (same column).
+// Per-entry quantities shared by a thread's pixels (same column).
 // Per pixel the backward keeps T and Q = sum_c dL/dC_c * S_c (the reference's
 // three running sums S_c only ever enter dalpha through this dot product), so
 //   dalpha = wc * T_before - Q / (1 - alpha),  Q += wc * alpha * T_before,
 // with wc = sum_c dL/dC_c * colour_c.  The conic and mean terms are moments
-// of dpower over the thread's pixels (s0 = sum dp, s1 = sum dp d1,
-// s2 = sum dp d1^2; d0 is shared), turned into linear moments by moment_terms.
-__device__ __forceinline__ void pair_grad(float a, float gw, float d1, float op, float wc, float wr,
+// of dpower = dalpha * o * g over the thread's pixels (s0 = sum dp,
+// s1 = sum dp d1, s2 = sum dp d1^2; d0 is shared), turned into linear moments
+// by moment_terms; s0 also carries the opacity term (dopacity = sum dalpha g
+// = s0 / o, divided once per (tile, entry) in the fold).
+__device__ __forceinline__ void pair_grad(float a, float og, float d1, float wc, float wr,
                                           float wg, float wb, float &T, float &Q, float (&v)[9],
                                           float &s0, float &s1, float &s2) {
     const float inv = rcpa(1.0f - a);
@@ -434,10 +447,8 @@ __device__ __forceinline__ void pair_grad(float a, float gw, float d1, float op,
     v[7] = fmaf(wb, at, v[7]);
     const float dalpha = fmaf(wc, ti, -(Q * inv));
     Q = fmaf(wc, at, Q);
-    if (!(__fmul_rn(op, gw) > 0.99f)) {  // clamped alpha: zero sub-gradient
-        const float dg = dalpha * gw;
-        v[8] += dg;
-        const float dp = dg * op;
+    if (!(og > 0.99f)) {  // clamped alpha: zero sub-gradient
+        const float dp = dalpha * og;
         const float t = dp * d1;
         s0 += dp;
         s1 += t;
@@ -454,6 +465,7 @@ __device__ __forceinline__ void pair_grad(float a, float gw, float d1, float op,
 //   dmean = (a v0 + b v1, b v0 + c v1), dconic = (-v2/2, -v3, -v4/2).
 __device__ __forceinline__ void moment_terms(float d0, float s0, float s1, float s2,
                                              float (&v)[9]) {
+    v[8] = s0;
     const float d0s0 = d0 * s0;
     v[0] = d0s0;
     v[1] = s1;
@@ -488,14 +500,14 @@ __device__ __forceinline__ int ld_volatile(const int *p) {
 
 constexpr int BNT = 64;  // backward threads per tile (two 16x8 halves)
 
-template <typename DL>
+template <typename DL, bool MASK>
 __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
     const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
     const float *__restrict__ feat, const int4 *__restrict__ rect_sorted,
     const int64_t *__restrict__ emit_off, float bg0, float bg1, float bg2,
     const float *__restrict__ t_final, const int32_t *__restrict__ n_last,
-    const DL *__restrict__ dl, float *__restrict__ partials) {
+    const DL *__restrict__ dl, float *__restrict__ partials, const uint32_t *__restrict__ cmask) {
     constexpr int NH = BNT / 32;  // warps per tile: one per 16x8 half
     __shared__ float4 sgh_all[NH][WB][2];
     __shared__ float4 scol_all[NH][WB];
@@ -544,23 +556,40 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
         // Q = sum_c w_c S_c with S_c starting at T_final * bg_c
         Q[q] = wr[q] * (T[q] * bg0) + wg[q] * (T[q] * bg1) + wb[q] * (T[q] * bg2);
     }
-    int wm = max(max(last[0], last[1]), max(last[2], last[3]));  // nothing composited at j >= wm
+    // nothing is composited at j >= wm; wq0 / wq1: the same bound over the
+    // left / right 8x8 quadrant of this half (columns lane & 8)
+    int wq = max(max(last[0], last[1]), max(last[2], last[3]));
+    wq = max(wq, __shfl_xor_sync(FULL, wq, 16));
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wm = max(wm, __shfl_xor_sync(FULL, wm, o));
+    for (int o = 4; o > 0; o >>= 1) wq = max(wq, __shfl_xor_sync(FULL, wq, o));
+    const int wq0 = __shfl_sync(FULL, wq, 0), wq1 = __shfl_sync(FULL, wq, 8);
+    const int wm = max(wq0, wq1);
     __syncthreads();  // ring state initialised
 
+    // batches of WB entries aligned at the list start (the forward's batches,
+    // so the contribution masks line up), walked last to first
     const int n_b = (n_ent + WB - 1) / WB;
     for (int bi = 0; bi < n_b; bi++) {
-        const int end = n_ent - bi * WB, start = max(end - WB, 0);
+        const int start = (n_b - 1 - bi) * WB, end = min(start + WB, n_ent);
         const int rs = bi % RING;
         if (lane == 0)
             while (ld_volatile(&sfolded[rs]) != bi - RING) __nanosleep(BWD_SLEEP);
         __syncwarp();
         const int j = start + lane;
         bool alive = false;
-        if (j < end && j < wm) {
+        if (MASK) {
+            // the forward's contribution masks of the half's two quadrants:
+            // exactly the entries some pixel of the half composited (a
+            // quadrant's mask is valid while its forward warp was running)
+            const int64_t w = 4 * ((int64_t)(e0 >> 5) + tl + (start >> 5)) + 2 * warp;
+            unsigned bm = 0u;
+            if (start < wq0) bm |= __ldg(cmask + w);
+            if (start < wq1) bm |= __ldg(cmask + w + 1);
+            alive = (bm >> lane) & 1u;
+        }
+        if (MASK ? alive : (j < end && j < wm)) {
             Staged st = stage(feat, entries[e0 + j]);
-            alive = !box_dead(st, qx0, qy0, 15.0f, 7.0f);
+            if (!MASK) alive = !box_dead(st, qx0, qy0, 15.0f, 7.0f);
             to_log2(st);
             sgh[lane][0] = st.g;
             sgh[lane][1] = st.h;
@@ -586,13 +615,12 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 if (jj < last[q]) {
-                    float gw;
+                    float og;
                     const float d1 = fpy[q] - g4.y;
-                    const float a = pair_alpha(d1, A, B, h4, gw);
+                    const float a = pair_alpha(d1, A, B, h4, og);
                     if (a > 0.0f) {
                         const float wc = fmaf(wb[q], col.z, fmaf(wg[q], col.y, wr[q] * col.x));
-                        pair_grad(a, gw, d1, h4.z, wc, wr[q], wg[q], wb[q], T[q], Q[q], v, s0,
-                                  s1, s2);
+                        pair_grad(a, og, d1, wc, wr[q], wg[q], wb[q], T[q], Q[q], v, s0, s1, s2);
                     }
                 }
             }
@@ -639,13 +667,15 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
 #pragma unroll
                             for (int q = 0; q < 9; q++) acc[q] += sred[rs][w][lane][q];
                         }
-                    // the conic (a, b, c) of the entry, as preprocessed
+                    // the conic (a, b, c) and opacity of the entry, as preprocessed
                     const float4 f0 = __ldg(reinterpret_cast<const float4 *>(feat) + 3 * (int64_t)rank);
-                    const float ca = f0.z, cb = f0.w, cc = __ldg(feat + 12 * (int64_t)rank + 4);
+                    const float2 f1 = __ldg(reinterpret_cast<const float2 *>(feat + 12 * (int64_t)rank + 4));
+                    const float ca = f0.z, cb = f0.w, cc = f1.x;
                     dst[0] = make_float4(fmaf(ca, acc[0], cb * acc[1]), fmaf(cb, acc[0], cc * acc[1]),
                                          -0.5f * acc[2], -acc[3]);
                     dst[1] = make_float4(-0.5f * acc[4], acc[5], acc[6], acc[7]);
-                    dst[2] = make_float4(acc[8], 0.0f, 0.0f, 0.0f);
+                    // staged entries have o >= 1/255 (box_dead drops the rest)
+                    dst[2] = make_float4(__fdiv_rn(acc[8], f1.y), 0.0f, 0.0f, 0.0f);
                 }
             }
             __syncwarp();
@@ -665,13 +695,13 @@ void launch_raster_fwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
                            const int32_t *tile_ids, const int32_t *offsets, const int32_t *entries,
                            const float *feat, float bg0, float bg1, float bg2, void *image,
                            int image_f64, float *t_final, int32_t *n_last, int32_t *n_contrib,
-                           int32_t *n_iter, int64_t *touched, cudaStream_t s) {
+                           int32_t *n_iter, int64_t *touched, uint32_t *cmask, cudaStream_t s) {
     const int mode = (touched ? f32::F_TOUCH : 0) | (n_contrib || n_iter ? f32::F_STATS : 0);
 #define ISG_FWD(M)                                                                               \
     f32::fwd_kernel<M><<<n_tiles, f32::NT, 0, s>>>(W, H, tiles_x, row_lo, tile_ids, offsets,     \
                                                    entries, feat, bg0, bg1, bg2, image,          \
                                                    image_f64, t_final, n_last, n_contrib, n_iter, \
-                                                   touched)
+                                                   touched, cmask)
     switch (mode) {
         case 0: ISG_FWD(0); break;
         case 1: ISG_FWD(1); break;
@@ -686,21 +716,27 @@ void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
                            const int32_t *tile_ids, const int32_t *offsets, const int32_t *entries,
                            const float *feat, const int4 *rect_sorted, const int64_t *emit_off,
                            float bg0, float bg1, float bg2, const float *t_final,
-                           const int32_t *n_last, const DL *dl, float *partials, cudaStream_t s) {
-    f32::bwd_kernel<DL><<<n_tiles, f32::BNT, 0, s>>>(W, H, tiles_x, row_lo, tile_ids, offsets,
-                                                    entries, feat, rect_sorted, emit_off, bg0, bg1,
-                                                    bg2, t_final, n_last, dl, partials);
+                           const int32_t *n_last, const DL *dl, float *partials,
+                           const uint32_t *cmask, cudaStream_t s) {
+    if (cmask)
+        f32::bwd_kernel<DL, true><<<n_tiles, f32::BNT, 0, s>>>(
+            W, H, tiles_x, row_lo, tile_ids, offsets, entries, feat, rect_sorted, emit_off, bg0, bg1,
+            bg2, t_final, n_last, dl, partials, cmask);
+    else
+        f32::bwd_kernel<DL, false><<<n_tiles, f32::BNT, 0, s>>>(
+            W, H, tiles_x, row_lo, tile_ids, offsets, entries, feat, rect_sorted, emit_off, bg0, bg1,
+            bg2, t_final, n_last, dl, partials, nullptr);
 }
 
 template void launch_raster_bwd_f32<float>(int, int, int, int, int, const int32_t *,
                                            const int32_t *, const int32_t *, const float *,
                                            const int4 *, const int64_t *, float, float, float,
                                            const float *, const int32_t *, const float *, float *,
-                                           cudaStream_t);
+                                           const uint32_t *, cudaStream_t);
 template void launch_raster_bwd_f32<double>(int, int, int, int, int, const int32_t *,
                                             const int32_t *, const int32_t *, const float *,
                                             const int4 *, const int64_t *, float, float, float,
                                             const float *, const int32_t *, const double *,
-                                            float *, cudaStream_t);
+                                            float *, const uint32_t *, cudaStream_t);
 
 }  // namespace isg

@@ -436,13 +436,12 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_ordered_f32_kernel(
 
 using namespace isg;
 
-extern "C" int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
-                              int32_t row_lo, int32_t row_hi, const int32_t *tile_ids,
-                              int32_t n_tile_ids, const int32_t *offsets,
-                              const int32_t *entries, const void *feat_sorted, const double *bg,
-                              void *image, int32_t image_dtype, void *t_final, int32_t *n_last,
-                              int32_t *n_contrib, int32_t *n_iter, int64_t *touched,
-                              void *stream) {
+static int raster_fwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
+                      int32_t row_lo, int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
+                      const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
+                      const double *bg, void *image, int32_t image_dtype, void *t_final,
+                      int32_t *n_last, int32_t *n_contrib, int32_t *n_iter, int64_t *touched,
+                      uint32_t *cmask, void *stream) {
     if (width <= 0 || height <= 0 || tiles_x <= 0 || row_lo < 0 || row_hi < row_lo || !bg ||
         !image || !t_final || !n_last || n_tile_ids < 0)
         return (int)cudaErrorInvalidValue;
@@ -454,7 +453,7 @@ extern "C" int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height,
         launch_raster_fwd_f32(n_tiles, width, height, tiles_x, row_lo, tile_ids, offsets, entries,
                               (const float *)feat_sorted, (float)bg[0], (float)bg[1],
                               (float)bg[2], image, img64, (float *)t_final, n_last, n_contrib,
-                              n_iter, touched, s);
+                              n_iter, touched, cmask, s);
     } else if (feat_dtype == ISG_F64) {
         if (touched)
             raster_fwd_kernel<double, true><<<n_tiles, THREADS, 0, s>>>(
@@ -471,14 +470,12 @@ extern "C" int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height,
     return 0;
 }
 
-extern "C" int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
-                              int32_t row_lo, int32_t row_hi, const int32_t *tile_ids,
-                              int32_t n_tile_ids, const int32_t *offsets,
-                              const int32_t *entries, const void *feat_sorted,
-                              const int32_t *rect_sorted, const int64_t *emit_off,
-                              const double *bg, const void *t_final, const int32_t *n_last,
-                              const void *dl_dimage, int32_t dl_dtype, void *partials,
-                              void *stream) {
+static int raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
+                      int32_t row_lo, int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
+                      const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
+                      const int32_t *rect_sorted, const int64_t *emit_off, const double *bg,
+                      const void *t_final, const int32_t *n_last, const void *dl_dimage,
+                      int32_t dl_dtype, void *partials, const uint32_t *cmask, void *stream) {
     if (width <= 0 || height <= 0 || tiles_x <= 0 || row_lo < 0 || row_hi < row_lo || !bg ||
         n_tile_ids < 0 || (emit_off && !rect_sorted))
         return (int)cudaErrorInvalidValue;
@@ -497,13 +494,13 @@ extern "C" int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height,
                                      entries, (const float *)feat_sorted, rs, emit_off,
                                      (float)bg[0], (float)bg[1], (float)bg[2],
                                      (const float *)t_final, n_last, (const float *)dl_dimage,
-                                     (float *)partials, s);
+                                     (float *)partials, cmask, s);
     else if (feat_dtype == ISG_F32 && dl_dtype == ISG_F64)
         launch_raster_bwd_f32<double>(n_tiles, width, height, tiles_x, row_lo, tile_ids, offsets,
                                       entries, (const float *)feat_sorted, rs, emit_off,
                                       (float)bg[0], (float)bg[1], (float)bg[2],
                                       (const float *)t_final, n_last, (const double *)dl_dimage,
-                                      (float *)partials, s);
+                                      (float *)partials, cmask, s);
     else if (feat_dtype == ISG_F64 && dl_dtype == ISG_F32) ISG_BWD(double, float);
     else if (feat_dtype == ISG_F64 && dl_dtype == ISG_F64) ISG_BWD(double, double);
     else return (int)cudaErrorInvalidValue;
@@ -533,4 +530,64 @@ extern "C" int isg_reduce_ordered(int32_t feat_dtype, int64_t m, const int64_t *
         return (int)cudaErrorInvalidValue;
     ISG_CHECK_LAUNCH();
     return 0;
+}
+
+extern "C" int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
+                              int32_t row_lo, int32_t row_hi, const int32_t *tile_ids,
+                              int32_t n_tile_ids, const int32_t *offsets,
+                              const int32_t *entries, const void *feat_sorted, const double *bg,
+                              void *image, int32_t image_dtype, void *t_final, int32_t *n_last,
+                              int32_t *n_contrib, int32_t *n_iter, int64_t *touched,
+                              void *stream) {
+    return raster_fwd(feat_dtype, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
+                      offsets, entries, feat_sorted, bg, image, image_dtype, t_final, n_last,
+                      n_contrib, n_iter, touched, nullptr, stream);
+}
+
+extern "C" int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
+                              int32_t row_lo, int32_t row_hi, const int32_t *tile_ids,
+                              int32_t n_tile_ids, const int32_t *offsets,
+                              const int32_t *entries, const void *feat_sorted,
+                              const int32_t *rect_sorted, const int64_t *emit_off,
+                              const double *bg, const void *t_final, const int32_t *n_last,
+                              const void *dl_dimage, int32_t dl_dtype, void *partials,
+                              void *stream) {
+    return raster_bwd(feat_dtype, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
+                      offsets, entries, feat_sorted, rect_sorted, emit_off, bg, t_final, n_last,
+                      dl_dimage, dl_dtype, partials, nullptr, stream);
+}
+
+extern "C" int64_t isg_contrib_mask_words(int64_t n_entries, int32_t n_tiles) {
+    if (n_entries < 0 || n_tiles < 0) return -1;
+    return 4 * ((n_entries >> 5) + (int64_t)n_tiles + 1);
+}
+
+extern "C" int isg_raster_fwd_masked(int32_t width, int32_t height, int32_t tiles_x,
+                                     int32_t row_lo, int32_t row_hi, const int32_t *tile_ids,
+                                     int32_t n_tile_ids, const int32_t *offsets,
+                                     const int32_t *entries, const void *feat_sorted,
+                                     const double *bg, void *image, int32_t image_dtype,
+                                     void *t_final, int32_t *n_last, int32_t *n_contrib,
+                                     int32_t *n_iter, int64_t *touched, uint32_t *contrib_mask,
+                                     void *stream) {
+    if (!contrib_mask) return (int)cudaErrorInvalidValue;
+    return raster_fwd(ISG_F32, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
+                      offsets, entries, feat_sorted, bg, image, image_dtype, t_final, n_last,
+                      n_contrib, n_iter, touched, contrib_mask, stream);
+}
+
+extern "C" int isg_raster_bwd_masked(int32_t width, int32_t height, int32_t tiles_x,
+                                     int32_t row_lo, int32_t row_hi, const int32_t *tile_ids,
+                                     int32_t n_tile_ids, const int32_t *offsets,
+                                     const int32_t *entries, const void *feat_sorted,
+                                     const int32_t *rect_sorted, const int64_t *emit_off,
+                                     const double *bg, const void *t_final,
+                                     const int32_t *n_last, const void *dl_dimage,
+                                     int32_t dl_dtype, void *partials,
+                                     const uint32_t *contrib_mask, void *stream) {
+    if (!contrib_mask || (dl_dtype != ISG_F32 && dl_dtype != ISG_F64))
+        return (int)cudaErrorInvalidValue;
+    return raster_bwd(ISG_F32, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
+                      offsets, entries, feat_sorted, rect_sorted, emit_off, bg, t_final, n_last,
+                      dl_dimage, dl_dtype, partials, contrib_mask, stream);
 }

@@ -526,14 +526,17 @@ class RankStep:
         L.check(offs(E, L.ptr(tk), self.n_tiles, L.ptr(self.offsets), s), "isg_tile_offsets")
         W3 = self.W * 3
         if self.n_tiles:
-            L.check(lib.isg_raster_fwd(
-                L.ISG_F32, self.W, self.H, self.tiles_x, self.trow0, self.trow1, None, 0,
+            # contribution masks for the band's backward (isg_raster_bwd_masked)
+            self.cmask = torch.empty(lib.isg_contrib_mask_words(E, self.n_tiles),
+                                     dtype=torch.int32, device=d)
+            L.check(lib.isg_raster_fwd_masked(
+                self.W, self.H, self.tiles_x, self.trow0, self.trow1, None, 0,
                 L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
                 ctypes.cast(self.bg, ctypes.c_void_p),
                 self._vptr(self.window, self.win0, W3), L.ISG_F32,
                 self._vptr(self.t_final, self.prow0, self.W),
-                self._vptr(self.n_last, self.prow0, self.W), None, None, None, s),
-                "isg_raster_fwd")
+                self._vptr(self.n_last, self.prow0, self.W), None, None, None, L.ptr(self.cmask),
+                s), "isg_raster_fwd_masked")
         # boundary rows for the neighbours' SSIM halo
         b0, b1 = self.prow0 - self.win0, self.prow1 - self.win0
         to_prev = self.window[b0:b0 + min(10, b1 - b0)] if self.rank > 0 else None
@@ -582,14 +585,14 @@ class RankStep:
         self.partials = torch.empty((max(E, 1), 12), dtype=torch.float32, device=d)
         W3 = self.W * 3
         if self.n_tiles:
-            L.check(lib.isg_raster_bwd(
-                L.ISG_F32, self.W, self.H, self.tiles_x, self.trow0, self.trow1, None, 0,
+            L.check(lib.isg_raster_bwd_masked(
+                self.W, self.H, self.tiles_x, self.trow0, self.trow1, None, 0,
                 L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
                 L.ptr(self.rect_sorted), L.ptr(self.emit_off), ctypes.cast(self.bg, ctypes.c_void_p),
                 self._vptr(self.t_final, self.prow0, self.W),
                 self._vptr(self.n_last, self.prow0, self.W),
-                self._vptr(self.dl, self.prow0, W3), L.ISG_F32, L.ptr(self.partials), s),
-                "isg_raster_bwd")
+                self._vptr(self.dl, self.prow0, W3), L.ISG_F32, L.ptr(self.partials),
+                L.ptr(self.cmask), s), "isg_raster_bwd_masked")
         nb = torch.empty(max(M, 1), dtype=torch.int64, device=d)
         rec_off = torch.empty(M + 1, dtype=torch.int64, device=d)
         if M:

@@ -23,6 +23,7 @@ steady state.  W > 1 lives in distributed.py.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass
 
@@ -112,6 +113,10 @@ class Rasterizer:
         self.offsets = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=dev)
         self.tile_keys = self.tile_vals = self.keys_sorted_t = self.entries = None
         self.partials = None
+        # float32: forward contribution masks drive the backward (ISOGS_CMASK=0: A/B off)
+        self.use_cmask = os.environ.get("ISOGS_CMASK", "1") != "0"
+        self.cmask = None
+        self.cmask_ok = False
         self.n_contrib_out = None  # set to (H, W) int32 tensors to count pairs
         self.n_iter_out = None
         self.timer: PhaseTimer | None = None
@@ -198,12 +203,26 @@ class Rasterizer:
         L.check(offs(e, L.ptr(self.keys_sorted_t), self.n_tiles, L.ptr(self.offsets), s),
                 "isg_tile_offsets")
         _mark(tm, "tile_offsets")
-        L.check(lib.isg_raster_fwd(self.ftag, self.width, self.height, self.tiles_x, 0,
-                                   self.tiles_y, None, 0, L.ptr(self.offsets), L.ptr(self.entries),
-                                   L.ptr(self.feat_sorted), ctypes.cast(self.bg, ctypes.c_void_p),
-                                   L.ptr(self.image), L.ISG_F32, L.ptr(self.t_final),
-                                   L.ptr(self.n_last), L.ptr(self.n_contrib_out),
-                                   L.ptr(self.n_iter_out), None, s), "isg_raster_fwd")
+        self.cmask_ok = self.use_cmask and self.feat_dtype == torch.float32
+        if self.cmask_ok:
+            # the forward leaves per-(tile, quadrant, batch) contribution masks
+            # that the backward walks instead of re-culling every entry
+            words = lib.isg_contrib_mask_words(e, self.n_tiles)
+            self.cmask = _grow(self.cmask, words, dtype=torch.int32, device=dev)
+            L.check(lib.isg_raster_fwd_masked(
+                self.width, self.height, self.tiles_x, 0, self.tiles_y, None, 0,
+                L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
+                ctypes.cast(self.bg, ctypes.c_void_p), L.ptr(self.image), L.ISG_F32,
+                L.ptr(self.t_final), L.ptr(self.n_last), L.ptr(self.n_contrib_out),
+                L.ptr(self.n_iter_out), None, L.ptr(self.cmask), s), "isg_raster_fwd_masked")
+        else:
+            L.check(lib.isg_raster_fwd(self.ftag, self.width, self.height, self.tiles_x, 0,
+                                       self.tiles_y, None, 0, L.ptr(self.offsets),
+                                       L.ptr(self.entries), L.ptr(self.feat_sorted),
+                                       ctypes.cast(self.bg, ctypes.c_void_p), L.ptr(self.image),
+                                       L.ISG_F32, L.ptr(self.t_final), L.ptr(self.n_last),
+                                       L.ptr(self.n_contrib_out), L.ptr(self.n_iter_out), None,
+                                       s), "isg_raster_fwd")
         _mark(tm, "raster_fwd")
         return ViewContext(m=m, e=e)
 
@@ -215,12 +234,22 @@ class Rasterizer:
         rec = 12 if self.feat_dtype == torch.float32 else 9
         self.partials = _grow(self.partials, max(ctx.e, 1), (rec,), dtype=self.feat_dtype,
                               device=self.device)
-        L.check(lib.isg_raster_bwd(self.ftag, self.width, self.height, self.tiles_x, 0,
-                                   self.tiles_y, None, 0, L.ptr(self.offsets), L.ptr(self.entries),
-                                   L.ptr(self.feat_sorted), L.ptr(self.rect_sorted),
-                                   L.ptr(self.emit_off), ctypes.cast(self.bg, ctypes.c_void_p),
-                                   L.ptr(self.t_final), L.ptr(self.n_last), L.ptr(self.dl),
-                                   L.ISG_F32, L.ptr(self.partials), s), "isg_raster_bwd")
+        if self.cmask_ok:
+            L.check(lib.isg_raster_bwd_masked(
+                self.width, self.height, self.tiles_x, 0, self.tiles_y, None, 0,
+                L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
+                L.ptr(self.rect_sorted), L.ptr(self.emit_off),
+                ctypes.cast(self.bg, ctypes.c_void_p), L.ptr(self.t_final), L.ptr(self.n_last),
+                L.ptr(self.dl), L.ISG_F32, L.ptr(self.partials), L.ptr(self.cmask), s),
+                "isg_raster_bwd_masked")
+        else:
+            L.check(lib.isg_raster_bwd(self.ftag, self.width, self.height, self.tiles_x, 0,
+                                       self.tiles_y, None, 0, L.ptr(self.offsets),
+                                       L.ptr(self.entries), L.ptr(self.feat_sorted),
+                                       L.ptr(self.rect_sorted), L.ptr(self.emit_off),
+                                       ctypes.cast(self.bg, ctypes.c_void_p), L.ptr(self.t_final),
+                                       L.ptr(self.n_last), L.ptr(self.dl), L.ISG_F32,
+                                       L.ptr(self.partials), s), "isg_raster_bwd")
         _mark(self.timer, "raster_bwd")
         if ctx.m:
             L.check(lib.isg_reduce_ordered(self.ftag, ctx.m, L.ptr(self.emit_off),

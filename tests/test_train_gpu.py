@@ -102,3 +102,40 @@ def test_resume_from_train_state_is_bitwise(tmp_path):
         c.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
     for k in P.PARAM_NAMES:
         assert torch.equal(getattr(a.cloud, k), getattr(c.cloud, k)), k
+
+
+def test_contribution_masks_change_no_result():
+    """isg_raster_fwd_masked / isg_raster_bwd_masked (the backward walks only
+    the entries the forward composited) == the unmasked pair: images and
+    T_final bitwise, subtotals equal (== ignores the sign of zero), and the
+    parameters after 4 training iterations bitwise."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200.engine import Trainer
+    d = load("config1")
+    ds = _dataset(d, "images_u8", d["images_u8"].shape[0])
+    cfg = P.TrainConfig(iterations=4, densify=False, seed=0)
+    gt = _images(ds)
+    sched = P.build_schedule(4, ds.view_count, 0)
+    runs = []
+    for masked in (True, False):
+        t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
+        t.r.use_cmask = masked
+        for it in range(1, 5):
+            t.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
+        torch.cuda.synchronize()
+        runs.append(t)
+    a, b = runs
+    assert a.r.cmask_ok and not b.r.cmask_ok
+    assert torch.equal(a.r.image, b.r.image) and torch.equal(a.r.t_final, b.r.t_final)
+    assert torch.equal(a.r.n_last, b.r.n_last)
+    e = int(a.r.offsets[-1])
+    assert torch.equal(a.r.partials[:e], b.r.partials[:e])
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(a.cloud, k), getattr(b.cloud, k)), k
+
+
+def _images(ds):
+    imgs = torch.from_numpy(np.ascontiguousarray(ds.images)).cuda()
+    if imgs.dtype == torch.uint8:
+        imgs = (imgs.to(torch.float64) / 255.0).to(torch.float32)
+    return imgs
