@@ -123,23 +123,27 @@ extern "C" int isg_sort_u64(void *workspace, size_t *ws_bytes, const uint64_t *k
 }
 
 namespace isg {
-// After a stable sort on key bits [16, 64) the only possible disorder is
-// inside runs of equal top-48 bits (depths equal to ~1e-11 relative).  One
-// thread per run start checks its run and insertion-sorts it by the full key
-// (strict comparison: equal keys keep their ascending-id order).  Runs of the
-// culled key ~0 are identical and already in id order.
+#ifndef DEPTH_LO_BIT
+#define DEPTH_LO_BIT 24
+#endif
+// After a stable sort on key bits [DEPTH_LO_BIT, 64) the only possible
+// disorder is inside runs of equal top bits (depths equal to ~2^-(52 -
+// DEPTH_LO_BIT) relative).  One thread per run start checks its run and
+// insertion-sorts it by the full key (strict comparison: equal keys keep their
+// ascending-id order).  Runs of the culled key ~0 are identical and already
+// in id order.
 __global__ void __launch_bounds__(256) depth_tie_fix_kernel(int64_t n, uint64_t *keys,
                                                             int32_t *vals) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t k = keys[i];
     if (k == ~0ull) return;
-    const uint64_t hi = k >> 16;
-    if (i > 0 && (keys[i - 1] >> 16) == hi) return;      // not a run start
-    if (i + 1 >= n || (keys[i + 1] >> 16) != hi) return;  // singleton
+    const uint64_t hi = k >> DEPTH_LO_BIT;
+    if (i > 0 && (keys[i - 1] >> DEPTH_LO_BIT) == hi) return;      // not a run start
+    if (i + 1 >= n || (keys[i + 1] >> DEPTH_LO_BIT) != hi) return;  // singleton
     int64_t j = i + 1;
     bool sorted = true;
-    while (j < n && (keys[j] >> 16) == hi) {
+    while (j < n && (keys[j] >> DEPTH_LO_BIT) == hi) {
         if (keys[j] < keys[j - 1]) sorted = false;
         j++;
     }
@@ -160,14 +164,14 @@ __global__ void __launch_bounds__(256) depth_tie_fix_kernel(int64_t n, uint64_t 
 }  // namespace isg
 
 // Depth order (np.lexsort((indices, depth)), rasterizer.py:161-163): stable
-// radix sort of the float64 depth bits over id-ordered values, in 6 passes of
-// the top 48 bits plus the run fix-up -- bit-identical to the full 64-bit sort.
+// radix sort of the float64 depth bits over id-ordered values, in 5 passes of
+// the top 40 bits plus the run fix-up -- bit-identical to the full 64-bit sort.
 extern "C" int isg_sort_depth(void *workspace, size_t *ws_bytes, const uint64_t *keys_in,
                               uint64_t *keys_out, const int32_t *vals_in, int32_t *vals_out,
                               int64_t n, void *stream) {
     if (!ws_bytes || n < 0 || n > INT32_MAX) return (int)cudaErrorInvalidValue;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, *ws_bytes, keys_in, keys_out,
-                                                    vals_in, vals_out, (int)n, 16, 64,
+                                                    vals_in, vals_out, (int)n, DEPTH_LO_BIT, 64,
                                                     (cudaStream_t)stream);
     if (e != cudaSuccess || !workspace || n == 0) return (int)e;
     depth_tie_fix_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, keys_out,
