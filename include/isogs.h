@@ -90,7 +90,7 @@ int isg_sort_u64(void *workspace, size_t *ws_bytes, const uint64_t *keys_in,
 /* The depth order (np.lexsort((indices, depth)), rasterizer.py:161-163):
  * stable sort of (float64 depth bits, id) pairs, bit-identical to
  * isg_sort_u64 over bits [0, 64) but with 5 radix passes (top 40 bits) and a
- * fix-up of equal-top-48 runs.  Workspace as isg_sort_u64. */
+ * fix-up of equal-top-40 runs.  Workspace as isg_sort_u64. */
 int isg_sort_depth(void *workspace, size_t *ws_bytes, const uint64_t *keys_in,
                    uint64_t *keys_out, const int32_t *vals_in, int32_t *vals_out, int64_t n,
                    void *stream);
