@@ -111,13 +111,14 @@ __device__ __forceinline__ float pair_alpha(float d1, float A, float B, const fl
 
 // pair_alpha without the early exit (ex2 always evaluated): the same bits for
 // every pair, so several pairs' alphas can be computed ahead of the
-// sequential compositing.
+// sequential compositing.  Returns the clamped alpha; `on` = the pair is
+// composited unless the pixel stops (the same decision as pair_alpha > 0).
 __device__ __forceinline__ float pair_alpha_bl(float d1, float A, float B, const float4 &h4,
-                                               float &gw) {
+                                               bool &on) {
     const float power = __fmaf_rn(d1, __fmaf_rn(h4.x, d1, B), A);
-    gw = ex2a(power);
-    const float a = fminf(__fmul_rn(h4.z, gw), 0.99f);
-    return (power > 0.0f || !(a >= (1.0f / 255.0f))) ? 0.0f : a;
+    const float a = fminf(__fmul_rn(h4.z, ex2a(power)), 0.99f);
+    on = !(power > 0.0f) && a >= (1.0f / 255.0f);
+    return a;
 }
 
 // True when no pixel centre of the box [x0, x0+edge] x [y0, y0+edge] can
@@ -199,11 +200,11 @@ constexpr int F_TOUCH = 1, F_STATS = 2;
 // carried.  CHECK re-tests that sentinel for an alpha computed before the
 // pixel finished (the second entry of a step).
 template <int MODE, bool CHECK>
-__device__ __forceinline__ void composite(float a, int slot, int base, uint32_t a_col,
+__device__ __forceinline__ void composite(float a, bool on, int slot, int base, uint32_t a_col,
                                           int64_t *touched, const int *srank, float &fpy,
                                           int &it, float &t, float &r, float &g, float &b,
                                           int &last, int &cnt, unsigned &cm) {
-    if (!(a > 0.0f) || (CHECK && fpy == FINF)) return;
+    if (!on || (CHECK && fpy == FINF)) return;
     const float test = t * (1.0f - a);
     if (test < 1e-4f) {
         fpy = FINF;
@@ -222,24 +223,28 @@ __device__ __forceinline__ void composite(float a, int slot, int base, uint32_t 
     if (MODE & F_TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
 }
 
-// composite() without branches, for the training launch (no touch / stats
-// counters): the same decisions and the same bits (a pair that does not
-// composite adds c * 0 to the colour sums, which is exact for finite c).
-// jn = the entry's list index + 1.
+// composite() for the training launch (no touch / stats counters), written so
+// the decisions are predicates and the updates predicated moves and FMAs
+// (the SM's ALU pipe, which carries compares and selects, is the forward's
+// busiest): the same decisions and the same bits.  jn = the entry's list
+// index + 1.  Returns whether the pair was composited.
 template <bool CHECK>
-__device__ __forceinline__ bool composite_bf(float a, const float4 &c, int jn, float &fpy,
-                                             float &t, float &r, float &g, float &b, int &last) {
-    const bool on = a > 0.0f && !(CHECK && fpy == FINF);
+__device__ __forceinline__ bool composite_pr(float a, bool on, const float4 &c, int jn,
+                                             float &fpy, float &t, float &r, float &g, float &b,
+                                             int &last) {
+    if (CHECK) on = on && fpy != FINF;
     const float test = t * (1.0f - a);
     const bool stop = test < 1e-4f;
     const bool comp = on && !stop;
-    const float w = comp ? a * t : 0.0f;
-    r = fmaf(c.x, w, r);
-    g = fmaf(c.y, w, g);
-    b = fmaf(c.z, w, b);
-    t = comp ? test : t;
-    last = comp ? jn : last;
-    fpy = (on && stop) ? FINF : fpy;
+    if (comp) {
+        const float w = a * t;
+        r = fmaf(c.x, w, r);
+        g = fmaf(c.y, w, g);
+        b = fmaf(c.z, w, b);
+        t = test;
+        last = jn;
+    }
+    if (on && stop) fpy = FINF;
     return comp;
 }
 
@@ -264,10 +269,12 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
     float *__restrict__ t_final, int32_t *__restrict__ n_last, int32_t *__restrict__ n_contrib,
     int32_t *__restrict__ n_iter, int64_t *__restrict__ touched, uint32_t *__restrict__ cmask) {
     constexpr bool TOUCH = MODE & F_TOUCH;
-    __shared__ float4 sgh_all[NW][WB][2];
-    __shared__ float4 scol_all[NW][WB];
+    // slot WB of each warp's slice is a sentinel entry that never composites
+    // (opacity 0): odd lists are padded with it, so entries go two at a time
+    __shared__ float4 sgh_all[NW][WB + 1][2];
+    __shared__ float4 scol_all[NW][WB + 1];
     __shared__ int srank_all[NW][TOUCH ? WB : 1];
-    __shared__ unsigned char slist_all[NW][WB];
+    __shared__ unsigned char slist_all[NW][WB + 1];
     const int tl = blockIdx.x;
     const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
     const int ty = tid / tiles_x, tx = tid - ty * tiles_x;
@@ -279,9 +286,15 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
     float fpy0 = in0 ? (float)py0 : FINF, fpy1 = in1 ? (float)py1 : FINF;
     const float qx0 = (float)(tx * 16 + (warp & 1) * 8), qy0 = (float)(ty * 16 + (warp >> 1) * 8);
     const int e0 = offsets[tl], n_ent = offsets[tl + 1] - e0;
-    float4(&sgh)[WB][2] = sgh_all[warp];
-    float4(&scol)[WB] = scol_all[warp];
+    float4(&sgh)[WB + 1][2] = sgh_all[warp];
+    float4(&scol)[WB + 1] = scol_all[warp];
     int *srank = srank_all[warp];
+    if (lane == 0) {
+        const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        sgh[WB][0] = z;
+        sgh[WB][1] = z;  // power 0, opacity 0: alpha 0 at every pixel
+        scol[WB] = z;
+    }
     const uint32_t a_gh = smem_addr(&sgh[0][0]), a_col = smem_addr(&scol[0]);
     const uint32_t a_list = smem_addr(&slist_all[warp][0]);
     const unsigned lt = (1u << lane) - 1u;
@@ -304,8 +317,9 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
         }
         const unsigned bal = __ballot_sync(FULL, alive);
         if (alive) slist_all[warp][__popc(bal & lt)] = (unsigned char)lane;
-        __syncwarp();
         const int total = __popc(bal);
+        if (lane == 0) slist_all[warp][total] = (unsigned char)WB;  // odd-length pad
+        __syncwarp();
         unsigned cm = 0u;  // batch slots this lane's pixels composited
         for (int k0 = 0; k0 < total; k0 += FCHK) {
             if (k0 && __all_sync(FULL, fpy0 == FINF && fpy1 == FINF)) break;
@@ -313,36 +327,36 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
             // two entries per step: the four pair alphas are independent and
             // computed ahead; compositing stays in list order per pixel
             for (int k = k0; k < kend; k += 2) {
-                const bool two = k + 1 < kend;
-                const int sa = ldsu8(a_list + k), sb = two ? ldsu8(a_list + k + 1) : sa;
+                // slot WB (the sentinel) when k + 1 == total
+                const int sa = ldsu8(a_list + k), sb = ldsu8(a_list + k + 1);
                 const float4 ga = lds4(a_gh + 32 * sa), ha = lds4(a_gh + 32 * sa + 16);
                 const float4 gb = lds4(a_gh + 32 * sb), hb = lds4(a_gh + 32 * sb + 16);
                 float Aa, Ba, Ab, Bb;
                 col_terms(fpx - ga.x, ga, Aa, Ba);
                 col_terms(fpx - gb.x, gb, Ab, Bb);
-                float gw;
-                const float aa0 = pair_alpha_bl(fpy0 - ga.y, Aa, Ba, ha, gw);
-                const float aa1 = pair_alpha_bl(fpy1 - ga.y, Aa, Ba, ha, gw);
-                const float ab0 = two ? pair_alpha_bl(fpy0 - gb.y, Ab, Bb, hb, gw) : 0.0f;
-                const float ab1 = two ? pair_alpha_bl(fpy1 - gb.y, Ab, Bb, hb, gw) : 0.0f;
+                bool oa0, oa1, ob0, ob1;
+                const float aa0 = pair_alpha_bl(fpy0 - ga.y, Aa, Ba, ha, oa0);
+                const float aa1 = pair_alpha_bl(fpy1 - ga.y, Aa, Ba, ha, oa1);
+                const float ab0 = pair_alpha_bl(fpy0 - gb.y, Ab, Bb, hb, ob0);
+                const float ab1 = pair_alpha_bl(fpy1 - gb.y, Ab, Bb, hb, ob1);
                 if (MODE == 0) {
                     const float4 ca = lds4(a_col + 16 * sa), cb = lds4(a_col + 16 * sb);
                     const int ja = base + sa + 1, jb = base + sb + 1;
-                    const bool ca0 = composite_bf<false>(aa0, ca, ja, fpy0, t0, r0, g0, b0, last0);
-                    const bool ca1 = composite_bf<false>(aa1, ca, ja, fpy1, t1, r1, g1, b1, last1);
-                    const bool cb0 = composite_bf<true>(ab0, cb, jb, fpy0, t0, r0, g0, b0, last0);
-                    const bool cb1 = composite_bf<true>(ab1, cb, jb, fpy1, t1, r1, g1, b1, last1);
+                    const bool ca0 = composite_pr<false>(aa0, oa0, ca, ja, fpy0, t0, r0, g0, b0, last0);
+                    const bool ca1 = composite_pr<false>(aa1, oa1, ca, ja, fpy1, t1, r1, g1, b1, last1);
+                    const bool cb0 = composite_pr<true>(ab0, ob0, cb, jb, fpy0, t0, r0, g0, b0, last0);
+                    const bool cb1 = composite_pr<true>(ab1, ob1, cb, jb, fpy1, t1, r1, g1, b1, last1);
                     if (ca0 || ca1) cm |= 1u << sa;
                     if (cb0 || cb1) cm |= 1u << sb;
                 } else {
-                    composite<MODE, false>(aa0, sa, base, a_col, touched, srank, fpy0, it0, t0,
-                                           r0, g0, b0, last0, cnt0, cm);
-                    composite<MODE, false>(aa1, sa, base, a_col, touched, srank, fpy1, it1, t1,
-                                           r1, g1, b1, last1, cnt1, cm);
-                    composite<MODE, true>(ab0, sb, base, a_col, touched, srank, fpy0, it0, t0,
-                                          r0, g0, b0, last0, cnt0, cm);
-                    composite<MODE, true>(ab1, sb, base, a_col, touched, srank, fpy1, it1, t1,
-                                          r1, g1, b1, last1, cnt1, cm);
+                    composite<MODE, false>(aa0, oa0, sa, base, a_col, touched, srank, fpy0, it0,
+                                           t0, r0, g0, b0, last0, cnt0, cm);
+                    composite<MODE, false>(aa1, oa1, sa, base, a_col, touched, srank, fpy1, it1,
+                                           t1, r1, g1, b1, last1, cnt1, cm);
+                    composite<MODE, true>(ab0, ob0, sb, base, a_col, touched, srank, fpy0, it0,
+                                          t0, r0, g0, b0, last0, cnt0, cm);
+                    composite<MODE, true>(ab1, ob1, sb, base, a_col, touched, srank, fpy1, it1,
+                                          t1, r1, g1, b1, last1, cnt1, cm);
                 }
             }
         }
