@@ -627,39 +627,6 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
             col_terms(d0, g4, A, B);
             const float4 col = lds4(a_col + 16 * slot);
 #pragma unroll
-#ifdef BWD_BF
-            // branch-free: every pair runs the gradient with alpha 0 / o*g 0
-            // when it is not composited (adds exact zeros, T unchanged)
-            float ae[4], oe[4], dd[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                dd[q] = fpy[q] - g4.y;
-                const float power = __fmaf_rn(dd[q], __fmaf_rn(h4.x, dd[q], B), A);
-                const float og = __fmul_rn(h4.z, ex2a(power));
-                const float a = fminf(og, 0.99f);
-                const bool on = jj < last[q] && !(power > 0.0f) && a >= (1.0f / 255.0f);
-                ae[q] = on ? a : 0.0f;
-                oe[q] = (on && !(og > 0.99f)) ? og : 0.0f;
-            }
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const float wc = fmaf(wb[q], col.z, fmaf(wg[q], col.y, wr[q] * col.x));
-                const float inv = rcpa(1.0f - ae[q]);
-                const float ti = T[q] * inv;
-                const float at = ae[q] * ti;
-                v[5] = fmaf(wr[q], at, v[5]);
-                v[6] = fmaf(wg[q], at, v[6]);
-                v[7] = fmaf(wb[q], at, v[7]);
-                const float dalpha = fmaf(wc, ti, -(Q[q] * inv));
-                Q[q] = fmaf(wc, at, Q[q]);
-                const float dp = dalpha * oe[q];
-                const float t = dp * dd[q];
-                s0 += dp;
-                s1 += t;
-                s2 = fmaf(t, dd[q], s2);
-                T[q] = ti;
-            }
-#else
             for (int q = 0; q < 4; q++) {
                 if (jj < last[q]) {
                     float og;
@@ -671,7 +638,6 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
                     }
                 }
             }
-#endif
             moment_terms(d0, s0, s1, s2, v);
             const float y = bfly9(v, lane);
             if (my_slot >= 0) sts(a_red + 36u * (uint32_t)slot, y);
