@@ -224,7 +224,7 @@ def run_ours(args, world, rank, local):
     if world > 1 or args.dist:
         from paper_2509_05216_b200.distributed import bench_distributed
         return bench_distributed(args, world, rank, local)
-    wl = S.make_workload(args.config, dev, log=log)
+    wl = S.make_workload(args.config, dev, log=log, resolution=args.res)
     n = wl.points.shape[0]
     res = wl.resolution
     cloud = P.cloud_from_points(wl.points, wl.log_scales, 1, dev)
@@ -272,7 +272,7 @@ def run_ours(args, world, rank, local):
     tr.r.timer = None
     phases = {k: v / phase_steps for k, v in phases.items()}
     counts = pair_counts(tr, wl, schedule[iters - 1])
-    roof = roofline(phases, counts, n, args.config)
+    roof = roofline(phases, counts, n, args.config if args.res is None else f"{args.config}_{args.res}")
     log("[ours] phases (ms): " + ", ".join(f"{k} {v:.3f}" for k, v in phases.items()))
 
     # ---- end-to-end through the public API: GT H2D from pinned host + loss D2H
@@ -491,6 +491,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="config3", choices=["config2", "config3", "config4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--res", type=int, default=None,
+                    help="override the config's image resolution (BASELINE config 5 sweep)")
     ap.add_argument("--warm-iters", type=int, default=500,
                     help="also time the post-warm-up regime after this many more "
                          "iterations (0: skip)")
