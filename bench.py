@@ -106,6 +106,8 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 or args.dist:
         import torch.distributed as dist
+        # NCCL's banner / debug lines go to a file, not to the JSON stdout
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/isogs_nccl.%h.%p.log")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
