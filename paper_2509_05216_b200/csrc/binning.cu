@@ -48,10 +48,11 @@ __global__ void finish_counts_kernel(int64_t n, const int64_t *emit_off, int64_t
 // contiguous slot span [emit_off[r0], emit_off[r0 + EMIT_R]); the block
 // stages the ranks' offsets and clipped rects in shared memory and writes the
 // span with consecutive threads on consecutive slots (coalesced stores).  Each
-// slot finds its rank by binary search in the staged offsets; its tile is the
+// slot finds its rank by a chunked max-scan over the ranks' first slots; its tile is the
 // row-major position inside the rank's rect -- the same (tile, rank) pairs in
 // the same slots as emit_kernel.
 constexpr int EMIT_R = 256;
+constexpr int ECH = 1024;  // slots per scan chunk (4 per thread)
 
 template <typename K>
 __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
@@ -62,6 +63,8 @@ __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
                                                         int32_t *__restrict__ tile_vals) {
     __shared__ int64_t soff[EMIT_R + 1];
     __shared__ int4 srect[EMIT_R];
+    __shared__ int srk[ECH];
+    __shared__ int swarp[8];
     const int64_t r0 = (int64_t)blockIdx.x * EMIT_R;
     const int nr = (int)min((int64_t)EMIT_R, m - r0);
     for (int i = threadIdx.x; i <= nr; i += blockDim.x) soff[i] = emit_off[r0 + i];
@@ -74,19 +77,50 @@ __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
     __syncthreads();
     const int64_t s0 = soff[0], s1 = soff[nr];
     const uint32_t base_tile = (uint32_t)row_lo * (uint32_t)tiles_x;
-    for (int64_t o = s0 + threadIdx.x; o < s1; o += blockDim.x) {
-        int lo = 0, hi = nr;  // last i with soff[i] <= o (ranks with no slots are skipped)
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (soff[mid] <= o) lo = mid;
-            else hi = mid;
+    // Each slot's rank: mark every non-empty rank's first slot with its index,
+    // then an inclusive max-scan over the chunk (ranks ascend with the slot),
+    // instead of a binary search per slot.
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int carry = -1;  // rank covering the chunk's first slot (from the previous chunk)
+    for (int64_t c = s0; c < s1; c += ECH) {
+        const int n = (int)min((int64_t)ECH, s1 - c);
+        for (int i = t; i < ECH; i += 256) srk[i] = -1;
+        __syncthreads();
+        for (int i = t; i < nr; i += 256) {
+            const int64_t a = soff[i];
+            if (soff[i + 1] > a && a >= c && a < c + ECH) srk[a - c] = i;
         }
-        const int4 rc = srect[lo];
-        const int k = (int)(o - soff[lo]);
-        const int dy = k / rc.w, dx = k - dy * rc.w;
-        tile_keys[o] =
-            (K)((uint32_t)(rc.y + dy) * (uint32_t)tiles_x - base_tile + (uint32_t)(rc.x + dx));
-        tile_vals[o] = (int32_t)(r0 + lo);
+        __syncthreads();
+        int v0 = srk[4 * t], v1 = max(v0, srk[4 * t + 1]), v2 = max(v1, srk[4 * t + 2]),
+            v3 = max(v2, srk[4 * t + 3]);
+        int x = v3;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = max(x, y);
+        }
+        if (lane == 31) swarp[warp] = x;
+        __syncthreads();
+        int ex = max(carry, __shfl_up_sync(0xffffffffu, x, 1));
+        if (lane == 0) ex = carry;
+        for (int w = 0; w < warp; w++) ex = max(ex, swarp[w]);
+        srk[4 * t] = max(ex, v0);
+        srk[4 * t + 1] = max(ex, v1);
+        srk[4 * t + 2] = max(ex, v2);
+        srk[4 * t + 3] = max(ex, v3);
+        __syncthreads();
+        for (int i = t; i < n; i += 256) {
+            const int64_t o = c + i;
+            const int lo = srk[i];
+            const int4 rc = srect[lo];
+            const int k = (int)(o - soff[lo]);
+            const int dy = k / rc.w, dx = k - dy * rc.w;
+            tile_keys[o] =
+                (K)((uint32_t)(rc.y + dy) * (uint32_t)tiles_x - base_tile + (uint32_t)(rc.x + dx));
+            tile_vals[o] = (int32_t)(r0 + lo);
+        }
+        carry = srk[n - 1];
+        __syncthreads();  // srk is rewritten by the next chunk
     }
 }
 
