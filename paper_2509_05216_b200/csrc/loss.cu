@@ -116,7 +116,10 @@ __device__ __forceinline__ double subblock_sum(double v, double *red /* [4][4] *
 // written for centre blocks whose first row lies in [own0, own1), indexed by
 // 16x16 centre block over the full image.
 template <typename T, typename IN, typename R>
-__global__ void __launch_bounds__(LTHREADS, 3) ssim_fields_kernel(
+#ifndef LF_MINB
+#define LF_MINB 4
+#endif
+__global__ void __launch_bounds__(LTHREADS, LF_MINB) ssim_fields_kernel(
     int H, int W, int C, const IN *__restrict__ img, int img_row0, const R *__restrict__ ref,
     T *__restrict__ fmap, int fmap_row0, int fmap_rows, int by_base, int own0, int own1,
     double *__restrict__ part) {
@@ -256,7 +259,10 @@ __global__ void __launch_bounds__(LTHREADS, 3) ssim_fields_kernel(
 // dL/dimage = sign(x-y)(1-lam)/n + gscale * (A f0 + x A f1 + y A f2).
 // grad is indexed by global row from grad_row0.
 template <typename T, typename IN, typename R>
-__global__ void __launch_bounds__(LTHREADS, 4) ssim_adjoint_kernel(
+#ifndef LA_MINB
+#define LA_MINB 4
+#endif
+__global__ void __launch_bounds__(LTHREADS, LA_MINB) ssim_adjoint_kernel(
     int H, int W, const IN *__restrict__ img, int img_row0, const R *__restrict__ ref,
     const T *__restrict__ fmap, int fmap_row0, int fmap_rows, IN *__restrict__ grad,
     int grad_row0, int row1, int by_base, T l1_scale, T gscale, double *__restrict__ part) {
