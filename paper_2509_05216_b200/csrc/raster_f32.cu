@@ -402,25 +402,30 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
 // lane L with bits (b4,b3,b2,b1) holds the full sum of value
 // 5*b4 + 3*b3 + 2*b2 + b1 (see bfly_slot).
 __device__ __forceinline__ float bfly9(const float (&v)[9], int lane) {
+    // Each level keeps one of a pair of value columns per lane and adds the
+    // partner's copy of the same column.  Where the pair's second column is
+    // padding (past the 9 values), every lane simply adds the partner's first
+    // column: the lanes that "keep" the padding then hold a duplicate in a
+    // padding column, which never reaches a valid slot (columns are summed
+    // independently) -- two selects fewer per padded pair.
     const bool s4 = lane & 16, s3 = lane & 8, s2 = lane & 4, s1 = lane & 2;
     float u[5];
 #pragma unroll
-    for (int i = 0; i < 5; i++) {
-        const float a = v[i], b = i + 5 < 9 ? v[i + 5] : 0.0f;
+    for (int i = 0; i < 4; i++) {
+        const float a = v[i], b = v[i + 5];
         u[i] = (s4 ? b : a) + __shfl_xor_sync(FULL, s4 ? a : b, 16);
     }
+    u[4] = v[4] + __shfl_xor_sync(FULL, v[4], 16);
     float w[3];
 #pragma unroll
-    for (int i = 0; i < 3; i++) {
-        const float a = u[i], b = i + 3 < 5 ? u[i + 3] : 0.0f;
+    for (int i = 0; i < 2; i++) {
+        const float a = u[i], b = u[i + 3];
         w[i] = (s3 ? b : a) + __shfl_xor_sync(FULL, s3 ? a : b, 8);
     }
+    w[2] = u[2] + __shfl_xor_sync(FULL, u[2], 8);
     float x[2];
-#pragma unroll
-    for (int i = 0; i < 2; i++) {
-        const float a = w[i], b = i + 2 < 3 ? w[i + 2] : 0.0f;
-        x[i] = (s2 ? b : a) + __shfl_xor_sync(FULL, s2 ? a : b, 4);
-    }
+    x[0] = (s2 ? w[2] : w[0]) + __shfl_xor_sync(FULL, s2 ? w[0] : w[2], 4);
+    x[1] = w[1] + __shfl_xor_sync(FULL, w[1], 4);
     float y = (s1 ? x[1] : x[0]) + __shfl_xor_sync(FULL, s1 ? x[0] : x[1], 2);
     return y + __shfl_xor_sync(FULL, y, 1);
 }
