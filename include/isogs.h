@@ -123,6 +123,20 @@ int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
                  int32_t tiles_x, int32_t row_lo, int32_t row_hi, uint32_t *tile_keys,
                  int32_t *tile_vals, void *stream);
 
+/* Training-path lists (float32 features): isg_bin_emit16 that also culls
+ * every (tile, splat) pair whose 16x16 tile no pixel centre of can reach
+ * alpha >= 1/255 (the rasteriser's exact conservative box test; such a pair is
+ * never composited).  A culled pair gets the key n_band_tiles, so after
+ * isg_sort_u16 over bits [0, tile_bits + 1) it lies past every list and
+ * isg_tile_offsets16 leaves it out; its zero float32 subtotal record is
+ * written into partials (full splat-major slot layout, emit_off).  Bands of
+ * fewer than 65536 tiles.  Images, subtotals and the fold are bit-identical to
+ * the full lists. */
+int isg_bin_emit16_cull(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
+                        const float *feat_sorted, int32_t tiles_x, int32_t row_lo,
+                        int32_t row_hi, uint16_t *tile_keys, int32_t *tile_vals, float *partials,
+                        void *stream);
+
 /* 16-bit tile-key variants (band of at most 65536 tiles, e.g. 4096^2 at
  * 16 px): the same pairs / order / offsets as isg_bin_emit + isg_sort_u32 +
  * isg_tile_offsets, with 2-byte keys (25 % less traffic in the tile sort). */

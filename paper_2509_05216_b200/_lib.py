@@ -70,6 +70,7 @@ SIGNATURES = {
     "isg_sort_u32": [_P, _SZ, _P, _P, _P, _P, _I64, _I32, _I32, _P],
     "isg_sort_depth": [_P, _SZ, _P, _P, _P, _P, _I64, _P],
     "isg_bin_count": [_P, _SZ, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P],
+    "isg_bin_emit16_cull": [_I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P],
     "isg_bin_emit": [_I64, _P, _P, _I32, _I32, _I32, _P, _P, _P],
     "isg_rank_of": [_I64, _P, _P, _P, _P],
     "isg_tile_offsets": [_I64, _P, _I32, _P, _P],

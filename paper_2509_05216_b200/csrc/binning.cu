@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "raster_common.cuh"
 
 namespace isg {
 
@@ -54,15 +55,26 @@ __global__ void finish_counts_kernel(int64_t n, const int64_t *emit_off, int64_t
 constexpr int EMIT_R = 256;
 constexpr int ECH = 1024;  // slots per scan chunk (4 per thread)
 
-template <typename K>
+// CULL (float32 training path): a (tile, splat) pair whose 16x16 tile no
+// pixel centre of can reach alpha >= 1/255 (the rasteriser's exact
+// conservative box test over the tile) is never composited: it gets the key
+// `dead_key` (one past the band's last tile, so the stable sort moves it past
+// every list and the CSR offsets leave it out) and its all-zero gradient
+// subtotal is written here.  30 % of the pairs at config 3; every image,
+// gradient and parameter stays bit-identical.
+template <typename K, bool CULL>
 __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
                                                         const int4 *__restrict__ rect_sorted,
                                                         const int64_t *__restrict__ emit_off,
                                                         int tiles_x, int row_lo, int row_hi,
                                                         K *__restrict__ tile_keys,
-                                                        int32_t *__restrict__ tile_vals) {
+                                                        int32_t *__restrict__ tile_vals,
+                                                        const float *__restrict__ feat_sorted,
+                                                        float *__restrict__ partials,
+                                                        uint32_t dead_key) {
     __shared__ int64_t soff[EMIT_R + 1];
     __shared__ int4 srect[EMIT_R];
+    __shared__ f32::CullForm scf[CULL ? EMIT_R : 1];
     __shared__ int srk[ECH];
     __shared__ int swarp[8];
     const int64_t r0 = (int64_t)blockIdx.x * EMIT_R;
@@ -73,6 +85,7 @@ __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
         rc.y = max(rc.y, row_lo);  // clipped rows, width in .w
         rc.w = rc.z - rc.x + 1;
         srect[i] = rc;
+        if (CULL) scf[i] = f32::cull_form(f32::stage(feat_sorted, (int)(r0 + i)));
     }
     __syncthreads();
     const int64_t s0 = soff[0], s1 = soff[nr];
@@ -115,8 +128,19 @@ __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
             const int4 rc = srect[lo];
             const int k = (int)(o - soff[lo]);
             const int dy = k / rc.w, dx = k - dy * rc.w;
-            tile_keys[o] =
-                (K)((uint32_t)(rc.y + dy) * (uint32_t)tiles_x - base_tile + (uint32_t)(rc.x + dx));
+            uint32_t key = (uint32_t)(rc.y + dy) * (uint32_t)tiles_x - base_tile + (uint32_t)(rc.x + dx);
+            if (CULL) {
+                const f32::CullForm cf = scf[lo];
+                if (f32::box_dead_cf(cf, (float)(16 * (rc.x + dx)), (float)(16 * (rc.y + dy)), 15.0f)) {
+                    key = dead_key;
+                    float4 *dst = reinterpret_cast<float4 *>(partials + partial_stride<float>() * o);
+                    const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    dst[0] = z;
+                    dst[1] = z;
+                    dst[2] = z;
+                }
+            }
+            tile_keys[o] = (K)key;
             tile_vals[o] = (int32_t)(r0 + lo);
         }
         carry = srk[n - 1];
@@ -293,8 +317,9 @@ extern "C" int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t
                             int32_t *tile_vals, void *stream) {
     if (m < 0 || tiles_x <= 0) return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
-    emit_span_kernel<uint32_t><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
-        m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals);
+    emit_span_kernel<uint32_t, false><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
+        m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals,
+        nullptr, nullptr, 0u);
     ISG_CHECK_LAUNCH();
     return 0;
 }
@@ -305,8 +330,24 @@ extern "C" int isg_bin_emit16(int64_t m, const int32_t *rect_sorted, const int64
     if (m < 0 || tiles_x <= 0 || (int64_t)(row_hi - row_lo) * tiles_x > 65536)
         return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
-    emit_span_kernel<uint16_t><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
-        m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals);
+    emit_span_kernel<uint16_t, false><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
+        m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals,
+        nullptr, nullptr, 0u);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_bin_emit16_cull(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
+                                   const float *feat_sorted, int32_t tiles_x, int32_t row_lo,
+                                   int32_t row_hi, uint16_t *tile_keys, int32_t *tile_vals,
+                                   float *partials, void *stream) {
+    const int64_t nt = (int64_t)(row_hi - row_lo) * tiles_x;
+    if (m < 0 || tiles_x <= 0 || nt >= 65536 || (m > 0 && (!feat_sorted || !partials)))
+        return (int)cudaErrorInvalidValue;
+    if (m == 0) return 0;
+    emit_span_kernel<uint16_t, true><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
+        m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals,
+        feat_sorted, partials, (uint32_t)nt);
     ISG_CHECK_LAUNCH();
     return 0;
 }

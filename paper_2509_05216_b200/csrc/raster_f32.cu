@@ -23,6 +23,7 @@
 // written as the entry's (tile, splat) subtotal.  Deterministic throughout.
 #include "common.cuh"
 #include "raster_f32.cuh"
+#include "raster_common.cuh"
 
 namespace isg {
 namespace f32 {
@@ -38,47 +39,6 @@ constexpr int FB = 128;  // staging batch (entries)
 #define BWD_BATCH 128
 #endif
 constexpr int BB = BWD_BATCH;  // backward staging batch (entries)
-constexpr float LOG2E = 1.4426950408889634f;
-constexpr float LN2 = 0.6931471805599453f;
-constexpr unsigned FULL = 0xffffffffu;
-
-__device__ __forceinline__ float ex2a(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-__device__ __forceinline__ float lg2a(float x) {
-    float y;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-// Staged entry: g = (mx, my, -a/2, -b), h = (-c/2, thr, opacity, 0),
-// c = (r, g, b, 0).  The scalings are exact (powers of two / sign).  box_dead
-// reads this form; the inner loops read the base-2 form of to_log2().
-struct Staged {
-    float4 g, h, c;
-};
-
-// Exponent threshold below which opacity * exp(power) < 1/255 for certain:
-// -ln(255 o) minus a margin far above the ex2/lg2 approximation error.
-__device__ __forceinline__ float skip_thr(float op) {
-    if (!(op > 0.0f)) return 1.0f;
-    return __fsub_rn(__fmul_rn(lg2a(__fmul_rn(255.0f, op)), -LN2), 1e-3f);
-}
-
-__device__ __forceinline__ Staged stage(const float *__restrict__ feat, int rank) {
-    const float4 *f = reinterpret_cast<const float4 *>(feat) + 3 * (int64_t)rank;
-    const float4 x = __ldg(f), y = __ldg(f + 1), z = __ldg(f + 2);
-    // x = (mx, my, a, b), y = (c, op, r, g), z = (b_col, 0, 0, 0)
-    Staged s;
-    s.g = make_float4(x.x, x.y, -0.5f * x.z, -x.w);
-    s.h = make_float4(-0.5f * y.x, skip_thr(y.y), y.y, 0.0f);
-    s.c = make_float4(y.z, y.w, z.x, 0.0f);
-    return s;
-}
-
 // The quadratic-form coefficients and the threshold in base-2 units
 // (multiplied by log2 e once per staged entry), so a pair's exponent feeds
 // ex2 directly: power2 = log2(e) * power.
@@ -119,36 +79,6 @@ __device__ __forceinline__ float pair_alpha_bl(float d1, float A, float B, const
     const float a = fminf(__fmul_rn(h4.z, ex2a(power)), 0.99f);
     on = !(power > 0.0f) && a >= (1.0f / 255.0f);
     return a;
-}
-
-// True when no pixel centre of the box [x0, x0+edge] x [y0, y0+edge] can
-// reach the skip threshold: the exact maximum exponent over the box (convex
-// quadratic: interior minimum or an edge minimum) is below thr by a margin
-// that bounds the float rounding of the per-pixel exponent.
-__device__ __forceinline__ bool box_dead(const Staged &s, float x0, float y0, float ex,
-                                         float ey) {
-    const float thr = s.h.y;
-    if (thr > 0.0f) return true;  // opacity < 1/255: every pair is skipped
-    const float a = -2.0f * s.g.z, b = -s.g.w, c = -2.0f * s.h.x;
-    const float lx = x0 - s.g.x, hx = lx + ex, ly = y0 - s.g.y, hy = ly + ey;
-    if (lx <= 0.0f && hx >= 0.0f && ly <= 0.0f && hy >= 0.0f) return false;
-    float q = __int_as_float(0x7f800000);
-#pragma unroll
-    for (int e = 0; e < 2; e++) {
-        const float d0 = e ? hx : lx;
-        const float d1 = fminf(fmaxf(-b * d0 / c, ly), hy);
-        q = fminf(q, a * d0 * d0 + 2.0f * b * d0 * d1 + c * d1 * d1);
-        const float e1 = e ? hy : ly;
-        const float e0 = fminf(fmaxf(-b * e1 / a, lx), hx);
-        q = fminf(q, a * e0 * e0 + 2.0f * b * e0 * e1 + c * e1 * e1);
-    }
-    const float mdx = fmaxf(fabsf(lx), fabsf(hx)), mdy = fmaxf(fabsf(ly), fabsf(hy));
-    const float scale = a * mdx * mdx + 2.0f * fabsf(b) * mdx * mdy + c * mdy * mdy;
-    return -0.5f * q < thr - (1e-3f + 1e-5f * scale);
-}
-
-__device__ __forceinline__ bool box_dead(const Staged &s, float x0, float y0, float edge) {
-    return box_dead(s, x0, y0, edge, edge);
 }
 
 // Reachability mask of one staged entry over the four 8x8 quadrants of the

@@ -83,7 +83,8 @@ class ViewContext:
     """Per-view forward state kept for the backward (the cache of RenderAux)."""
 
     m: int
-    e: int
+    e: int          # tile-list entries
+    slots: int = 0  # subtotal slots (= e unless the lists are live-only)
 
 
 class Rasterizer:
@@ -181,7 +182,11 @@ class Rasterizer:
         torch.cuda.current_stream().synchronize()
         _mark(tm, "host_sync")
         m, e = int(self.counts_host[0]), int(self.counts_host[1])
+        slots = e
         dev = self.device
+        # float32 training lists leave out the pairs no pixel of their tile can
+        # composite (isg_bin_emit16_cull; their zero subtotals are written there)
+        cull = self.use_cmask and self.feat_dtype == torch.float32 and self.n_tiles < 65536
         k16 = self.n_tiles <= 65536  # 2-byte tile keys: 25 % less sort traffic
         kdt = torch.int16 if k16 else torch.int32
         if self.tile_keys is None or self.tile_keys.dtype != kdt:
@@ -193,11 +198,21 @@ class Rasterizer:
         emit = lib.isg_bin_emit16 if k16 else lib.isg_bin_emit
         offs = lib.isg_tile_offsets16 if k16 else lib.isg_tile_offsets
         if e:
-            L.check(emit(m, L.ptr(self.rect_sorted), L.ptr(self.emit_off), self.tiles_x, 0,
-                         self.tiles_y, L.ptr(self.tile_keys), L.ptr(self.tile_vals), s),
-                    "isg_bin_emit")
+            if cull:
+                self.partials = _grow(self.partials, e, (12,), dtype=self.feat_dtype, device=dev)
+                L.check(lib.isg_bin_emit16_cull(m, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
+                                                L.ptr(self.feat_sorted), self.tiles_x, 0,
+                                                self.tiles_y, L.ptr(self.tile_keys),
+                                                L.ptr(self.tile_vals), L.ptr(self.partials), s),
+                        "isg_bin_emit16_cull")
+            else:
+                L.check(emit(m, L.ptr(self.rect_sorted), L.ptr(self.emit_off), self.tiles_x, 0,
+                             self.tiles_y, L.ptr(self.tile_keys), L.ptr(self.tile_vals), s),
+                        "isg_bin_emit")
             _mark(tm, "bin_emit")
-            L.sort_pairs(self.tile_keys[:e], self.tile_vals[:e], (0, self.tile_bits),
+            # culled pairs carry the key n_tiles: one more key bit
+            bits = max(self.tile_bits, int(self.n_tiles).bit_length()) if cull else self.tile_bits
+            L.sort_pairs(self.tile_keys[:e], self.tile_vals[:e], (0, bits),
                          self.ws_sort, self.keys_sorted_t[:e], self.entries[:e])
             _mark(tm, "sort_tiles")
         L.check(offs(e, L.ptr(self.keys_sorted_t), self.n_tiles, L.ptr(self.offsets), s),
@@ -224,7 +239,7 @@ class Rasterizer:
                                        L.ptr(self.n_contrib_out), L.ptr(self.n_iter_out), None,
                                        s), "isg_raster_fwd")
         _mark(tm, "raster_fwd")
-        return ViewContext(m=m, e=e)
+        return ViewContext(m=m, e=e, slots=slots)
 
     # -- backward --------------------------------------------------------
     def backward(self, ctx: ViewContext) -> None:
@@ -232,7 +247,7 @@ class Rasterizer:
         s = L.stream_ptr()
         # float32 records are padded to 12 floats (isogs.h: isg_raster_bwd)
         rec = 12 if self.feat_dtype == torch.float32 else 9
-        self.partials = _grow(self.partials, max(ctx.e, 1), (rec,), dtype=self.feat_dtype,
+        self.partials = _grow(self.partials, max(ctx.slots, ctx.e, 1), (rec,), dtype=self.feat_dtype,
                               device=self.device)
         if self.cmask_ok:
             L.check(lib.isg_raster_bwd_masked(

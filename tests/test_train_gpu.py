@@ -105,10 +105,12 @@ def test_resume_from_train_state_is_bitwise(tmp_path):
 
 
 def test_contribution_masks_change_no_result():
-    """isg_raster_fwd_masked / isg_raster_bwd_masked (the backward walks only
-    the entries the forward composited) == the unmasked pair: images and
-    T_final bitwise, subtotals equal (== ignores the sign of zero), and the
-    parameters after 4 training iterations bitwise."""
+    """The training lists and raster pair (isg_bin_emit16_cull: pairs no pixel
+    of their tile can composite left out, zero subtotals written at emit;
+    isg_raster_fwd_masked / isg_raster_bwd_masked: the backward walks only the
+    entries the forward composited) == the full lists and the unmasked pair:
+    images and T_final bitwise, subtotals and 2-D gradients equal (== ignores
+    the sign of zero), and the parameters after 4 training iterations bitwise."""
     import paper_2509_05216_b200 as P
     from paper_2509_05216_b200.engine import Trainer
     d = load("config1")
@@ -127,9 +129,12 @@ def test_contribution_masks_change_no_result():
     a, b = runs
     assert a.r.cmask_ok and not b.r.cmask_ok
     assert torch.equal(a.r.image, b.r.image) and torch.equal(a.r.t_final, b.r.t_final)
-    assert torch.equal(a.r.n_last, b.r.n_last)
-    e = int(a.r.offsets[-1])
-    assert torch.equal(a.r.partials[:e], b.r.partials[:e])
+    # (n_last are list positions: the culled lists are shorter)
+    # masked: culled lists (fewer entries), the same subtotal slots
+    assert int(a.r.offsets[-1]) < int(b.r.offsets[-1])
+    slots = int(b.r.offsets[-1])
+    assert torch.equal(a.r.partials[:slots], b.r.partials[:slots])
+    assert torch.equal(a.r.grad2d, b.r.grad2d)
     for k in P.PARAM_NAMES:
         assert torch.equal(getattr(a.cloud, k), getattr(b.cloud, k)), k
 
