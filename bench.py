@@ -308,12 +308,19 @@ def run_ours(args, world, rank, local):
 
 def pair_counts(tr, wl, view):
     """Per-image pair counts of the forward (I_f iterated, C contributing) and
-    the backward (I_b = sum of per-pixel last contributor index)."""
+    the backward (I_b = sum of per-pixel last contributor index), counted over
+    the reference's full tile lists (SURVEY 8d units; the training launches
+    walk culled lists, which would shrink I_f and I_b)."""
     import torch
     r = tr.r
     r.n_contrib_out = torch.empty((r.height, r.width), dtype=torch.int32, device=r.device)
     r.n_iter_out = torch.empty((r.height, r.width), dtype=torch.int32, device=r.device)
-    ctx = r.forward(tr.cloud, wl.cameras[view])
+    use = r.use_cmask
+    r.use_cmask = False
+    try:
+        ctx = r.forward(tr.cloud, wl.cameras[view])
+    finally:
+        r.use_cmask = use
     out = {"M": ctx.m, "E": ctx.e, "P": r.width * r.height,
            "I_f": int(r.n_iter_out.sum(dtype=torch.int64)),
            "C": int(r.n_contrib_out.sum(dtype=torch.int64)),
