@@ -52,7 +52,10 @@ __global__ void finish_counts_kernel(int64_t n, const int64_t *emit_off, int64_t
 // slot finds its rank by a chunked max-scan over the ranks' first slots; its tile is the
 // row-major position inside the rank's rect -- the same (tile, rank) pairs in
 // the same slots as emit_kernel.
-constexpr int EMIT_R = 256;
+#ifndef EMIT_RANKS
+#define EMIT_RANKS 256
+#endif
+constexpr int EMIT_R = EMIT_RANKS;
 constexpr int ECH = 1024;  // slots per scan chunk (4 per thread)
 
 // CULL (float32 training path): a (tile, splat) pair whose 16x16 tile no

@@ -32,7 +32,10 @@ __device__ __forceinline__ void store_feat<double>(double *base, const double (&
 
 // _kernels.py:144-198 (+ the `keep` compaction flag of rasterizer.py:142-158).
 template <typename P, typename F>
-__global__ void __launch_bounds__(128, 6) preprocess_kernel(isg_params p, Cam cam, int tile,
+#ifndef PRE_MINB
+#define PRE_MINB 8
+#endif
+__global__ void __launch_bounds__(128, PRE_MINB) preprocess_kernel(isg_params p, Cam cam, int tile,
                                                          int tiles_x, int tiles_y, uint64_t *key,
                                                          int4 *rect, F *feat, uint8_t *flag,
                                                          double *full64) {
