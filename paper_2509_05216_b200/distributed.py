@@ -518,10 +518,21 @@ class RankStep:
         tv = torch.empty(max(E, 1), dtype=torch.int32, device=d)
         emit = lib.isg_bin_emit16 if k16 else lib.isg_bin_emit
         offs = lib.isg_tile_offsets16 if k16 else lib.isg_tile_offsets
+        # band lists leave out the pairs no pixel of their tile can composite
+        # (isg_bin_emit16_cull writes their zero subtotals; see engine.Rasterizer)
+        cull = self.n_tiles < 65536
+        self.partials = torch.empty((max(E, 1), 12), dtype=torch.float32, device=d)
         if E:
-            L.check(emit(M, L.ptr(self.rect_sorted), L.ptr(self.emit_off), self.tiles_x,
-                         self.trow0, self.trow1, L.ptr(tk), L.ptr(tv), s), "isg_bin_emit")
-            tk, tv = L.sort_pairs(tk[:E], tv[:E], (0, self.tile_bits), self.ws[0])
+            if cull:
+                L.check(lib.isg_bin_emit16_cull(M, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
+                                                L.ptr(self.feat_sorted), self.tiles_x, self.trow0,
+                                                self.trow1, L.ptr(tk), L.ptr(tv),
+                                                L.ptr(self.partials), s), "isg_bin_emit16_cull")
+            else:
+                L.check(emit(M, L.ptr(self.rect_sorted), L.ptr(self.emit_off), self.tiles_x,
+                             self.trow0, self.trow1, L.ptr(tk), L.ptr(tv), s), "isg_bin_emit")
+            bits = max(self.tile_bits, int(self.n_tiles).bit_length()) if cull else self.tile_bits
+            tk, tv = L.sort_pairs(tk[:E], tv[:E], (0, bits), self.ws[0])
         self.entries = tv
         L.check(offs(E, L.ptr(tk), self.n_tiles, L.ptr(self.offsets), s), "isg_tile_offsets")
         W3 = self.W * 3
@@ -582,7 +593,6 @@ class RankStep:
     def phase_backward(self):
         lib, s, d = L.lib(), L.stream_ptr(), self.dev
         E, M = self.E, self.M
-        self.partials = torch.empty((max(E, 1), 12), dtype=torch.float32, device=d)
         W3 = self.W * 3
         if self.n_tiles:
             L.check(lib.isg_raster_bwd_masked(
