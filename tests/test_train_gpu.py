@@ -144,3 +144,42 @@ def _images(ds):
     if imgs.dtype == torch.uint8:
         imgs = (imgs.to(torch.float64) / 255.0).to(torch.float32)
     return imgs
+
+
+def test_culled_lists_are_ordered_sublists_of_the_full_lists():
+    """isg_bin_emit16_cull keeps, per tile, a subsequence of the reference's
+    list (same relative order), drops only pairs with zero subtotals, and the
+    culled pairs' slots hold zeros."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200.engine import Trainer
+    d = load("config1")
+    ds = _dataset(d, "images_u8", d["images_u8"].shape[0])
+    cfg = P.TrainConfig(iterations=1, densify=False, seed=0)
+    lists = []
+    for masked in (True, False):
+        t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
+        t.r.use_cmask = masked
+        t.r.forward(t.cloud, ds.cameras[0])
+        torch.cuda.synchronize()
+        off = t.r.offsets.cpu().numpy()
+        ent = t.r.entries[:int(off[-1])].cpu().numpy()
+        lists.append([ent[off[k]:off[k + 1]] for k in range(len(off) - 1)])
+        if masked:
+            parts, emit_off, rect = t.r.partials, t.r.emit_off, t.r.rect_sorted
+    culled_total = 0
+    for lc, lf in zip(*lists):
+        assert np.all(np.isin(lc, lf))
+        pos = np.searchsorted(lf, lc)  # both lists ascend in rank
+        assert np.array_equal(lf[pos], lc) and np.all(np.diff(pos) > 0)
+        culled_total += len(lf) - len(lc)
+    assert culled_total > 0
+    # every culled (tile, rank) slot holds a zero record
+    tiles_x = t.r.tiles_x
+    eo, rc = emit_off.cpu().numpy(), rect.cpu().numpy()
+    p = parts.cpu().numpy()
+    for tile, (lc, lf) in enumerate(zip(*lists)):
+        ty, tx = divmod(tile, tiles_x)
+        for r in np.setdiff1d(lf, lc):
+            x0, y0, x1, _ = rc[r]
+            slot = eo[r] + (ty - max(y0, 0)) * (x1 - x0 + 1) + (tx - x0)
+            assert not p[slot].any()
