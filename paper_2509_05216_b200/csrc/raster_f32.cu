@@ -1,26 +1,27 @@
 // raster_f32.cu -- production float32 tile rasteriser (sm_100a).
 //
 // _forward_tiles / _backward_tiles (_kernels.py:229-374) re-designed for the
-// B200 SM: one 128-thread CTA per 16x16 tile, two pixels per thread (rows r
-// and r+8 of the same column, so the x offset d0 is shared).  Each round
-// stages a batch of the tile's entries in shared memory; while staging, one
-// thread per entry runs an exact conservative tile test -- the maximum of the
-// Gaussian exponent over the tile's pixel-centre box -- and entries that
-// cannot reach alpha >= 1/255 at any pixel of the tile are dropped from the
-// batch (ballot + prefix compaction).  Dropping them changes no result: every
-// pixel would have skipped them (the margin covers the float rounding of the
-// per-pixel exponent).  Per pair the exponent is 4 explicit FMA/FMULs against
-// a per-splat log threshold; only pairs that can pass pay for the SFU ex2.
+// B200 SM.  Forward: one 128-thread CTA per 16x16 tile, warp w owns 8x8
+// quadrant w, two pixels per lane (rows r and r+4 of one column, so the x
+// terms of the exponent are shared).  Each warp stages 32 list entries at a
+// time and keeps those its quadrant can see -- the exact maximum of the
+// Gaussian exponent over the quadrant's pixel-centre box against the skip
+// threshold (box_dead, raster_common.cuh; the margin covers the per-pixel
+// rounding, so dropping an entry changes no result) -- then composites two
+// entries per step with the decisions as predicates.  The training launch also
+// leaves per-(tile, quadrant, batch) contribution masks for the backward.
 //
-// All decisions (skip, 0.99 clamp, stop) come from pair_alpha(), written with
-// explicit rounding intrinsics so the forward and the backward kernels compute
-// bit-identical exponents and alphas and therefore the same contributor sets.
+// All decisions (skip, 0.99 clamp, stop) come from pair_alpha / pair_alpha_bl,
+// written with explicit rounding intrinsics so the forward and the backward
+// compute bit-identical exponents and alphas and therefore the same
+// contributor sets.
 //
-// The backward walks each pixel's contributors back to front (T recovered by
-// division from T_final), sums the two pixels of a thread in registers and
-// reduces the 9 gradient terms of an entry over the warp with a 12-shuffle
-// butterfly reduce-scatter; the 4 warp sums are folded in fixed order and
-// written as the entry's (tile, splat) subtotal.  Deterministic throughout.
+// Backward: one 64-thread CTA per tile, warp h owns 16x8 half h, four pixels
+// per lane; contributors walked back to front (T recovered by division from
+// T_final).  The 9 gradient terms of an entry are reduced over the warp with a
+// butterfly reduce-scatter; the last warp to finish a batch folds both halves'
+// sums in fixed order into the entry's (tile, splat) subtotal.  Deterministic
+// throughout, no atomics on the data path.
 #include "common.cuh"
 #include "raster_f32.cuh"
 #include "raster_common.cuh"
@@ -31,14 +32,9 @@ namespace f32 {
 constexpr int NT = 128;  // threads per tile (2 pixels each)
 constexpr int NW = NT / 32;
 constexpr int PSTRIDE = partial_stride<float>();  // floats per subtotal record
-constexpr int FB = 128;  // staging batch (entries)
 #ifndef BWD_MINB
 #define BWD_MINB 12
 #endif
-#ifndef BWD_BATCH
-#define BWD_BATCH 128
-#endif
-constexpr int BB = BWD_BATCH;  // backward staging batch (entries)
 // The quadratic-form coefficients and the threshold in base-2 units
 // (multiplied by log2 e once per staged entry), so a pair's exponent feeds
 // ex2 directly: power2 = log2(e) * power.
