@@ -181,7 +181,10 @@ __device__ __forceinline__ bool composite_pr(float a, bool on, const float4 &c, 
 // entries that can reach its quadrant (box_dead over the 8x8 pixel box) and
 // composites them.  "All pixels done" is tested every FCHK entries (a
 // finished pixel only skips work, so the late test changes no result).
-constexpr int FCHK = 4;
+#ifndef FWD_FCHK
+#define FWD_FCHK 16
+#endif
+constexpr int FCHK = FWD_FCHK;
 constexpr int WB = 32;  // per-warp staging batch
 
 #ifndef FWD_MINB
