@@ -337,7 +337,10 @@ __global__ void __launch_bounds__(256) reduce_ordered_kernel(
 // per-warp shared buffers with TMA bulk copies (cp.async.bulk, completion on
 // an mbarrier): chunk k+1 lands while the lanes fold chunk k, each lane its
 // own slots -- the same FoldState arithmetic as fold_rank.  No block barriers.
-constexpr int RED_WARPS = 4;
+#ifndef RED_WARPS_N
+#define RED_WARPS_N 4
+#endif
+constexpr int RED_WARPS = RED_WARPS_N;
 constexpr int RED_THREADS = 32 * RED_WARPS;
 #ifndef RED_SLOTS_N
 #define RED_SLOTS_N 96
