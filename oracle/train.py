@@ -115,12 +115,54 @@ def evaluate(params, degree, cameras, images, cfg: Config, it: int) -> Record:
     return Record(it, float(np.mean(losses)), float(np.mean(psnrs)), float(np.mean(ssims)))
 
 
+def iteration(params: dict, state: dict, seen, grad_accum, degree: int, it: int, cam, ref,
+              cfg: Config, extent: float):
+    """One W=1 training iteration in place (engine.py:481-537): render, loss,
+    backward, 2-D fold, stats, chain, Adam.  Returns (loss, details) with the
+    iteration's canvas, parameter gradients, 2-D gradients (cloud row order)
+    and visible rows."""
+    n = params["positions"].shape[0]
+    h, w = ref.shape[0], ref.shape[1]
+    img, (cloud, batch, aux, order) = render_view(params, degree, cam, cfg)
+    loss, dimg = O.loss_l1_dssim(img, ref, cfg.lambda_dssim)
+    b2d, _ = O.render_backward_2d(batch, order, aux, dimg)
+    rows = batch.indices
+    full = {k: np.zeros((n,) + v.shape[1:]) for k, v in b2d.items()}
+    for k in full:
+        full[k][rows] = b2d[k]
+    seen[rows] += 1
+    grad_accum[rows] += np.hypot(full["dmean"][rows, 0] * (0.5 * w),
+                                 full["dmean"][rows, 1] * (0.5 * h))
+    flags = np.zeros(n, dtype=np.uint8)
+    flags[rows] = 1
+    pg = O.chain_to_params(cloud, cam, flags, full["dmean"], full["dconic"],
+                           full["dcolor"], full["dopac"])
+    grads = {k: getattr(pg, k) for k in PARAM_NAMES}
+    lrs = {
+        "positions": extent * position_lr(cfg.lr_position, it, cfg.iterations,
+                                          cfg.lr_position_final),
+        "log_scales": cfg.lr_scale,
+        "rotations": cfg.lr_rotation,
+        "opacity_logits": cfg.lr_opacity,
+        "sh_coeffs": cfg.lr_sh,
+    }
+    details = {"iteration": it, "image": img, "loss": float(loss),
+               "param_grads": {k: np.array(v, copy=True) for k, v in grads.items()},
+               "grad2d": full, "visible": rows.copy(), "lrs": lrs}
+    O.adam_step(params, grads, state, it, lrs)
+    return float(loss), details
+
+
 def train_w1(images, cameras, init_params: dict, cfg: Config, extent: float | None = None,
              evaluate_views: bool = True, max_iters: int | None = None,
-             wall_budget_s: float | None = None) -> Result:
+             wall_budget_s: float | None = None, schedule=None,
+             keep_grads: bool = False) -> Result:
     """engine.py:465-562 with W=1.  ``max_iters`` / ``wall_budget_s`` stop early
     (the schedule and learning rates still follow cfg.iterations), used for
-    bounded CPU samples; per-iteration wall times land in Result.iter_times."""
+    bounded CPU samples; per-iteration wall times land in Result.iter_times.
+    ``schedule`` overrides the view order (indices into ``cameras``);
+    ``keep_grads`` keeps the last iteration's parameter gradients, 2-D
+    gradients (cloud row order) and canvas in Result.last."""
     params = {k: np.array(init_params[k], dtype=np.float32, copy=True) for k in PARAM_NAMES}
     state = {k: {"m": np.zeros_like(v), "v": np.zeros_like(v)} for k, v in params.items()}
     degree = cfg.sh_degree
@@ -134,36 +176,16 @@ def train_w1(images, cameras, init_params: dict, cfg: Config, extent: float | No
     res.iter_times = []
     if evaluate_views:
         res.records.append(evaluate(params, degree, cameras, images, cfg, 0))
-    schedule = build_schedule(cfg.iterations, len(cameras), cfg.seed)
+    if schedule is None:
+        schedule = build_schedule(cfg.iterations, len(cameras), cfg.seed)
     last = cfg.iterations if max_iters is None else min(max_iters, cfg.iterations)
     for it in range(1, last + 1):
         t0 = time.perf_counter()
         cam = cameras[schedule[it - 1]]
         ref = images[schedule[it - 1]]
-        img, (cloud, batch, aux, order) = render_view(params, degree, cam, cfg)
-        loss, dimg = O.loss_l1_dssim(img, ref, cfg.lambda_dssim)
-        b2d, _ = O.render_backward_2d(batch, order, aux, dimg)
-        rows = batch.indices
-        full = {k: np.zeros((n,) + v.shape[1:]) for k, v in b2d.items()}
-        for k in full:
-            full[k][rows] = b2d[k]
-        seen[rows] += 1
-        grad_accum[rows] += np.hypot(full["dmean"][rows, 0] * (0.5 * w),
-                                     full["dmean"][rows, 1] * (0.5 * h))
-        flags = np.zeros(n, dtype=np.uint8)
-        flags[rows] = 1
-        pg = O.chain_to_params(cloud, cam, flags, full["dmean"], full["dconic"],
-                               full["dcolor"], full["dopac"])
-        grads = {k: getattr(pg, k) for k in PARAM_NAMES}
-        lrs = {
-            "positions": extent * position_lr(cfg.lr_position, it, cfg.iterations,
-                                              cfg.lr_position_final),
-            "log_scales": cfg.lr_scale,
-            "rotations": cfg.lr_rotation,
-            "opacity_logits": cfg.lr_opacity,
-            "sh_coeffs": cfg.lr_sh,
-        }
-        O.adam_step(params, grads, state, it, lrs)
+        loss, det = iteration(params, state, seen, grad_accum, degree, it, cam, ref, cfg, extent)
+        if keep_grads:
+            res.last = det
         dt = time.perf_counter() - t0
         res.total_wall_s += dt
         res.iter_times.append(dt)

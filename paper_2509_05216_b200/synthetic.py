@@ -94,7 +94,10 @@ class Workload:
 
 
 def make_workload(name: str, device, views: int | None = None, max_points: int | None = None,
-                  resolution: int | None = None, log=print) -> Workload:
+                  resolution: int | None = None, log=print, view_ids=None) -> Workload:
+    """The named workload on `device`.  view_ids: raycast the GT of only these
+    views of the full orbit (images_u8[k] is view view_ids[k]; `cameras`
+    still holds every orbit view)."""
     import time
     from .training import init_log_scales
     n, periods, mp, res, nv = CONFIGS[name]
@@ -112,12 +115,13 @@ def make_workload(name: str, device, views: int | None = None, max_points: int |
     cams = orbit(n, nv, res)
     data = grid.device_data(device)
     grid = V.VolumeGrid(grid.dims, grid.spacing, grid.origin, data)
-    imgs = torch.empty((nv, res, res, 3), dtype=torch.uint8, device=device)
-    for v, cam in enumerate(cams):
-        imgs[v] = V.raycast_isosurface(grid, 0.0, cam, codes=True)
+    ids = list(range(nv)) if view_ids is None else [int(v) for v in view_ids]
+    imgs = torch.empty((len(ids), res, res, 3), dtype=torch.uint8, device=device)
+    for k, v in enumerate(ids):
+        imgs[k] = V.raycast_isosurface(grid, 0.0, cams[v], codes=True)
     torch.cuda.synchronize()
     t3 = time.time()
     log(f"[workload {name}] {pos.shape[0]} points ({t1 - t0:.1f}s), kNN scales ({t2 - t1:.1f}s), "
-        f"{nv} raycast GT views at {res}^2 ({t3 - t2:.1f}s)")
+        f"{len(ids)} raycast GT views at {res}^2 ({t3 - t2:.1f}s)")
     del grid, data
     return Workload(name, pos, normals, ls, cams, imgs, res)
