@@ -148,7 +148,9 @@ def iteration(params: dict, state: dict, seen, grad_accum, degree: int, it: int,
     }
     details = {"iteration": it, "image": img, "loss": float(loss),
                "param_grads": {k: np.array(v, copy=True) for k, v in grads.items()},
-               "grad2d": full, "visible": rows.copy(), "lrs": lrs}
+               "grad2d": full, "visible": rows.copy(), "lrs": lrs,
+               "depth_order_rows": rows[order].copy(), "offsets": aux.cache["offsets"],
+               "entries": aux.cache["entries"]}
     O.adam_step(params, grads, state, it, lrs)
     return float(loss), details
 

@@ -44,6 +44,13 @@ from . import _lib as L
 
 TILE = 16
 CANON_ROWS = 8
+# our kernels per sharded step (CUB scan/sort passes not counted): preprocess,
+# route_count, route_emit, dest offsets, route_gather | records_unpack,
+# depth tie fix, gather_rank, finish_counts, bin_emit16_cull, tile_offsets16,
+# raster_fwd_masked | ssim_fields, ssim_adjoint, loss_finish | raster_bwd_masked,
+# block_count, block_fold, owner offsets, grad_gather | grad_rows, seg
+# offsets, owner_fold, chain_train, adam_groups
+LAUNCHES_PER_STEP = 24
 
 
 class ProtocolError(RuntimeError):
@@ -486,7 +493,11 @@ class RankStep:
                                  L.ptr(total), L.stream_ptr()), "isg_scan_i64")
 
     # -- phase 2: render the band -----------------------------------------
-    def phase_render(self, records: torch.Tensor):
+    def phase_render(self, records: torch.Tensor, count: bool = False):
+        """count=True: the reference's full band lists and the unmasked
+        forward with per-pixel pair counters (n_contrib, n_iter; n_last is
+        then the full-list last-contributor index) for the roofline units;
+        leaves no state for a backward."""
         lib, s, d = L.lib(), L.stream_ptr(), self.dev
         R = int(records.shape[0])
         self.R = R
@@ -520,7 +531,7 @@ class RankStep:
         offs = lib.isg_tile_offsets16 if k16 else lib.isg_tile_offsets
         # band lists leave out the pairs no pixel of their tile can composite
         # (isg_bin_emit16_cull writes their zero subtotals; see engine.Rasterizer)
-        cull = self.n_tiles < 65536
+        cull = self.n_tiles < 65536 and not count
         self.partials = torch.empty((max(E, 1), 12), dtype=torch.float32, device=d)
         if E:
             if cull:
@@ -536,6 +547,21 @@ class RankStep:
         self.entries = tv
         L.check(offs(E, L.ptr(tk), self.n_tiles, L.ptr(self.offsets), s), "isg_tile_offsets")
         W3 = self.W * 3
+        if count:
+            band_px = max((self.prow1 - self.prow0) * self.W, 1)
+            self.n_contrib = torch.zeros(band_px, dtype=torch.int32, device=d)
+            self.n_iter = torch.zeros(band_px, dtype=torch.int32, device=d)
+            if self.n_tiles:
+                L.check(lib.isg_raster_fwd(
+                    L.ISG_F32, self.W, self.H, self.tiles_x, self.trow0, self.trow1, None, 0,
+                    L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
+                    ctypes.cast(self.bg, ctypes.c_void_p),
+                    self._vptr(self.window, self.win0, W3), L.ISG_F32,
+                    self._vptr(self.t_final, self.prow0, self.W),
+                    self._vptr(self.n_last, self.prow0, self.W),
+                    self._vptr(self.n_contrib, self.prow0, self.W),
+                    self._vptr(self.n_iter, self.prow0, self.W), None, s), "isg_raster_fwd")
+            return None, None
         if self.n_tiles:
             # contribution masks for the band's backward (isg_raster_bwd_masked)
             self.cmask = torch.empty(lib.isg_contrib_mask_words(E, self.n_tiles),
@@ -590,7 +616,8 @@ class RankStep:
         return self.loss_dev
 
     # -- phase 4: backward + per-block records for the owners --------------
-    def phase_backward(self):
+    def phase_backward(self, timer=None):
+        from .engine import _mark
         lib, s, d = L.lib(), L.stream_ptr(), self.dev
         E, M = self.E, self.M
         W3 = self.W * 3
@@ -603,6 +630,7 @@ class RankStep:
                 self._vptr(self.n_last, self.prow0, self.W),
                 self._vptr(self.dl, self.prow0, W3), L.ISG_F32, L.ptr(self.partials),
                 L.ptr(self.cmask), s), "isg_raster_bwd_masked")
+        _mark(timer, "raster_bwd")
         nb = torch.empty(max(M, 1), dtype=torch.int64, device=d)
         rec_off = torch.empty(M + 1, dtype=torch.int64, device=d)
         if M:
@@ -838,13 +866,29 @@ def comm_step(rs: RankStep, comm: TorchComm, cam, gt: torch.Tensor, it: int,
     comm.allreduce_sum_(parts)
     loss = rs.finish_loss()
     _mark(timer, "loss_allreduce")
-    grec, gcnt = rs.phase_backward()
-    _mark(timer, "backward_blockfold")
+    grec, gcnt = rs.phase_backward(timer)
+    _mark(timer, "block_fold")
     rg, _ = comm.alltoallv(grec, gcnt)
     _mark(timer, "a2a_grads")
     rs.phase_update(rg, it)
     _mark(timer, "owner_fold_chain_adam")
     return loss
+
+
+def comm_pair_counts(rs: RankStep, comm: TorchComm, cam) -> dict:
+    """Roofline units of this rank's band for view `cam`: pairs
+    iterated (I_f), contributing (C) and the backward's I_b (sum of the
+    last-contributor index) over the reference's full lists; no state change."""
+    rec, cnt = rs.phase_project(cam)
+    rrec, _ = comm.alltoallv(rec, cnt)
+    rs.phase_render(rrec, count=True)
+    px = (rs.prow1 - rs.prow0) * rs.W
+    out = {"M": rs.M, "E": rs.E, "P": px,
+           "I_f": int(rs.n_iter[:px].sum(dtype=torch.int64)),
+           "C": int(rs.n_contrib[:px].sum(dtype=torch.int64)),
+           "I_b": int(rs.n_last[:px].sum(dtype=torch.int64))}
+    rs.n_contrib = rs.n_iter = None
+    return out
 
 
 def emulated_step(ranks: list, cam, gt: torch.Tensor, it: int) -> torch.Tensor:
@@ -972,98 +1016,3 @@ def _all_sizes(rs: "RankStep", comm: "TorchComm") -> list:
     allc = [torch.empty_like(mine) for _ in range(comm.world)]
     comm.dist.all_gather(allc, mine, group=comm.group)
     return [int(c.item()) for c in allc]
-
-
-def bench_distributed(args, world: int, rank: int, local: int):
-    """bench.py's N>1 arm: the sharded step on `world` GPUs (one process each).
-    Device time = max over ranks of the CUDA-event time of K steps."""
-    import json
-    import sys
-    import torch.distributed as dist
-    from . import synthetic as S
-    from .gaussians import cloud_from_points
-    from .training import TrainConfig, TrainDataset, PointCloud, build_schedule
-    dev = torch.device("cuda", local)
-    comm = TorchComm()
-    # torchrun pins OMP_NUM_THREADS=1; the host side of the step (collective
-    # bookkeeping between the device phases) runs measurably slower that way
-    import os
-    torch.set_num_threads(max(1, (os.cpu_count() or 1) // max(world, 1)))
-    log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
-    wl = S.make_workload(args.config, dev, log=log)
-    n = wl.points.shape[0]
-    res = wl.resolution
-    cloud = cloud_from_points(wl.points, wl.log_scales, 1, dev)
-    iters = args.warmup + args.steps
-    cfg = TrainConfig(iterations=max(iters, 1), densify=False, eval_interval=0)
-    ext = TrainDataset(wl.cameras, np.zeros((len(wl.cameras), 1, 1, 3)),
-                       PointCloud(wl.points, wl.normals)).scene_extent
-    (rs,), smap, part = make_ranks(cloud, res, res, cfg, ext, world, dev, only_rank=rank)
-    del cloud
-    schedule = build_schedule(iters, len(wl.cameras), 0)
-    for it in range(1, args.warmup + 1):
-        v = schedule[it - 1]
-        comm_step(rs, comm, wl.cameras[v], wl.images_u8[v], it)
-    torch.cuda.synchronize()
-    dist.barrier()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    from bench import ClockSampler  # noqa: E402  (repo root on sys.path)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        dist.barrier()
-        start.record()
-        for it in range(args.warmup + 1, iters + 1):
-            v = schedule[it - 1]
-            comm_step(rs, comm, wl.cameras[v], wl.images_u8[v], it)
-        stop.record()
-        torch.cuda.synchronize()
-        dist.barrier()
-    ms = torch.tensor([start.elapsed_time(stop)], dtype=torch.float64, device=dev)
-    comm.max_(ms)
-    ms_per_step = float(ms[0]) / args.steps
-    # per-phase device times of one more step (untimed), rank 0's view
-    from .engine import PhaseTimer
-    timer = PhaseTimer()
-    v = schedule[iters - 1]
-    comm_step(rs, comm, wl.cameras[v], wl.images_u8[v], iters, timer=timer)
-    phases = {k: round(x, 4) for k, x in timer.phases().items()}
-    log("[dist] phases (ms): " + ", ".join(f"{k} {x:.3f}" for k, x in phases.items()))
-    # end to end: each step's GT H2D from pinned host memory + loss D2H
-    first = iters - args.steps + 1
-    host = torch.empty((args.steps,) + tuple(wl.images_u8.shape[1:]), dtype=torch.uint8).pin_memory()
-    for k in range(args.steps):
-        host[k].copy_(wl.images_u8[schedule[first + k - 1]].cpu())
-    gt = torch.empty_like(wl.images_u8[0])
-    lh = torch.zeros(1, dtype=torch.float64).pin_memory()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for k in range(args.steps):
-        it = first + k
-        v = schedule[it - 1]
-        gt.copy_(host[k], non_blocking=True)
-        loss = comm_step(rs, comm, wl.cameras[v], gt, it)
-        lh.copy_(loss, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        _ = float(lh[0])
-    e1.record()
-    torch.cuda.synchronize()
-    ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    comm.max_(ems)
-    if rank == 0:
-        from bench import METRIC, UNIT, workload_config
-        line = {
-            "metric": METRIC, "value": 1000.0 / ms_per_step, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic gyroid isosurface; GT = quantize8(raycast_isosurface) on the GPU (the reference dataset recipe, 8-bit codes)",
-            "config": workload_config(args.config, n, res, len(wl.cameras)),
-            "e2e": {"value": 1000.0 * args.steps / float(ems[0]), "unit": UNIT,
-                    "h2d_bytes_per_step": int(gt.numel()), "d2h_bytes_per_step": 8},
-            "clocks": clk.summary(), "gpu_launches": 22 * args.steps,
-            "roofline": None, "cpu_baseline": None,
-            "partition": {"bands_tile_rows": part.band_rows, "shard_sizes": smap.sizes},
-            "phases_ms": phases,
-        }
-        print(json.dumps(line), flush=True)

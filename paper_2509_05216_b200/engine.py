@@ -366,6 +366,13 @@ class Trainer:
         """One training iteration on view `cam` with ground truth `gt`
         (H, W, 3) float32 on the device.  The loss lands in loss_slot (or
         self.loss_dev[it])."""
+        if it < 1:
+            raise ValueError(f"iteration must be >= 1, got {it}")  # optim.py:36-38
+        if loss_slot is None and it >= self.loss_dev.numel():
+            # resumed / extended runs: grow the per-iteration loss record
+            grown = torch.zeros(it + 1, dtype=torch.float64, device=self.device)
+            grown[:self.loss_dev.numel()] = self.loss_dev
+            self.loss_dev = grown
         r = self.r
         ctx = r.forward(self.cloud, cam)
         slot = loss_slot if loss_slot is not None else self.loss_dev[it:it + 1]
