@@ -316,6 +316,7 @@ def run_ours(args, world, rank, local):
         v = schedule[it - 1]
         tr.step(it, wl.cameras[v], wl.images_u8[v])
     torch.cuda.synchronize()
+    log(f"[ours] FP32 FMA probe: {measure_fp32_peak()}")
     # ---- device-timed region
     stream = torch.cuda.current_stream()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -425,8 +426,7 @@ def roofline(phases, c, n, config="config3"):
         return {"kernel": dom, "bound": "fp32", "achieved": achieved, "peak": fp32,
                 "unit": "TFLOP/s", "frac": achieved / fp32 if fp32 else None,
                 "traffic": traffic, "traffic_source": tsrc,
-                "peak_source": "FP32 FFMA peak 148 SM x 128 lanes x 2 x max "
-                "SM clock (no FP32 entry in MEASURED_PEAKS.json)",
+                "peak_source": fp32_peak_source(),
                 "algorithmic": f"{flops[dom]:.4g} flops per launch (SURVEY 8d)"}
     b = bytes_.get(dom)
     if b is None:
@@ -450,10 +450,62 @@ def ncu_traffic(kernel: str, config: str):
         return None, None
 
 
+_FP32 = {}
+
+
+def measure_fp32_peak() -> dict:
+    """FP32 FMA-pipe throughput measured on this GPU now (isg_probe_ffma:
+    8 independent FFMA chains per thread, 8 CTAs of 256 per SM): best of 10
+    launches (burst) and the mean of 200 back-to-back launches (sustained,
+    ~0.4 s, the state a kernel inside a long step runs in)."""
+    import torch
+    from paper_2509_05216_b200 import _lib as L
+    blocks, iters = 148 * 8, 2048
+    flops = blocks * 256 * iters * 16 * 8 * 2
+    out = torch.empty(blocks, dtype=torch.float32, device="cuda")
+    s = L.stream_ptr()
+    fn = L.lib().isg_probe_ffma
+
+    def launch():
+        L.check(fn(blocks, iters, L.ptr(out), s), "isg_probe_ffma")
+
+    launch()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(11)]
+    ev[0].record()
+    for k in range(10):
+        launch()
+        ev[k + 1].record()
+    torch.cuda.synchronize()
+    best = min(ev[k].elapsed_time(ev[k + 1]) for k in range(10))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(200):
+        launch()
+    b.record()
+    torch.cuda.synchronize()
+    mean = a.elapsed_time(b) / 200
+    _FP32.update({"burst_tflops": flops / (best * 1e-3) / 1e12,
+                  "sustained_tflops": flops / (mean * 1e-3) / 1e12})
+    return dict(_FP32)
+
+
 def fp32_peak():
+    """The roofline denominator of the raster kernels: the measured sustained
+    FFMA rate when bench.py has probed it, else 148 SM x 128 lanes x 2 x max
+    clock."""
+    if "sustained_tflops" in _FP32:
+        return _FP32["sustained_tflops"]
     peaks, _ = read_peaks()
     mhz = peaks.get("sm_max_mhz", 1965.0)
     return 148 * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def fp32_peak_source() -> str:
+    if "sustained_tflops" in _FP32:
+        return ("measured in this run: isg_probe_ffma, mean of 200 back-to-back launches "
+                f"(burst {_FP32['burst_tflops']:.2f} TFLOP/s)")
+    return "FP32 FFMA peak 148 SM x 128 lanes x 2 x max SM clock (not measured)"
 
 
 def end_to_end(tr, wl, schedule, args):
@@ -696,6 +748,7 @@ def run_dist(args, world: int, rank: int, local: int):
         v = schedule[it - 1]
         D.comm_step(rs, comm, wl.cameras[v], wl.images_u8[v], it)
     torch.cuda.synchronize()
+    say(f"[dist] FP32 FMA probe (rank 0): {measure_fp32_peak()}")
     dist.barrier()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -765,7 +818,7 @@ def run_dist(args, world: int, rank: int, local: int):
                 "peak": fp32, "unit": "TFLOP/s", "frac": slow["raster_bwd_frac"],
                 "traffic": None, "rank": slow["rank"],
                 "algorithmic": "13 I_b + 55 C flops over the rank's band (SURVEY 8d)",
-                "peak_source": "FP32 FFMA peak 148 SM x 128 lanes x 2 x max SM clock",
+                "peak_source": fp32_peak_source(),
                 "per_rank": [{"rank": r["rank"], "achieved": r["raster_bwd_tflops"],
                               "frac": r["raster_bwd_frac"]} for r in per_rank]}
         line = {

@@ -378,6 +378,13 @@ int isg_adam_groups(int32_t count, float *const *p, const float *const *g, float
 /* glibc-exact exp over an array (verification hook for the key path). */
 int isg_exp_f64(int64_t n, const double *x, double *y, void *stream);
 
+/* FP32 FMA-pipe throughput probe (the measured roofline denominator of the
+ * raster kernels): `blocks` x 256 threads, each running 8 independent
+ * fma.rn.f32 chains for iters x 16 steps (blocks * 256 * iters * 256 flops).
+ * `out` (blocks floats) is never written in practice.  Not a reference
+ * interface: measurement support for bench.py. */
+int isg_probe_ffma(int32_t blocks, int32_t iters, float *out, void *stream);
+
 /* Library identification: returns a static string (arch, build flags). */
 const char *isg_version(void);
 

@@ -115,6 +115,7 @@ SIGNATURES = {
                                _P, _P, _P, _P, _P, _P, _D, _D, _P],
     "isg_adam_groups": [_I32, _P, _P, _P, _P, _P, _P, ctypes.POINTER(AdamConsts_t), _P],
     "isg_exp_f64": [_I64, _P, _P, _P],
+    "isg_probe_ffma": [_I32, _I32, _P, _P],
     "isg_knn_mean_grid": [_P, _SZ, _P, _I64, _I32, _P, _D, _I64, _I64, _I64, _P, _P],
     "isg_raycast": [_P, _P, _P, _P, _D, ctypes.POINTER(Camera_t), _D, _I32, _P, _P, _P, _P, _P],
     "isg_iso_edges": [_P, _SZ, _P, _P, _I32, _I32, _D, _P, _P, _P],

@@ -34,6 +34,7 @@ SOURCES = {
     "knn.cu": ["-fmad=false"],
     "chain_f32.cu": [],
     "volume.cu": ["-fmad=false"],
+    "probe.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
