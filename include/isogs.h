@@ -105,7 +105,13 @@ int isg_sort_u32(void *workspace, size_t *ws_bytes, const uint32_t *keys_in,
  * (the caller's own tiles; all rows for one GPU).  order[r] = row of rank r
  * (the sorted values); ranks whose sorted key is ~0 are culled (0 tiles).
  * emit_off has n+1 entries (exclusive scan); counts[0] = visible ranks M,
- * counts[1] = total entries E (int64, device).  Workspace as above. */
+ * counts[1] = total entries E (int64, device).  Workspace as above.
+ * isg_bin_count_rows: the same over the 64-byte payload rows of received
+ * splat records (rect, 12 float32 features; isg_route_pack), float32. */
+int isg_bin_count_rows(void *workspace, size_t *ws_bytes, int64_t n, const uint64_t *sorted_keys,
+                       const int32_t *order, const int32_t *payload, int32_t row_lo,
+                       int32_t row_hi, int32_t *rect_sorted, float *feat_sorted, int64_t *emit_off,
+                       int64_t *counts, void *stream);
 int isg_bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_t *sorted_keys,
                   const int32_t *order, const int32_t *rect, const void *feat,
                   int32_t feat_dtype, int32_t row_lo, int32_t row_hi, int32_t *rect_sorted,
@@ -271,43 +277,54 @@ int isg_reduce_ordered(int32_t feat_dtype, int64_t m, const int64_t *emit_off,
 int isg_scan_i64(void *workspace, size_t *ws_bytes, int64_t n, const int64_t *cnt, int64_t *off,
                  int64_t *total, void *stream);
 
-/* Per visible shard row: number of bands its rect overlaps and the first one
- * (_route_mask, _kernels.py:378-394, for row bands). */
-int isg_route_count(int64_t n, const uint8_t *flag, const int32_t *rect, const int32_t *band_rows,
-                    int32_t n_bands, int64_t *cnt, int32_t *dlo, void *stream);
+/* Route plan of a shard: per plan block of 256 rows and per band, the
+ * exclusive prefixes of the rows' splat records (1 per band reached) and
+ * canonical-block gradient records (blocks of canon_rows tile rows inside the
+ * band), plus per-band totals[3 * d + {0, 1, 2}] = (splat records, block
+ * records, tile entries).  A visible row reaches the contiguous band range its
+ * rect's tile rows overlap (_route_mask, _kernels.py:378-394, for row bands).
+ * plan holds isg_route_plan_size() int64 elements. */
+int isg_route_plan_size(int64_t n, int32_t n_bands, int64_t *plan_elems);
+int isg_route_plan(int64_t n, const uint8_t *flag, const int32_t *rect, const int32_t *band_rows,
+                   int32_t n_bands, int32_t canon_rows, int64_t *plan, int64_t *totals,
+                   void *stream);
 
-/* (band, row) pairs in row order at off[row] (then stably sorted by band). */
-int isg_route_emit(int64_t n, const int64_t *off, const int32_t *dlo, uint32_t *keys,
-                   int32_t *vals, void *stream);
+/* Splat records (the reference's mailbox `splats`, engine.py:201-215): for
+ * each band d a row reaches, its depth key at keys[dest_off[d] + j] and a
+ * 64-byte payload (rect, 12 float32 raster features) at pay[...], j = the
+ * row's rank among the shard rows reaching d (shard row order).  Band
+ * self_band's records go to keys_self / pay_self (this rank's receive
+ * buffers), every other band's to keys_send / pay_send.  dest_off: HOST. */
+int isg_route_pack(int64_t n, const uint8_t *flag, const int32_t *rect, const uint64_t *key,
+                   const float *feat, const int32_t *band_rows, int32_t n_bands,
+                   const int64_t *plan, const int64_t *dest_off, int32_t self_band,
+                   uint64_t *keys_send, int32_t *pay_send, uint64_t *keys_self,
+                   int32_t *pay_self, void *stream);
 
-/* Pack the routed rows into 80-byte splat records (20 x int32): depth key,
- * global id (id_base + row), rect, 12 raster features (float32). */
-int isg_route_gather(int64_t s, const int32_t *rows, const uint64_t *key, const int32_t *rect,
-                     const float *feat, int64_t id_base, int32_t *records, void *stream);
-
-/* Unpack received splat records into SoA arrays. */
-int isg_records_unpack(int64_t r, const int32_t *records, uint64_t *key, int32_t *gid,
-                       int32_t *rect, float *feat, void *stream);
-
-/* Number of canonical blocks (canon_rows tile rows) each rank's clipped rect
- * spans inside [row_lo, row_hi). */
-int isg_block_count(int64_t m, const int32_t *rect_sorted, int32_t row_lo, int32_t row_hi,
+/* Canonical blocks (canon_rows tile rows) of each received splat's rect
+ * inside the band [row_lo, row_hi) (payload rows as isg_route_pack). */
+int isg_band_blocks(int64_t r, const int32_t *payload, int32_t row_lo, int32_t row_hi,
                     int32_t canon_rows, int64_t *nb, void *stream);
 
-/* Per rank: fold its subtotals per canonical block (float64) into records at
- * rec_off[r] + b with the owner shard (of gid[order[r]]), owner-local row and
- * the 9 block sums.  The owner's in-order sum of these records equals the
- * canonical two-level fold of isg_reduce_ordered bit for bit. */
-int isg_block_fold(int32_t feat_dtype, int64_t m, const int64_t *emit_off, const void *partials,
-                   const int32_t *rect_sorted, int32_t row_lo, int32_t row_hi,
-                   int32_t canon_rows, const int64_t *rec_off, const int32_t *order,
-                   const int32_t *gid, const int64_t *shard_start, int32_t n_shards,
-                   uint32_t *rec_owner, int32_t *rec_row, double *rec_val, void *stream);
+/* Band fold (the per-tile GradChunks of engine.py:256-284, pre-folded):
+ * rank r's float32 subtotals folded per canonical block (float64, tiles
+ * ascending) into 9-double records at gbuf[9 * (gpos[order[r]] + b)] --
+ * records by receive index, so each source rank's segment is its own rows'
+ * records in its shard row order. */
+int isg_band_fold(int64_t m, const int64_t *emit_off, const float *partials,
+                  const int32_t *rect_sorted, const int32_t *order, const int64_t *gpos,
+                  int32_t row_lo, int32_t canon_rows, double *gbuf, void *stream);
 
-/* Pack block records (in idx order) into 80-byte gradient records
- * [row, 0, 9 doubles]. */
-int isg_grad_gather(int64_t s, const int32_t *idx, const int32_t *rec_row, const double *rec_val,
-                    int32_t *out, void *stream);
+/* Owner fold over the route plan (reduce_gradients_fused,
+ * distributed.py:178-226): per shard row, the block records of the bands it
+ * reached (seg[d]: HOST array of device pointers to band d's records for
+ * this shard) summed bands ascending, blocks ascending, in float64 -- the
+ * canonical two-level fold, bit-identical to isg_reduce_ordered with
+ * canon_rows.  Rows not visible get zeros. */
+int isg_owner_fold_plan(int64_t n, const uint8_t *flag, const int32_t *rect,
+                        const int32_t *band_rows, int32_t n_bands, int32_t canon_rows,
+                        const int64_t *plan, const double *const *seg, double *grad2d,
+                        void *stream);
 
 /* Keys (owner-local rows) and identity values of received gradient records. */
 int isg_grad_rows(int64_t r, const int32_t *records, uint32_t *rows, int32_t *idx, void *stream);

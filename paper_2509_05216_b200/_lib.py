@@ -69,6 +69,7 @@ SIGNATURES = {
     "isg_sort_u64": [_P, _SZ, _P, _P, _P, _P, _I64, _I32, _I32, _P],
     "isg_sort_u32": [_P, _SZ, _P, _P, _P, _P, _I64, _I32, _I32, _P],
     "isg_sort_depth": [_P, _SZ, _P, _P, _P, _P, _I64, _P],
+    "isg_bin_count_rows": [_P, _SZ, _I64, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P],
     "isg_bin_count": [_P, _SZ, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P],
     "isg_bin_emit16_cull": [_I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P],
     "isg_bin_emit": [_I64, _P, _P, _I32, _I32, _I32, _P, _P, _P],
@@ -94,14 +95,12 @@ SIGNATURES = {
                       _P],
     "isg_loss_finish": [_I32, _I32, _D, _P, _P, _P, _P],
     "isg_scan_i64": [_P, _SZ, _I64, _P, _P, _P, _P],
-    "isg_route_count": [_I64, _P, _P, _P, _I32, _P, _P, _P],
-    "isg_route_emit": [_I64, _P, _P, _P, _P, _P],
-    "isg_route_gather": [_I64, _P, _P, _P, _P, _I64, _P, _P],
-    "isg_records_unpack": [_I64, _P, _P, _P, _P, _P, _P],
-    "isg_block_count": [_I64, _P, _I32, _I32, _I32, _P, _P],
-    "isg_block_fold": [_I32, _I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _I32, _P, _P,
-                       _P, _P],
-    "isg_grad_gather": [_I64, _P, _P, _P, _P, _P],
+    "isg_route_plan_size": [_I64, _I32, _P],
+    "isg_route_plan": [_I64, _P, _P, _P, _I32, _I32, _P, _P, _P],
+    "isg_route_pack": [_I64, _P, _P, _P, _P, _P, _I32, _P, _P, _I32, _P, _P, _P, _P, _P],
+    "isg_band_blocks": [_I64, _P, _I32, _I32, _I32, _P, _P],
+    "isg_band_fold": [_I64, _P, _P, _P, _P, _P, _I32, _I32, _P, _P],
+    "isg_owner_fold_plan": [_I64, _P, _P, _P, _I32, _I32, _P, _P, _P, _P],
     "isg_grad_rows": [_I64, _P, _P, _P, _P],
     "isg_owner_fold": [_I64, _P, _P, _P, _P, _P],
     "isg_chain": [ctypes.POINTER(Params_t), ctypes.POINTER(Camera_t), _P, _P, _P, _P, _P, _P,

@@ -18,9 +18,9 @@ namespace isg {
 
 __global__ void __launch_bounds__(256) gather_rank_kernel(
     int64_t n, const uint64_t *__restrict__ sorted_keys, const int32_t *__restrict__ order,
-    const int4 *__restrict__ rect, const float4 *__restrict__ feat, int feat_vec4,
-    int row_lo, int row_hi, int4 *__restrict__ rect_sorted, float4 *__restrict__ feat_sorted,
-    int64_t *__restrict__ cnt, int64_t *__restrict__ counts) {
+    const int4 *__restrict__ rect, int rect_stride4, const float4 *__restrict__ feat,
+    int feat_stride4, int feat_vec4, int row_lo, int row_hi, int4 *__restrict__ rect_sorted,
+    float4 *__restrict__ feat_sorted, int64_t *__restrict__ cnt, int64_t *__restrict__ counts) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const uint64_t key = sorted_keys[r];
@@ -28,10 +28,10 @@ __global__ void __launch_bounds__(256) gather_rank_kernel(
     int64_t c = 0;
     if (vis) {
         const int32_t row = order[r];
-        int4 rc = rect[row];
+        int4 rc = rect[(int64_t)rect_stride4 * row];
         rect_sorted[r] = rc;
         for (int j = 0; j < feat_vec4; j++) feat_sorted[(int64_t)feat_vec4 * r + j] =
-            feat[(int64_t)feat_vec4 * row + j];
+            feat[(int64_t)feat_stride4 * row + j];
         int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
         if (y1 >= y0) c = (int64_t)(rc.z - rc.x + 1) * (int64_t)(y1 - y0 + 1);
         if (r + 1 == n || sorted_keys[r + 1] == ~0ull) counts[0] = r + 1;
@@ -253,12 +253,11 @@ extern "C" int isg_sort_u32(void *workspace, size_t *ws_bytes, const uint32_t *k
     return (int)e;
 }
 
-extern "C" int isg_bin_count(void *workspace, size_t *ws_bytes, int64_t n,
-                             const uint64_t *sorted_keys, const int32_t *order,
-                             const int32_t *rect, const void *feat, int32_t feat_dtype,
-                             int32_t row_lo, int32_t row_hi, int32_t *rect_sorted,
-                             void *feat_sorted, int64_t *emit_off, int64_t *counts,
-                             void *stream) {
+static int bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_t *sorted_keys,
+                     const int32_t *order, const int4 *rect, int rect_stride4,
+                     const float4 *feat, int feat_stride4, int vec4, int32_t row_lo,
+                     int32_t row_hi, int32_t *rect_sorted, void *feat_sorted, int64_t *emit_off,
+                     int64_t *counts, void *stream) {
     if (!ws_bytes || n < 0 || n > INT32_MAX || row_lo < 0 || row_hi < row_lo)
         return (int)cudaErrorInvalidValue;
     size_t scan_bytes = 0;
@@ -278,9 +277,8 @@ extern "C" int isg_bin_count(void *workspace, size_t *ws_bytes, int64_t n,
     if (n == 0) return 0;
     int64_t *cnt = (int64_t *)workspace;
     void *scan_ws = (char *)workspace + align_up(sizeof(int64_t) * (size_t)n);
-    const int vec4 = feat_dtype == ISG_F64 ? 6 : 3;  // 12 values per splat
     gather_rank_kernel<<<blocks_for(n, 256), 256, 0, s>>>(
-        n, sorted_keys, order, (const int4 *)rect, (const float4 *)feat, vec4, row_lo, row_hi,
+        n, sorted_keys, order, rect, rect_stride4, feat, feat_stride4, vec4, row_lo, row_hi,
         (int4 *)rect_sorted, (float4 *)feat_sorted, cnt, counts);
     ISG_CHECK_LAUNCH();
     e = cub::DeviceScan::InclusiveSum(scan_ws, scan_bytes, cnt, emit_off + 1, (int)n, s);
@@ -288,6 +286,30 @@ extern "C" int isg_bin_count(void *workspace, size_t *ws_bytes, int64_t n,
     finish_counts_kernel<<<1, 1, 0, s>>>(n, emit_off, counts);
     ISG_CHECK_LAUNCH();
     return 0;
+}
+
+extern "C" int isg_bin_count(void *workspace, size_t *ws_bytes, int64_t n,
+                             const uint64_t *sorted_keys, const int32_t *order,
+                             const int32_t *rect, const void *feat, int32_t feat_dtype,
+                             int32_t row_lo, int32_t row_hi, int32_t *rect_sorted,
+                             void *feat_sorted, int64_t *emit_off, int64_t *counts,
+                             void *stream) {
+    const int vec4 = feat_dtype == ISG_F64 ? 6 : 3;  // 12 values per splat
+    return bin_count(workspace, ws_bytes, n, sorted_keys, order, (const int4 *)rect, 1,
+                     (const float4 *)feat, vec4, vec4, row_lo, row_hi, rect_sorted, feat_sorted,
+                     emit_off, counts, stream);
+}
+
+extern "C" int isg_bin_count_rows(void *workspace, size_t *ws_bytes, int64_t n,
+                                  const uint64_t *sorted_keys, const int32_t *order,
+                                  const int32_t *payload, int32_t row_lo, int32_t row_hi,
+                                  int32_t *rect_sorted, float *feat_sorted, int64_t *emit_off,
+                                  int64_t *counts, void *stream) {
+    // 64-byte payload rows: rect (4 x int32) then the 12 float32 features
+    const int4 *p = (const int4 *)payload;
+    return bin_count(workspace, ws_bytes, n, sorted_keys, order, p, 4,
+                     (const float4 *)(p ? p + 1 : nullptr), 4, 3, row_lo, row_hi, rect_sorted,
+                     feat_sorted, emit_off, counts, stream);
 }
 
 namespace isg {

@@ -44,146 +44,421 @@ __device__ __forceinline__ int band_of(const Bands &b, int row) {
     return lo;
 }
 
-__global__ void route_count_kernel(int64_t n, const uint8_t *__restrict__ flag,
-                                   const int4 *__restrict__ rect, Bands bands,
-                                   int64_t *__restrict__ cnt, int32_t *__restrict__ dlo) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int64_t c = 0;
-    int lo = 0;
-    if (flag[i]) {
-        const int4 rc = rect[i];
-        lo = band_of(bands, rc.y);
-        const int hi = band_of(bands, rc.w);
-        c = hi - lo + 1;
-    }
-    cnt[i] = c;
-    dlo[i] = lo;
+// ------------------------------------------------------------ routing --
+// A visible splat reaches the contiguous band range [lo, hi] its tile rect's
+// rows overlap.  Per band it carries three weights: 1 splat record, nb
+// canonical-block gradient records (blocks of `canon` tile rows inside the
+// band) and its tile entries in the band (the band's list length).
+__device__ __forceinline__ void splat_bands(const Bands &b, const int4 rc, int &lo, int &hi) {
+    lo = band_of(b, rc.y);
+    hi = band_of(b, rc.w);
 }
 
-__global__ void route_emit_kernel(int64_t n, const int64_t *__restrict__ off,
-                                  const int32_t *__restrict__ dlo, uint32_t *__restrict__ keys,
-                                  int32_t *__restrict__ vals) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int64_t o = off[i], c = off[i + 1] - o;
-    for (int64_t k = 0; k < c; k++) {
-        keys[o + k] = (uint32_t)(dlo[i] + k);
-        vals[o + k] = (int32_t)i;
-    }
-}
-
-// record: [key lo, key hi, gid, 0, rect x4, feat x12] as 20 x 32-bit words
-__global__ void route_gather_kernel(int64_t s, const int32_t *__restrict__ rows,
-                                    const uint64_t *__restrict__ key, const int4 *__restrict__ rect,
-                                    const int4 *__restrict__ feat, int64_t id_base,
-                                    int4 *__restrict__ rec) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= s) return;
-    const int64_t i = rows[k];
-    const uint64_t kk = key[i];
-    int4 *r = rec + 5 * k;
-    r[0] = make_int4((int)(uint32_t)kk, (int)(uint32_t)(kk >> 32), (int)(id_base + i), 0);
-    r[1] = rect[i];
-    r[2] = feat[3 * i];
-    r[3] = feat[3 * i + 1];
-    r[4] = feat[3 * i + 2];
-}
-
-__global__ void unpack_kernel(int64_t r, const int4 *__restrict__ rec, uint64_t *__restrict__ key,
-                              int32_t *__restrict__ gid, int4 *__restrict__ rect,
-                              int4 *__restrict__ feat) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= r) return;
-    const int4 *p = rec + 5 * k;
-    const int4 h = p[0];
-    key[k] = (uint64_t)(uint32_t)h.x | ((uint64_t)(uint32_t)h.y << 32);
-    gid[k] = h.z;
-    rect[k] = p[1];
-    feat[3 * k] = p[2];
-    feat[3 * k + 1] = p[3];
-    feat[3 * k + 2] = p[4];
-}
-
-__global__ void block_count_kernel(int64_t m, const int4 *__restrict__ rect_sorted, int row_lo,
-                                   int row_hi, int canon, int64_t *__restrict__ nb) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= m) return;
-    const int4 rc = rect_sorted[r];
-    const int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
-    nb[r] = y1 >= y0 ? (int64_t)(y1 / canon - y0 / canon + 1) : 0;
-}
-
-struct Shards {
-    int n;
-    int64_t start[MAX_BANDS + 1];  // global id boundaries of the Gaussian shards
+struct BandWeights {
+    int64_t nb, tiles;
 };
 
-__device__ __forceinline__ int shard_of(const Shards &s, int64_t gid) {
-    int lo = 0, hi = s.n - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s.start[mid] <= gid) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
+__device__ __forceinline__ BandWeights band_weights(const Bands &b, const int4 rc, int d,
+                                                    int canon) {
+    const int y0 = max(rc.y, b.start[d]), y1 = min(rc.w, b.start[d + 1] - 1);
+    BandWeights w;
+    w.nb = (int64_t)(y1 / canon - y0 / canon + 1);
+    w.tiles = (int64_t)(rc.z - rc.x + 1) * (int64_t)(y1 - y0 + 1);
+    return w;
 }
 
-// Per rank r: fold its slots [emit_off[r], emit_off[r+1]) per canonical block
-// (float64) into records rec_off[r] + b: owner shard (sort key), owner-local
-// row and the 9 block sums.
-template <typename T>
-__global__ void block_fold_kernel(int64_t m, const int64_t *__restrict__ emit_off,
-                                  const T *__restrict__ partials,
-                                  const int4 *__restrict__ rect_sorted, int row_lo, int row_hi,
-                                  int canon, const int64_t *__restrict__ rec_off,
-                                  const int32_t *__restrict__ order,
-                                  const int32_t *__restrict__ gid, Shards shards,
-                                  uint32_t *__restrict__ rec_owner, int32_t *__restrict__ rec_row,
-                                  double *__restrict__ rec_val) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= m) return;
-    const int4 rc = rect_sorted[r];
+constexpr int PLAN_T = 256;  // shard rows per plan block (route_plan/pack, owner_fold)
+
+// Per plan block and band: (splat records, block records) in plan[blk][d][0..1]
+// and the tile entries in tiles_blk[blk][d].  Bands are visited over the
+// block's band range with warp reductions (no contended shared atomics).
+__global__ void __launch_bounds__(PLAN_T) route_plan_kernel(int64_t n,
+                                                            const uint8_t *__restrict__ flag,
+                                                            const int4 *__restrict__ rect,
+                                                            Bands bands, int canon,
+                                                            int64_t *__restrict__ plan,
+                                                            int64_t *__restrict__ tiles_blk) {
+    __shared__ long long s_w[3][PLAN_T / 32];
+    __shared__ int s_lo, s_hi;
+    const int nbands = bands.n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * PLAN_T + threadIdx.x;
+    int lo = nbands, hi = -1;
+    int4 rc = make_int4(0, 0, -1, -1);
+    if (i < n && flag[i]) {
+        rc = rect[i];
+        splat_bands(bands, rc, lo, hi);
+    }
+    if (threadIdx.x == 0) {
+        s_lo = nbands;
+        s_hi = -1;
+    }
+    __syncthreads();
+    if (hi >= lo) {
+        atomicMin(&s_lo, lo);
+        atomicMax(&s_hi, hi);
+    }
+    __syncthreads();
+    const int blo = s_lo, bhi = s_hi;
+    int64_t *pb = plan + 2 * (int64_t)blockIdx.x * nbands;
+    int64_t *tb = tiles_blk + (int64_t)blockIdx.x * nbands;
+    for (int d = threadIdx.x; d < nbands; d += PLAN_T) {
+        if (d < blo || d > bhi) {
+            pb[2 * d] = pb[2 * d + 1] = 0;
+            tb[d] = 0;
+        }
+    }
+    for (int d = blo; d <= bhi; d++) {
+        long long c = 0, nb = 0, t = 0;
+        if (lo <= d && d <= hi) {
+            const BandWeights w = band_weights(bands, rc, d, canon);
+            c = 1;
+            nb = w.nb;
+            t = w.tiles;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+            nb += __shfl_xor_sync(0xffffffffu, nb, o);
+            t += __shfl_xor_sync(0xffffffffu, t, o);
+        }
+        if (lane == 0) {
+            s_w[0][warp] = c;
+            s_w[1][warp] = nb;
+            s_w[2][warp] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+            for (int w = 0; w < PLAN_T / 32; w++) {
+                a0 += s_w[0][w];
+                a1 += s_w[1][w];
+                a2 += s_w[2][w];
+            }
+            pb[2 * d] = a0;
+            pb[2 * d + 1] = a1;
+            tb[d] = a2;
+        }
+        __syncthreads();
+    }
+}
+
+// One CTA per band: exclusive prefix over the plan blocks of the two record
+// counts (in place) and the band totals (records, block records, tiles).
+__global__ void __launch_bounds__(1024) route_scan_kernel(int64_t nblk, int nbands,
+                                                          int64_t *__restrict__ plan,
+                                                          const int64_t *__restrict__ tiles_blk,
+                                                          int64_t *__restrict__ totals) {
+    typedef cub::BlockScan<long long, 1024> Scan;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ long long s_tiles[32];
+    const int d = blockIdx.x;
+    long long carry0 = 0, carry1 = 0, tiles = 0;
+    for (int64_t c = 0; c < nblk; c += 1024) {
+        const int64_t b = c + threadIdx.x;
+        int64_t *p = plan + 2 * (b * nbands + d);
+        const long long v0 = b < nblk ? p[0] : 0, v1 = b < nblk ? p[1] : 0;
+        tiles += b < nblk ? tiles_blk[b * nbands + d] : 0;
+        long long e0, e1, t0, t1;
+        Scan(tmp).ExclusiveSum(v0, e0, t0);
+        __syncthreads();
+        Scan(tmp).ExclusiveSum(v1, e1, t1);
+        __syncthreads();
+        if (b < nblk) {
+            p[0] = carry0 + e0;
+            p[1] = carry1 + e1;
+        }
+        carry0 += t0;
+        carry1 += t1;
+    }
+    for (int o = 16; o > 0; o >>= 1) tiles += __shfl_xor_sync(0xffffffffu, tiles, o);
+    if ((threadIdx.x & 31) == 0) s_tiles[threadIdx.x >> 5] = tiles;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < 32; w++) t += s_tiles[w];
+        totals[3 * d] = carry0;
+        totals[3 * d + 1] = carry1;
+        totals[3 * d + 2] = t;
+    }
+}
+
+// In-block exclusive prefix of `v` over the CTA's threads (thread order =
+// shard row order); `total` is the CTA total.  All threads must call.
+template <int T>
+__device__ __forceinline__ int64_t block_excl(int64_t v, int64_t *s_warp, int64_t &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    int64_t before = 0;
+    total = 0;
+#pragma unroll
+    for (int w = 0; w < T / 32; w++) {
+        const int64_t t = s_warp[w];
+        if (w < warp) before += t;
+        total += t;
+    }
+    __syncthreads();
+    return before + x - v;
+}
+
+struct PackDest {
+    int64_t off[MAX_BANDS];  // base slot of each band's segment in its buffer
+    int self;                // the band whose records go to the self buffers
+};
+
+// Splat records of every visible shard row for each band it reaches, in
+// shard row order inside each band's segment: the depth key (8 B) and a
+// 64-byte payload (rect, 12 raster features).  The self band's segment is
+// written straight into this rank's receive buffers.
+__global__ void __launch_bounds__(PLAN_T) route_pack_kernel(
+    int64_t n, const uint8_t *__restrict__ flag, const int4 *__restrict__ rect,
+    const uint64_t *__restrict__ key, const int4 *__restrict__ feat, Bands bands,
+    const int64_t *__restrict__ plan, PackDest dst, uint64_t *__restrict__ keys_send,
+    int4 *__restrict__ pay_send, uint64_t *__restrict__ keys_self, int4 *__restrict__ pay_self) {
+    __shared__ int64_t s_warp[PLAN_T / 32];
+    __shared__ int s_lo, s_hi;
+    const int nbands = bands.n;
+    const int64_t i = (int64_t)blockIdx.x * PLAN_T + threadIdx.x;
+    int lo = nbands, hi = -1;
+    int4 rc = make_int4(0, 0, -1, -1);
+    if (i < n && flag[i]) {
+        rc = rect[i];
+        splat_bands(bands, rc, lo, hi);
+    }
+    if (threadIdx.x == 0) {
+        s_lo = nbands;
+        s_hi = -1;
+    }
+    __syncthreads();
+    if (hi >= lo) {
+        atomicMin(&s_lo, lo);
+        atomicMax(&s_hi, hi);
+    }
+    __syncthreads();
+    const int blo = s_lo, bhi = s_hi;
+    const int64_t *pb = plan + 2 * (int64_t)blockIdx.x * nbands;
+    for (int d = blo; d <= bhi; d++) {
+        const bool on = lo <= d && d <= hi;
+        int64_t tot;
+        const int64_t ex = block_excl<PLAN_T>(on ? 1 : 0, s_warp, tot);
+        if (on) {
+            const int64_t slot = dst.off[d] + pb[2 * d] + ex;
+            uint64_t *kk = d == dst.self ? keys_self : keys_send;
+            int4 *pp = (d == dst.self ? pay_self : pay_send) + 4 * slot;
+            kk[slot] = key[i];
+            pp[0] = rc;
+            pp[1] = feat[3 * i];
+            pp[2] = feat[3 * i + 1];
+            pp[3] = feat[3 * i + 2];
+        }
+    }
+}
+
+// Canonical blocks of each received splat inside the band.
+__global__ void band_blocks_kernel(int64_t r, const int4 *__restrict__ pay, int row_lo,
+                                   int row_hi, int canon, int64_t *__restrict__ nb) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= r) return;
+    const int4 rc = pay[4 * k];
     const int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
-    if (y1 < y0) return;
-    const int64_t p0 = emit_off[r], w = rc.z - rc.x + 1;
-    const int64_t g = gid[order[r]];
-    const int owner = shard_of(shards, g);
-    const int32_t row = (int32_t)(g - shards.start[owner]);
-    int64_t o = rec_off[r];
-    for (int b = y0 / canon; b <= y1 / canon; b++, o++) {
-        const int ys = max(y0, b * canon), ye = min(y1, b * canon + canon - 1);
-        double bs[9];
+    nb[k] = y1 >= y0 ? (int64_t)(y1 / canon - y0 / canon + 1) : 0;
+}
+// ------------------------------------------------------ gradient fold --
+// Band side: every rank's (tile, splat) subtotals are folded per canonical
+// block (tiles ascending inside the block, float64) and each block sum is
+// written as a 9-double record at gpos[order[r]] + b: records are laid out by
+// RECEIVE index, so the segment that goes back to source rank s is exactly
+// its splats in its shard row order.  Streaming as in reduce_ordered_f32:
+// every warp owns 32 consecutive ranks whose slots are one contiguous span,
+// staged through shared memory with TMA bulk copies (cp.async.bulk +
+// mbarrier, double buffered).
+constexpr int BF_WARPS = 4;
+constexpr int BF_THREADS = 32 * BF_WARPS;
+constexpr int BF_SLOTS = 96;
+
+__device__ __forceinline__ void bf_mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void bf_bulk_load(void *dst, const void *src, unsigned bytes,
+                                             uint64_t *bar) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"((unsigned)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void bf_mbar_wait(uint64_t *bar, unsigned parity) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(b), "r"(parity)
+            : "memory");
+    }
+}
+
+// One rank's block sums, emitted as they close (same arithmetic as FoldState).
+struct BlockEmit {
+    double bs[9];
+    int y, w, dx, canon;
+    bool open;
+    double *out;
+
+    __device__ __forceinline__ void init(int4 rc, int row_lo, int canon_rows, double *o) {
+        y = max(rc.y, row_lo);
+        w = rc.z - rc.x + 1;
+        dx = 0;
+        canon = canon_rows;
+        open = false;
+        out = o;
 #pragma unroll
         for (int k = 0; k < 9; k++) bs[k] = 0.0;
-        for (int64_t p = p0 + (ys - y0) * w; p < p0 + (ye - y0 + 1) * w; p++) {
-            const T *src = partials + partial_stride<T>() * p;
+    }
+    __device__ __forceinline__ void close() {
 #pragma unroll
-            for (int k = 0; k < 9; k++) bs[k] += (double)src[k];
+        for (int k = 0; k < 9; k++) {
+            out[k] = bs[k];
+            bs[k] = 0.0;
         }
-        rec_owner[o] = (uint32_t)owner;
-        rec_row[o] = row;
-        double *dst = rec_val + 9 * o;
+        out += 9;
+        open = false;
+    }
+    __device__ __forceinline__ void step(const float *v) {
 #pragma unroll
-        for (int k = 0; k < 9; k++) dst[k] = bs[k];
+        for (int k = 0; k < 9; k++) bs[k] += (double)v[k];
+        open = true;
+        if (++dx == w) {
+            dx = 0;
+            y++;
+            if (y % canon == 0) close();
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        if (open) close();
+    }
+};
+
+__global__ void __launch_bounds__(BF_THREADS) band_fold_kernel(
+    int64_t m, const int64_t *__restrict__ emit_off, const float *__restrict__ partials,
+    const int4 *__restrict__ rect_sorted, const int32_t *__restrict__ order,
+    const int64_t *__restrict__ gpos, int row_lo, int canon, double *__restrict__ gbuf) {
+    constexpr int PS = partial_stride<float>();
+    __shared__ __align__(128) float sbuf[BF_WARPS][2][BF_SLOTS * PS];
+    __shared__ __align__(8) uint64_t sbar[BF_WARPS][2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r0 = ((int64_t)blockIdx.x * BF_WARPS + warp) * 32;
+    if (r0 >= m) return;
+    const int64_t r = r0 + lane;
+    const bool live = r < m;
+    const int64_t span0 = emit_off[r0];
+    const int64_t span1 = emit_off[min(r0 + 32, m)];
+    int64_t p = live ? emit_off[r] : 0;
+    const int64_t p1 = live ? emit_off[r + 1] : 0;
+    BlockEmit st;
+    st.init(live ? rect_sorted[r] : make_int4(0, 0, 0, 0), row_lo, canon,
+            live ? gbuf + 9 * gpos[order[r]] : gbuf);
+    const int nch = (int)((span1 - span0 + BF_SLOTS - 1) / BF_SLOTS);
+    float(*buf)[BF_SLOTS * PS] = sbuf[warp];
+    uint64_t *bar = sbar[warp];
+    auto issue = [&](int k) {
+        const int64_t c0 = span0 + (int64_t)k * BF_SLOTS;
+        const unsigned cnt = (unsigned)min((int64_t)BF_SLOTS, span1 - c0);
+        bf_bulk_load(buf[k & 1], partials + PS * c0, cnt * PS * (unsigned)sizeof(float),
+                     &bar[k & 1]);
+    };
+    if (lane == 0) {
+        bf_mbar_init(&bar[0], 1);
+        bf_mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (nch > 0) issue(0);
+        if (nch > 1) issue(1);
+    }
+    __syncwarp();
+    for (int k = 0; k < nch; k++) {
+        bf_mbar_wait(&bar[k & 1], (unsigned)((k >> 1) & 1));
+        const int64_t c0 = span0 + (int64_t)k * BF_SLOTS;
+        const int64_t e = min(p1, c0 + BF_SLOTS);
+        const float *b = buf[k & 1];
+        for (; p < e; p++) st.step(b + PS * (p - c0));
+        __syncwarp();
+        if (lane == 0 && k + 2 < nch) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(k + 2);
+        }
+    }
+    if (live) st.finish();
+}
+
+struct SegPtrs {
+    const double *seg[MAX_BANDS];  // band d's gradient records for this shard
+};
+
+// Owner side (reduce_gradients_fused, distributed.py:178-226): per shard row,
+// its block records from every band it reached, bands ascending then blocks
+// ascending -- the canonical two-level order -- summed in float64.  Record
+// positions come from the route plan (the same per-band prefix the band used
+// to lay them out), so nothing is sorted.  Rows not visible get zeros.
+__global__ void __launch_bounds__(PLAN_T) owner_fold_plan_kernel(
+    int64_t n, const uint8_t *__restrict__ flag, const int4 *__restrict__ rect, Bands bands,
+    int canon, const int64_t *__restrict__ plan, SegPtrs segs, double *__restrict__ grad2d) {
+    __shared__ int64_t s_warp[PLAN_T / 32];
+    __shared__ int s_lo, s_hi;
+    const int nbands = bands.n;
+    const int64_t i = (int64_t)blockIdx.x * PLAN_T + threadIdx.x;
+    int lo = nbands, hi = -1;
+    int4 rc = make_int4(0, 0, -1, -1);
+    if (i < n && flag[i]) {
+        rc = rect[i];
+        splat_bands(bands, rc, lo, hi);
+    }
+    if (threadIdx.x == 0) {
+        s_lo = nbands;
+        s_hi = -1;
+    }
+    __syncthreads();
+    if (hi >= lo) {
+        atomicMin(&s_lo, lo);
+        atomicMax(&s_hi, hi);
+    }
+    __syncthreads();
+    const int blo = s_lo, bhi = s_hi;
+    const int64_t *pb = plan + 2 * (int64_t)blockIdx.x * nbands;
+    double acc[9];
+#pragma unroll
+    for (int k = 0; k < 9; k++) acc[k] = 0.0;
+    for (int d = blo; d <= bhi; d++) {
+        const bool on = lo <= d && d <= hi;
+        const int64_t nb = on ? band_weights(bands, rc, d, canon).nb : 0;
+        int64_t tot;
+        const int64_t ex = block_excl<PLAN_T>(nb, s_warp, tot);
+        const double *src = segs.seg[d] + 9 * (pb[2 * d + 1] + ex);
+        for (int64_t b = 0; b < nb; b++) {
+#pragma unroll
+            for (int k = 0; k < 9; k++) acc[k] += src[9 * b + k];
+        }
+    }
+    if (i < n) {
+#pragma unroll
+        for (int k = 0; k < 9; k++) grad2d[9 * i + k] = acc[k];
     }
 }
-
-// grad record: [row, 0, 9 doubles] = 20 words
-__global__ void grad_gather_kernel(int64_t s, const int32_t *__restrict__ idx,
-                                   const int32_t *__restrict__ rec_row,
-                                   const double *__restrict__ rec_val, int32_t *__restrict__ out) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= s) return;
-    const int64_t i = idx[k];
-    int32_t *o = out + 20 * k;
-    o[0] = rec_row[i];
-    o[1] = 0;
-    double *d = reinterpret_cast<double *>(o + 2);
-#pragma unroll
-    for (int q = 0; q < 9; q++) d[q] = rec_val[9 * i + q];
-}
-
 __global__ void grad_rows_kernel(int64_t r, const int32_t *__restrict__ rec, uint32_t *__restrict__ rows,
                                  int32_t *__restrict__ idx) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -257,93 +532,91 @@ static int fill_bands(Bands &b, const int32_t *band_rows, int32_t n_bands) {
     return 0;
 }
 
-extern "C" int isg_route_count(int64_t n, const uint8_t *flag, const int32_t *rect,
-                               const int32_t *band_rows, int32_t n_bands, int64_t *cnt,
-                               int32_t *dlo, void *stream) {
+extern "C" int isg_route_plan_size(int64_t n, int32_t n_bands, int64_t *plan_elems) {
+    if (n < 0 || n_bands < 1 || n_bands > MAX_BANDS || !plan_elems)
+        return (int)cudaErrorInvalidValue;
+    const int64_t nblk = (n + PLAN_T - 1) / PLAN_T;
+    *plan_elems = 3 * nblk * n_bands;  // plan (2 per band) + tiles (1 per band)
+    return 0;
+}
+
+extern "C" int isg_route_plan(int64_t n, const uint8_t *flag, const int32_t *rect,
+                              const int32_t *band_rows, int32_t n_bands, int32_t canon_rows,
+                              int64_t *plan, int64_t *totals, void *stream) {
     Bands b;
-    if (n < 0 || fill_bands(b, band_rows, n_bands)) return (int)cudaErrorInvalidValue;
-    if (n == 0) return 0;
-    route_count_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
-        n, flag, (const int4 *)rect, b, cnt, dlo);
+    if (n < 0 || canon_rows < 1 || fill_bands(b, band_rows, n_bands) || !plan || !totals)
+        return (int)cudaErrorInvalidValue;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nblk = (n + PLAN_T - 1) / PLAN_T;
+    if (nblk == 0) {
+        cudaError_t e = cudaMemsetAsync(totals, 0, sizeof(int64_t) * 3 * n_bands, s);
+        return (int)e;
+    }
+    int64_t *tiles_blk = plan + 2 * nblk * n_bands;
+    route_plan_kernel<<<(unsigned)nblk, PLAN_T, 0, s>>>(n, flag, (const int4 *)rect, b,
+                                                        canon_rows, plan, tiles_blk);
+    ISG_CHECK_LAUNCH();
+    route_scan_kernel<<<n_bands, 1024, 0, s>>>(nblk, n_bands, plan, tiles_blk, totals);
     ISG_CHECK_LAUNCH();
     return 0;
 }
 
-extern "C" int isg_route_emit(int64_t n, const int64_t *off, const int32_t *dlo, uint32_t *keys,
-                              int32_t *vals, void *stream) {
-    if (n < 0) return (int)cudaErrorInvalidValue;
-    if (n == 0) return 0;
-    route_emit_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, off, dlo, keys,
-                                                                            vals);
+extern "C" int isg_route_pack(int64_t n, const uint8_t *flag, const int32_t *rect,
+                              const uint64_t *key, const float *feat, const int32_t *band_rows,
+                              int32_t n_bands, const int64_t *plan, const int64_t *dest_off,
+                              int32_t self_band, uint64_t *keys_send, int32_t *pay_send,
+                              uint64_t *keys_self, int32_t *pay_self, void *stream) {
+    Bands b;
+    if (n < 0 || fill_bands(b, band_rows, n_bands) || !dest_off || self_band < -1 ||
+        self_band >= n_bands)
+        return (int)cudaErrorInvalidValue;
+    const int64_t nblk = (n + PLAN_T - 1) / PLAN_T;
+    if (nblk == 0) return 0;
+    PackDest dst;
+    for (int d = 0; d < n_bands; d++) dst.off[d] = dest_off[d];
+    dst.self = self_band;
+    route_pack_kernel<<<(unsigned)nblk, PLAN_T, 0, (cudaStream_t)stream>>>(
+        n, flag, (const int4 *)rect, key, (const int4 *)feat, b, plan, dst, keys_send,
+        (int4 *)pay_send, keys_self, (int4 *)pay_self);
     ISG_CHECK_LAUNCH();
     return 0;
 }
 
-extern "C" int isg_route_gather(int64_t s, const int32_t *rows, const uint64_t *key,
-                                const int32_t *rect, const float *feat, int64_t id_base,
-                                int32_t *records, void *stream) {
-    if (s < 0) return (int)cudaErrorInvalidValue;
-    if (s == 0) return 0;
-    route_gather_kernel<<<blocks_for(s, 256), 256, 0, (cudaStream_t)stream>>>(
-        s, rows, key, (const int4 *)rect, (const int4 *)feat, id_base, (int4 *)records);
-    ISG_CHECK_LAUNCH();
-    return 0;
-}
-
-extern "C" int isg_records_unpack(int64_t r, const int32_t *records, uint64_t *key, int32_t *gid,
-                                  int32_t *rect, float *feat, void *stream) {
-    if (r < 0) return (int)cudaErrorInvalidValue;
+extern "C" int isg_band_blocks(int64_t r, const int32_t *payload, int32_t row_lo, int32_t row_hi,
+                               int32_t canon_rows, int64_t *nb, void *stream) {
+    if (r < 0 || canon_rows < 1) return (int)cudaErrorInvalidValue;
     if (r == 0) return 0;
-    unpack_kernel<<<blocks_for(r, 256), 256, 0, (cudaStream_t)stream>>>(
-        r, (const int4 *)records, key, gid, (int4 *)rect, (int4 *)feat);
+    band_blocks_kernel<<<blocks_for(r, 256), 256, 0, (cudaStream_t)stream>>>(
+        r, (const int4 *)payload, row_lo, row_hi, canon_rows, nb);
     ISG_CHECK_LAUNCH();
     return 0;
 }
 
-extern "C" int isg_block_count(int64_t m, const int32_t *rect_sorted, int32_t row_lo,
-                               int32_t row_hi, int32_t canon_rows, int64_t *nb, void *stream) {
+extern "C" int isg_band_fold(int64_t m, const int64_t *emit_off, const float *partials,
+                             const int32_t *rect_sorted, const int32_t *order,
+                             const int64_t *gpos, int32_t row_lo, int32_t canon_rows,
+                             double *gbuf, void *stream) {
     if (m < 0 || canon_rows < 1) return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
-    block_count_kernel<<<blocks_for(m, 256), 256, 0, (cudaStream_t)stream>>>(
-        m, (const int4 *)rect_sorted, row_lo, row_hi, canon_rows, nb);
+    band_fold_kernel<<<blocks_for(m, BF_THREADS), BF_THREADS, 0, (cudaStream_t)stream>>>(
+        m, emit_off, partials, (const int4 *)rect_sorted, order, gpos, row_lo, canon_rows, gbuf);
     ISG_CHECK_LAUNCH();
     return 0;
 }
 
-extern "C" int isg_block_fold(int32_t feat_dtype, int64_t m, const int64_t *emit_off,
-                              const void *partials, const int32_t *rect_sorted, int32_t row_lo,
-                              int32_t row_hi, int32_t canon_rows, const int64_t *rec_off,
-                              const int32_t *order, const int32_t *gid,
-                              const int64_t *shard_start, int32_t n_shards, uint32_t *rec_owner,
-                              int32_t *rec_row, double *rec_val, void *stream) {
-    if (m < 0 || canon_rows < 1 || n_shards < 1 || n_shards > MAX_BANDS || !shard_start)
+extern "C" int isg_owner_fold_plan(int64_t n, const uint8_t *flag, const int32_t *rect,
+                                   const int32_t *band_rows, int32_t n_bands, int32_t canon_rows,
+                                   const int64_t *plan, const double *const *seg,
+                                   double *grad2d, void *stream) {
+    Bands b;
+    if (n < 0 || canon_rows < 1 || fill_bands(b, band_rows, n_bands) || !seg)
         return (int)cudaErrorInvalidValue;
-    if (m == 0) return 0;
-    Shards sh;
-    sh.n = n_shards;
-    for (int i = 0; i <= n_shards; i++) sh.start[i] = shard_start[i];
-    cudaStream_t s = (cudaStream_t)stream;
-    const int4 *rs = (const int4 *)rect_sorted;
-    if (feat_dtype == ISG_F32)
-        block_fold_kernel<float><<<blocks_for(m, 256), 256, 0, s>>>(
-            m, emit_off, (const float *)partials, rs, row_lo, row_hi, canon_rows, rec_off, order,
-            gid, sh, rec_owner, rec_row, rec_val);
-    else if (feat_dtype == ISG_F64)
-        block_fold_kernel<double><<<blocks_for(m, 256), 256, 0, s>>>(
-            m, emit_off, (const double *)partials, rs, row_lo, row_hi, canon_rows, rec_off, order,
-            gid, sh, rec_owner, rec_row, rec_val);
-    else
-        return (int)cudaErrorInvalidValue;
-    ISG_CHECK_LAUNCH();
-    return 0;
-}
-
-extern "C" int isg_grad_gather(int64_t s, const int32_t *idx, const int32_t *rec_row,
-                               const double *rec_val, int32_t *out, void *stream) {
-    if (s < 0) return (int)cudaErrorInvalidValue;
-    if (s == 0) return 0;
-    grad_gather_kernel<<<blocks_for(s, 256), 256, 0, (cudaStream_t)stream>>>(s, idx, rec_row,
-                                                                             rec_val, out);
+    const int64_t nblk = (n + PLAN_T - 1) / PLAN_T;
+    if (nblk == 0) return 0;
+    SegPtrs sp;
+    for (int d = 0; d < n_bands; d++) sp.seg[d] = seg[d];
+    owner_fold_plan_kernel<<<(unsigned)nblk, PLAN_T, 0, (cudaStream_t)stream>>>(
+        n, flag, (const int4 *)rect, b, canon_rows, plan, sp, grad2d);
     ISG_CHECK_LAUNCH();
     return 0;
 }

@@ -7,22 +7,29 @@ reference's round-robin tiles ship 2.3x more splat records at 8 GPUs, SURVEY
 §8e).  One iteration, per rank, is a fixed sequence of phases separated by
 collectives -- the reference's barrier-separated phases (engine.py:184-537):
 
-  project   isg_preprocess on the shard, isg_route_* -> 80 B splat records
-            grouped by destination band                      -> all-to-all #1
-  render    unpack, depth sort, bin the band's tiles, raster forward into a
-            window buffer                                    -> halo rows
+  plan      isg_preprocess on the shard; isg_route_plan: per destination band
+            the shard's splat records, canonical-block gradient records and
+            tile entries                      -> counts all-to-all (3 x W int64)
+  sizes     the iteration's ONE host synchronisation: every buffer size and
+            exchange split of the step
+  pack      isg_route_pack: key + 64 B payload per (splat, band), in shard row
+            order per band; the own band's straight into the receive buffers
+                                              -> point-to-point group #1
+  render    depth sort of the received splats (receive order = global id
+            order), band tile lists, raster forward into a window buffer
+                                              -> halo rows
   loss      isg_loss_rows on the band (+16/+10 halo rows); block partials of
-            the loss                                         -> all-reduce
-  backward  raster backward on the band, per-(splat, canonical block) fold,
-            records grouped by owner shard                   -> all-to-all #2
-  update    owner fold (bands ascending), chain rule + stats + Adam on the
-            shard (isg_chain_adam)
+            the loss                          -> all-reduce
+  backward  raster backward on the band, per-(splat, canonical block) fold
+            into records by receive index     -> point-to-point group #2
+  update    owner fold through the route plan (bands ascending, no sort),
+            chain rule + stats + Adam on the shard
 
 Every cross-GPU meeting point has a canonical order (global (depth, id) sort;
 canonical 8-tile-row blocks summed in band order; fixed-order loss sums), so
 the result is bitwise identical for any GPU count (tests/test_dist_gpu.py
-checks W = 1, 2, 3 against the single-GPU engine on one B200 by running the
-ranks' phases in sequence with an in-process exchange).
+checks W = 1..8 against the single-GPU engine on one B200 by running the
+ranks' phases in sequence with an in-process exchange, up to config 3).
 
 The reference's public data-plane API (ShardMap, partition_gaussians,
 PixelPartition, partition_pixels, route_rows, GradChunk/GradMessage,
@@ -44,13 +51,12 @@ from . import _lib as L
 
 TILE = 16
 CANON_ROWS = 8
-# our kernels per sharded step (CUB scan/sort passes not counted): preprocess,
-# route_count, route_emit, dest offsets, route_gather | records_unpack,
-# depth tie fix, gather_rank, finish_counts, bin_emit16_cull, tile_offsets16,
-# raster_fwd_masked | ssim_fields, ssim_adjoint, loss_finish | raster_bwd_masked,
-# block_count, block_fold, owner offsets, grad_gather | grad_rows, seg
-# offsets, owner_fold, chain_train, adam_groups
-LAUNCHES_PER_STEP = 24
+# our kernels per sharded step (CUB scan/sort passes not counted):
+# preprocess, route_plan, route_scan, route_pack | depth tie fix, gather_rank,
+# finish_counts, bin_emit16_cull, tile_offsets16, raster_fwd_masked |
+# ssim_fields, ssim_adjoint, loss_finish | raster_bwd_masked, band_blocks,
+# band_fold | owner_fold_plan, chain_train, adam_groups
+LAUNCHES_PER_STEP = 19
 
 
 class ProtocolError(RuntimeError):
@@ -340,6 +346,28 @@ class TorchComm:
                                     input_split_sizes=list(send_counts), group=self.group)
         return recv, recv_counts
 
+    def counts(self, mine: torch.Tensor, out: torch.Tensor) -> None:
+        """(W, 3) per-destination counts -> out[s] = source s's row for this
+        rank (one all-to-all of 3 int64 per pair, on the device)."""
+        self.dist.all_to_all_single(out, mine.contiguous(), group=self.group)
+
+    def exchange(self, ops: list) -> None:
+        """Point-to-point segments: ops = [(peer, [send tensors], [recv
+        tensors])], the same tensor count per peer on both sides; one NCCL
+        group (batch_isend_irecv).  Empty segments are skipped."""
+        P2POp = self.dist.P2POp
+        p2p = []
+        for peer, sends, recvs in ops:
+            for t in recvs:
+                if t.numel():
+                    p2p.append(P2POp(self.dist.irecv, t, peer, self.group))
+            for t in sends:
+                if t.numel():
+                    p2p.append(P2POp(self.dist.isend, t, peer, self.group))
+        if p2p:
+            for req in self.dist.batch_isend_irecv(p2p):
+                req.wait()
+
     def halo(self, to_prev: torch.Tensor | None, to_next: torch.Tensor | None,
              from_prev_shape, from_next_shape, dtype, dev) -> tuple:
         """Exchange boundary rows with the neighbouring ranks."""
@@ -372,8 +400,26 @@ class TorchComm:
 
 # --------------------------------------------------------------- rank state --
 
+def _grow(buf, n: int, tail=(), dtype=torch.float32, device=None, slack: float = 1.25):
+    """Capacity-managed buffer: reallocated only when `n` rows do not fit."""
+    if buf is None or buf.shape[0] < n:
+        return torch.empty((max(int(n * slack), 16),) + tuple(tail), dtype=dtype, device=device)
+    return buf
+
+
 class RankStep:
-    """One rank's shard, band and buffers, with the phases of an iteration."""
+    """One rank's shard, band and buffers, with the phases of an iteration.
+
+    Per iteration there is exactly ONE host synchronisation (phase_sizes):
+    after the route plan, every rank knows per destination band the number of
+    splat records, canonical-block gradient records and tile entries its
+    shard produces; one all-to-all of those 3 x W counts and one 48 x W-byte
+    read give every size of the iteration (receive counts, the band's tile
+    entries, both directions of the gradient exchange).  Records of the
+    rank's own band are written straight into its receive buffers (no self
+    copy); gradient records are laid out by receive index, so the segment for
+    each owner is already in its shard row order and the owner folds them
+    through its route plan with no sort."""
 
     def __init__(self, rank: int, world: int, shards: ShardMap, part: PixelPartition,
                  params: dict, degree: int, config, scene_extent: float, device,
@@ -383,7 +429,6 @@ class RankStep:
         self.dev = device
         self.cfg = config
         self.scene_extent = float(scene_extent)
-        self.part = part
         self.shard_starts = shards.starts
         self.id_base = self.shard_starts[rank]
         self.cloud = GaussianCloud(*(params[k] for k in PARAM_NAMES), degree=degree)
@@ -394,16 +439,7 @@ class RankStep:
         self.grad_accum = torch.zeros(self.n, dtype=torch.float64, device=device)
         self.W, self.H = part.width, part.height
         self.tiles_x = part.tiles_x
-        self.trow0, self.trow1 = part.band_rows[rank], part.band_rows[rank + 1]
-        self.prow0, self.prow1 = part.pixel_rows(rank)
-        self.win0 = max(0, self.prow0 - 16)
-        self.win1 = min(self.H, self.prow1 + 10)
         self.bg = (ctypes.c_double * 3)(*[float(v) for v in background])
-        self.band_host = (ctypes.c_int32 * (world + 1))(*part.band_rows)
-        self.shard_host = (ctypes.c_int64 * (world + 1))(*self.shard_starts)
-        n_tiles = (self.trow1 - self.trow0) * self.tiles_x
-        self.n_tiles = n_tiles
-        self.tile_bits = _bits(n_tiles)
         d = device
         n = self.n
         # shard-side buffers
@@ -411,20 +447,14 @@ class RankStep:
         self.rect = torch.empty((n, 4), dtype=torch.int32, device=d)
         self.feat = torch.empty((n, 12), dtype=torch.float32, device=d)
         self.flag = torch.empty(n, dtype=torch.uint8, device=d)
-        self.cnt = torch.empty(n, dtype=torch.int64, device=d)
-        self.dlo = torch.empty(n, dtype=torch.int32, device=d)
-        self.roff = torch.empty(n + 1, dtype=torch.int64, device=d)
         self.grad2d = torch.zeros((n, 9), dtype=torch.float64, device=d)
-        self.total = torch.zeros(1, dtype=torch.int64, device=d)
-        self.counts = torch.zeros(2, dtype=torch.int64, device=d)
-        self.host = torch.zeros(4, dtype=torch.int64).pin_memory()
-        rows = self.win1 - self.win0
-        self.window = torch.zeros((max(rows, 1), self.W, 3), dtype=torch.float32, device=d)
-        band_px = (self.prow1 - self.prow0) * self.W
-        self.t_final = torch.empty(max(band_px, 1), dtype=torch.float32, device=d)
-        self.n_last = torch.empty(max(band_px, 1), dtype=torch.int32, device=d)
-        self.dl = torch.empty((max(band_px, 1), 3), dtype=torch.float32, device=d)
-        self.offsets = torch.empty(n_tiles + 1, dtype=torch.int32, device=d)
+        pe = ctypes.c_int64(0)
+        L.check(L.lib().isg_route_plan_size(n, world, ctypes.byref(pe)), "route plan size")
+        self.plan = torch.empty(max(pe.value, 1), dtype=torch.int64, device=d)
+        # counts[0] = this shard's per-band totals, counts[1] = every source's for this band
+        self.counts = torch.zeros((2, world, 3), dtype=torch.int64, device=d)
+        self.counts_host = torch.zeros((2, world, 3), dtype=torch.int64).pin_memory()
+        self.bin_counts = torch.zeros(2, dtype=torch.int64, device=d)  # (M, E), not read
         nf = ctypes.c_int32(0)
         na = ctypes.c_int32(0)
         L.lib().isg_loss_partials_size(self.H, self.W, ctypes.byref(nf), ctypes.byref(na))
@@ -432,24 +462,44 @@ class RankStep:
         self.parts = torch.zeros(self.n_ps + self.n_pl, dtype=torch.float64, device=d)
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=d)
         self.ws = [L.Workspace() for _ in range(4)]
-        self.lr_host = (ctypes.c_float * 5)()
+        # receive-side / band buffers (grown on demand)
+        self.keys_recv = self.pay_recv = self.keys_send = self.pay_send = None
+        self.vals0 = self.key_sorted = self.order = None
+        self.rect_sorted = self.feat_sorted = self.emit_off = None
+        self.tk = self.tv = self.tk_sorted = self.entries = self.partials = None
+        self.cmask = self.nb = self.gpos = self.gbuf = self.grad_recv = None
+        self.set_partition(part)
 
-    # -- helpers --------------------------------------------------------
-    def _sync_ints(self, *tensors) -> list:
-        k = 0
-        for t in tensors:
-            self.host[k:k + t.numel()].copy_(t, non_blocking=True)
-            k += t.numel()
-        torch.cuda.current_stream().synchronize()
-        return [int(v) for v in self.host[:k].tolist()]
+    def set_partition(self, part: PixelPartition) -> None:
+        """Adopt a (new) row-band partition; results do not depend on it."""
+        self.part = part
+        rank = self.rank
+        self.trow0, self.trow1 = part.band_rows[rank], part.band_rows[rank + 1]
+        self.prow0, self.prow1 = part.pixel_rows(rank)
+        self.win0 = max(0, self.prow0 - 16)
+        self.win1 = min(self.H, self.prow1 + 10)
+        self.band_host = (ctypes.c_int32 * (self.world + 1))(*part.band_rows)
+        self.n_tiles = (self.trow1 - self.trow0) * self.tiles_x
+        self.tile_bits = _bits(self.n_tiles)
+        d = self.dev
+        rows = self.win1 - self.win0
+        self.window = torch.zeros((max(rows, 1), self.W, 3), dtype=torch.float32, device=d)
+        band_px = (self.prow1 - self.prow0) * self.W
+        self.t_final = torch.empty(max(band_px, 1), dtype=torch.float32, device=d)
+        self.n_last = torch.empty(max(band_px, 1), dtype=torch.int32, device=d)
+        self.dl = torch.empty((max(band_px, 1), 3), dtype=torch.float32, device=d)
+        self.offsets = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=d)
 
     def _vptr(self, t: torch.Tensor, row0: int, row_elems: int) -> int:
         """Virtual base pointer so that global row `row0` maps to t's start."""
         return t.data_ptr() - row0 * row_elems * t.element_size()
 
-    # -- phase 1: project + route ----------------------------------------
-    def phase_project(self, cam):
-        lib, s, d = L.lib(), L.stream_ptr(), self.dev
+    # -- phase 1: project + route plan ------------------------------------
+    def phase_plan(self, cam) -> torch.Tensor:
+        """Preprocess the shard and plan its records per band; returns the
+        (W, 3) per-band totals (splat records, block records, tile entries)
+        to exchange."""
+        lib, s = L.lib(), L.stream_ptr()
         c = self.cloud
         self.cam_struct = L.camera_struct(cam)
         if self.n:
@@ -462,90 +512,122 @@ class RankStep:
             out.flag, out.full64, out.feat_dtype = L.ptr(self.flag), None, L.ISG_F32
             L.check(lib.isg_preprocess(ctypes.byref(p), ctypes.byref(self.cam_struct), TILE,
                                        ctypes.byref(out), s), "isg_preprocess")
-            L.check(lib.isg_route_count(self.n, L.ptr(self.flag), L.ptr(self.rect),
-                                        self.band_host, self.world, L.ptr(self.cnt),
-                                        L.ptr(self.dlo), s), "isg_route_count")
-        self._scan(self.n, self.cnt, self.roff, self.total)
-        (S,) = self._sync_ints(self.total)
-        keys = torch.empty(max(S, 1), dtype=torch.int32, device=d)
-        vals = torch.empty(max(S, 1), dtype=torch.int32, device=d)
-        if S:
-            L.check(lib.isg_route_emit(self.n, L.ptr(self.roff), L.ptr(self.dlo), L.ptr(keys),
-                                       L.ptr(vals), s), "isg_route_emit")
-            keys, vals = L.sort_pairs(keys[:S], vals[:S], (0, _bits(self.world)), self.ws[0])
-        doff = torch.empty(self.world + 1, dtype=torch.int32, device=d)
-        L.check(lib.isg_tile_offsets(S, L.ptr(keys), self.world, L.ptr(doff), s), "dest offsets")
-        rec = torch.empty((max(S, 1), 20), dtype=torch.int32, device=d)
-        if S:
-            L.check(lib.isg_route_gather(S, L.ptr(vals), L.ptr(self.key), L.ptr(self.rect),
-                                         L.ptr(self.feat), self.id_base, L.ptr(rec), s),
-                    "isg_route_gather")
-        counts = (doff[1:] - doff[:-1]).tolist()
-        return rec[:S], [int(v) for v in counts]
+        L.check(lib.isg_route_plan(self.n, L.ptr(self.flag), L.ptr(self.rect), self.band_host,
+                                   self.world, self.part.canon_rows, L.ptr(self.plan),
+                                   L.ptr(self.counts[0]), s), "isg_route_plan")
+        return self.counts[0]
 
-    def _scan(self, n, cnt, off, total):
-        lib = L.lib()
-        sz = ctypes.c_size_t(0)
-        L.check(lib.isg_scan_i64(None, ctypes.byref(sz), n, None, None, None, None), "scan size")
-        buf = self.ws[1].get(sz.value, self.dev)
-        sz = ctypes.c_size_t(buf.numel())
-        L.check(lib.isg_scan_i64(L.ptr(buf), ctypes.byref(sz), n, L.ptr(cnt), L.ptr(off),
-                                 L.ptr(total), L.stream_ptr()), "isg_scan_i64")
+    # -- the one host synchronisation --------------------------------------
+    def phase_sizes(self) -> None:
+        """Read this shard's totals and every source's totals for this band
+        (counts[1], filled by the counts exchange) and size the iteration."""
+        self.counts_host.copy_(self.counts, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        h = self.counts_host.numpy()
+        mine, recv = h[0], h[1]
+        W, me = self.world, self.rank
+        self.send_cnt = [int(x) for x in mine[:, 0]]
+        self.recv_cnt = [int(x) for x in recv[:, 0]]
+        self.gsend_cnt = [int(x) for x in recv[:, 1]]   # band -> owner s
+        self.grecv_cnt = [int(x) for x in mine[:, 1]]   # owner <- band d
+        self.R = sum(self.recv_cnt)
+        self.E = int(recv[:, 2].sum())
+        self.NR = sum(self.gsend_cnt)
+        self.recv_off = np.concatenate([[0], np.cumsum(self.recv_cnt)]).astype(np.int64)
+        self.gpos_off = np.concatenate([[0], np.cumsum(self.gsend_cnt)]).astype(np.int64)
+        others = [c if d != me else 0 for d, c in enumerate(self.send_cnt)]
+        self.send_off = np.concatenate([[0], np.cumsum(others)]).astype(np.int64)
+        gothers = [c if d != me else 0 for d, c in enumerate(self.grecv_cnt)]
+        self.grecv_off = np.concatenate([[0], np.cumsum(gothers)]).astype(np.int64)
 
-    # -- phase 2: render the band -----------------------------------------
-    def phase_render(self, records: torch.Tensor, count: bool = False):
-        """count=True: the reference's full band lists and the unmasked
-        forward with per-pixel pair counters (n_contrib, n_iter; n_last is
-        then the full-list last-contributor index) for the roofline units;
-        leaves no state for a backward."""
+    # -- phase 2: pack splat records ----------------------------------------
+    def phase_pack(self) -> list:
+        """Splat records into the send buffers (own band: receive buffers).
+        Returns the exchange list [(peer, send tensors, recv tensors)]."""
         lib, s, d = L.lib(), L.stream_ptr(), self.dev
-        R = int(records.shape[0])
-        self.R = R
-        self.r_key = torch.empty(max(R, 1), dtype=torch.int64, device=d)
-        self.r_gid = torch.empty(max(R, 1), dtype=torch.int32, device=d)
-        self.r_rect = torch.empty((max(R, 1), 4), dtype=torch.int32, device=d)
-        self.r_feat = torch.empty((max(R, 1), 12), dtype=torch.float32, device=d)
-        L.check(lib.isg_records_unpack(R, L.ptr(records), L.ptr(self.r_key), L.ptr(self.r_gid),
-                                       L.ptr(self.r_rect), L.ptr(self.r_feat), s), "unpack")
-        vals0 = torch.arange(max(R, 1), dtype=torch.int32, device=d)
-        self.key_sorted, self.order = L.sort_depth(self.r_key[:R], vals0[:R], self.ws[0])
-        self.rect_sorted = torch.empty((max(R, 1), 4), dtype=torch.int32, device=d)
-        self.feat_sorted = torch.empty((max(R, 1), 12), dtype=torch.float32, device=d)
-        self.emit_off = torch.empty(R + 1, dtype=torch.int64, device=d)
+        me = self.rank
+        R, S = self.R, int(self.send_off[-1])
+        self.keys_recv = _grow(self.keys_recv, R, dtype=torch.int64, device=d)
+        self.pay_recv = _grow(self.pay_recv, R, (16,), dtype=torch.int32, device=d)
+        self.keys_send = _grow(self.keys_send, S, dtype=torch.int64, device=d)
+        self.pay_send = _grow(self.pay_send, S, (16,), dtype=torch.int32, device=d)
+        dest = (ctypes.c_int64 * self.world)(*[
+            int(self.recv_off[me]) if k == me else int(self.send_off[k])
+            for k in range(self.world)])
+        if self.n:
+            L.check(lib.isg_route_pack(self.n, L.ptr(self.flag), L.ptr(self.rect), L.ptr(self.key),
+                                       L.ptr(self.feat), self.band_host, self.world,
+                                       L.ptr(self.plan), dest, me, L.ptr(self.keys_send),
+                                       L.ptr(self.pay_send), L.ptr(self.keys_recv),
+                                       L.ptr(self.pay_recv), s), "isg_route_pack")
+        ops = []
+        for peer in range(self.world):
+            if peer == me:
+                continue
+            a, b = int(self.send_off[peer]), int(self.send_off[peer + 1])
+            c0, c1 = int(self.recv_off[peer]), int(self.recv_off[peer + 1])
+            ops.append((peer, [self.keys_send[a:b], self.pay_send[a:b]],
+                        [self.keys_recv[c0:c1], self.pay_recv[c0:c1]]))
+        return ops
+
+    # -- phase 3: render the band -----------------------------------------
+    def phase_render(self, count: bool = False):
+        """Depth order over the received splats (receive order = global id
+        order, so the stable sort is the reference's lexsort), the band's
+        tile lists and the forward.  count=True: the reference's full band
+        lists and the unmasked forward with per-pixel pair counters (n_contrib,
+        n_iter) for the roofline units; leaves no state for a backward."""
+        lib, s, d = L.lib(), L.stream_ptr(), self.dev
+        R, E = self.R, self.E
+        if self.vals0 is None or self.vals0.shape[0] < R:
+            self.vals0 = torch.arange(max(int(R * 1.25), 16), dtype=torch.int32, device=d)
+        self.key_sorted = _grow(self.key_sorted, R, dtype=torch.int64, device=d)
+        self.order = _grow(self.order, R, dtype=torch.int32, device=d)
+        L.sort_depth(self.keys_recv[:R], self.vals0[:R], self.ws[0], self.key_sorted[:R],
+                     self.order[:R])
+        self.rect_sorted = _grow(self.rect_sorted, R, (4,), dtype=torch.int32, device=d)
+        self.feat_sorted = _grow(self.feat_sorted, R, (12,), dtype=torch.float32, device=d)
+        self.emit_off = _grow(self.emit_off, R + 1, dtype=torch.int64, device=d)
         sz = ctypes.c_size_t(0)
-        L.check(lib.isg_bin_count(None, ctypes.byref(sz), R, None, None, None, None, L.ISG_F32,
-                                  self.trow0, self.trow1, None, None, None, None, None), "bin size")
+        L.check(lib.isg_bin_count_rows(None, ctypes.byref(sz), R, None, None, None, self.trow0,
+                                       self.trow1, None, None, None, None, None), "bin size")
         ws = self.ws[2].get(sz.value, d)
         sz = ctypes.c_size_t(ws.numel())
-        L.check(lib.isg_bin_count(L.ptr(ws), ctypes.byref(sz), R, L.ptr(self.key_sorted),
-                                  L.ptr(self.order), L.ptr(self.r_rect), L.ptr(self.r_feat),
-                                  L.ISG_F32, self.trow0, self.trow1, L.ptr(self.rect_sorted),
-                                  L.ptr(self.feat_sorted), L.ptr(self.emit_off),
-                                  L.ptr(self.counts), s), "isg_bin_count")
-        M, E = self._sync_ints(self.counts)
-        self.M, self.E = M, E
+        L.check(lib.isg_bin_count_rows(L.ptr(ws), ctypes.byref(sz), R, L.ptr(self.key_sorted),
+                                       L.ptr(self.order), L.ptr(self.pay_recv), self.trow0,
+                                       self.trow1, L.ptr(self.rect_sorted),
+                                       L.ptr(self.feat_sorted), L.ptr(self.emit_off),
+                                       L.ptr(self.bin_counts), s), "isg_bin_count_rows")
+        self.M = R
         k16 = self.n_tiles <= 65536  # 2-byte tile keys (see engine.Rasterizer.forward)
-        tk = torch.empty(max(E, 1), dtype=torch.int16 if k16 else torch.int32, device=d)
-        tv = torch.empty(max(E, 1), dtype=torch.int32, device=d)
+        kdt = torch.int16 if k16 else torch.int32
+        if self.tk is None or self.tk.dtype != kdt:
+            self.tk = self.tk_sorted = None
+        self.tk = _grow(self.tk, E, dtype=kdt, device=d)
+        self.tv = _grow(self.tv, E, dtype=torch.int32, device=d)
+        self.tk_sorted = _grow(self.tk_sorted, E, dtype=kdt, device=d)
+        self.entries = _grow(self.entries, E, dtype=torch.int32, device=d)
+        self.partials = _grow(self.partials, E, (12,), dtype=torch.float32, device=d)
         emit = lib.isg_bin_emit16 if k16 else lib.isg_bin_emit
         offs = lib.isg_tile_offsets16 if k16 else lib.isg_tile_offsets
         # band lists leave out the pairs no pixel of their tile can composite
         # (isg_bin_emit16_cull writes their zero subtotals; see engine.Rasterizer)
         cull = self.n_tiles < 65536 and not count
-        self.partials = torch.empty((max(E, 1), 12), dtype=torch.float32, device=d)
         if E:
             if cull:
-                L.check(lib.isg_bin_emit16_cull(M, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
+                L.check(lib.isg_bin_emit16_cull(R, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
                                                 L.ptr(self.feat_sorted), self.tiles_x, self.trow0,
-                                                self.trow1, L.ptr(tk), L.ptr(tv),
+                                                self.trow1, L.ptr(self.tk), L.ptr(self.tv),
                                                 L.ptr(self.partials), s), "isg_bin_emit16_cull")
             else:
-                L.check(emit(M, L.ptr(self.rect_sorted), L.ptr(self.emit_off), self.tiles_x,
-                             self.trow0, self.trow1, L.ptr(tk), L.ptr(tv), s), "isg_bin_emit")
+                L.check(emit(R, L.ptr(self.rect_sorted), L.ptr(self.emit_off), self.tiles_x,
+                             self.trow0, self.trow1, L.ptr(self.tk), L.ptr(self.tv), s),
+                        "isg_bin_emit")
             bits = max(self.tile_bits, int(self.n_tiles).bit_length()) if cull else self.tile_bits
-            tk, tv = L.sort_pairs(tk[:E], tv[:E], (0, bits), self.ws[0])
-        self.entries = tv
-        L.check(offs(E, L.ptr(tk), self.n_tiles, L.ptr(self.offsets), s), "isg_tile_offsets")
+            L.sort_pairs(self.tk[:E], self.tv[:E], (0, bits), self.ws[0], self.tk_sorted[:E],
+                         self.entries[:E])
+        L.check(offs(E, L.ptr(self.tk_sorted), self.n_tiles, L.ptr(self.offsets), s),
+                "isg_tile_offsets")
         W3 = self.W * 3
         if count:
             band_px = max((self.prow1 - self.prow0) * self.W, 1)
@@ -564,8 +646,8 @@ class RankStep:
             return None, None
         if self.n_tiles:
             # contribution masks for the band's backward (isg_raster_bwd_masked)
-            self.cmask = torch.empty(lib.isg_contrib_mask_words(E, self.n_tiles),
-                                     dtype=torch.int32, device=d)
+            self.cmask = _grow(self.cmask, lib.isg_contrib_mask_words(E, self.n_tiles),
+                               dtype=torch.int32, device=d)
             L.check(lib.isg_raster_fwd_masked(
                 self.W, self.H, self.tiles_x, self.trow0, self.trow1, None, 0,
                 L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
@@ -585,7 +667,7 @@ class RankStep:
         nxt = (self.win1 - self.prow1, self.W, 3) if self.rank + 1 < self.world else None
         return prev, nxt
 
-    # -- phase 3: loss on the band ----------------------------------------
+    # -- phase 4: loss on the band ----------------------------------------
     def phase_loss(self, from_prev, from_next, gt: torch.Tensor):
         lib, s = L.lib(), L.stream_ptr()
         if from_prev is not None and from_prev.shape[0]:
@@ -615,13 +697,15 @@ class RankStep:
                                         L.ptr(self.loss_dev), L.stream_ptr()), "isg_loss_finish")
         return self.loss_dev
 
-    # -- phase 4: backward + per-block records for the owners --------------
-    def phase_backward(self, timer=None):
+    # -- phase 5: backward + block records for the owners ------------------
+    def phase_backward(self, timer=None) -> list:
+        """Raster backward on the band, per-(splat, canonical block) fold into
+        records by receive index; returns the exchange list."""
         from .engine import _mark
         lib, s, d = L.lib(), L.stream_ptr(), self.dev
-        E, M = self.E, self.M
         W3 = self.W * 3
-        if self.n_tiles:
+        R, me = self.R, self.rank
+        if self.n_tiles and self.E:
             L.check(lib.isg_raster_bwd_masked(
                 self.W, self.H, self.tiles_x, self.trow0, self.trow1, None, 0,
                 L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
@@ -631,51 +715,64 @@ class RankStep:
                 self._vptr(self.dl, self.prow0, W3), L.ISG_F32, L.ptr(self.partials),
                 L.ptr(self.cmask), s), "isg_raster_bwd_masked")
         _mark(timer, "raster_bwd")
-        nb = torch.empty(max(M, 1), dtype=torch.int64, device=d)
-        rec_off = torch.empty(M + 1, dtype=torch.int64, device=d)
-        if M:
-            L.check(lib.isg_block_count(M, L.ptr(self.rect_sorted), self.trow0, self.trow1,
-                                        self.part.canon_rows, L.ptr(nb), s), "isg_block_count")
-        self._scan(M, nb, rec_off, self.total)
-        (NR,) = self._sync_ints(self.total)
-        owner = torch.empty(max(NR, 1), dtype=torch.int32, device=d)
-        rrow = torch.empty(max(NR, 1), dtype=torch.int32, device=d)
-        rval = torch.empty((max(NR, 1), 9), dtype=torch.float64, device=d)
-        if NR:
-            L.check(lib.isg_block_fold(L.ISG_F32, M, L.ptr(self.emit_off), L.ptr(self.partials),
-                                       L.ptr(self.rect_sorted), self.trow0, self.trow1,
-                                       self.part.canon_rows, L.ptr(rec_off), L.ptr(self.order),
-                                       L.ptr(self.r_gid), self.shard_host, self.world,
-                                       L.ptr(owner), L.ptr(rrow), L.ptr(rval), s), "isg_block_fold")
-        idx0 = torch.arange(max(NR, 1), dtype=torch.int32, device=d)
-        okeys, oidx = owner[:NR], idx0[:NR]
-        if NR:
-            okeys, oidx = L.sort_pairs(owner[:NR], idx0[:NR], (0, _bits(self.world)), self.ws[0])
-        doff = torch.empty(self.world + 1, dtype=torch.int32, device=d)
-        L.check(lib.isg_tile_offsets(NR, L.ptr(okeys) if NR else None, self.world, L.ptr(doff), s),
-                "owner offsets")
-        out = torch.empty((max(NR, 1), 20), dtype=torch.int32, device=d)
-        if NR:
-            L.check(lib.isg_grad_gather(NR, L.ptr(oidx), L.ptr(rrow), L.ptr(rval), L.ptr(out), s),
-                    "isg_grad_gather")
-        counts = [int(v) for v in (doff[1:] - doff[:-1]).tolist()]
-        return out[:NR], counts
+        self.nb = _grow(self.nb, R, dtype=torch.int64, device=d)
+        self.gpos = _grow(self.gpos, R + 1, dtype=torch.int64, device=d)
+        self.gbuf = _grow(self.gbuf, self.NR, (9,), dtype=torch.float64, device=d)
+        if R:
+            L.check(lib.isg_band_blocks(R, L.ptr(self.pay_recv), self.trow0, self.trow1,
+                                        self.part.canon_rows, L.ptr(self.nb), s), "band blocks")
+            _scan_i64(self, R, self.nb, self.gpos)
+            L.check(lib.isg_band_fold(R, L.ptr(self.emit_off), L.ptr(self.partials),
+                                      L.ptr(self.rect_sorted), L.ptr(self.order),
+                                      L.ptr(self.gpos), self.trow0, self.part.canon_rows,
+                                      L.ptr(self.gbuf), s), "isg_band_fold")
+        G = int(self.grecv_off[-1])
+        self.grad_recv = _grow(self.grad_recv, G, (9,), dtype=torch.float64, device=d)
+        ops = []
+        for peer in range(self.world):
+            if peer == me:
+                continue
+            a, b = int(self.gpos_off[peer]), int(self.gpos_off[peer + 1])
+            c0, c1 = int(self.grecv_off[peer]), int(self.grecv_off[peer + 1])
+            ops.append((peer, [self.gbuf[a:b]], [self.grad_recv[c0:c1]]))
+        return ops
 
-    # -- phase 5: owner fold + chain + Adam -------------------------------
-    def phase_update(self, grad_records: torch.Tensor, it: int):
-        from .optim import adam_consts, position_lr
-        _owner_fold(grad_records, self.n, self.dev, self.ws[0], self.grad2d)
+    # -- phase 6: owner fold + chain + Adam -------------------------------
+    def phase_update(self, it: int):
+        from .engine import update_params
+        from .optim import position_lr
+        me = self.rank
+        segs = []
+        for b in range(self.world):
+            if b == me:
+                segs.append(self.gbuf.data_ptr() + 72 * int(self.gpos_off[me]))
+            else:
+                segs.append(self.grad_recv.data_ptr() + 72 * int(self.grecv_off[b]))
+        seg = (ctypes.c_void_p * self.world)(*segs)
         if not self.n:
             return
+        L.check(L.lib().isg_owner_fold_plan(self.n, L.ptr(self.flag), L.ptr(self.rect),
+                                            self.band_host, self.world, self.part.canon_rows,
+                                            L.ptr(self.plan), seg, L.ptr(self.grad2d),
+                                            L.stream_ptr()), "isg_owner_fold_plan")
         cfg = self.cfg
         lrs = [self.scene_extent * position_lr(cfg.lr_position, it, cfg.iterations,
                                                cfg.lr_position_final),
                cfg.lr_scale, cfg.lr_rotation, cfg.lr_opacity, cfg.lr_sh]
-        from .engine import update_params
         if getattr(self, "grads", None) is None:
             self.grads = {k: torch.empty_like(v) for k, v in self.m.items()}
         update_params(self.cloud, self.m, self.v, self.grads, self.seen, self.grad_accum,
                       self.flag, self.grad2d, self.cam_struct, lrs, it, self.W, self.H)
+
+
+def _scan_i64(rs: RankStep, n: int, cnt: torch.Tensor, off: torch.Tensor) -> None:
+    lib = L.lib()
+    sz = ctypes.c_size_t(0)
+    L.check(lib.isg_scan_i64(None, ctypes.byref(sz), n, None, None, None, None), "scan size")
+    buf = rs.ws[1].get(sz.value, rs.dev)
+    sz = ctypes.c_size_t(buf.numel())
+    L.check(lib.isg_scan_i64(L.ptr(buf), ctypes.byref(sz), n, L.ptr(cnt), L.ptr(off), None,
+                             L.stream_ptr()), "isg_scan_i64")
 
 
 # ------------------------------------------------------- densify + rebalance --
@@ -849,15 +946,21 @@ def emulated_densify(ranks: list, it: int) -> list:
 
 def comm_step(rs: RankStep, comm: TorchComm, cam, gt: torch.Tensor, it: int,
               timer=None) -> torch.Tensor:
-    """One iteration on this rank (multi-process, one GPU per rank).  timer:
-    optional engine.PhaseTimer (CUDA events between the phases)."""
+    """One iteration on this rank (multi-process, one GPU per rank), with one
+    host synchronisation (phase_sizes).  timer: optional engine.PhaseTimer
+    (CUDA events between the phases)."""
     from .engine import _mark
     _mark(timer, "begin")
-    rec, cnt = rs.phase_project(cam)
-    _mark(timer, "project_route")
-    rrec, _ = comm.alltoallv(rec, cnt)
-    _mark(timer, "a2a_splats")
-    to_prev, to_next = rs.phase_render(rrec)
+    mine = rs.phase_plan(cam)
+    _mark(timer, "project_plan")
+    comm.counts(mine, rs.counts[1])
+    rs.phase_sizes()
+    _mark(timer, "counts_sync")
+    ops = rs.phase_pack()
+    _mark(timer, "pack")
+    comm.exchange(ops)
+    _mark(timer, "exchange_splats")
+    to_prev, to_next = rs.phase_render()
     _mark(timer, "bin_render")
     sp, sn = rs.halo_shapes()
     got_prev, got_next = comm.halo(to_prev, to_next, sp, sn, torch.float32, rs.dev)
@@ -866,11 +969,11 @@ def comm_step(rs: RankStep, comm: TorchComm, cam, gt: torch.Tensor, it: int,
     comm.allreduce_sum_(parts)
     loss = rs.finish_loss()
     _mark(timer, "loss_allreduce")
-    grec, gcnt = rs.phase_backward(timer)
-    _mark(timer, "block_fold")
-    rg, _ = comm.alltoallv(grec, gcnt)
-    _mark(timer, "a2a_grads")
-    rs.phase_update(rg, it)
+    gops = rs.phase_backward(timer)
+    _mark(timer, "band_fold")
+    comm.exchange(gops)
+    _mark(timer, "exchange_grads")
+    rs.phase_update(it)
     _mark(timer, "owner_fold_chain_adam")
     return loss
 
@@ -879,11 +982,16 @@ def comm_pair_counts(rs: RankStep, comm: TorchComm, cam) -> dict:
     """Roofline units of this rank's band for view `cam`: pairs
     iterated (I_f), contributing (C) and the backward's I_b (sum of the
     last-contributor index) over the reference's full lists; no state change."""
-    rec, cnt = rs.phase_project(cam)
-    rrec, _ = comm.alltoallv(rec, cnt)
-    rs.phase_render(rrec, count=True)
+    comm.counts(rs.phase_plan(cam), rs.counts[1])
+    rs.phase_sizes()
+    comm.exchange(rs.phase_pack())
+    rs.phase_render(count=True)
+    return _band_pair_counts(rs)
+
+
+def _band_pair_counts(rs: RankStep) -> dict:
     px = (rs.prow1 - rs.prow0) * rs.W
-    out = {"M": rs.M, "E": rs.E, "P": px,
+    out = {"M": rs.R, "E": rs.E, "P": px,
            "I_f": int(rs.n_iter[:px].sum(dtype=torch.int64)),
            "C": int(rs.n_contrib[:px].sum(dtype=torch.int64)),
            "I_b": int(rs.n_last[:px].sum(dtype=torch.int64))}
@@ -891,40 +999,100 @@ def comm_pair_counts(rs: RankStep, comm: TorchComm, cam) -> dict:
     return out
 
 
-def emulated_step(ranks: list, cam, gt: torch.Tensor, it: int) -> torch.Tensor:
-    """The same phases for W ranks executed in sequence on ONE GPU with the
-    exchanges done by in-process copies (no kernel waits on another rank).
-    Used to check bitwise W-invariance on a single B200."""
-    W = len(ranks)
-    sent = [r.phase_project(cam) for r in ranks]
+class SpanTimer:
+    """Per-rank device time of named phases (CUDA event pairs), for ranks
+    whose phases interleave on one stream (the emulated step)."""
 
-    def exchange(sent_lists):
-        out = []
-        for dst in range(W):
-            parts = []
-            for src in range(W):
-                rec, cnt = sent_lists[src]
-                o = sum(cnt[:dst])
-                parts.append(rec[o:o + cnt[dst]])
-            out.append(torch.cat(parts, 0) if parts else None)
+    def __init__(self):
+        self.spans: list = []
+
+    def span(self, name: str):
+        timer = self
+
+        class _Span:
+            def __enter__(self_):
+                self_.a = torch.cuda.Event(enable_timing=True)
+                self_.a.record()
+
+            def __exit__(self_, *exc):
+                b = torch.cuda.Event(enable_timing=True)
+                b.record()
+                timer.spans.append((name, self_.a, b))
+                return False
+        return _Span()
+
+    def phases(self) -> dict:
+        torch.cuda.synchronize()
+        out: dict = {}
+        for name, a, b in self.spans:
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
         return out
 
-    recv = exchange(sent)
-    bounds = [r.phase_render(recv[i]) for i, r in enumerate(ranks)]
-    for i, r in enumerate(ranks):
+
+class _NoSpan:
+    def span(self, name):
+        import contextlib
+        return contextlib.nullcontext()
+
+
+def _emulated_exchange(ranks: list, ops: list) -> None:
+    """Deliver every rank's point-to-point segments by device copies."""
+    for src, rank_ops in enumerate(ops):
+        for peer, sends, _ in rank_ops:
+            recvs = next(r for p, _, r in ops[peer] if p == src)
+            for a, b in zip(sends, recvs):
+                if a.numel():
+                    b.copy_(a)
+
+
+def emulated_step(ranks: list, cam, gt: torch.Tensor, it: int, timers=None,
+                  count: bool = False):
+    """The same phases for W ranks executed in sequence on ONE GPU with the
+    exchanges done by in-process copies (no kernel waits on another rank).
+    Used to check bitwise W-invariance on a single B200.  timers: optional
+    per-rank SpanTimer list (each rank's device time per phase, i.e. what
+    its own GPU would spend outside the exchanges).  count=True: stop after
+    the forward with the pair counters (returns the per-rank counts)."""
+    W = len(ranks)
+    tm = timers or [_NoSpan()] * W
+    for r, t in zip(ranks, tm):
+        with t.span("project_plan"):
+            r.phase_plan(cam)
+    for dst in range(W):
+        for src in range(W):
+            ranks[dst].counts[1, src].copy_(ranks[src].counts[0, dst])
+    for r in ranks:
+        r.phase_sizes()
+    ops = []
+    for r, t in zip(ranks, tm):
+        with t.span("pack"):
+            ops.append(r.phase_pack())
+    _emulated_exchange(ranks, ops)
+    bounds = []
+    for r, t in zip(ranks, tm):
+        with t.span("bin_render"):
+            bounds.append(r.phase_render(count=count))
+    if count:
+        return [_band_pair_counts(r) for r in ranks]
+    for i, (r, t) in enumerate(zip(ranks, tm)):
         got_prev = bounds[i - 1][1] if i > 0 else None
         got_next = bounds[i + 1][0] if i + 1 < W else None
-        r.phase_loss(got_prev, got_next, gt)
+        with t.span("loss"):
+            r.phase_loss(got_prev, got_next, gt)
     total = torch.zeros_like(ranks[0].parts)
     for r in ranks:
         total += r.parts
     for r in ranks:
         r.parts.copy_(total)
     loss = ranks[0].finish_loss()
-    grads = [r.phase_backward() for r in ranks]
-    grecv = exchange(grads)
-    for i, r in enumerate(ranks):
-        r.phase_update(grecv[i], it)
+    gops = []
+    for r, t in zip(ranks, tm):
+        with t.span("backward_fold"):
+            gops.append(r.phase_backward())
+    _emulated_exchange(ranks, gops)
+    for r, t in zip(ranks, tm):
+        with t.span("owner_fold_chain_adam"):
+            r.phase_update(it)
     return loss
 
 

@@ -124,7 +124,20 @@ def _worker(rank, world, port, q):
         comm.allreduce_sum_(parts)
         ref = torch.cat([torch.tensor([0.1, 1e-17, -3.0, 1e300]) * (r + 1) for r in range(world)])
         ok_red = torch.equal(parts, ref)
-        q.put((rank, ok_a2a, ok_halo, ok_red))
+        # per-destination counts (3 int64 per pair) and point-to-point segments
+        mine = torch.tensor([[10 * rank + d, rank, d] for d in range(world)], dtype=torch.int64)
+        got = torch.empty_like(mine)
+        comm.counts(mine, got)
+        ok_counts = torch.equal(got, torch.tensor([[10 * s + rank, s, rank] for s in range(world)]))
+        peer = 1 - rank
+        keys = torch.arange(5, dtype=torch.int64) + 100 * rank
+        pay = torch.full((5, 16), rank, dtype=torch.int32)
+        rk = torch.zeros(7, dtype=torch.int64)
+        rp = torch.zeros((7, 16), dtype=torch.int32)
+        comm.exchange([(peer, [keys, pay], [rk[1:6], rp[1:6]])])
+        ok_counts &= torch.equal(rk[1:6], torch.arange(5) + 100 * peer) and \
+            bool((rp[1:6] == peer).all()) and int(rk[0]) == 0 and int(rk[6]) == 0
+        q.put((rank, ok_a2a and ok_counts, ok_halo, ok_red))
     finally:
         dist.destroy_process_group()
 
