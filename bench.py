@@ -831,7 +831,9 @@ def run_dist(args, world: int, rank: int, local: int):
                     "h2d_bytes_per_step": int(gt.numel()), "d2h_bytes_per_step": 8},
             "clocks": clk.summary(), "gpu_launches": D.LAUNCHES_PER_STEP * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "parity": parity,
-            "partition": {"bands_tile_rows": part.band_rows, "shard_sizes": smap.sizes},
+            "partition": {"bands_tile_rows": rs.part.band_rows, "initial": part.band_rows,
+                          "canon_rows": part.canon_rows, "shard_sizes": smap.sizes,
+                          "balance": rs.balance},
             "per_rank": per_rank,
         }
         emit(line)

@@ -315,6 +315,13 @@ int isg_band_fold(int64_t m, const int64_t *emit_off, const float *partials,
                   const int32_t *rect_sorted, const int32_t *order, const int64_t *gpos,
                   int32_t row_lo, int32_t canon_rows, double *gbuf, void *stream);
 
+/* Band raster cost per canonical block (load balance of the row bands):
+ * hist[(prow0 + y) / (16 * canon_rows)] += sum_x n_last[y][x] for the band's
+ * pixel rows [prow0, prow1) (n_last band-local, width per row), as exact
+ * integer sums in float64. */
+int isg_band_cost(const int32_t *n_last, int32_t prow0, int32_t prow1, int32_t width,
+                  int32_t canon_rows, double *hist, void *stream);
+
 /* Owner fold over the route plan (reduce_gradients_fused,
  * distributed.py:178-226): per shard row, the block records of the bands it
  * reached (seg[d]: HOST array of device pointers to band d's records for

@@ -100,6 +100,7 @@ SIGNATURES = {
     "isg_route_pack": [_I64, _P, _P, _P, _P, _P, _I32, _P, _P, _I32, _P, _P, _P, _P, _P],
     "isg_band_blocks": [_I64, _P, _I32, _I32, _I32, _P, _P],
     "isg_band_fold": [_I64, _P, _P, _P, _P, _P, _I32, _I32, _P, _P],
+    "isg_band_cost": [_P, _I32, _I32, _I32, _I32, _P, _P],
     "isg_owner_fold_plan": [_I64, _P, _P, _P, _I32, _I32, _P, _P, _P, _P],
     "isg_grad_rows": [_I64, _P, _P, _P, _P],
     "isg_owner_fold": [_I64, _P, _P, _P, _P, _P],

@@ -406,6 +406,28 @@ __global__ void __launch_bounds__(BF_THREADS) band_fold_kernel(
     if (live) st.finish();
 }
 
+// Raster cost of the band per canonical block: sum over its pixels of n_last
+// (the backward's last list position, a proxy of both raster passes), added
+// as integers to a float64 histogram over all blocks of the image (exact:
+// integer sums below 2^53 do not depend on the order of the atomics).
+__global__ void __launch_bounds__(256) band_cost_kernel(const int32_t *__restrict__ n_last,
+                                                        int prow0, int width, int block_px_rows,
+                                                        double *__restrict__ hist) {
+    const int row = blockIdx.x;  // pixel row inside the band
+    const int32_t *p = n_last + (int64_t)row * width;
+    long long s = 0;
+    for (int x = threadIdx.x; x < width; x += 256) s += p[x];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __shared__ long long sw[8];
+    if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < 8; w++) t += sw[w];
+        atomicAdd(hist + (prow0 + row) / block_px_rows, (double)t);
+    }
+}
+
 struct SegPtrs {
     const double *seg[MAX_BANDS];  // band d's gradient records for this shard
 };
@@ -600,6 +622,17 @@ extern "C" int isg_band_fold(int64_t m, const int64_t *emit_off, const float *pa
     if (m == 0) return 0;
     band_fold_kernel<<<blocks_for(m, BF_THREADS), BF_THREADS, 0, (cudaStream_t)stream>>>(
         m, emit_off, partials, (const int4 *)rect_sorted, order, gpos, row_lo, canon_rows, gbuf);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_band_cost(const int32_t *n_last, int32_t prow0, int32_t prow1, int32_t width,
+                              int32_t canon_rows, double *hist, void *stream) {
+    if (prow0 < 0 || prow1 < prow0 || width <= 0 || canon_rows < 1)
+        return (int)cudaErrorInvalidValue;
+    if (prow1 == prow0) return 0;
+    band_cost_kernel<<<prow1 - prow0, 256, 0, (cudaStream_t)stream>>>(n_last, prow0, width,
+                                                                     16 * canon_rows, hist);
     ISG_CHECK_LAUNCH();
     return 0;
 }

@@ -50,7 +50,7 @@ import torch
 from . import _lib as L
 
 TILE = 16
-CANON_ROWS = 8
+CANON_ROWS = 2
 # our kernels per sharded step (CUB scan/sort passes not counted):
 # preprocess, route_plan, route_scan, route_pack | depth tie fix, gather_rank,
 # finish_counts, bin_emit16_cull, tile_offsets16, raster_fwd_masked |
@@ -190,16 +190,44 @@ def partition_pixels(width: int, height: int, tile_size: int, workers: int,
     if weights is None:
         cuts = [round(w * n_blocks / workers) for w in range(workers + 1)]
     else:
-        cw = np.concatenate([[0.0], np.cumsum(np.asarray(weights, dtype=np.float64))])
-        cuts = [0]
-        for w in range(1, workers):
-            target = cw[-1] * w / workers
-            b = int(np.searchsorted(cw, target))
-            cuts.append(min(max(b, cuts[-1] + 1), n_blocks - (workers - w)))
-        cuts.append(n_blocks)
+        wts = np.asarray(weights, dtype=np.float64)
+        if wts.shape != (n_blocks,):
+            raise ValueError(f"weights: {wts.shape} != ({n_blocks},) canonical blocks")
+        cuts = minmax_cuts(wts, workers)
     band_rows = [min(c * canon_rows, tiles_y) for c in cuts]
     return PixelPartition(width, height, tile_size, workers, tiles_x, tiles_y, band_rows,
                           canon_rows)
+
+
+def minmax_cuts(weights: np.ndarray, parts: int) -> list:
+    """Contiguous cut of `weights` into `parts` non-empty groups that
+    minimises the largest group sum (exact DP over the cut positions, ties to
+    the earliest cut); cuts[0] = 0, cuts[parts] = len(weights)."""
+    w = np.asarray(weights, dtype=np.float64)
+    b = w.shape[0]
+    pre = np.concatenate([[0.0], np.cumsum(w)])
+    seg = pre[None, :] - pre[:, None]          # seg[i, j] = sum of w[i:j]
+    invalid = np.tril(np.ones((b + 1, b + 1), dtype=bool))  # j <= i: empty group
+    dp = np.full(b + 1, np.inf)
+    dp[0] = 0.0
+    args = []
+    for _ in range(parts):
+        m = np.maximum(dp[:, None], seg)
+        m[invalid] = np.inf
+        args.append(np.argmin(m, axis=0))
+        dp = m[args[-1], np.arange(b + 1)]
+    cuts = [b]
+    for a in reversed(args):
+        cuts.append(int(a[cuts[-1]]))
+    return cuts[::-1]
+
+
+def band_cost_ratio(weights: np.ndarray, band_rows: list, canon_rows: int) -> float:
+    """max / mean of the per-band sums of per-block costs."""
+    w = np.asarray(weights, dtype=np.float64)
+    sums = np.array([w[band_rows[k] // canon_rows:(band_rows[k + 1] + canon_rows - 1)
+                      // canon_rows].sum() for k in range(len(band_rows) - 1)])
+    return float(sums.max() / max(sums.mean(), 1e-300))
 
 
 def route_rows(tile_min, tile_max, part: PixelPartition) -> np.ndarray:
@@ -459,7 +487,6 @@ class RankStep:
         na = ctypes.c_int32(0)
         L.lib().isg_loss_partials_size(self.H, self.W, ctypes.byref(nf), ctypes.byref(na))
         self.n_ps, self.n_pl = nf.value, na.value
-        self.parts = torch.zeros(self.n_ps + self.n_pl, dtype=torch.float64, device=d)
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=d)
         self.ws = [L.Workspace() for _ in range(4)]
         # receive-side / band buffers (grown on demand)
@@ -468,6 +495,21 @@ class RankStep:
         self.rect_sorted = self.feat_sorted = self.emit_off = None
         self.tk = self.tv = self.tk_sorted = self.entries = self.partials = None
         self.cmask = self.nb = self.gpos = self.gbuf = self.grad_recv = None
+        # band-side image buffers at full-image size: bands move when the
+        # partition is rebalanced, the buffers do not
+        self.window = torch.zeros((self.H, self.W, 3), dtype=torch.float32, device=d)
+        self.t_final = torch.empty(self.H * self.W, dtype=torch.float32, device=d)
+        self.n_last = torch.empty(self.H * self.W, dtype=torch.int32, device=d)
+        self.dl = torch.empty((self.H * self.W, 3), dtype=torch.float32, device=d)
+        # load balance: per-canonical-block raster cost (all-reduced with the
+        # loss partials), its moving average, re-cut every REBALANCE_EVERY steps
+        self.n_blk = (part.tiles_y + part.canon_rows - 1) // part.canon_rows
+        self.parts = torch.zeros(self.n_ps + self.n_pl + self.n_blk, dtype=torch.float64,
+                                 device=d)
+        self.cost_host = torch.zeros(self.n_blk, dtype=torch.float64).pin_memory()
+        self.cost_ema = None
+        self.pending_part = None
+        self.balance = {"recuts": 0, "ratio_equal": None, "ratio_now": None}
         self.set_partition(part)
 
     def set_partition(self, part: PixelPartition) -> None:
@@ -481,14 +523,7 @@ class RankStep:
         self.band_host = (ctypes.c_int32 * (self.world + 1))(*part.band_rows)
         self.n_tiles = (self.trow1 - self.trow0) * self.tiles_x
         self.tile_bits = _bits(self.n_tiles)
-        d = self.dev
-        rows = self.win1 - self.win0
-        self.window = torch.zeros((max(rows, 1), self.W, 3), dtype=torch.float32, device=d)
-        band_px = (self.prow1 - self.prow0) * self.W
-        self.t_final = torch.empty(max(band_px, 1), dtype=torch.float32, device=d)
-        self.n_last = torch.empty(max(band_px, 1), dtype=torch.int32, device=d)
-        self.dl = torch.empty((max(band_px, 1), 3), dtype=torch.float32, device=d)
-        self.offsets = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=d)
+        self.offsets = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=self.dev)
 
     def _vptr(self, t: torch.Tensor, row0: int, row_elems: int) -> int:
         """Virtual base pointer so that global row `row0` maps to t's start."""
@@ -500,6 +535,9 @@ class RankStep:
         (W, 3) per-band totals (splat records, block records, tile entries)
         to exchange."""
         lib, s = L.lib(), L.stream_ptr()
+        if self.pending_part is not None:
+            self.set_partition(self.pending_part)
+            self.pending_part = None
         c = self.cloud
         self.cam_struct = L.camera_struct(cam)
         if self.n:
@@ -522,6 +560,8 @@ class RankStep:
         """Read this shard's totals and every source's totals for this band
         (counts[1], filled by the counts exchange) and size the iteration."""
         self.counts_host.copy_(self.counts, non_blocking=True)
+        # the previous step's all-reduced band costs ride on the same sync
+        self.cost_host.copy_(self.parts[self.n_ps + self.n_pl:], non_blocking=True)
         torch.cuda.current_stream().synchronize()
         h = self.counts_host.numpy()
         mine, recv = h[0], h[1]
@@ -673,7 +713,8 @@ class RankStep:
         if from_prev is not None and from_prev.shape[0]:
             self.window[:from_prev.shape[0]].copy_(from_prev)
         if from_next is not None and from_next.shape[0]:
-            self.window[self.prow1 - self.win0:].copy_(from_next)
+            o = self.prow1 - self.win0
+            self.window[o:o + from_next.shape[0]].copy_(from_next)
         self.parts.zero_()
         u8 = 1 if gt.dtype == torch.uint8 else 0
         if self.prow1 > self.prow0:
@@ -689,6 +730,10 @@ class RankStep:
                                       L.ptr(gt), u8, float(self.cfg.lambda_dssim),
                                       L.ptr(self.dl), L.ptr(self.parts),
                                       self.parts.data_ptr() + 8 * self.n_ps, s), "isg_loss_rows")
+            L.check(lib.isg_band_cost(L.ptr(self.n_last), self.prow0, self.prow1, self.W,
+                                      self.part.canon_rows,
+                                      self.parts.data_ptr() + 8 * (self.n_ps + self.n_pl), s),
+                    "isg_band_cost")
         return self.parts
 
     def finish_loss(self):
@@ -736,6 +781,39 @@ class RankStep:
             c0, c1 = int(self.grecv_off[peer]), int(self.grecv_off[peer + 1])
             ops.append((peer, [self.gbuf[a:b]], [self.grad_recv[c0:c1]]))
         return ops
+
+    REBALANCE_EVERY = 8
+    COST_EMA = 0.25
+
+    def rebalance(self) -> None:
+        """Host side of the load balance, run after the step's launches are
+        issued (it overlaps the GPU): fold the previous step's all-reduced
+        per-block costs into a moving average and, every REBALANCE_EVERY
+        steps, re-cut the bands (exact min-max cut) for the next step if that
+        lowers the predicted max/mean by >= 1 %.  Every rank sees the same
+        all-reduced costs, so every rank makes the same cut."""
+        if self.world == 1:
+            return
+        cost = self.cost_host.numpy().astype(np.float64)
+        tot = cost.sum()
+        if tot <= 0:
+            return
+        cost = cost / tot
+        self.cost_ema = cost if self.cost_ema is None else \
+            (1.0 - self.COST_EMA) * self.cost_ema + self.COST_EMA * cost
+        p = self.part
+        self.balance["ratio_now"] = band_cost_ratio(cost, p.band_rows, p.canon_rows)
+        eq = partition_pixels(p.width, p.height, p.tile_size, p.workers, p.canon_rows)
+        self.balance["ratio_equal"] = band_cost_ratio(cost, eq.band_rows, p.canon_rows)
+        self._steps_seen = getattr(self, "_steps_seen", 0) + 1
+        if self._steps_seen % self.REBALANCE_EVERY:
+            return
+        new = partition_pixels(p.width, p.height, p.tile_size, p.workers, p.canon_rows,
+                               weights=self.cost_ema)
+        now = band_cost_ratio(self.cost_ema, p.band_rows, p.canon_rows)
+        if band_cost_ratio(self.cost_ema, new.band_rows, p.canon_rows) <= 0.99 * now:
+            self.pending_part = new
+            self.balance["recuts"] += 1
 
     # -- phase 6: owner fold + chain + Adam -------------------------------
     def phase_update(self, it: int):
@@ -975,6 +1053,7 @@ def comm_step(rs: RankStep, comm: TorchComm, cam, gt: torch.Tensor, it: int,
     _mark(timer, "exchange_grads")
     rs.phase_update(it)
     _mark(timer, "owner_fold_chain_adam")
+    rs.rebalance()
     return loss
 
 
@@ -1093,6 +1172,8 @@ def emulated_step(ranks: list, cam, gt: torch.Tensor, it: int, timers=None,
     for r, t in zip(ranks, tm):
         with t.span("owner_fold_chain_adam"):
             r.phase_update(it)
+    for r in ranks:
+        r.rebalance()
     return loss
 
 

@@ -39,10 +39,13 @@ from .training import (EvalRecord, TrainConfig, TrainDataset, TrainReport, Train
 
 TILE = 16
 # Canonical fold grouping (tile rows per block): every per-splat gradient is
-# summed tiles-ascending inside 8-tile-row blocks, then block sums ascending.
+# summed tiles-ascending inside 2-tile-row blocks, then block sums ascending.
 # Pixel bands of the multi-GPU step are unions of whole blocks, which makes
-# the result bitwise independent of the GPU count (see csrc/dist.cu).
-CANON_ROWS = 8
+# the result bitwise independent of the GPU count (see csrc/dist.cu).  Two
+# rows: bands can be cut at 32-pixel granularity for load balance
+# (tools/band_balance.py: 8 rows leave 1.26-1.30 max/mean at W=8) for ~1.7
+# gradient records per splat instead of ~1.2.
+CANON_ROWS = 2
 
 
 def _grow(buf: torch.Tensor | None, n: int, shape_tail=(), dtype=torch.float32, device=None,

@@ -41,15 +41,30 @@ def test_row_bands_are_unions_of_canonical_blocks(workers):
 
 def test_row_bands_need_enough_blocks():
     with pytest.raises(ValueError):
-        D.partition_pixels(64, 64, 16, 2)  # 4 tile rows = 1 block of 8
+        D.partition_pixels(64, 64, 16, 3)  # 4 tile rows = 2 blocks of 2
     part = D.partition_pixels(64, 64, 16, 4, canon_rows=1)
     assert part.band_rows == [0, 1, 2, 3, 4]
 
 
 def test_cost_weighted_bands():
-    part = D.partition_pixels(2048, 2048, 16, 2, weights=[10, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1,
-                                                          1, 1, 1, 1, 1])
+    part = D.partition_pixels(2048, 2048, 16, 2, weights=[40] + [1] * 63)
     assert part.band_rows[1] < 64  # the heavy first block pulls the cut up
+    with pytest.raises(ValueError):
+        D.partition_pixels(2048, 2048, 16, 2, weights=[1] * 16)
+
+
+def test_minmax_cuts_is_optimal():
+    import itertools
+    rng = np.random.default_rng(0)
+    for _ in range(300):
+        b = int(rng.integers(2, 11))
+        p = int(rng.integers(1, b + 1))
+        w = rng.random(b) * (rng.random(b) < 0.8)
+        c = D.minmax_cuts(w, p)
+        assert c[0] == 0 and c[-1] == b and all(c[k] < c[k + 1] for k in range(p))
+        best = min(max(w[a:e].sum() for a, e in zip((0,) + cs, cs + (b,)))
+                   for cs in itertools.combinations(range(1, b), p - 1))
+        assert max(w[c[k]:c[k + 1]].sum() for k in range(p)) <= best + 1e-12
 
 
 def test_route_rows_band_mask():

@@ -7,7 +7,8 @@ every data-plane kernel of the multi-GPU step runs on real config-2/3 data:
 route plan and pack, band binning, halo'd loss, band fold, owner fold, and
 the sharded densify + rebalance.  The run must reproduce the single-GPU
 engine bit for bit: every loss and every final parameter, for W = 2, 4, 8
-over 20 iterations with a densify event at iteration 10 -- the reference's
+over 20 iterations with a densify event at iteration 10 and the bands
+re-cut for load balance while the run goes on -- the reference's
 headline property (tests/test_acceptance.py:101-123 of the reference).
 """
 
@@ -76,7 +77,7 @@ def test_sharded_run_bitwise_equals_single_gpu_at_scale(name, workers):
     P, wl, sched, ext, cloud0, ref, cfg = _workload(name)
     ranks, smap, part = D.make_ranks(cloud0.copy(), wl.resolution, wl.resolution, cfg, ext,
                                      workers, torch.device("cuda", 0))
-    assert part.canon_rows == 8
+    assert part.canon_rows == D.CANON_ROWS
     losses = []
     for it in range(1, ITERS + 1):
         loss = D.emulated_step(ranks, wl.cameras[sched[it - 1]], wl.images_u8[it - 1], it)
@@ -84,6 +85,8 @@ def test_sharded_run_bitwise_equals_single_gpu_at_scale(name, workers):
         if D.densify_due(cfg, it):
             ranks = D.emulated_densify(ranks, it)
     got = D.gather_cloud(ranks)
+    print(f"{name} W={workers}: bands {part.band_rows} -> {ranks[0].part.band_rows}, "
+          f"balance {ranks[0].balance}")
     assert losses == ref["losses"], (losses, ref["losses"])
     assert got.count == ref["cloud"].count
     for k in P.PARAM_NAMES:
