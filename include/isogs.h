@@ -237,21 +237,58 @@ int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t ti
  * with feat_dtype ISG_F32.  contrib_mask holds isg_contrib_mask_words(E,
  * n_tiles) uint32 words for a launch over n_tiles tiles with E list entries;
  * it needs no initialisation.  The two calls must see the same tiles,
- * offsets and n_last. */
+ * offsets and n_last.  tile_order (optional, n_tiles entries): CTA b
+ * processes list position tile_order[b] -- the launch order only (heaviest
+ * lists first, isg_tile_order); results do not depend on it. */
 int64_t isg_contrib_mask_words(int64_t n_entries, int32_t n_tiles);
+
+/* Backward list chunking (optional argument of the masked raster pair): the
+ * backward runs each tile's list as chunks of `chunk` entries (a multiple of
+ * 32), each its own CTA, so a long list no longer serialises the end of the
+ * launch.  The forward leaves, per pixel, (T, r, g, b) before every internal
+ * chunk boundary in `state` (isg_chunk_state_floats floats); the backward
+ * starts a chunk from that state (S = image - accumulated colour).  `items`
+ * / `n_items` come from isg_chunk_items (max_items = isg_chunk_items_max).
+ * The chunk size must not depend on the partition (bitwise W-invariance). */
+typedef struct isg_chunks {
+    int32_t chunk;          /* entries per backward work item; 0 = one item per tile */
+    float *state;           /* forward -> backward state at chunk boundaries */
+    const int32_t *items;   /* (tile list position, chunk) int32 pairs */
+    const int32_t *n_items; /* device count of items */
+    int32_t max_items;      /* grid of the backward launch */
+    const float *image;     /* the forward's float32 image (same pixels as t_final) */
+    int32_t *tile_last;     /* forward -> items: last composited position per (tile, quadrant), 4 x n_tiles */
+} isg_chunks;
+int64_t isg_chunk_state_floats(int64_t n_entries, int32_t n_tiles, int32_t chunk);
+int32_t isg_chunk_items_max(int64_t n_entries, int32_t n_tiles, int32_t chunk);
+/* Work items in launch order, built between the forward and the backward:
+ * for every list position of tile_order (NULL: 0..n_tiles-1) with tile_last
+ * maximum L over its quadrants, ceil(L / chunk) chunks (at least one; the
+ * last one runs to the end of the list, whose entries past L contribute
+ * nothing), written as (position, chunk | 1 << 30 for the last) pairs;
+ * *n_items (device) = their number. */
+int isg_chunk_items(int32_t n_tiles, const int32_t *offsets, const int32_t *tile_order,
+                    const int32_t *tile_last, int32_t chunk, int32_t *items, int32_t *n_items,
+                    void *stream);
 int isg_raster_fwd_masked(int32_t width, int32_t height, int32_t tiles_x, int32_t row_lo,
                           int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
-                          const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
+                          const int32_t *tile_order, const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
                           const double *bg, void *image, int32_t image_dtype, void *t_final,
                           int32_t *n_last, int32_t *n_contrib, int32_t *n_iter, int64_t *touched,
-                          uint32_t *contrib_mask, void *stream);
+                          uint32_t *contrib_mask, const isg_chunks *chunks, void *stream);
 int isg_raster_bwd_masked(int32_t width, int32_t height, int32_t tiles_x, int32_t row_lo,
                           int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
-                          const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
+                          const int32_t *tile_order, const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
                           const int32_t *rect_sorted, const int64_t *emit_off, const double *bg,
                           const void *t_final, const int32_t *n_last, const void *dl_dimage,
                           int32_t dl_dtype, void *partials, const uint32_t *contrib_mask,
-                          void *stream);
+                          const isg_chunks *chunks, void *stream);
+
+/* Heaviest-first launch order of n_tiles tile lists: keys16[t] = 65535 -
+ * min(list length, 65535) and vals[t] = t, to be sorted ascending with
+ * isg_sort_u16 (16 bits) into the tile_order of the raster pair. */
+int isg_tile_order_keys(int32_t n_tiles, const int32_t *offsets, uint16_t *keys16,
+                        int32_t *vals, void *stream);
 
 /* Ordered fold (_reduce_scratch, _kernels.py:398-411): for rank r < m sum its
  * subtotal slots [emit_off[r], emit_off[r+1]) in float64 and write

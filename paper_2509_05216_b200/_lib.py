@@ -49,6 +49,14 @@ class AdamConsts_t(ctypes.Structure):
     _fields_ = [(k, ctypes.c_double) for k in ("b1", "omb1", "b2", "omb2", "bc1", "bc2", "lr", "eps")]
 
 
+class Chunks_t(ctypes.Structure):
+    """isg_chunks (isogs.h): backward list chunking of the masked raster pair."""
+    _fields_ = [("chunk", ctypes.c_int32), ("state", ctypes.c_void_p),
+                ("items", ctypes.c_void_p), ("n_items", ctypes.c_void_p),
+                ("max_items", ctypes.c_int32), ("image", ctypes.c_void_p),
+                ("tile_last", ctypes.c_void_p)]
+
+
 class TrainState_t(ctypes.Structure):
     _fields_ = ([(k, ctypes.c_void_p) for k in (
         "positions", "log_scales", "rotations", "opacity_logits", "sh",
@@ -80,10 +88,14 @@ SIGNATURES = {
     "isg_tile_offsets16": [_I64, _P, _I32, _P, _P],
     "isg_raster_fwd": [_I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _I32,
                        _P, _P, _P, _P, _P, _P],
-    "isg_raster_fwd_masked": [_I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _I32,
-                              _P, _P, _P, _P, _P, _P, _P],
+    "isg_raster_fwd_masked": [_I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P,
+                              _I32, _P, _P, _P, _P, _P, _P, _P, _P],
     "isg_raster_bwd_masked": [_I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P,
-                              _P, _P, _P, _I32, _P, _P, _P],
+                              _P, _P, _P, _P, _I32, _P, _P, _P, _P],
+    "isg_chunk_state_floats": [_I64, _I32, _I32],
+    "isg_chunk_items_max": [_I64, _I32, _I32],
+    "isg_chunk_items": [_I32, _P, _P, _P, _I32, _P, _P, _P],
+    "isg_tile_order_keys": [_I32, _P, _P, _P, _P],
     "isg_contrib_mask_words": [_I64, _I32],
     "isg_loss_l1_dssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _I32, _D, _P, _P, _P],
     "isg_ssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _P, _P],
@@ -125,7 +137,7 @@ SIGNATURES = {
 }
 
 
-RET_I64 = ("isg_contrib_mask_words",)
+RET_I64 = ("isg_contrib_mask_words", "isg_chunk_state_floats")
 
 
 def lib():

@@ -165,6 +165,14 @@ __global__ void tile_offsets_kernel(int64_t e, const K *__restrict__ keys, int n
     offsets[t] = (int32_t)lo;
 }
 
+__global__ void tile_order_keys_kernel(int n_tiles, const int32_t *__restrict__ offsets,
+                                       uint16_t *__restrict__ keys, int32_t *__restrict__ vals) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    keys[t] = (uint16_t)(65535 - min(offsets[t + 1] - offsets[t], 65535));
+    vals[t] = t;
+}
+
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace isg
@@ -251,6 +259,17 @@ extern "C" int isg_sort_u32(void *workspace, size_t *ws_bytes, const uint32_t *k
                                                     vals_in, vals_out, (int)n, begin_bit,
                                                     end_bit, (cudaStream_t)stream);
     return (int)e;
+}
+
+extern "C" int isg_tile_order_keys(int32_t n_tiles, const int32_t *offsets, uint16_t *keys16,
+                                   int32_t *vals, void *stream) {
+    if (n_tiles < 0 || (n_tiles > 0 && (!offsets || !keys16 || !vals)))
+        return (int)cudaErrorInvalidValue;
+    if (n_tiles == 0) return 0;
+    tile_order_keys_kernel<<<blocks_for(n_tiles, 256), 256, 0, (cudaStream_t)stream>>>(
+        n_tiles, offsets, keys16, vals);
+    ISG_CHECK_LAUNCH();
+    return 0;
 }
 
 static int bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_t *sorted_keys,

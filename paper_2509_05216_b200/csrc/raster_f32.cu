@@ -114,6 +114,16 @@ __device__ __forceinline__ int ldsu8(uint32_t a) {
     return (int)v;
 }
 
+// Backward work items: a tile's list is cut into chunks of `chunk` entries
+// (a multiple of WB; 0 = one chunk per tile) that run as separate CTAs; the
+// forward leaves, per pixel, (T, r, g, b) before every internal chunk
+// boundary at cstate[256 * chunk_slot + pixel].  Slots are unique per
+// (tile, boundary): e0 / chunk + tl + k <= E / chunk + n_tiles.
+constexpr int LAST_CHUNK = 1 << 30;  // item flag: the chunk runs to the list end
+__device__ __forceinline__ int64_t chunk_slot(int e0, int tl, int base, int chunk) {
+    return (int64_t)(e0 / chunk) + tl + base / chunk;
+}
+
 // Forward kernel modes: TOUCH counts per-splat touches (the reference's
 // `touched`), STATS records n_contrib / n_iter (bench statistics only).
 constexpr int F_TOUCH = 1, F_STATS = 2;
@@ -193,10 +203,12 @@ constexpr int WB = 32;  // per-warp staging batch
 template <int MODE>
 __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
-    const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
-    const float *__restrict__ feat, float bg0, float bg1, float bg2, void *image, int image_f64,
+    const int32_t *__restrict__ tile_order, const int32_t *__restrict__ offsets,
+    const int32_t *__restrict__ entries, const float *__restrict__ feat, float bg0, float bg1,
+    float bg2, void *image, int image_f64,
     float *__restrict__ t_final, int32_t *__restrict__ n_last, int32_t *__restrict__ n_contrib,
-    int32_t *__restrict__ n_iter, int64_t *__restrict__ touched, uint32_t *__restrict__ cmask) {
+    int32_t *__restrict__ n_iter, int64_t *__restrict__ touched, uint32_t *__restrict__ cmask,
+    int chunk, float4 *__restrict__ cstate, int32_t *__restrict__ qlast) {
     constexpr bool TOUCH = MODE & F_TOUCH;
     // slot WB of each warp's slice is a sentinel entry that never composites
     // (opacity 0): odd lists are padded with it, so entries go two at a time
@@ -204,7 +216,7 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
     __shared__ float4 scol_all[NW][WB + 1];
     __shared__ int srank_all[NW][TOUCH ? WB : 1];
     __shared__ unsigned char slist_all[NW][WB + 1];
-    const int tl = blockIdx.x;
+    const int tl = tile_order ? tile_order[blockIdx.x] : blockIdx.x;
     const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
     const int ty = tid / tiles_x, tx = tid - ty * tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -232,6 +244,15 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
     int last0 = 0, last1 = 0, cnt0 = 0, cnt1 = 0, it0 = 0, it1 = 0;
     for (int base = 0; base < n_ent; base += WB) {
         if (__all_sync(FULL, fpy0 == FINF && fpy1 == FINF)) break;
+        if (cstate && base > 0 && base % chunk == 0) {
+            // state before entry `base` for the backward's chunk ending there
+            // (a warp with every pixel done has left the loop: the backward
+            // never reads a boundary past a pixel's last contributor)
+            float4 *cs = cstate + 256 * chunk_slot(e0, tl, base, chunk);
+            const int c = (warp & 1) * 8 + (lane & 7), r = (warp >> 1) * 8 + (lane >> 3);
+            cs[16 * r + c] = make_float4(t0, r0, g0, b0);
+            cs[16 * (r + 4) + c] = make_float4(t1, r1, g1, b1);
+        }
         const int j = base + lane;
         bool alive = false;
         if (j < n_ent) {
@@ -296,6 +317,14 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
             if (lane == 0) cmask[4 * ((int64_t)(e0 >> 5) + tl + (base >> 5)) + warp] = cm;
         }
         __syncwarp();  // the slice is restaged next batch
+    }
+    if (qlast) {
+        // the quadrant's last composited list position: the backward cuts
+        // chunks only below it (past it every entry's subtotal is zero)
+        int ql = max(last0, last1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ql = max(ql, __shfl_xor_sync(FULL, ql, o));
+        if (lane == 0) qlast[4 * tl + warp] = ql;
     }
 #pragma unroll
     for (int p = 0; p < 2; p++) {
@@ -448,14 +477,17 @@ __device__ __forceinline__ int ld_volatile(const int *p) {
 
 constexpr int BNT = 64;  // backward threads per tile (two 16x8 halves)
 
-template <typename DL, bool MASK>
+template <typename DL, bool MASK, bool CHUNKED>
 __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
-    const int32_t *__restrict__ offsets, const int32_t *__restrict__ entries,
-    const float *__restrict__ feat, const int4 *__restrict__ rect_sorted,
+    const int32_t *__restrict__ tile_order, const int32_t *__restrict__ offsets,
+    const int32_t *__restrict__ entries, const float *__restrict__ feat,
+    const int4 *__restrict__ rect_sorted,
     const int64_t *__restrict__ emit_off, float bg0, float bg1, float bg2,
     const float *__restrict__ t_final, const int32_t *__restrict__ n_last,
-    const DL *__restrict__ dl, float *__restrict__ partials, const uint32_t *__restrict__ cmask) {
+    const DL *__restrict__ dl, float *__restrict__ partials, const uint32_t *__restrict__ cmask,
+    const int2 *__restrict__ items, const int32_t *__restrict__ n_items, int chunk,
+    const float4 *__restrict__ cstate, const float *__restrict__ image) {
     constexpr int NH = BNT / 32;  // warps per tile: one per 16x8 half
     __shared__ float4 sgh_all[NH][WB][2];
     __shared__ float4 scol_all[NH][WB];
@@ -464,7 +496,15 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
     __shared__ unsigned spres[RING][NH];
     __shared__ int sarrive[RING];
     __shared__ int sfolded[RING];
-    const int tl = blockIdx.x;
+    int tl, ck = 0;  // tile list position, chunk
+    if (CHUNKED) {
+        if ((int)blockIdx.x >= __ldg(n_items)) return;
+        const int2 it = items[blockIdx.x];
+        tl = it.x;
+        ck = it.y;  // chunk index | LAST_CHUNK
+    } else {
+        tl = tile_order ? tile_order[blockIdx.x] : blockIdx.x;
+    }
     const int tid = tile_ids ? tile_ids[tl] : row_lo * tiles_x + tl;
     const int ty = tid / tiles_x, tx = tid - ty * tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -473,7 +513,14 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
     const int pyb = ty * 16 + warp * 8 + (lane >> 4);
     const float fpx = (float)px;
     const float qx0 = (float)(tx * 16), qy0 = (float)(ty * 16 + warp * 8);
-    const int e0 = offsets[tl], n_ent = offsets[tl + 1] - e0;
+    const int e0t = offsets[tl], n_ent = offsets[tl + 1] - e0t;
+    // this item's entries [c_a, c_b) of the tile's list; the walk below is
+    // relative to c_a (entries, list positions, contribution-mask words), so
+    // the chunked and whole-tile instantiations run the same loop
+    const int c_a = CHUNKED ? (ck & ~LAST_CHUNK) * chunk : 0;
+    const int c_b = CHUNKED && !(ck & LAST_CHUNK) ? c_a + chunk : n_ent;
+    const int e0 = e0t + c_a, n_item = c_b - c_a;
+    const int64_t cm_base = 4 * ((int64_t)(e0t >> 5) + tl + (c_a >> 5)) + 2 * warp;
     const int my_slot = bfly_slot(lane);
     float4(&sgh)[WB][2] = sgh_all[warp];
     float4(&scol)[WB] = scol_all[warp];
@@ -501,8 +548,20 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
             wg[q] = (float)dl[3 * pix + 1];
             wb[q] = (float)dl[3 * pix + 2];
         }
-        // Q = sum_c w_c S_c with S_c starting at T_final * bg_c
-        Q[q] = wr[q] * (T[q] * bg0) + wg[q] * (T[q] * bg1) + wb[q] * (T[q] * bg2);
+        if (CHUNKED && last[q] > c_b) {
+            // the pixel composited past this chunk: start from the forward's
+            // state before entry c_b, with S = image - colour accumulated so far
+            const float4 st = cstate[256 * chunk_slot(e0t, tl, c_b, chunk) +
+                                     16 * (pyb + 2 * q - ty * 16) + (px - tx * 16)];
+            const int64_t pix = (int64_t)(pyb + 2 * q) * W + px;
+            T[q] = st.x;
+            Q[q] = wr[q] * (image[3 * pix] - st.y) + wg[q] * (image[3 * pix + 1] - st.z) +
+                   wb[q] * (image[3 * pix + 2] - st.w);
+        } else {
+            // Q = sum_c w_c S_c with S_c starting at T_final * bg_c
+            Q[q] = wr[q] * (T[q] * bg0) + wg[q] * (T[q] * bg1) + wb[q] * (T[q] * bg2);
+        }
+        last[q] -= c_a;  // item-relative (<= 0: nothing of this item)
     }
     // nothing is composited at j >= wm; wq0 / wq1: the same bound over the
     // left / right 8x8 quadrant of this half (columns lane & 8)
@@ -516,9 +575,9 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
 
     // batches of WB entries aligned at the list start (the forward's batches,
     // so the contribution masks line up), walked last to first
-    const int n_b = (n_ent + WB - 1) / WB;
+    const int n_b = (n_item + WB - 1) / WB;
     for (int bi = 0; bi < n_b; bi++) {
-        const int start = (n_b - 1 - bi) * WB, end = min(start + WB, n_ent);
+        const int start = (n_b - 1 - bi) * WB, end = min(start + WB, n_item);
         const int rs = bi % RING;
         if (lane == 0)
             while (ld_volatile(&sfolded[rs]) != bi - RING) __nanosleep(BWD_SLEEP);
@@ -529,7 +588,7 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
             // the forward's contribution masks of the half's two quadrants:
             // exactly the entries some pixel of the half composited (a
             // quadrant's mask is valid while its forward warp was running)
-            const int64_t w = 4 * ((int64_t)(e0 >> 5) + tl + (start >> 5)) + 2 * warp;
+            const int64_t w = cm_base + 4 * (start >> 5);
             unsigned bm = 0u;
             if (start < wq0) bm |= __ldg(cmask + w);
             if (start < wq1) bm |= __ldg(cmask + w + 1);
@@ -640,16 +699,22 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
 }  // namespace f32
 
 void launch_raster_fwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
-                           const int32_t *tile_ids, const int32_t *offsets, const int32_t *entries,
+                           const int32_t *tile_ids, const int32_t *tile_order,
+                           const int32_t *offsets, const int32_t *entries,
                            const float *feat, float bg0, float bg1, float bg2, void *image,
                            int image_f64, float *t_final, int32_t *n_last, int32_t *n_contrib,
-                           int32_t *n_iter, int64_t *touched, uint32_t *cmask, cudaStream_t s) {
+                           int32_t *n_iter, int64_t *touched, uint32_t *cmask,
+                           const ChunkArgs *ch, cudaStream_t s) {
     const int mode = (touched ? f32::F_TOUCH : 0) | (n_contrib || n_iter ? f32::F_STATS : 0);
+    const int chunk = ch ? ch->chunk : 0;
+    float4 *cstate = ch && ch->chunk ? (float4 *)ch->state : nullptr;
+    int32_t *qlast = ch && ch->chunk ? ch->tile_last : nullptr;
 #define ISG_FWD(M)                                                                               \
-    f32::fwd_kernel<M><<<n_tiles, f32::NT, 0, s>>>(W, H, tiles_x, row_lo, tile_ids, offsets,     \
+    f32::fwd_kernel<M><<<n_tiles, f32::NT, 0, s>>>(W, H, tiles_x, row_lo, tile_ids, tile_order,  \
+                                                   offsets,                                      \
                                                    entries, feat, bg0, bg1, bg2, image,          \
                                                    image_f64, t_final, n_last, n_contrib, n_iter, \
-                                                   touched, cmask)
+                                                   touched, cmask, chunk, cstate, qlast)
     switch (mode) {
         case 0: ISG_FWD(0); break;
         case 1: ISG_FWD(1); break;
@@ -661,30 +726,45 @@ void launch_raster_fwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
 
 template <typename DL>
 void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
-                           const int32_t *tile_ids, const int32_t *offsets, const int32_t *entries,
+                           const int32_t *tile_ids, const int32_t *tile_order,
+                           const int32_t *offsets, const int32_t *entries,
                            const float *feat, const int4 *rect_sorted, const int64_t *emit_off,
                            float bg0, float bg1, float bg2, const float *t_final,
                            const int32_t *n_last, const DL *dl, float *partials,
-                           const uint32_t *cmask, cudaStream_t s) {
-    if (cmask)
-        f32::bwd_kernel<DL, true><<<n_tiles, f32::BNT, 0, s>>>(
-            W, H, tiles_x, row_lo, tile_ids, offsets, entries, feat, rect_sorted, emit_off, bg0, bg1,
-            bg2, t_final, n_last, dl, partials, cmask);
-    else
-        f32::bwd_kernel<DL, false><<<n_tiles, f32::BNT, 0, s>>>(
-            W, H, tiles_x, row_lo, tile_ids, offsets, entries, feat, rect_sorted, emit_off, bg0, bg1,
-            bg2, t_final, n_last, dl, partials, nullptr);
+                           const uint32_t *cmask, const ChunkArgs *ch, cudaStream_t s) {
+    const bool chunked = ch && ch->chunk;
+    const int grid = chunked ? ch->max_items : n_tiles;
+    const int2 *items = chunked ? (const int2 *)ch->items : nullptr;
+    const int32_t *n_items = chunked ? ch->n_items : nullptr;
+    const int chunk = chunked ? ch->chunk : 0;
+    const float4 *cstate = chunked ? (const float4 *)ch->state : nullptr;
+    const float *image = chunked ? ch->image : nullptr;
+#define ISG_BWD32(MASK, CH)                                                                  \
+    f32::bwd_kernel<DL, MASK, CH><<<grid, f32::BNT, 0, s>>>(                                     \
+        W, H, tiles_x, row_lo, tile_ids, tile_order, offsets, entries, feat, rect_sorted,        \
+        emit_off, bg0, bg1, bg2, t_final, n_last, dl, partials, MASK ? cmask : nullptr, items,    \
+        n_items, chunk, cstate, image)
+    if (cmask) {
+        if (chunked) ISG_BWD32(true, true);
+        else ISG_BWD32(true, false);
+    } else {
+        ISG_BWD32(false, false);  // the unmasked launch is never chunked
+    }
+#undef ISG_BWD32
 }
 
 template void launch_raster_bwd_f32<float>(int, int, int, int, int, const int32_t *,
+                                           const int32_t *,
                                            const int32_t *, const int32_t *, const float *,
                                            const int4 *, const int64_t *, float, float, float,
                                            const float *, const int32_t *, const float *, float *,
-                                           const uint32_t *, cudaStream_t);
+                                           const uint32_t *, const ChunkArgs *, cudaStream_t);
 template void launch_raster_bwd_f32<double>(int, int, int, int, int, const int32_t *,
+                                            const int32_t *,
                                             const int32_t *, const int32_t *, const float *,
                                             const int4 *, const int64_t *, float, float, float,
                                             const float *, const int32_t *, const double *,
-                                            float *, const uint32_t *, cudaStream_t);
+                                            float *, const uint32_t *, const ChunkArgs *,
+                                            cudaStream_t);
 
 }  // namespace isg

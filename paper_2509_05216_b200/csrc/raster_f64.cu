@@ -441,10 +441,11 @@ using namespace isg;
 
 static int raster_fwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
                       int32_t row_lo, int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
+                      const int32_t *tile_order,
                       const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
                       const double *bg, void *image, int32_t image_dtype, void *t_final,
                       int32_t *n_last, int32_t *n_contrib, int32_t *n_iter, int64_t *touched,
-                      uint32_t *cmask, void *stream) {
+                      uint32_t *cmask, const isg_chunks *chunks, void *stream) {
     if (width <= 0 || height <= 0 || tiles_x <= 0 || row_lo < 0 || row_hi < row_lo || !bg ||
         !image || !t_final || !n_last || n_tile_ids < 0)
         return (int)cudaErrorInvalidValue;
@@ -453,10 +454,11 @@ static int raster_fwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t
     cudaStream_t s = (cudaStream_t)stream;
     const int img64 = image_dtype == ISG_F64 ? 1 : 0;
     if (feat_dtype == ISG_F32) {
-        launch_raster_fwd_f32(n_tiles, width, height, tiles_x, row_lo, tile_ids, offsets, entries,
+        launch_raster_fwd_f32(n_tiles, width, height, tiles_x, row_lo, tile_ids, tile_order,
+                              offsets, entries,
                               (const float *)feat_sorted, (float)bg[0], (float)bg[1],
                               (float)bg[2], image, img64, (float *)t_final, n_last, n_contrib,
-                              n_iter, touched, cmask, s);
+                              n_iter, touched, cmask, chunks, s);
     } else if (feat_dtype == ISG_F64) {
         if (touched)
             raster_fwd_kernel<double, true><<<n_tiles, THREADS, 0, s>>>(
@@ -475,10 +477,12 @@ static int raster_fwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t
 
 static int raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
                       int32_t row_lo, int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
+                      const int32_t *tile_order,
                       const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
                       const int32_t *rect_sorted, const int64_t *emit_off, const double *bg,
                       const void *t_final, const int32_t *n_last, const void *dl_dimage,
-                      int32_t dl_dtype, void *partials, const uint32_t *cmask, void *stream) {
+                      int32_t dl_dtype, void *partials, const uint32_t *cmask,
+                      const isg_chunks *chunks, void *stream) {
     if (width <= 0 || height <= 0 || tiles_x <= 0 || row_lo < 0 || row_hi < row_lo || !bg ||
         n_tile_ids < 0 || (emit_off && !rect_sorted))
         return (int)cudaErrorInvalidValue;
@@ -493,17 +497,19 @@ static int raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t
         emit_off, (T)bg[0], (T)bg[1], (T)bg[2], (const T *)t_final, n_last,                  \
         (const DL *)dl_dimage, (T *)partials)
     if (feat_dtype == ISG_F32 && dl_dtype == ISG_F32)
-        launch_raster_bwd_f32<float>(n_tiles, width, height, tiles_x, row_lo, tile_ids, offsets,
+        launch_raster_bwd_f32<float>(n_tiles, width, height, tiles_x, row_lo, tile_ids,
+                                     tile_order, offsets,
                                      entries, (const float *)feat_sorted, rs, emit_off,
                                      (float)bg[0], (float)bg[1], (float)bg[2],
                                      (const float *)t_final, n_last, (const float *)dl_dimage,
-                                     (float *)partials, cmask, s);
+                                     (float *)partials, cmask, chunks, s);
     else if (feat_dtype == ISG_F32 && dl_dtype == ISG_F64)
-        launch_raster_bwd_f32<double>(n_tiles, width, height, tiles_x, row_lo, tile_ids, offsets,
+        launch_raster_bwd_f32<double>(n_tiles, width, height, tiles_x, row_lo, tile_ids,
+                                      tile_order, offsets,
                                       entries, (const float *)feat_sorted, rs, emit_off,
                                       (float)bg[0], (float)bg[1], (float)bg[2],
                                       (const float *)t_final, n_last, (const double *)dl_dimage,
-                                      (float *)partials, cmask, s);
+                                      (float *)partials, cmask, chunks, s);
     else if (feat_dtype == ISG_F64 && dl_dtype == ISG_F32) ISG_BWD(double, float);
     else if (feat_dtype == ISG_F64 && dl_dtype == ISG_F64) ISG_BWD(double, double);
     else return (int)cudaErrorInvalidValue;
@@ -543,8 +549,9 @@ extern "C" int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height,
                               int32_t *n_contrib, int32_t *n_iter, int64_t *touched,
                               void *stream) {
     return raster_fwd(feat_dtype, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
+                      nullptr,
                       offsets, entries, feat_sorted, bg, image, image_dtype, t_final, n_last,
-                      n_contrib, n_iter, touched, nullptr, stream);
+                      n_contrib, n_iter, touched, nullptr, nullptr, stream);
 }
 
 extern "C" int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
@@ -556,8 +563,75 @@ extern "C" int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height,
                               const void *dl_dimage, int32_t dl_dtype, void *partials,
                               void *stream) {
     return raster_bwd(feat_dtype, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
+                      nullptr,
                       offsets, entries, feat_sorted, rect_sorted, emit_off, bg, t_final, n_last,
-                      dl_dimage, dl_dtype, partials, nullptr, stream);
+                      dl_dimage, dl_dtype, partials, nullptr, nullptr, stream);
+}
+
+namespace isg {
+// Work items of the chunked backward: positions of tile_order in launch
+// order, each expanded into its ceil(len / chunk) chunks.  One CTA, block
+// scan over the positions in rounds of 1024.
+__global__ void __launch_bounds__(1024) chunk_items_kernel(int n_tiles,
+                                                           const int32_t *__restrict__ offsets,
+                                                           const int32_t *__restrict__ order,
+                                                           const int4 *__restrict__ tile_last,
+                                                           int chunk, int2 *__restrict__ items,
+                                                           int32_t *__restrict__ n_items) {
+    __shared__ int swarp[32];
+    __shared__ int scarry;
+    if (threadIdx.x == 0) scarry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int c0 = 0; c0 < n_tiles; c0 += 1024) {
+        const int p = c0 + threadIdx.x;
+        int tl = 0, nc = 0;
+        if (p < n_tiles) {
+            tl = order ? order[p] : p;
+            const int4 q = tile_last[tl];
+            const int len = max(max(q.x, q.y), max(q.z, q.w));
+            nc = max(1, (len + chunk - 1) / chunk);
+        }
+        int x = nc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) swarp[warp] = x;
+        __syncthreads();
+        int before = scarry;
+        for (int w = 0; w < warp; w++) before += swarp[w];
+        const int ex = before + x - nc;
+        for (int k = 0; k < nc; k++) items[ex + k] = make_int2(tl, k | (k + 1 == nc ? 1 << 30 : 0));
+        __syncthreads();
+        if (threadIdx.x == 1023) scarry = before + x;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) n_items[0] = scarry;
+}
+}  // namespace isg
+
+extern "C" int64_t isg_chunk_state_floats(int64_t n_entries, int32_t n_tiles, int32_t chunk) {
+    if (chunk <= 0 || n_entries < 0 || n_tiles < 0) return 0;
+    return 4 * 256 * (n_entries / chunk + (int64_t)n_tiles + 2);
+}
+
+extern "C" int32_t isg_chunk_items_max(int64_t n_entries, int32_t n_tiles, int32_t chunk) {
+    if (chunk <= 0 || n_entries < 0 || n_tiles < 0) return n_tiles;
+    return (int32_t)(n_entries / chunk + (int64_t)n_tiles + 1);
+}
+
+extern "C" int isg_chunk_items(int32_t n_tiles, const int32_t *offsets, const int32_t *tile_order,
+                               const int32_t *tile_last, int32_t chunk, int32_t *items,
+                               int32_t *n_items, void *stream) {
+    if (n_tiles < 0 || chunk <= 0 || chunk % 32 || !items || !n_items ||
+        (n_tiles && (!offsets || !tile_last)))
+        return (int)cudaErrorInvalidValue;
+    chunk_items_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
+        n_tiles, offsets, tile_order, (const int4 *)tile_last, chunk, (int2 *)items, n_items);
+    ISG_CHECK_LAUNCH();
+    return 0;
 }
 
 extern "C" int64_t isg_contrib_mask_words(int64_t n_entries, int32_t n_tiles) {
@@ -567,30 +641,35 @@ extern "C" int64_t isg_contrib_mask_words(int64_t n_entries, int32_t n_tiles) {
 
 extern "C" int isg_raster_fwd_masked(int32_t width, int32_t height, int32_t tiles_x,
                                      int32_t row_lo, int32_t row_hi, const int32_t *tile_ids,
-                                     int32_t n_tile_ids, const int32_t *offsets,
+                                     int32_t n_tile_ids, const int32_t *tile_order,
+                                     const int32_t *offsets,
                                      const int32_t *entries, const void *feat_sorted,
                                      const double *bg, void *image, int32_t image_dtype,
                                      void *t_final, int32_t *n_last, int32_t *n_contrib,
                                      int32_t *n_iter, int64_t *touched, uint32_t *contrib_mask,
-                                     void *stream) {
+                                     const isg_chunks *chunks, void *stream) {
     if (!contrib_mask) return (int)cudaErrorInvalidValue;
     return raster_fwd(ISG_F32, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
+                      tile_order,
                       offsets, entries, feat_sorted, bg, image, image_dtype, t_final, n_last,
-                      n_contrib, n_iter, touched, contrib_mask, stream);
+                      n_contrib, n_iter, touched, contrib_mask, chunks, stream);
 }
 
 extern "C" int isg_raster_bwd_masked(int32_t width, int32_t height, int32_t tiles_x,
                                      int32_t row_lo, int32_t row_hi, const int32_t *tile_ids,
-                                     int32_t n_tile_ids, const int32_t *offsets,
+                                     int32_t n_tile_ids, const int32_t *tile_order,
+                                     const int32_t *offsets,
                                      const int32_t *entries, const void *feat_sorted,
                                      const int32_t *rect_sorted, const int64_t *emit_off,
                                      const double *bg, const void *t_final,
                                      const int32_t *n_last, const void *dl_dimage,
                                      int32_t dl_dtype, void *partials,
-                                     const uint32_t *contrib_mask, void *stream) {
+                                     const uint32_t *contrib_mask, const isg_chunks *chunks,
+                                     void *stream) {
     if (!contrib_mask || (dl_dtype != ISG_F32 && dl_dtype != ISG_F64))
         return (int)cudaErrorInvalidValue;
     return raster_bwd(ISG_F32, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
+                      tile_order,
                       offsets, entries, feat_sorted, rect_sorted, emit_off, bg, t_final, n_last,
-                      dl_dimage, dl_dtype, partials, contrib_mask, stream);
+                      dl_dimage, dl_dtype, partials, contrib_mask, chunks, stream);
 }

@@ -495,6 +495,10 @@ class RankStep:
         self.rect_sorted = self.feat_sorted = self.emit_off = None
         self.tk = self.tv = self.tk_sorted = self.entries = self.partials = None
         self.cmask = self.nb = self.gpos = self.gbuf = self.grad_recv = None
+        self.to_keys = self.to_vals = self.to_keys_s = self.to_order = self.tile_order = None
+        self.chunks = None
+        import os
+        self.heavy_first = os.environ.get("ISOGS_HEAVY_FIRST", "1") != "0"
         # band-side image buffers at full-image size: bands move when the
         # partition is rebalanced, the buffers do not
         self.window = torch.zeros((self.H, self.W, 3), dtype=torch.float32, device=d)
@@ -668,6 +672,10 @@ class RankStep:
                          self.entries[:E])
         L.check(offs(E, L.ptr(self.tk_sorted), self.n_tiles, L.ptr(self.offsets), s),
                 "isg_tile_offsets")
+        from .engine import chunk_setup, heavy_first_order
+        self.tile_order = heavy_first_order(self, self.n_tiles, self.offsets)
+        self.chunks = None if count else chunk_setup(
+            self, self.n_tiles, E, self._vptr(self.window, self.win0, self.W * 3))
         W3 = self.W * 3
         if count:
             band_px = max((self.prow1 - self.prow0) * self.W, 1)
@@ -690,12 +698,14 @@ class RankStep:
                                dtype=torch.int32, device=d)
             L.check(lib.isg_raster_fwd_masked(
                 self.W, self.H, self.tiles_x, self.trow0, self.trow1, None, 0,
+                L.ptr(self.tile_order),
                 L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
                 ctypes.cast(self.bg, ctypes.c_void_p),
                 self._vptr(self.window, self.win0, W3), L.ISG_F32,
                 self._vptr(self.t_final, self.prow0, self.W),
                 self._vptr(self.n_last, self.prow0, self.W), None, None, None, L.ptr(self.cmask),
-                s), "isg_raster_fwd_masked")
+                ctypes.byref(self.chunks) if self.chunks is not None else None, s),
+                "isg_raster_fwd_masked")
         # boundary rows for the neighbours' SSIM halo
         b0, b1 = self.prow0 - self.win0, self.prow1 - self.win0
         to_prev = self.window[b0:b0 + min(10, b1 - b0)] if self.rank > 0 else None
@@ -751,14 +761,18 @@ class RankStep:
         W3 = self.W * 3
         R, me = self.R, self.rank
         if self.n_tiles and self.E:
+            from .engine import chunk_items
+            chunk_items(self, self.n_tiles)
             L.check(lib.isg_raster_bwd_masked(
                 self.W, self.H, self.tiles_x, self.trow0, self.trow1, None, 0,
+                L.ptr(self.tile_order),
                 L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
                 L.ptr(self.rect_sorted), L.ptr(self.emit_off), ctypes.cast(self.bg, ctypes.c_void_p),
                 self._vptr(self.t_final, self.prow0, self.W),
                 self._vptr(self.n_last, self.prow0, self.W),
                 self._vptr(self.dl, self.prow0, W3), L.ISG_F32, L.ptr(self.partials),
-                L.ptr(self.cmask), s), "isg_raster_bwd_masked")
+                L.ptr(self.cmask), ctypes.byref(self.chunks) if self.chunks is not None else None,
+                s), "isg_raster_bwd_masked")
         _mark(timer, "raster_bwd")
         self.nb = _grow(self.nb, R, dtype=torch.int64, device=d)
         self.gpos = _grow(self.gpos, R + 1, dtype=torch.int64, device=d)

@@ -117,6 +117,12 @@ class Rasterizer:
         self.offsets = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=dev)
         self.tile_keys = self.tile_vals = self.keys_sorted_t = self.entries = None
         self.partials = None
+        self.to_keys = self.to_vals = self.to_keys_s = self.to_order = None
+        self.tile_order = None
+        self.chunks = None
+        self.chunk = CHUNK  # backward entries per work item (0: one CTA per tile)
+        # launch the raster pair heaviest tile lists first (ISOGS_HEAVY_FIRST=0: list order)
+        self.heavy_first = os.environ.get("ISOGS_HEAVY_FIRST", "1") != "0"
         # float32: forward contribution masks drive the backward (ISOGS_CMASK=0: A/B off)
         self.use_cmask = os.environ.get("ISOGS_CMASK", "1") != "0"
         self.cmask = None
@@ -220,6 +226,9 @@ class Rasterizer:
             _mark(tm, "sort_tiles")
         L.check(offs(e, L.ptr(self.keys_sorted_t), self.n_tiles, L.ptr(self.offsets), s),
                 "isg_tile_offsets")
+        self.tile_order = heavy_first_order(self, self.n_tiles, self.offsets)
+        self.chunks = (chunk_setup(self, self.n_tiles, e, L.ptr(self.image))
+                       if self.use_cmask and self.feat_dtype == torch.float32 else None)
         _mark(tm, "tile_offsets")
         self.cmask_ok = self.use_cmask and self.feat_dtype == torch.float32
         if self.cmask_ok:
@@ -229,10 +238,13 @@ class Rasterizer:
             self.cmask = _grow(self.cmask, words, dtype=torch.int32, device=dev)
             L.check(lib.isg_raster_fwd_masked(
                 self.width, self.height, self.tiles_x, 0, self.tiles_y, None, 0,
+                L.ptr(self.tile_order),
                 L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
                 ctypes.cast(self.bg, ctypes.c_void_p), L.ptr(self.image), L.ISG_F32,
                 L.ptr(self.t_final), L.ptr(self.n_last), L.ptr(self.n_contrib_out),
-                L.ptr(self.n_iter_out), None, L.ptr(self.cmask), s), "isg_raster_fwd_masked")
+                L.ptr(self.n_iter_out), None, L.ptr(self.cmask),
+                ctypes.byref(self.chunks) if self.chunks is not None else None, s),
+                "isg_raster_fwd_masked")
         else:
             L.check(lib.isg_raster_fwd(self.ftag, self.width, self.height, self.tiles_x, 0,
                                        self.tiles_y, None, 0, L.ptr(self.offsets),
@@ -253,12 +265,15 @@ class Rasterizer:
         self.partials = _grow(self.partials, max(ctx.slots, ctx.e, 1), (rec,), dtype=self.feat_dtype,
                               device=self.device)
         if self.cmask_ok:
+            chunk_items(self, self.n_tiles)
             L.check(lib.isg_raster_bwd_masked(
                 self.width, self.height, self.tiles_x, 0, self.tiles_y, None, 0,
+                L.ptr(self.tile_order),
                 L.ptr(self.offsets), L.ptr(self.entries), L.ptr(self.feat_sorted),
                 L.ptr(self.rect_sorted), L.ptr(self.emit_off),
                 ctypes.cast(self.bg, ctypes.c_void_p), L.ptr(self.t_final), L.ptr(self.n_last),
-                L.ptr(self.dl), L.ISG_F32, L.ptr(self.partials), L.ptr(self.cmask), s),
+                L.ptr(self.dl), L.ISG_F32, L.ptr(self.partials), L.ptr(self.cmask),
+                ctypes.byref(self.chunks) if self.chunks is not None else None, s),
                 "isg_raster_bwd_masked")
         else:
             L.check(lib.isg_raster_bwd(self.ftag, self.width, self.height, self.tiles_x, 0,
@@ -279,6 +294,71 @@ class Rasterizer:
         _mark(self.timer, "reduce")
 
     LAUNCHES_PER_STEP = None  # filled by Trainer (documented count)
+
+
+def heavy_first_order(st, n_tiles: int, offsets: torch.Tensor):
+    """Launch order of the raster pair, heaviest tile lists first
+    (isg_tile_order_keys + a 16-bit stable sort): with one CTA per tile, a
+    long list launched last runs alone at the end of the kernel; launched
+    first it overlaps the light ones.  `st` holds the scratch buffers and the
+    heavy_first switch.  Returns None (list order) when off."""
+    if not st.heavy_first or n_tiles < 2:
+        return None
+    lib = L.lib()
+    dev = offsets.device
+    st.to_keys = _grow(st.to_keys, n_tiles, dtype=torch.int16, device=dev)
+    st.to_vals = _grow(st.to_vals, n_tiles, dtype=torch.int32, device=dev)
+    st.to_keys_s = _grow(st.to_keys_s, n_tiles, dtype=torch.int16, device=dev)
+    st.to_order = _grow(st.to_order, n_tiles, dtype=torch.int32, device=dev)
+    L.check(lib.isg_tile_order_keys(n_tiles, L.ptr(offsets), L.ptr(st.to_keys),
+                                    L.ptr(st.to_vals), L.stream_ptr()), "isg_tile_order_keys")
+    if not hasattr(st, "ws_order"):
+        st.ws_order = L.Workspace()
+    L.sort_pairs(st.to_keys[:n_tiles], st.to_vals[:n_tiles], (0, 16), st.ws_order,
+                 st.to_keys_s[:n_tiles], st.to_order[:n_tiles])
+    return st.to_order
+
+
+# Backward list chunking: entries per backward work item (isg_chunks).  A
+# constant, so the chunking of every tile is the same for any band partition
+# (bitwise W-invariance).  Measured (tools/ab_chunk.sh, profiles/r02_chunk):
+# chunks of 512 take config 2's backward 1.14 -> 0.91 ms and an emulated W=8
+# band's 1.03 -> 0.80 ms, but config 3's 3.88 -> 4.35 ms (more, shorter CTAs
+# lower the achieved occupancy), so the default is off (0: one CTA per tile).
+CHUNK = int(os.environ.get("ISOGS_CHUNK", "0"))
+
+
+def chunk_setup(st, n_tiles: int, e: int, image_ptr: int):
+    """isg_chunks for the masked raster pair over `n_tiles` lists with `e`
+    entries (the boundary-state and per-quadrant last-position buffers); the
+    work items are built between the forward and the backward by
+    chunk_items().  `st` holds the buffers.  None when off."""
+    chunk = getattr(st, "chunk", CHUNK)
+    if chunk <= 0 or n_tiles == 0:
+        return None
+    lib = L.lib()
+    dev = st.offsets.device
+    nst = int(lib.isg_chunk_state_floats(e, n_tiles, chunk))
+    st.ch_state = _grow(getattr(st, "ch_state", None), nst, dtype=torch.float32, device=dev)
+    mx = int(lib.isg_chunk_items_max(e, n_tiles, chunk))
+    st.ch_items = _grow(getattr(st, "ch_items", None), 2 * mx, dtype=torch.int32, device=dev)
+    st.ch_last = _grow(getattr(st, "ch_last", None), 4 * n_tiles, dtype=torch.int32, device=dev)
+    if getattr(st, "ch_n", None) is None:
+        st.ch_n = torch.zeros(1, dtype=torch.int32, device=dev)
+    c = L.Chunks_t()
+    c.chunk, c.state, c.items, c.n_items = chunk, L.ptr(st.ch_state), L.ptr(st.ch_items), L.ptr(st.ch_n)
+    c.max_items, c.image, c.tile_last = mx, image_ptr, L.ptr(st.ch_last)
+    return c
+
+
+def chunk_items(st, n_tiles: int) -> None:
+    """The backward's work items from the forward's per-quadrant last
+    positions (isg_chunk_items), in the heaviest-first tile order."""
+    if st.chunks is None:
+        return
+    L.check(L.lib().isg_chunk_items(n_tiles, L.ptr(st.offsets), L.ptr(st.tile_order),
+                                    L.ptr(st.ch_last), st.chunks.chunk, L.ptr(st.ch_items),
+                                    L.ptr(st.ch_n), L.stream_ptr()), "isg_chunk_items")
 
 
 def update_params(cloud: GaussianCloud, m: dict, v: dict, grads: dict, seen, grad_accum, flag,

@@ -122,6 +122,7 @@ def test_contribution_masks_change_no_result():
     for masked in (True, False):
         t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
         t.r.use_cmask = masked
+        t.r.chunk = 0  # one backward CTA per tile: the same arithmetic as the unmasked pair
         for it in range(1, 5):
             t.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
         torch.cuda.synchronize()
@@ -137,6 +138,42 @@ def test_contribution_masks_change_no_result():
     assert torch.equal(a.r.grad2d, b.r.grad2d)
     for k in P.PARAM_NAMES:
         assert torch.equal(getattr(a.cloud, k), getattr(b.cloud, k)), k
+
+
+def test_backward_chunking_matches_one_cta_per_tile():
+    """The chunked backward (isg_chunks: long lists cut into 32-entry-aligned
+    chunks, each started from the forward's boundary state) against one CTA
+    per tile: images bitwise (the forward only records state), 2-D gradients
+    within float32 rounding of the chunk-start colour (S = image - C), and
+    4 training iterations within the same bar."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200.engine import Trainer
+    d = load("config1")
+    ds = _dataset(d, "images_u8", d["images_u8"].shape[0])
+    cfg = P.TrainConfig(iterations=4, densify=False, seed=0)
+    gt = _images(ds)
+    sched = P.build_schedule(4, ds.view_count, 0)
+    runs = []
+    for chunk in (64, 0):  # config 1 lists reach 6.3K entries: many chunks per tile
+        t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
+        t.r.chunk = chunk
+        for it in range(1, 5):
+            t.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
+            if it == 1:
+                g1 = t.r.grad2d.clone()
+                img1 = t.r.image.clone()
+        torch.cuda.synchronize()
+        runs.append((t, g1, img1))
+    (a, ga, ia), (b, gb, ib) = runs
+    assert a.r.chunks is not None and b.r.chunks is None
+    assert torch.equal(ia, ib)
+    rel = float((ga - gb).abs().max() / gb.abs().max())
+    assert rel <= 1e-4, rel
+    la, lb = a.loss_dev[1:5], b.loss_dev[1:5]
+    assert float(((la - lb).abs() / lb).max()) <= 1e-6
+    for k in P.PARAM_NAMES:
+        x, y = getattr(a.cloud, k), getattr(b.cloud, k)
+        assert float((x - y).abs().max()) <= 2.5 * 4 * 5e-2, k  # Adam's bound (lr_opacity)
 
 
 def _images(ds):
