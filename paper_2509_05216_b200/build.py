@@ -35,6 +35,7 @@ SOURCES = {
     "chain_f32.cu": [],
     "volume.cu": ["-fmad=false"],
     "probe.cu": [],
+    "radix.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -9,9 +9,8 @@
 // (tile, rank) pairs in rank order and stably sorting on the tile id, so each
 // tile's list is in global compositing order -- bit-identical to the
 // reference's count/cumsum/fill.  All kernels are HBM-bound integer work.
-#include <cub/cub.cuh>
-
 #include "common.cuh"
+#include "radix.cuh"
 #include "raster_common.cuh"
 
 namespace isg {
@@ -41,9 +40,6 @@ __global__ void __launch_bounds__(256) gather_rank_kernel(
     cnt[r] = c;
 }
 
-__global__ void finish_counts_kernel(int64_t n, const int64_t *emit_off, int64_t *counts) {
-    counts[1] = emit_off[n];
-}
 
 // Entry-parallel emission: a block of EMIT_R consecutive ranks owns the
 // contiguous slot span [emit_off[r0], emit_off[r0 + EMIT_R]); the block
@@ -185,22 +181,55 @@ extern "C" int isg_sort_u64(void *workspace, size_t *ws_bytes, const uint64_t *k
     if (!ws_bytes || n < 0 || n > INT32_MAX || begin_bit < 0 || end_bit > 64 ||
         begin_bit >= end_bit)
         return (int)cudaErrorInvalidValue;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, *ws_bytes, keys_in, keys_out,
-                                                    vals_in, vals_out, (int)n, begin_bit,
-                                                    end_bit, (cudaStream_t)stream);
-    return (int)e;
+    return radix::sort_pairs<uint64_t>(workspace, ws_bytes, keys_in, keys_out, vals_in, vals_out, n,
+                                  begin_bit, end_bit, (cudaStream_t)stream);
 }
 
 namespace isg {
 #ifndef DEPTH_LO_BIT
 #define DEPTH_LO_BIT 24
 #endif
+constexpr int64_t TIE_INSERTION_MAX = 64;
+
+__device__ __forceinline__ bool kv_less(uint64_t ka, int32_t va, uint64_t kb, int32_t vb) {
+    return ka < kb || (ka == kb && va < vb);
+}
+
+__device__ void sift_down(uint64_t *k, int32_t *v, int64_t root, int64_t end) {
+    while (2 * root + 1 < end) {
+        int64_t c = 2 * root + 1;
+        if (c + 1 < end && kv_less(k[c], v[c], k[c + 1], v[c + 1])) c++;
+        if (!kv_less(k[root], v[root], k[c], v[c])) return;
+        const uint64_t tk = k[root];
+        const int32_t tv = v[root];
+        k[root] = k[c];
+        v[root] = v[c];
+        k[c] = tk;
+        v[c] = tv;
+        root = c;
+    }
+}
+
+__device__ void heap_sort_run(uint64_t *k, int32_t *v, int64_t len) {
+    for (int64_t s = len / 2 - 1; s >= 0; s--) sift_down(k, v, s, len);
+    for (int64_t e = len - 1; e > 0; e--) {
+        const uint64_t tk = k[0];
+        const int32_t tv = v[0];
+        k[0] = k[e];
+        v[0] = v[e];
+        k[e] = tk;
+        v[e] = tv;
+        sift_down(k, v, 0, e);
+    }
+}
+
 // After a stable sort on key bits [DEPTH_LO_BIT, 64) the only possible
 // disorder is inside runs of equal top bits (depths equal to ~2^-(52 -
 // DEPTH_LO_BIT) relative).  One thread per run start checks its run and
 // insertion-sorts it by the full key (strict comparison: equal keys keep their
-// ascending-id order).  Runs of the culled key ~0 are identical and already
-// in id order.
+// ascending-id order; runs longer than TIE_INSERTION_MAX are heap-sorted by
+// (key, id): O(k log k) for any run).  Runs of the culled key ~0 are
+// identical and already in id order.
 __global__ void __launch_bounds__(256) depth_tie_fix_kernel(int64_t n, uint64_t *keys,
                                                             int32_t *vals) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -217,18 +246,24 @@ __global__ void __launch_bounds__(256) depth_tie_fix_kernel(int64_t n, uint64_t 
         j++;
     }
     if (sorted) return;
-    for (int64_t a = i + 1; a < j; a++) {
-        const uint64_t key = keys[a];
-        const int32_t val = vals[a];
-        int64_t b = a - 1;
-        while (b >= i && keys[b] > key) {
-            keys[b + 1] = keys[b];
-            vals[b + 1] = vals[b];
-            b--;
+    if (j - i <= TIE_INSERTION_MAX) {
+        for (int64_t a = i + 1; a < j; a++) {
+            const uint64_t key = keys[a];
+            const int32_t val = vals[a];
+            int64_t b = a - 1;
+            while (b >= i && keys[b] > key) {
+                keys[b + 1] = keys[b];
+                vals[b + 1] = vals[b];
+                b--;
+            }
+            keys[b + 1] = key;
+            vals[b + 1] = val;
         }
-        keys[b + 1] = key;
-        vals[b + 1] = val;
+        return;
     }
+    // long run: heapsort by (key, value) -- values are the ascending ids of
+    // equal keys, so this is the stable order; O(k log k) worst case
+    heap_sort_run(keys + i, vals + i, j - i);
 }
 }  // namespace isg
 
@@ -239,10 +274,10 @@ extern "C" int isg_sort_depth(void *workspace, size_t *ws_bytes, const uint64_t 
                               uint64_t *keys_out, const int32_t *vals_in, int32_t *vals_out,
                               int64_t n, void *stream) {
     if (!ws_bytes || n < 0 || n > INT32_MAX) return (int)cudaErrorInvalidValue;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, *ws_bytes, keys_in, keys_out,
-                                                    vals_in, vals_out, (int)n, DEPTH_LO_BIT, 64,
-                                                    (cudaStream_t)stream);
-    if (e != cudaSuccess || !workspace || n == 0) return (int)e;
+    const int e = radix::sort_pairs<uint64_t>(workspace, ws_bytes, keys_in, keys_out, vals_in,
+                                              vals_out, n, DEPTH_LO_BIT, 64,
+                                              (cudaStream_t)stream);
+    if (e != 0 || !workspace || n == 0) return e;
     depth_tie_fix_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(n, keys_out,
                                                                               vals_out);
     ISG_CHECK_LAUNCH();
@@ -255,10 +290,8 @@ extern "C" int isg_sort_u32(void *workspace, size_t *ws_bytes, const uint32_t *k
     if (!ws_bytes || n < 0 || n > INT32_MAX || begin_bit < 0 || end_bit > 32 ||
         begin_bit >= end_bit)
         return (int)cudaErrorInvalidValue;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, *ws_bytes, keys_in, keys_out,
-                                                    vals_in, vals_out, (int)n, begin_bit,
-                                                    end_bit, (cudaStream_t)stream);
-    return (int)e;
+    return radix::sort_pairs<uint32_t>(workspace, ws_bytes, keys_in, keys_out, vals_in, vals_out, n,
+                                  begin_bit, end_bit, (cudaStream_t)stream);
 }
 
 extern "C" int isg_tile_order_keys(int32_t n_tiles, const int32_t *offsets, uint16_t *keys16,
@@ -279,9 +312,7 @@ static int bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_
                      int64_t *counts, void *stream) {
     if (!ws_bytes || n < 0 || n > INT32_MAX || row_lo < 0 || row_hi < row_lo)
         return (int)cudaErrorInvalidValue;
-    size_t scan_bytes = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, (const int64_t *)nullptr,
-                                  (int64_t *)nullptr, (int)(n > 0 ? n : 1));
+    const size_t scan_bytes = scan_i64_ws_bytes(n > 0 ? n : 1);
     const size_t need = align_up(sizeof(int64_t) * (size_t)(n > 0 ? n : 1)) + align_up(scan_bytes);
     if (!workspace) {
         *ws_bytes = need;
@@ -300,9 +331,8 @@ static int bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_
         n, sorted_keys, order, rect, rect_stride4, feat, feat_stride4, vec4, row_lo, row_hi,
         (int4 *)rect_sorted, (float4 *)feat_sorted, cnt, counts);
     ISG_CHECK_LAUNCH();
-    e = cub::DeviceScan::InclusiveSum(scan_ws, scan_bytes, cnt, emit_off + 1, (int)n, s);
-    if (e != cudaSuccess) return (int)e;
-    finish_counts_kernel<<<1, 1, 0, s>>>(n, emit_off, counts);
+    const int se = scan_i64(scan_ws, scan_bytes, n, cnt, emit_off, counts + 1, s);
+    if (se != 0) return se;
     ISG_CHECK_LAUNCH();
     return 0;
 }
@@ -402,10 +432,8 @@ extern "C" int isg_sort_u16(void *workspace, size_t *ws_bytes, const uint16_t *k
     if (!ws_bytes || n < 0 || n > INT32_MAX || begin_bit < 0 || end_bit > 16 ||
         begin_bit >= end_bit)
         return (int)cudaErrorInvalidValue;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(workspace, *ws_bytes, keys_in, keys_out,
-                                                    vals_in, vals_out, (int)n, begin_bit,
-                                                    end_bit, (cudaStream_t)stream);
-    return (int)e;
+    return radix::sort_pairs<uint16_t>(workspace, ws_bytes, keys_in, keys_out, vals_in, vals_out, n,
+                                  begin_bit, end_bit, (cudaStream_t)stream);
 }
 
 extern "C" int isg_tile_offsets16(int64_t e, const uint16_t *sorted_tile_keys, int32_t n_tiles,

@@ -21,9 +21,8 @@
 //             of the GPU count, the reference's headline property.
 //   fold    : the owner groups received records by shard row (stable) and
 //             sums them in arrival order (bands ascending).
-#include <cub/cub.cuh>
-
 #include "common.cuh"
+#include "radix.cuh"
 
 namespace isg {
 
@@ -150,30 +149,49 @@ __global__ void __launch_bounds__(1024) route_scan_kernel(int64_t nblk, int nban
                                                           int64_t *__restrict__ plan,
                                                           const int64_t *__restrict__ tiles_blk,
                                                           int64_t *__restrict__ totals) {
-    typedef cub::BlockScan<long long, 1024> Scan;
-    __shared__ typename Scan::TempStorage tmp;
-    __shared__ long long s_tiles[32];
+    __shared__ long long sw0[32], sw1[32], s_tiles[32];
     const int d = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     long long carry0 = 0, carry1 = 0, tiles = 0;
     for (int64_t c = 0; c < nblk; c += 1024) {
         const int64_t b = c + threadIdx.x;
         int64_t *p = plan + 2 * (b * nbands + d);
         const long long v0 = b < nblk ? p[0] : 0, v1 = b < nblk ? p[1] : 0;
         tiles += b < nblk ? tiles_blk[b * nbands + d] : 0;
-        long long e0, e1, t0, t1;
-        Scan(tmp).ExclusiveSum(v0, e0, t0);
+        long long x0 = v0, x1 = v1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y0 = __shfl_up_sync(0xffffffffu, x0, o);
+            const long long y1 = __shfl_up_sync(0xffffffffu, x1, o);
+            if (lane >= o) {
+                x0 += y0;
+                x1 += y1;
+            }
+        }
+        if (lane == 31) {
+            sw0[warp] = x0;
+            sw1[warp] = x1;
+        }
         __syncthreads();
-        Scan(tmp).ExclusiveSum(v1, e1, t1);
-        __syncthreads();
+        long long b0 = carry0, b1 = carry1, t0 = 0, t1 = 0;
+        for (int w = 0; w < 32; w++) {
+            if (w < warp) {
+                b0 += sw0[w];
+                b1 += sw1[w];
+            }
+            t0 += sw0[w];
+            t1 += sw1[w];
+        }
         if (b < nblk) {
-            p[0] = carry0 + e0;
-            p[1] = carry1 + e1;
+            p[0] = b0 + x0 - v0;
+            p[1] = b1 + x1 - v1;
         }
         carry0 += t0;
         carry1 += t1;
+        __syncthreads();
     }
     for (int o = 16; o > 0; o >>= 1) tiles += __shfl_xor_sync(0xffffffffu, tiles, o);
-    if ((threadIdx.x & 31) == 0) s_tiles[threadIdx.x >> 5] = tiles;
+    if (lane == 0) s_tiles[warp] = tiles;
     __syncthreads();
     if (threadIdx.x == 0) {
         long long t = 0;
@@ -509,10 +527,6 @@ __global__ void owner_fold_kernel(int64_t n_rows, const int32_t *__restrict__ se
     for (int q = 0; q < 9; q++) grad2d[9 * i + q] = acc[q];
 }
 
-__global__ void scan_finish_kernel(int64_t n, const int64_t *__restrict__ off,
-                                   int64_t *__restrict__ total) {
-    total[0] = off[n];
-}
 
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -524,27 +538,13 @@ using namespace isg;
 extern "C" int isg_scan_i64(void *workspace, size_t *ws_bytes, int64_t n, const int64_t *cnt,
                             int64_t *off, int64_t *total, void *stream) {
     if (!ws_bytes || n < 0 || n > INT32_MAX) return (int)cudaErrorInvalidValue;
-    size_t need = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, need, (const int64_t *)nullptr, (int64_t *)nullptr,
-                                  (int)(n > 0 ? n : 1));
-    need = al(need);
+    const size_t need = scan_i64_ws_bytes(n);
     if (!workspace) {
         *ws_bytes = need;
         return 0;
     }
     if (*ws_bytes < need) return (int)cudaErrorInvalidValue;
-    cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(off, 0, sizeof(int64_t), s);
-    if (e != cudaSuccess) return (int)e;
-    if (n > 0) {
-        e = cub::DeviceScan::InclusiveSum(workspace, need, cnt, off + 1, (int)n, s);
-        if (e != cudaSuccess) return (int)e;
-    }
-    if (total) {
-        scan_finish_kernel<<<1, 1, 0, s>>>(n, off, total);
-        ISG_CHECK_LAUNCH();
-    }
-    return 0;
+    return scan_i64(workspace, *ws_bytes, n, cnt, off, total, (cudaStream_t)stream);
 }
 
 static int fill_bands(Bands &b, const int32_t *band_rows, int32_t n_bands) {

@@ -3,7 +3,7 @@
 One iteration is a fixed chain of libisogs launches on the current stream:
 
   isg_preprocess   project every Gaussian (fp64 key path)        N rows
-  isg_sort_u64     global (depth, id) order                        N keys
+  isg_sort_depth   global (depth, id) order (hand-written radix)   N keys
   isg_bin_count    rank-order gather + tile-count scan             N ranks
   [D2H 16 B]       M visible, E tile entries (sizes the E buffers)
   isg_bin_emit     (tile, rank) pairs in rank order                E pairs

@@ -266,6 +266,51 @@ def test_sort_depth_equals_full_64bit_sort():
     assert torch.equal(k1, k2) and torch.equal(v1, v2)
 
 
+@pytest.mark.parametrize("width,bits", [(2, (0, 15)), (2, (0, 16)), (4, (0, 14)), (4, (3, 29)),
+                                        (8, (0, 64)), (8, (24, 64))])
+def test_radix_sort_is_a_stable_sort(width, bits):
+    """The hand-written LSD radix sort (radix.cu) == torch's stable sort on
+    the same key bits: keys, and values (original positions) for ties; sizes
+    with a partial last CTA and many equal digits."""
+    from paper_2509_05216_b200 import _lib as L
+    g = torch.Generator().manual_seed(width * 100 + bits[1])
+    for n in (1, 4095, 4096, 100_003, 3_000_001):
+        dt = {2: torch.int16, 4: torch.int32, 8: torch.int64}[width]
+        raw = torch.randint(-2**62, 2**62, (n,), generator=g, dtype=torch.int64)
+        raw[: n // 3] = raw[: n // 3] % 7  # heavy duplicates
+        keys = raw.to(dt) if width < 8 else raw
+        keys = keys.cuda()
+        vals = torch.arange(n, dtype=torch.int32, device="cuda")
+        ko, vo = L.sort_pairs(keys, vals, bits, L.Workspace())
+        # reference: stable sort on the selected bits (unsigned)
+        u = keys.to(torch.int64) & ((1 << (8 * width)) - 1) if width < 8 else keys
+        b0, b1 = bits
+        if width == 8:
+            sel = (u >> b0) & ((1 << (b1 - b0)) - 1) if b1 - b0 < 64 else u
+            # unsigned order of 64-bit keys: flip the sign bit
+            sel = sel ^ (-2**63) if b1 - b0 == 64 else sel
+        else:
+            sel = (u >> b0) & ((1 << (b1 - b0)) - 1)
+        _, idx = torch.sort(sel, stable=True)
+        assert torch.equal(vo, idx.to(torch.int32)), (n, width, bits)
+        assert torch.equal(ko, keys[idx]), (n, width, bits)
+
+
+def test_depth_sort_long_reversed_run_is_bounded():
+    """A 200K-key run with equal top 40 bits in reverse order of the low
+    bits (the tie fix-up's worst case: heap sort, not quadratic insertion)."""
+    from paper_2509_05216_b200 import _lib as L
+    n = 200_000
+    keys = (torch.full((n,), 0x40A00000, dtype=torch.int64) << 24) | \
+        torch.arange(n - 1, -1, -1, dtype=torch.int64)
+    keys = keys.cuda()
+    vals = torch.arange(n, dtype=torch.int32, device="cuda")
+    k2, v2 = L.sort_depth(keys, vals, L.Workspace())
+    torch.cuda.synchronize()
+    assert torch.equal(v2, torch.arange(n - 1, -1, -1, dtype=torch.int32, device="cuda"))
+    assert bool((k2[1:] >= k2[:-1]).all())
+
+
 def test_gpu_knn_init_matches_reference_bitwise():
     """init_log_scales on the GPU (isg_knn_mean_grid) reproduces the
     reference's init_from_points log-scales bit for bit (config 1: 20000
