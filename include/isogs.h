@@ -129,19 +129,6 @@ int isg_bin_emit(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
                  int32_t tiles_x, int32_t row_lo, int32_t row_hi, uint32_t *tile_keys,
                  int32_t *tile_vals, void *stream);
 
-/* Training-path lists (float32 features): isg_bin_emit16 that also culls
- * every (tile, splat) pair whose 16x16 tile no pixel centre of can reach
- * alpha >= 1/255 (the rasteriser's exact conservative box test; such a pair is
- * never composited).  A culled pair gets the key n_band_tiles, so after
- * isg_sort_u16 over bits [0, tile_bits + 1) it lies past every list and
- * isg_tile_offsets16 leaves it out; its zero float32 subtotal record is
- * written into partials (full splat-major slot layout, emit_off).  Bands of
- * fewer than 65536 tiles.  Images, subtotals and the fold are bit-identical to
- * the full lists. */
-int isg_bin_emit16_cull(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
-                        const float *feat_sorted, int32_t tiles_x, int32_t row_lo,
-                        int32_t row_hi, uint16_t *tile_keys, int32_t *tile_vals, float *partials,
-                        void *stream);
 
 /* 16-bit tile-key variants (band of at most 65536 tiles, e.g. 4096^2 at
  * 16 px): the same pairs / order / offsets as isg_bin_emit + isg_sort_u32 +
@@ -237,7 +224,10 @@ int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t ti
  * with feat_dtype ISG_F32.  contrib_mask holds isg_contrib_mask_words(E,
  * n_tiles) uint32 words for a launch over n_tiles tiles with E list entries;
  * it needs no initialisation.  The two calls must see the same tiles,
- * offsets and n_last.  tile_order (optional, n_tiles entries): CTA b
+ * offsets and n_last.  slot_rank (optional): the lists are live-only
+ * subtotal slots (isg_bin_emit_live); entries map to ranks through it and the
+ * backward writes each list entry's record at that slot with its tile row as
+ * int32 bits in float 9.  tile_order (optional, n_tiles entries): CTA b
  * processes list position tile_order[b] -- the launch order only (heaviest
  * lists first, isg_tile_order); results do not depend on it. */
 int64_t isg_contrib_mask_words(int64_t n_entries, int32_t n_tiles);
@@ -275,20 +265,58 @@ int isg_raster_fwd_masked(int32_t width, int32_t height, int32_t tiles_x, int32_
                           const int32_t *tile_order, const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
                           const double *bg, void *image, int32_t image_dtype, void *t_final,
                           int32_t *n_last, int32_t *n_contrib, int32_t *n_iter, int64_t *touched,
-                          uint32_t *contrib_mask, const isg_chunks *chunks, void *stream);
+                          uint32_t *contrib_mask, const isg_chunks *chunks,
+                          const int32_t *slot_rank, void *stream);
 int isg_raster_bwd_masked(int32_t width, int32_t height, int32_t tiles_x, int32_t row_lo,
                           int32_t row_hi, const int32_t *tile_ids, int32_t n_tile_ids,
                           const int32_t *tile_order, const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
                           const int32_t *rect_sorted, const int64_t *emit_off, const double *bg,
                           const void *t_final, const int32_t *n_last, const void *dl_dimage,
                           int32_t dl_dtype, void *partials, const uint32_t *contrib_mask,
-                          const isg_chunks *chunks, void *stream);
+                          const isg_chunks *chunks, const int32_t *slot_rank, void *stream);
+
+/* The sort and the CSR offsets with the item count on the device (*n_dev,
+ * *e_dev; n_max / e_max host-side upper bounds that size grids and the
+ * workspace): the band path sorts its live-only lists without a host sync.
+ * key_bytes 2, 4 or 8. */
+int isg_sort_pairs_dev(void *workspace, size_t *ws_bytes, int32_t key_bytes, const void *keys_in,
+                       void *keys_out, const int32_t *vals_in, int32_t *vals_out, int64_t n_max,
+                       const int64_t *n_dev, int32_t begin_bit, int32_t end_bit, void *stream);
+int isg_tile_offsets_dev(int64_t e_max, const int64_t *e_dev, const void *sorted_keys,
+                         int32_t key_bytes, int32_t n_tiles, int32_t *offsets, void *stream);
 
 /* Heaviest-first launch order of n_tiles tile lists: keys16[t] = 65535 -
  * min(list length, 65535) and vals[t] = t, to be sorted ascending with
  * isg_sort_u16 (16 bits) into the tile_order of the raster pair. */
 int isg_tile_order_keys(int32_t n_tiles, const int32_t *offsets, uint16_t *keys16,
                         int32_t *vals, void *stream);
+
+/* The ordered fold over the live-only layout (float32 records of
+ * isg_raster_bwd_masked with slot_rank: rank r's slots live_off[r] ..
+ * live_off[r + 1], tile row in float 9), canonical blocks of canon_rows >= 1
+ * tile rows: bit-identical to isg_reduce_ordered over the full layout (the
+ * uncomposited pairs' zero subtotals only ever add zeros). */
+int isg_reduce_live(int64_t m, const int64_t *live_off, const float *partials,
+                    const int32_t *order, const int32_t *rect_sorted, int32_t row_lo,
+                    int32_t row_hi, int32_t canon_rows, double *grad2d, double *grad_norm,
+                    void *stream);
+
+/* Live-only binning (the float32 training lists): isg_bin_count plus, per
+ * rank, the tiles some pixel can composite (the rasteriser's conservative box
+ * test): live_off (n+1, exclusive scan), live_mask (bit k = k-th tile of the
+ * clipped rect in row-major order, rects of <= 64 tiles) and counts[2] = live
+ * total.  rect/feat (float32 SoA) or payload (64-byte rows).  isg_bin_emit_live
+ * then writes the live (tile, slot) pairs compacted in rank order: keys[p] =
+ * band tile, slot_rank[p] = rank for slot p in [0, live total). */
+int isg_bin_count_live(void *workspace, size_t *ws_bytes, int64_t n, const uint64_t *sorted_keys,
+                       const int32_t *order, const int32_t *rect, const int32_t *payload,
+                       const float *feat, int32_t row_lo, int32_t row_hi, int32_t *rect_sorted,
+                       float *feat_sorted, int64_t *emit_off, int64_t *live_off,
+                       uint64_t *live_mask, int64_t *counts, void *stream);
+int isg_bin_emit_live(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
+                      const int64_t *live_off, const uint64_t *live_mask, const float *feat_sorted,
+                      int32_t tiles_x, int32_t row_lo, int32_t row_hi, void *tile_keys,
+                      int32_t key_bytes, int32_t *slot_rank, void *stream);
 
 /* Ordered fold (_reduce_scratch, _kernels.py:398-411): for rank r < m sum its
  * subtotal slots [emit_off[r], emit_off[r+1]) in float64 and write
@@ -347,10 +375,13 @@ int isg_band_blocks(int64_t r, const int32_t *payload, int32_t row_lo, int32_t r
  * rank r's float32 subtotals folded per canonical block (float64, tiles
  * ascending) into 9-double records at gbuf[9 * (gpos[order[r]] + b)] --
  * records by receive index, so each source rank's segment is its own rows'
- * records in its shard row order. */
+ * records in its shard row order.  live_layout: emit_off is the live-only
+ * slot offsets (isg_bin_emit_live; records carry their tile row) and every
+ * block of the rank's clipped rows in [row_lo, row_hi) gets a record. */
 int isg_band_fold(int64_t m, const int64_t *emit_off, const float *partials,
                   const int32_t *rect_sorted, const int32_t *order, const int64_t *gpos,
-                  int32_t row_lo, int32_t canon_rows, double *gbuf, void *stream);
+                  int32_t row_lo, int32_t row_hi, int32_t canon_rows, int32_t live_layout,
+                  double *gbuf, void *stream);
 
 /* Band raster cost per canonical block (load balance of the row bands):
  * hist[(prow0 + y) / (16 * canon_rows)] += sum_x n_last[y][x] for the band's

@@ -79,7 +79,6 @@ SIGNATURES = {
     "isg_sort_depth": [_P, _SZ, _P, _P, _P, _P, _I64, _P],
     "isg_bin_count_rows": [_P, _SZ, _I64, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P],
     "isg_bin_count": [_P, _SZ, _I64, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P, _P],
-    "isg_bin_emit16_cull": [_I64, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P],
     "isg_bin_emit": [_I64, _P, _P, _I32, _I32, _I32, _P, _P, _P],
     "isg_rank_of": [_I64, _P, _P, _P, _P],
     "isg_tile_offsets": [_I64, _P, _I32, _P, _P],
@@ -89,13 +88,18 @@ SIGNATURES = {
     "isg_raster_fwd": [_I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _I32,
                        _P, _P, _P, _P, _P, _P],
     "isg_raster_fwd_masked": [_I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P,
-                              _I32, _P, _P, _P, _P, _P, _P, _P, _P],
+                              _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "isg_raster_bwd_masked": [_I32, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P,
-                              _P, _P, _P, _P, _I32, _P, _P, _P, _P],
+                              _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P],
+    "isg_bin_count_live": [_P, _SZ, _I64, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P,
+                           _P, _P],
+    "isg_bin_emit_live": [_I64, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P, _I32, _P, _P],
     "isg_chunk_state_floats": [_I64, _I32, _I32],
     "isg_chunk_items_max": [_I64, _I32, _I32],
     "isg_chunk_items": [_I32, _P, _P, _P, _I32, _P, _P, _P],
     "isg_tile_order_keys": [_I32, _P, _P, _P, _P],
+    "isg_sort_pairs_dev": [_P, _SZ, _I32, _P, _P, _P, _P, _I64, _P, _I32, _I32, _P],
+    "isg_tile_offsets_dev": [_I64, _P, _P, _I32, _I32, _P, _P],
     "isg_contrib_mask_words": [_I64, _I32],
     "isg_loss_l1_dssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _I32, _D, _P, _P, _P],
     "isg_ssim": [_P, _SZ, _I32, _I32, _I32, _P, _P, _P, _P],
@@ -111,7 +115,8 @@ SIGNATURES = {
     "isg_route_plan": [_I64, _P, _P, _P, _I32, _I32, _P, _P, _P],
     "isg_route_pack": [_I64, _P, _P, _P, _P, _P, _I32, _P, _P, _I32, _P, _P, _P, _P, _P],
     "isg_band_blocks": [_I64, _P, _I32, _I32, _I32, _P, _P],
-    "isg_band_fold": [_I64, _P, _P, _P, _P, _P, _I32, _I32, _P, _P],
+    "isg_band_fold": [_I64, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P],
+    "isg_reduce_live": [_I64, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P],
     "isg_band_cost": [_P, _I32, _I32, _I32, _I32, _P, _P],
     "isg_owner_fold_plan": [_I64, _P, _P, _P, _I32, _I32, _P, _P, _P, _P],
     "isg_grad_rows": [_I64, _P, _P, _P, _P],

@@ -19,12 +19,14 @@ __global__ void __launch_bounds__(256) gather_rank_kernel(
     int64_t n, const uint64_t *__restrict__ sorted_keys, const int32_t *__restrict__ order,
     const int4 *__restrict__ rect, int rect_stride4, const float4 *__restrict__ feat,
     int feat_stride4, int feat_vec4, int row_lo, int row_hi, int4 *__restrict__ rect_sorted,
-    float4 *__restrict__ feat_sorted, int64_t *__restrict__ cnt, int64_t *__restrict__ counts) {
+    float4 *__restrict__ feat_sorted, int64_t *__restrict__ cnt, int64_t *__restrict__ counts,
+    int64_t *__restrict__ cnt_live, uint64_t *__restrict__ live_mask) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const uint64_t key = sorted_keys[r];
     const bool vis = key != ~0ull;
-    int64_t c = 0;
+    int64_t c = 0, cl = 0;
+    uint64_t lm = 0;
     if (vis) {
         const int32_t row = order[r];
         int4 rc = rect[(int64_t)rect_stride4 * row];
@@ -34,10 +36,28 @@ __global__ void __launch_bounds__(256) gather_rank_kernel(
         int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
         if (y1 >= y0) c = (int64_t)(rc.z - rc.x + 1) * (int64_t)(y1 - y0 + 1);
         if (r + 1 == n || sorted_keys[r + 1] == ~0ull) counts[0] = r + 1;
+        if (cnt_live && c) {
+            // live tiles: those some pixel centre of can reach alpha >= 1/255
+            // (the rasteriser's conservative box test); a bit mask of them in
+            // row-major rect order for rects of <= 64 tiles
+            const f32::CullForm cf =
+                f32::cull_form(f32::stage(reinterpret_cast<const float *>(feat_sorted), (int)r));
+            int k = 0;
+            for (int ty = y0; ty <= y1; ty++)
+                for (int tx = rc.x; tx <= rc.z; tx++, k++)
+                    if (!f32::box_dead_cf(cf, (float)(16 * tx), (float)(16 * ty), 15.0f)) {
+                        cl++;
+                        if (k < 64) lm |= 1ull << k;
+                    }
+        }
     } else {
         rect_sorted[r] = make_int4(0, 0, -1, -1);
     }
     cnt[r] = c;
+    if (cnt_live) {
+        cnt_live[r] = cl;
+        if (live_mask) live_mask[r] = lm;
+    }
 }
 
 
@@ -54,13 +74,6 @@ __global__ void __launch_bounds__(256) gather_rank_kernel(
 constexpr int EMIT_R = EMIT_RANKS;
 constexpr int ECH = 1024;  // slots per scan chunk (4 per thread)
 
-// CULL (float32 training path): a (tile, splat) pair whose 16x16 tile no
-// pixel centre of can reach alpha >= 1/255 (the rasteriser's exact
-// conservative box test over the tile) is never composited: it gets the key
-// `dead_key` (one past the band's last tile, so the stable sort moves it past
-// every list and the CSR offsets leave it out) and its all-zero gradient
-// subtotal is written here.  30 % of the pairs at config 3; every image,
-// gradient and parameter stays bit-identical.
 template <typename K, bool CULL>
 __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
                                                         const int4 *__restrict__ rect_sorted,
@@ -147,11 +160,115 @@ __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
     }
 }
 
+// Live-only emission (the float32 training lists): the same entry-parallel
+// walk over the full rect span, but only the pairs some pixel of their tile
+// can composite are written, compacted in walk order: pair p (its subtotal
+// slot) gets key[p] = tile and slot_rank[p] = rank, p = live_off[rank] +
+// live index.  Live decisions come from gather's mask (rects of <= 64 tiles)
+// or are recomputed.  No zero records: an uncomposited pair has no slot.
+template <typename K>
+__global__ void __launch_bounds__(256) emit_live_kernel(
+    int64_t m, const int4 *__restrict__ rect_sorted, const int64_t *__restrict__ emit_off,
+    const int64_t *__restrict__ live_off, const uint64_t *__restrict__ live_mask,
+    const float *__restrict__ feat_sorted, int tiles_x, int row_lo, K *__restrict__ tile_keys,
+    int32_t *__restrict__ slot_rank) {
+    __shared__ int64_t soff[EMIT_R + 1];
+    __shared__ int4 srect[EMIT_R];
+    __shared__ uint64_t smask[EMIT_R];
+    __shared__ f32::CullForm scf[EMIT_R];
+    __shared__ int srk[ECH];
+    __shared__ int swarp[8];
+    __shared__ int scnt[8];
+    const int64_t r0 = (int64_t)blockIdx.x * EMIT_R;
+    const int nr = (int)min((int64_t)EMIT_R, m - r0);
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) soff[i] = emit_off[r0 + i];
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+        int4 rc = rect_sorted[r0 + i];
+        rc.y = max(rc.y, row_lo);
+        rc.w = rc.z - rc.x + 1;
+        srect[i] = rc;
+        smask[i] = live_mask[r0 + i];
+        scf[i] = f32::cull_form(f32::stage(feat_sorted, (int)(r0 + i)));
+    }
+    __syncthreads();
+    const int64_t s0 = soff[0], s1 = soff[nr];
+    const uint32_t base_tile = (uint32_t)row_lo * (uint32_t)tiles_x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int carry = -1;
+    int64_t out = live_off[r0];  // this block's first live slot
+    for (int64_t c = s0; c < s1; c += ECH) {
+        const int n = (int)min((int64_t)ECH, s1 - c);
+        for (int i = t; i < ECH; i += 256) srk[i] = -1;
+        __syncthreads();
+        for (int i = t; i < nr; i += 256) {
+            const int64_t a = soff[i];
+            if (soff[i + 1] > a && a >= c && a < c + ECH) srk[a - c] = i;
+        }
+        __syncthreads();
+        int v0 = srk[4 * t], v1 = max(v0, srk[4 * t + 1]), v2 = max(v1, srk[4 * t + 2]),
+            v3 = max(v2, srk[4 * t + 3]);
+        int x = v3;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = max(x, y);
+        }
+        if (lane == 31) swarp[warp] = x;
+        __syncthreads();
+        int ex = max(carry, __shfl_up_sync(0xffffffffu, x, 1));
+        if (lane == 0) ex = carry;
+        for (int w = 0; w < warp; w++) ex = max(ex, swarp[w]);
+        srk[4 * t] = max(ex, v0);
+        srk[4 * t + 1] = max(ex, v1);
+        srk[4 * t + 2] = max(ex, v2);
+        srk[4 * t + 3] = max(ex, v3);
+        __syncthreads();
+        // rounds of 256 consecutive slots: live flags -> block prefix -> slots
+        for (int i0 = 0; i0 < n; i0 += 256) {
+            const int i = i0 + t;
+            bool live = false;
+            int lo = 0, dx = 0, dy = 0;
+            if (i < n) {
+                lo = srk[i];
+                const int4 rc = srect[lo];
+                const int k = (int)(c + i - soff[lo]);
+                dy = k / rc.w;
+                dx = k - dy * rc.w;
+                live = k < 64 ? ((smask[lo] >> k) & 1ull)
+                              : !f32::box_dead_cf(scf[lo], (float)(16 * (rc.x + dx)),
+                                                  (float)(16 * (rc.y + dy)), 15.0f);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, live);
+            if (lane == 0) scnt[warp] = __popc(bal);
+            __syncthreads();
+            int before = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < 8; w++) {
+                if (w < warp) before += scnt[w];
+                tot += scnt[w];
+            }
+            if (live) {
+                const int64_t p = out + before + __popc(bal & ((1u << lane) - 1u));
+                const int4 rc = srect[lo];
+                tile_keys[p] = (K)((uint32_t)(rc.y + dy) * (uint32_t)tiles_x - base_tile +
+                                   (uint32_t)(rc.x + dx));
+                slot_rank[p] = (int32_t)(r0 + lo);
+            }
+            out += tot;
+            __syncthreads();  // scnt is rewritten next round
+        }
+        carry = srk[n - 1];
+        __syncthreads();  // srk is rewritten by the next chunk
+    }
+}
+
 template <typename K>
 __global__ void tile_offsets_kernel(int64_t e, const K *__restrict__ keys, int n_tiles,
-                                    int32_t *__restrict__ offsets) {
+                                    int32_t *__restrict__ offsets,
+                                    const int64_t *__restrict__ e_dev) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t > n_tiles) return;
+    if (e_dev) e = min(e, *e_dev);
     int64_t lo = 0, hi = e;  // lower_bound(keys, t)
     while (lo < hi) {
         int64_t mid = (lo + hi) >> 1;
@@ -309,31 +426,38 @@ static int bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_
                      const int32_t *order, const int4 *rect, int rect_stride4,
                      const float4 *feat, int feat_stride4, int vec4, int32_t row_lo,
                      int32_t row_hi, int32_t *rect_sorted, void *feat_sorted, int64_t *emit_off,
-                     int64_t *counts, void *stream) {
+                     int64_t *counts, void *stream, bool live = false,
+                     int64_t *live_off = nullptr, uint64_t *live_mask = nullptr) {
     if (!ws_bytes || n < 0 || n > INT32_MAX || row_lo < 0 || row_hi < row_lo)
         return (int)cudaErrorInvalidValue;
     const size_t scan_bytes = scan_i64_ws_bytes(n > 0 ? n : 1);
-    const size_t need = align_up(sizeof(int64_t) * (size_t)(n > 0 ? n : 1)) + align_up(scan_bytes);
+    const size_t cnt_bytes = align_up(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    const size_t need = (live ? 2 : 1) * cnt_bytes + align_up(scan_bytes);
     if (!workspace) {
         *ws_bytes = need;
         return 0;
     }
-    if (*ws_bytes < need) return (int)cudaErrorInvalidValue;
+    if (*ws_bytes < need || (live && (!live_off || !live_mask))) return (int)cudaErrorInvalidValue;
     cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), s);
+    cudaError_t e = cudaMemsetAsync(counts, 0, (live ? 3 : 2) * sizeof(int64_t), s);
     if (e != cudaSuccess) return (int)e;
     e = cudaMemsetAsync(emit_off, 0, sizeof(int64_t), s);
+    if (e == cudaSuccess && live_off) e = cudaMemsetAsync(live_off, 0, sizeof(int64_t), s);
     if (e != cudaSuccess) return (int)e;
     if (n == 0) return 0;
     int64_t *cnt = (int64_t *)workspace;
-    void *scan_ws = (char *)workspace + align_up(sizeof(int64_t) * (size_t)n);
+    int64_t *cnt_live = live_off ? (int64_t *)((char *)workspace + cnt_bytes) : nullptr;
+    void *scan_ws = (char *)workspace + (live_off ? 2 : 1) * cnt_bytes;
     gather_rank_kernel<<<blocks_for(n, 256), 256, 0, s>>>(
         n, sorted_keys, order, rect, rect_stride4, feat, feat_stride4, vec4, row_lo, row_hi,
-        (int4 *)rect_sorted, (float4 *)feat_sorted, cnt, counts);
+        (int4 *)rect_sorted, (float4 *)feat_sorted, cnt, counts, cnt_live, live_mask);
     ISG_CHECK_LAUNCH();
-    const int se = scan_i64(scan_ws, scan_bytes, n, cnt, emit_off, counts + 1, s);
+    int se = scan_i64(scan_ws, scan_bytes, n, cnt, emit_off, counts + 1, s);
     if (se != 0) return se;
-    ISG_CHECK_LAUNCH();
+    if (live_off) {
+        se = scan_i64(scan_ws, scan_bytes, n, cnt_live, live_off, counts + 2, s);
+        if (se != 0) return se;
+    }
     return 0;
 }
 
@@ -347,6 +471,46 @@ extern "C" int isg_bin_count(void *workspace, size_t *ws_bytes, int64_t n,
     return bin_count(workspace, ws_bytes, n, sorted_keys, order, (const int4 *)rect, 1,
                      (const float4 *)feat, vec4, vec4, row_lo, row_hi, rect_sorted, feat_sorted,
                      emit_off, counts, stream);
+}
+
+extern "C" int isg_bin_count_live(void *workspace, size_t *ws_bytes, int64_t n,
+                                  const uint64_t *sorted_keys, const int32_t *order,
+                                  const int32_t *rect, const int32_t *payload, const float *feat,
+                                  int32_t row_lo, int32_t row_hi, int32_t *rect_sorted,
+                                  float *feat_sorted, int64_t *emit_off, int64_t *live_off,
+                                  uint64_t *live_mask, int64_t *counts, void *stream) {
+    const int4 *p = (const int4 *)payload;
+    if (payload)  // 64-byte payload rows: rect then the 12 float32 features
+        return bin_count(workspace, ws_bytes, n, sorted_keys, order, p, 4, (const float4 *)(p + 1),
+                         4, 3, row_lo, row_hi, rect_sorted, feat_sorted, emit_off, counts, stream,
+                         true, live_off, live_mask);
+    return bin_count(workspace, ws_bytes, n, sorted_keys, order, (const int4 *)rect, 1,
+                     (const float4 *)feat, 3, 3, row_lo, row_hi, rect_sorted, feat_sorted,
+                     emit_off, counts, stream, true, live_off, live_mask);
+}
+
+extern "C" int isg_bin_emit_live(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
+                                 const int64_t *live_off, const uint64_t *live_mask,
+                                 const float *feat_sorted, int32_t tiles_x, int32_t row_lo,
+                                 int32_t row_hi, void *tile_keys, int32_t key_bytes,
+                                 int32_t *slot_rank, void *stream) {
+    const int64_t nt = (int64_t)(row_hi - row_lo) * tiles_x;
+    if (m < 0 || tiles_x <= 0 || (key_bytes != 2 && key_bytes != 4) ||
+        (key_bytes == 2 && nt > 65536) ||
+        (m > 0 && (!rect_sorted || !emit_off || !live_off || !live_mask || !feat_sorted ||
+                   !tile_keys || !slot_rank)))
+        return (int)cudaErrorInvalidValue;
+    if (m == 0) return 0;
+    if (key_bytes == 2)
+        emit_live_kernel<uint16_t><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
+            m, (const int4 *)rect_sorted, emit_off, live_off, live_mask, feat_sorted, tiles_x,
+            row_lo, (uint16_t *)tile_keys, slot_rank);
+    else
+        emit_live_kernel<uint32_t><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
+            m, (const int4 *)rect_sorted, emit_off, live_off, live_mask, feat_sorted, tiles_x,
+            row_lo, (uint32_t *)tile_keys, slot_rank);
+    ISG_CHECK_LAUNCH();
+    return 0;
 }
 
 extern "C" int isg_bin_count_rows(void *workspace, size_t *ws_bytes, int64_t n,
@@ -411,20 +575,6 @@ extern "C" int isg_bin_emit16(int64_t m, const int32_t *rect_sorted, const int64
     return 0;
 }
 
-extern "C" int isg_bin_emit16_cull(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
-                                   const float *feat_sorted, int32_t tiles_x, int32_t row_lo,
-                                   int32_t row_hi, uint16_t *tile_keys, int32_t *tile_vals,
-                                   float *partials, void *stream) {
-    const int64_t nt = (int64_t)(row_hi - row_lo) * tiles_x;
-    if (m < 0 || tiles_x <= 0 || nt >= 65536 || (m > 0 && (!feat_sorted || !partials)))
-        return (int)cudaErrorInvalidValue;
-    if (m == 0) return 0;
-    emit_span_kernel<uint16_t, true><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
-        m, (const int4 *)rect_sorted, emit_off, tiles_x, row_lo, row_hi, tile_keys, tile_vals,
-        feat_sorted, partials, (uint32_t)nt);
-    ISG_CHECK_LAUNCH();
-    return 0;
-}
 
 extern "C" int isg_sort_u16(void *workspace, size_t *ws_bytes, const uint16_t *keys_in,
                             uint16_t *keys_out, const int32_t *vals_in, int32_t *vals_out,
@@ -436,11 +586,52 @@ extern "C" int isg_sort_u16(void *workspace, size_t *ws_bytes, const uint16_t *k
                                   begin_bit, end_bit, (cudaStream_t)stream);
 }
 
+extern "C" int isg_sort_pairs_dev(void *workspace, size_t *ws_bytes, int32_t key_bytes,
+                                  const void *keys_in, void *keys_out, const int32_t *vals_in,
+                                  int32_t *vals_out, int64_t n_max, const int64_t *n_dev,
+                                  int32_t begin_bit, int32_t end_bit, void *stream) {
+    if (!ws_bytes || n_max < 0 || n_max > INT32_MAX || begin_bit < 0 || begin_bit >= end_bit ||
+        end_bit > 8 * key_bytes)
+        return (int)cudaErrorInvalidValue;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (key_bytes == 2)
+        return radix::sort_pairs<uint16_t>(workspace, ws_bytes, (const uint16_t *)keys_in,
+                                           (uint16_t *)keys_out, vals_in, vals_out, n_max,
+                                           begin_bit, end_bit, s, n_dev);
+    if (key_bytes == 4)
+        return radix::sort_pairs<uint32_t>(workspace, ws_bytes, (const uint32_t *)keys_in,
+                                           (uint32_t *)keys_out, vals_in, vals_out, n_max,
+                                           begin_bit, end_bit, s, n_dev);
+    if (key_bytes == 8)
+        return radix::sort_pairs<uint64_t>(workspace, ws_bytes, (const uint64_t *)keys_in,
+                                           (uint64_t *)keys_out, vals_in, vals_out, n_max,
+                                           begin_bit, end_bit, s, n_dev);
+    return (int)cudaErrorInvalidValue;
+}
+
+extern "C" int isg_tile_offsets_dev(int64_t e_max, const int64_t *e_dev, const void *sorted_keys,
+                                    int32_t key_bytes, int32_t n_tiles, int32_t *offsets,
+                                    void *stream) {
+    if (e_max < 0 || n_tiles < 0 || !offsets || (key_bytes != 2 && key_bytes != 4) ||
+        (key_bytes == 2 && n_tiles > 65536))
+        return (int)cudaErrorInvalidValue;
+    if (key_bytes == 2)
+        tile_offsets_kernel<uint16_t><<<blocks_for(n_tiles + 1, 256), 256, 0,
+                                        (cudaStream_t)stream>>>(
+            e_max, (const uint16_t *)sorted_keys, n_tiles, offsets, e_dev);
+    else
+        tile_offsets_kernel<uint32_t><<<blocks_for(n_tiles + 1, 256), 256, 0,
+                                        (cudaStream_t)stream>>>(
+            e_max, (const uint32_t *)sorted_keys, n_tiles, offsets, e_dev);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
 extern "C" int isg_tile_offsets16(int64_t e, const uint16_t *sorted_tile_keys, int32_t n_tiles,
                                   int32_t *offsets, void *stream) {
     if (e < 0 || n_tiles < 0 || n_tiles > 65536) return (int)cudaErrorInvalidValue;
     tile_offsets_kernel<uint16_t><<<blocks_for(n_tiles + 1, 256), 256, 0, (cudaStream_t)stream>>>(
-        e, sorted_tile_keys, n_tiles, offsets);
+        e, sorted_tile_keys, n_tiles, offsets, nullptr);
     ISG_CHECK_LAUNCH();
     return 0;
 }
@@ -449,7 +640,7 @@ extern "C" int isg_tile_offsets(int64_t e, const uint32_t *sorted_tile_keys, int
                                 int32_t *offsets, void *stream) {
     if (e < 0 || n_tiles < 0) return (int)cudaErrorInvalidValue;
     tile_offsets_kernel<<<blocks_for(n_tiles + 1, 256), 256, 0, (cudaStream_t)stream>>>(
-        e, sorted_tile_keys, n_tiles, offsets);
+        e, sorted_tile_keys, n_tiles, offsets, (const int64_t *)nullptr);
     ISG_CHECK_LAUNCH();
     return 0;
 }

@@ -21,6 +21,8 @@
 //             of the GPU count, the reference's headline property.
 //   fold    : the owner groups received records by shard row (stable) and
 //             sums them in arrival order (bands ascending).
+#include <type_traits>
+
 #include "common.cuh"
 #include "radix.cuh"
 
@@ -373,10 +375,48 @@ struct BlockEmit {
     }
 };
 
+// Live-only layout: rows from the records (float 9), a record for every block
+// of the rank's clipped rows in the band (zero when no slot of it is live).
+struct BlockEmitLive {
+    double bs[9];
+    int blk, last, canon;
+    double *out;
+
+    __device__ __forceinline__ void init(int4 rc, int row_lo, int row_hi, int canon_rows,
+                                         double *o) {
+        canon = canon_rows;
+        blk = max(rc.y, row_lo) / canon;
+        last = min(rc.w, row_hi - 1) / canon;
+        out = o;
+#pragma unroll
+        for (int k = 0; k < 9; k++) bs[k] = 0.0;
+    }
+    __device__ __forceinline__ void close() {
+#pragma unroll
+        for (int k = 0; k < 9; k++) {
+            out[k] = bs[k];
+            bs[k] = 0.0;
+        }
+        out += 9;
+        blk++;
+    }
+    __device__ __forceinline__ void step(const float *v) {
+        const int b = __float_as_int(v[9]) / canon;
+        while (blk < b) close();
+#pragma unroll
+        for (int k = 0; k < 9; k++) bs[k] += (double)v[k];
+    }
+    __device__ __forceinline__ void finish() {
+        while (blk <= last) close();
+    }
+};
+
+template <bool LIVE>
 __global__ void __launch_bounds__(BF_THREADS) band_fold_kernel(
     int64_t m, const int64_t *__restrict__ emit_off, const float *__restrict__ partials,
     const int4 *__restrict__ rect_sorted, const int32_t *__restrict__ order,
-    const int64_t *__restrict__ gpos, int row_lo, int canon, double *__restrict__ gbuf) {
+    const int64_t *__restrict__ gpos, int row_lo, int row_hi, int canon,
+    double *__restrict__ gbuf) {
     constexpr int PS = partial_stride<float>();
     __shared__ __align__(128) float sbuf[BF_WARPS][2][BF_SLOTS * PS];
     __shared__ __align__(8) uint64_t sbar[BF_WARPS][2];
@@ -389,9 +429,14 @@ __global__ void __launch_bounds__(BF_THREADS) band_fold_kernel(
     const int64_t span1 = emit_off[min(r0 + 32, m)];
     int64_t p = live ? emit_off[r] : 0;
     const int64_t p1 = live ? emit_off[r + 1] : 0;
-    BlockEmit st;
-    st.init(live ? rect_sorted[r] : make_int4(0, 0, 0, 0), row_lo, canon,
-            live ? gbuf + 9 * gpos[order[r]] : gbuf);
+    typename std::conditional<LIVE, BlockEmitLive, BlockEmit>::type st;
+    if constexpr (LIVE) {
+        st.init(live ? rect_sorted[r] : make_int4(0, 0, -1, -1), row_lo, row_hi, canon,
+                live ? gbuf + 9 * gpos[order[r]] : gbuf);
+    } else {
+        st.init(live ? rect_sorted[r] : make_int4(0, 0, 0, 0), row_lo, canon,
+                live ? gbuf + 9 * gpos[order[r]] : gbuf);
+    }
     const int nch = (int)((span1 - span0 + BF_SLOTS - 1) / BF_SLOTS);
     float(*buf)[BF_SLOTS * PS] = sbuf[warp];
     uint64_t *bar = sbar[warp];
@@ -616,12 +661,19 @@ extern "C" int isg_band_blocks(int64_t r, const int32_t *payload, int32_t row_lo
 
 extern "C" int isg_band_fold(int64_t m, const int64_t *emit_off, const float *partials,
                              const int32_t *rect_sorted, const int32_t *order,
-                             const int64_t *gpos, int32_t row_lo, int32_t canon_rows,
-                             double *gbuf, void *stream) {
+                             const int64_t *gpos, int32_t row_lo, int32_t row_hi,
+                             int32_t canon_rows, int32_t live_layout, double *gbuf, void *stream) {
     if (m < 0 || canon_rows < 1) return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
-    band_fold_kernel<<<blocks_for(m, BF_THREADS), BF_THREADS, 0, (cudaStream_t)stream>>>(
-        m, emit_off, partials, (const int4 *)rect_sorted, order, gpos, row_lo, canon_rows, gbuf);
+    if (live_layout)
+        band_fold_kernel<true><<<blocks_for(m, BF_THREADS), BF_THREADS, 0, (cudaStream_t)stream>>>(
+            m, emit_off, partials, (const int4 *)rect_sorted, order, gpos, row_lo, row_hi,
+            canon_rows, gbuf);
+    else
+        band_fold_kernel<false><<<blocks_for(m, BF_THREADS), BF_THREADS, 0,
+                                  (cudaStream_t)stream>>>(
+            m, emit_off, partials, (const int4 *)rect_sorted, order, gpos, row_lo, row_hi,
+            canon_rows, gbuf);
     ISG_CHECK_LAUNCH();
     return 0;
 }

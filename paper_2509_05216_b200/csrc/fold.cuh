@@ -63,6 +63,43 @@ struct FoldState {
     }
 };
 
+// The same fold over the live-only layout (isg_bin_emit_live): a rank's slots
+// are its composited tiles only, each record carrying its tile row (int32 bits
+// in float 9).  Every canonical block of the rank's clipped rows closes in
+// order -- blocks without a slot add a zero block sum -- so the sequence of
+// block sums, and the result, is the full-layout fold's.
+struct FoldLive {
+    double acc[9], bs[9];
+    int blk, last, canon;
+
+    __device__ __forceinline__ void init(const int4 *__restrict__ rect_sorted, int64_t r,
+                                         int row_lo, int row_hi, int canon_rows) {
+        const int4 rc = rect_sorted[r];
+        canon = canon_rows;
+        blk = max(rc.y, row_lo) / canon;
+        last = min(rc.w, row_hi - 1) / canon;
+#pragma unroll
+        for (int k = 0; k < 9; k++) acc[k] = bs[k] = 0.0;
+    }
+    __device__ __forceinline__ void close() {
+#pragma unroll
+        for (int k = 0; k < 9; k++) {
+            acc[k] += bs[k];
+            bs[k] = 0.0;
+        }
+        blk++;
+    }
+    __device__ __forceinline__ void step(const float *v) {
+        const int b = __float_as_int(v[9]) / canon;
+        while (blk < b) close();
+#pragma unroll
+        for (int k = 0; k < 9; k++) bs[k] += (double)v[k];
+    }
+    __device__ __forceinline__ void finish() {
+        while (blk <= last) close();
+    }
+};
+
 template <typename T>
 __device__ __forceinline__ void fold_rank(const T *__restrict__ partials, int64_t p0, int64_t p1,
                                           const int4 *__restrict__ rect_sorted, int64_t r,

@@ -10,10 +10,10 @@
 //                keys) in warp-private shared-memory counters -> counts[digit][cta]
 //     scan     : digit-major exclusive scan of the counts (4096-element
 //                chunks in shared memory + one CTA over the chunk sums)
-//     scatter  : each CTA stages its keys/values in shared memory, ranks them
-//                stably (warp-level multi-split: peers from one ballot per
-//                digit bit, per-warp digit counters, warps in item order),
-//                permutes them into
+//     scatter  : each warp loads its slice of the CTA's keys/values into
+//                registers, ranks them stably (warp-level multi-split: peers
+//                from one ballot per digit bit, per-warp digit counters,
+//                warps in item order), permutes them into
 //                digit order in shared memory and writes each digit run to
 //                its global offset with consecutive threads on consecutive
 //                addresses (coalesced stores)
@@ -36,9 +36,7 @@ template <typename K>
 constexpr int ipc() { return sizeof(K) == 8 ? 2048 : 4096; }
 constexpr int BINS = 256;
 constexpr int SC = 4096;       // scan chunk (elements per CTA)
-#ifndef RADIX_STAGE_OUT
-#define RADIX_STAGE_OUT 1
-#endif
+
 
 template <typename K>
 __device__ __forceinline__ unsigned digit_of(K k, int shift, unsigned mask) {
@@ -69,14 +67,16 @@ constexpr int kvec() { return ipt<K>() * (int)sizeof(K) / 16; }
 template <typename K, bool VEC>
 __global__ void __launch_bounds__(RT) upsweep_kernel(const K *__restrict__ keys, int64_t n,
                                                      int shift, unsigned mask, int nblk,
-                                                     uint32_t *__restrict__ counts) {
+                                                     uint32_t *__restrict__ counts,
+                                                     const int64_t *__restrict__ n_dev) {
     constexpr int IPC = ipc<K>(), IPT = ipt<K>();
+    if (n_dev) n = min(n, *n_dev);  // device-side item count (upper bound n)
     __shared__ uint32_t h[NWARP][BINS];
     const int warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < NWARP * BINS; i += RT) (&h[0][0])[i] = 0u;
     __syncthreads();
     const int64_t base = (int64_t)blockIdx.x * IPC;
-    const int nv = (int)min((int64_t)IPC, n - base);
+    const int nv = (int)max((int64_t)0, min((int64_t)IPC, n - base));
     if (VEC && nv == IPC) {
         // blocked: thread t owns items [t * IPT, (t + 1) * IPT), all loads in flight
         union {
@@ -101,19 +101,27 @@ __global__ void __launch_bounds__(RT) upsweep_kernel(const K *__restrict__ keys,
     }
 }
 
-// Exclusive scan of a CTA's chunk of SC elements in place; chunk total to sums.
+// Exclusive scan of a CTA's chunk of SC elements (in -> out, may alias);
+// chunk total to sums.  Coalesced through shared memory.
 template <typename T>
-__global__ void __launch_bounds__(RT) scan_chunks_kernel(T *__restrict__ a, int64_t n,
+__global__ void __launch_bounds__(RT) scan_chunks_kernel(const T *in, T *out, int64_t n,
                                                          T *__restrict__ sums) {
-    constexpr int PER = SC / RT;  // elements per thread (contiguous)
+    constexpr int PER = SC / RT;  // elements per thread (contiguous in shared memory)
+    __shared__ T sm[SC];
     __shared__ T swarp[NWARP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t base = (int64_t)blockIdx.x * SC + (int64_t)threadIdx.x * PER;
+    const int64_t cb = (int64_t)blockIdx.x * SC;
+#pragma unroll
+    for (int k = 0; k < PER; k++) {
+        const int64_t i = cb + k * RT + threadIdx.x;
+        sm[k * RT + threadIdx.x] = i < n ? in[i] : (T)0;
+    }
+    __syncthreads();
     T v[PER];
     T s = 0;
 #pragma unroll
     for (int k = 0; k < PER; k++) {
-        v[k] = base + k < n ? a[base + k] : (T)0;
+        v[k] = sm[threadIdx.x * PER + k];
         s += v[k];
     }
     T x = s;
@@ -133,8 +141,14 @@ __global__ void __launch_bounds__(RT) scan_chunks_kernel(T *__restrict__ a, int6
     T run = before + x - s;
 #pragma unroll
     for (int k = 0; k < PER; k++) {
-        if (base + k < n) a[base + k] = run;
+        sm[threadIdx.x * PER + k] = run;
         run += v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PER; k++) {
+        const int64_t i = cb + k * RT + threadIdx.x;
+        if (i < n) out[i] = sm[k * RT + threadIdx.x];
     }
     if (threadIdx.x == 0) sums[blockIdx.x] = total;
 }
@@ -180,22 +194,129 @@ __global__ void __launch_bounds__(RT) scatter_kernel(const K *__restrict__ keys_
                                                      int32_t *__restrict__ vals_out, int64_t n,
                                                      int shift, unsigned mask, int nblk,
                                                      const uint32_t *__restrict__ offs,
-                                                     const uint32_t *__restrict__ chunk_off) {
+                                                     const uint32_t *__restrict__ chunk_off,
+                                                     const int64_t *__restrict__ n_dev) {
+    constexpr int IPC = ipc<K>(), IPT = ipt<K>();
+    constexpr int SLICE = IPC / NWARP;  // = 32 * IPT
+    const int bits = __popc(mask);
+    extern __shared__ __align__(16) unsigned char smem[];
+    K *sk = reinterpret_cast<K *>(smem);                   // digit-ordered staging
+    int32_t *sv = reinterpret_cast<int32_t *>(sk + IPC);
+    __shared__ uint32_t wcnt[NWARP][BINS];
+    __shared__ uint32_t dstart[BINS];
+    __shared__ int64_t gdelta[BINS];
+    __shared__ uint32_t sw[NWARP];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (n_dev) n = min(n, *n_dev);
+    const int64_t base = (int64_t)blockIdx.x * IPC;
+    if (base >= n) return;
+    const int nv = (int)min((int64_t)IPC, n - base);
+    for (int i = threadIdx.x; i < NWARP * BINS; i += RT) (&wcnt[0][0])[i] = 0u;
+    // a warp's slice, lane-interleaved: item r * 32 + lane of the slice
+    K k[IPT];
+    int32_t v[IPT];
+    const int64_t sbase = base + warp * SLICE;
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        const int i = warp * SLICE + r * 32 + lane;
+        if (i < nv) {
+            k[r] = keys_in[sbase + r * 32 + lane];
+            v[r] = vals_in[sbase + r * 32 + lane];
+        }
+    }
+    __syncthreads();
+    // warp-level multi-split: rank of every item among the same digit in its
+    // slice (items in slice order), kept in registers
+    uint32_t lp[IPT];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        const bool valid = warp * SLICE + r * 32 + lane < nv;
+        const unsigned d = valid ? digit_of(k[r], shift, mask) : BINS;
+        const unsigned peers = digit_peers(d, bits);
+        uint32_t c = 0;
+        if (valid) c = wcnt[warp][d];
+        lp[r] = c + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (__ffs(peers) - 1) == lane) wcnt[warp][d] = c + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: warp prefixes, CTA total; exclusive scan over digits
+    const int d = threadIdx.x;  // RT == BINS
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < NWARP; w++) {
+        const uint32_t c = wcnt[w][d];
+        wcnt[w][d] = tot;
+        tot += c;
+    }
+    uint32_t x = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sw[warp] = x;
+    const int64_t ci = (int64_t)d * nblk + blockIdx.x;
+    const int64_t go = (int64_t)offs[ci] + chunk_off[ci / SC];
+    __syncthreads();
+    uint32_t before = 0;
+#pragma unroll
+    for (int w = 0; w < NWARP; w++)
+        if (w < warp) before += sw[w];
+    const uint32_t ds = before + x - tot;
+    dstart[d] = ds;
+    gdelta[d] = go - (int64_t)ds;
+    __syncthreads();
+    // permute into digit order in shared memory
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        if (warp * SLICE + r * 32 + lane < nv) {
+            const unsigned dd = digit_of(k[r], shift, mask);
+            const uint32_t dest = dstart[dd] + wcnt[warp][dd] + lp[r];
+            sk[dest] = k[r];
+            sv[dest] = v[r];
+        }
+    }
+    __syncthreads();
+    // each digit run to its global offset (consecutive threads, consecutive addresses)
+    for (int j = threadIdx.x; j < nv; j += RT) {
+        const K kk = sk[j];
+        const int64_t g = gdelta[digit_of(kk, shift, mask)] + j;
+        keys_out[g] = kk;
+        vals_out[g] = sv[j];
+    }
+}
+
+// 2- and 4-byte keys: the CTA's items staged in shared memory with 16-byte
+// vector loads, ranked, permuted into a second staging area, written out.
+template <typename K, bool VEC>
+__global__ void __launch_bounds__(RT) scatter_staged_kernel(const K *__restrict__ keys_in,
+                                                     const int32_t *__restrict__ vals_in,
+                                                     K *__restrict__ keys_out,
+                                                     int32_t *__restrict__ vals_out, int64_t n,
+                                                     int shift, unsigned mask, int nblk,
+                                                     const uint32_t *__restrict__ offs,
+                                                     const uint32_t *__restrict__ chunk_off,
+                                                     const int64_t *__restrict__ n_dev) {
     constexpr int IPC = ipc<K>();
     constexpr int SLICE = IPC / NWARP;
     const int bits = __popc(mask);
     extern __shared__ __align__(16) unsigned char smem[];
     K *sk = reinterpret_cast<K *>(smem);
     K *sk2 = sk + IPC;
-    int32_t *sv = reinterpret_cast<int32_t *>(RADIX_STAGE_OUT ? sk2 + IPC : sk2);
+    int32_t *sv = reinterpret_cast<int32_t *>(sk2 + IPC);
     int32_t *sv2 = sv + IPC;
-    uint16_t *slp = reinterpret_cast<uint16_t *>(RADIX_STAGE_OUT ? sv2 + IPC : sv2);
+    uint16_t *slp = reinterpret_cast<uint16_t *>(sv2 + IPC);
     __shared__ uint32_t wcnt[NWARP][BINS];
     __shared__ uint32_t dstart[BINS];
     __shared__ uint32_t goff[BINS];
     __shared__ uint32_t sw[NWARP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (n_dev) n = min(n, *n_dev);
     const int64_t base = (int64_t)blockIdx.x * IPC;
+    if (base >= n) return;
     const int nv = (int)min((int64_t)IPC, n - base);
     if (VEC && nv == IPC) {
         // all of a thread's loads in flight at once (16-byte vectors), then
@@ -260,7 +381,6 @@ __global__ void __launch_bounds__(RT) scatter_kernel(const K *__restrict__ keys_
         if (w < warp) before += sw[w];
     dstart[d] = before + x - tot;
     __syncthreads();
-#if RADIX_STAGE_OUT
     // permute into digit order in shared memory
     for (int i = threadIdx.x; i < nv; i += RT) {
         const unsigned dd = digit_of(sk[i], shift, mask);
@@ -277,24 +397,18 @@ __global__ void __launch_bounds__(RT) scatter_kernel(const K *__restrict__ keys_
         keys_out[g] = k;
         vals_out[g] = sv2[j];
     }
-#else
-    // straight to the global position (runs of one digit land contiguously)
-    for (int i = threadIdx.x; i < nv; i += RT) {
-        const K k = sk[i];
-        const unsigned dd = digit_of(k, shift, mask);
-        const int64_t g = (int64_t)goff[dd] + wcnt[i / SLICE][dd] + slp[i];
-        keys_out[g] = k;
-        vals_out[g] = sv[i];
-    }
-#endif
 }
 
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// 8-byte keys: items in registers (scatter_kernel); smaller keys: staged
+// twice in shared memory (scatter_staged_kernel)
+template <typename K>
+constexpr bool staged() { return sizeof(K) < 8; }
 template <typename K>
 constexpr size_t scatter_smem() {
-    return (size_t)ipc<K>() * ((RADIX_STAGE_OUT ? 2 : 1) * (sizeof(K) + sizeof(int32_t)) +
-                               sizeof(uint16_t));
+    return staged<K>() ? (size_t)ipc<K>() * (2 * (sizeof(K) + sizeof(int32_t)) + sizeof(uint16_t))
+                       : (size_t)ipc<K>() * (sizeof(K) + sizeof(int32_t));
 }
 
 // Workspace: key/value ping-pong buffers, digit counts, chunk sums.
@@ -310,7 +424,7 @@ size_t sort_ws_bytes(int64_t n) {
 template <typename K>
 int sort_pairs(void *ws, size_t *ws_bytes, const K *keys_in, K *keys_out,
                const int32_t *vals_in, int32_t *vals_out, int64_t n, int b0, int b1,
-               cudaStream_t s) {
+               cudaStream_t s, const int64_t *n_dev) {
     if (!ws_bytes || n < 0 || n > INT32_MAX || b0 < 0 || b1 > (int)(8 * sizeof(K)) || b0 >= b1)
         return (int)cudaErrorInvalidValue;
     const size_t need = sort_ws_bytes<K>(n);
@@ -332,7 +446,8 @@ int sort_pairs(void *ws, size_t *ws_bytes, const K *keys_in, K *keys_out,
     p += al(sizeof(uint32_t) * (size_t)nc);
     uint32_t *csum = (uint32_t *)p;
     const int passes = (b1 - b0 + 7) / 8;
-    for (auto fn : {scatter_kernel<K, true>, scatter_kernel<K, false>}) {
+    for (auto fn : {scatter_kernel<K, true>, scatter_kernel<K, false>,
+                    scatter_staged_kernel<K, true>, scatter_staged_kernel<K, false>}) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)scatter_smem<K>());
         if (e == cudaSuccess)
@@ -353,21 +468,24 @@ int sort_pairs(void *ws, size_t *ws_bytes, const K *keys_in, K *keys_out,
         const bool vec = ((uintptr_t)src_k % 16 == 0) && ((uintptr_t)src_v % 16 == 0);
         if (vec)
             upsweep_kernel<K, true><<<(unsigned)nblk, RT, 0, s>>>(src_k, n, shift, mask,
-                                                                  (int)nblk, counts);
+                                                                  (int)nblk, counts, n_dev);
         else
             upsweep_kernel<K, false><<<(unsigned)nblk, RT, 0, s>>>(src_k, n, shift, mask,
-                                                                   (int)nblk, counts);
+                                                                   (int)nblk, counts, n_dev);
         ISG_CHECK_LAUNCH();
-        scan_chunks_kernel<uint32_t><<<(unsigned)nch, RT, 0, s>>>(counts, nc, csum);
+        scan_chunks_kernel<uint32_t><<<(unsigned)nch, RT, 0, s>>>(counts, counts, nc, csum);
         ISG_CHECK_LAUNCH();
         scan_sums_kernel<uint32_t><<<1, 1024, 0, s>>>(csum, nch, nullptr);
         ISG_CHECK_LAUNCH();
-        if (vec)
+        if (!staged<K>())
             scatter_kernel<K, true><<<(unsigned)nblk, RT, scatter_smem<K>(), s>>>(
-                src_k, src_v, dst_k, dst_v, n, shift, mask, (int)nblk, counts, csum);
+                src_k, src_v, dst_k, dst_v, n, shift, mask, (int)nblk, counts, csum, n_dev);
+        else if (vec)
+            scatter_staged_kernel<K, true><<<(unsigned)nblk, RT, scatter_smem<K>(), s>>>(
+                src_k, src_v, dst_k, dst_v, n, shift, mask, (int)nblk, counts, csum, n_dev);
         else
-            scatter_kernel<K, false><<<(unsigned)nblk, RT, scatter_smem<K>(), s>>>(
-                src_k, src_v, dst_k, dst_v, n, shift, mask, (int)nblk, counts, csum);
+            scatter_staged_kernel<K, false><<<(unsigned)nblk, RT, scatter_smem<K>(), s>>>(
+                src_k, src_v, dst_k, dst_v, n, shift, mask, (int)nblk, counts, csum, n_dev);
         ISG_CHECK_LAUNCH();
         src_k = dst_k;
         src_v = dst_v;
@@ -383,11 +501,6 @@ size_t scan_i64_ws_bytes(int64_t n) {
     return radix::al(sizeof(int64_t) * (size_t)((n + radix::SC - 1) / radix::SC + 1));
 }
 
-__global__ void copy_i64_kernel(int64_t n, const int64_t *__restrict__ in,
-                                int64_t *__restrict__ out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = in[i];
-}
 
 __global__ void scan_tail_kernel(int64_t n, int64_t *__restrict__ off,
                                  const int64_t *__restrict__ csum, const int64_t *__restrict__ cnt,
@@ -413,9 +526,7 @@ int scan_i64(void *ws, size_t ws_bytes, int64_t n, const int64_t *cnt, int64_t *
     }
     const int64_t nch = (n + radix::SC - 1) / radix::SC;
     int64_t *csum = (int64_t *)ws;
-    copy_i64_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, cnt, off);
-    ISG_CHECK_LAUNCH();
-    radix::scan_chunks_kernel<int64_t><<<(unsigned)nch, radix::RT, 0, s>>>(off, n, csum);
+    radix::scan_chunks_kernel<int64_t><<<(unsigned)nch, radix::RT, 0, s>>>(cnt, off, n, csum);
     ISG_CHECK_LAUNCH();
     radix::scan_sums_kernel<int64_t><<<1, 1024, 0, s>>>(csum, nch, nullptr);
     ISG_CHECK_LAUNCH();
@@ -426,12 +537,12 @@ int scan_i64(void *ws, size_t ws_bytes, int64_t n, const int64_t *cnt, int64_t *
 
 template int radix::sort_pairs<uint16_t>(void *, size_t *, const uint16_t *, uint16_t *,
                                          const int32_t *, int32_t *, int64_t, int, int,
-                                         cudaStream_t);
+                                         cudaStream_t, const int64_t *);
 template int radix::sort_pairs<uint32_t>(void *, size_t *, const uint32_t *, uint32_t *,
                                          const int32_t *, int32_t *, int64_t, int, int,
-                                         cudaStream_t);
+                                         cudaStream_t, const int64_t *);
 template int radix::sort_pairs<uint64_t>(void *, size_t *, const uint64_t *, uint64_t *,
                                          const int32_t *, int32_t *, int64_t, int, int,
-                                         cudaStream_t);
+                                         cudaStream_t, const int64_t *);
 
 }  // namespace isg

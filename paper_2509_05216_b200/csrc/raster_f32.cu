@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
     float bg2, void *image, int image_f64,
     float *__restrict__ t_final, int32_t *__restrict__ n_last, int32_t *__restrict__ n_contrib,
     int32_t *__restrict__ n_iter, int64_t *__restrict__ touched, uint32_t *__restrict__ cmask,
-    int chunk, float4 *__restrict__ cstate, int32_t *__restrict__ qlast) {
+    int chunk, float4 *__restrict__ cstate, int32_t *__restrict__ qlast,
+    const int32_t *__restrict__ slot_rank) {
     constexpr bool TOUCH = MODE & F_TOUCH;
     // slot WB of each warp's slice is a sentinel entry that never composites
     // (opacity 0): odd lists are padded with it, so entries go two at a time
@@ -256,7 +257,9 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
         const int j = base + lane;
         bool alive = false;
         if (j < n_ent) {
-            const int rank = entries[e0 + j];
+            // live-only lists hold subtotal slots: slot_rank maps them to ranks
+            const int32_t ent = entries[e0 + j];
+            const int rank = slot_rank ? slot_rank[ent] : ent;
             Staged st = stage(feat, rank);
             alive = !box_dead(st, qx0, qy0, 7.0f);
             to_log2(st);
@@ -487,7 +490,8 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
     const float *__restrict__ t_final, const int32_t *__restrict__ n_last,
     const DL *__restrict__ dl, float *__restrict__ partials, const uint32_t *__restrict__ cmask,
     const int2 *__restrict__ items, const int32_t *__restrict__ n_items, int chunk,
-    const float4 *__restrict__ cstate, const float *__restrict__ image) {
+    const float4 *__restrict__ cstate, const float *__restrict__ image,
+    const int32_t *__restrict__ slot_rank) {
     constexpr int NH = BNT / 32;  // warps per tile: one per 16x8 half
     __shared__ float4 sgh_all[NH][WB][2];
     __shared__ float4 scol_all[NH][WB];
@@ -595,7 +599,8 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
             alive = (bm >> lane) & 1u;
         }
         if (MASK ? alive : (j < end && j < wm)) {
-            Staged st = stage(feat, entries[e0 + j]);
+            const int32_t ent = entries[e0 + j];
+            Staged st = stage(feat, slot_rank ? slot_rank[ent] : ent);
             if (!MASK) alive = !box_dead(st, qx0, qy0, 15.0f, 7.0f);
             to_log2(st);
             sgh[lane][0] = st.g;
@@ -646,9 +651,12 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
             __threadfence_block();
             const int jf = start + lane;
             if (jf < end) {
-                const int rank = entries[e0 + jf];
+                const int32_t ent = entries[e0 + jf];
+                const int rank = slot_rank ? slot_rank[ent] : ent;
                 int64_t slot;
-                if (emit_off) {
+                if (slot_rank) {
+                    slot = ent;  // live-only layout: the list entry is the slot
+                } else if (emit_off) {
                     const int4 rc = rect_sorted[rank];
                     slot = emit_off[rank] + (int64_t)(ty - max(rc.y, row_lo)) * (rc.z - rc.x + 1) +
                            (tx - rc.x);
@@ -659,11 +667,13 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
                 unsigned pm = 0u;
 #pragma unroll
                 for (int w = 0; w < NH; w++) pm |= ((spres[rs][w] >> lane) & 1u) << w;
+                // live-only records carry their tile row (the fold's block key)
+                const float rowf = slot_rank ? __int_as_float(ty) : 0.0f;
                 if (pm == 0u) {
                     const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                     dst[0] = z;
                     dst[1] = z;
-                    dst[2] = z;
+                    dst[2] = make_float4(0.0f, rowf, 0.0f, 0.0f);
                 } else {
                     float acc[9];
 #pragma unroll
@@ -682,7 +692,7 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
                                          -0.5f * acc[2], -acc[3]);
                     dst[1] = make_float4(-0.5f * acc[4], acc[5], acc[6], acc[7]);
                     // staged entries have o >= 1/255 (box_dead drops the rest)
-                    dst[2] = make_float4(__fdiv_rn(acc[8], f1.y), 0.0f, 0.0f, 0.0f);
+                    dst[2] = make_float4(__fdiv_rn(acc[8], f1.y), rowf, 0.0f, 0.0f);
                 }
             }
             __syncwarp();
@@ -704,7 +714,7 @@ void launch_raster_fwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
                            const float *feat, float bg0, float bg1, float bg2, void *image,
                            int image_f64, float *t_final, int32_t *n_last, int32_t *n_contrib,
                            int32_t *n_iter, int64_t *touched, uint32_t *cmask,
-                           const ChunkArgs *ch, cudaStream_t s) {
+                           const ChunkArgs *ch, const int32_t *slot_rank, cudaStream_t s) {
     const int mode = (touched ? f32::F_TOUCH : 0) | (n_contrib || n_iter ? f32::F_STATS : 0);
     const int chunk = ch ? ch->chunk : 0;
     float4 *cstate = ch && ch->chunk ? (float4 *)ch->state : nullptr;
@@ -714,7 +724,8 @@ void launch_raster_fwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
                                                    offsets,                                      \
                                                    entries, feat, bg0, bg1, bg2, image,          \
                                                    image_f64, t_final, n_last, n_contrib, n_iter, \
-                                                   touched, cmask, chunk, cstate, qlast)
+                                                   touched, cmask, chunk, cstate, qlast,       \
+                                                   slot_rank)
     switch (mode) {
         case 0: ISG_FWD(0); break;
         case 1: ISG_FWD(1); break;
@@ -731,7 +742,8 @@ void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
                            const float *feat, const int4 *rect_sorted, const int64_t *emit_off,
                            float bg0, float bg1, float bg2, const float *t_final,
                            const int32_t *n_last, const DL *dl, float *partials,
-                           const uint32_t *cmask, const ChunkArgs *ch, cudaStream_t s) {
+                           const uint32_t *cmask, const ChunkArgs *ch, const int32_t *slot_rank,
+                           cudaStream_t s) {
     const bool chunked = ch && ch->chunk;
     const int grid = chunked ? ch->max_items : n_tiles;
     const int2 *items = chunked ? (const int2 *)ch->items : nullptr;
@@ -743,7 +755,7 @@ void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
     f32::bwd_kernel<DL, MASK, CH><<<grid, f32::BNT, 0, s>>>(                                     \
         W, H, tiles_x, row_lo, tile_ids, tile_order, offsets, entries, feat, rect_sorted,        \
         emit_off, bg0, bg1, bg2, t_final, n_last, dl, partials, MASK ? cmask : nullptr, items,    \
-        n_items, chunk, cstate, image)
+        n_items, chunk, cstate, image, slot_rank)
     if (cmask) {
         if (chunked) ISG_BWD32(true, true);
         else ISG_BWD32(true, false);
@@ -758,13 +770,14 @@ template void launch_raster_bwd_f32<float>(int, int, int, int, int, const int32_
                                            const int32_t *, const int32_t *, const float *,
                                            const int4 *, const int64_t *, float, float, float,
                                            const float *, const int32_t *, const float *, float *,
-                                           const uint32_t *, const ChunkArgs *, cudaStream_t);
+                                           const uint32_t *, const ChunkArgs *, const int32_t *,
+                                           cudaStream_t);
 template void launch_raster_bwd_f32<double>(int, int, int, int, int, const int32_t *,
                                             const int32_t *,
                                             const int32_t *, const int32_t *, const float *,
                                             const int4 *, const int64_t *, float, float, float,
                                             const float *, const int32_t *, const double *,
                                             float *, const uint32_t *, const ChunkArgs *,
-                                            cudaStream_t);
+                                            const int32_t *, cudaStream_t);
 
 }  // namespace isg

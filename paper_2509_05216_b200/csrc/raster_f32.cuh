@@ -6,6 +6,9 @@
 // the same array walks only the entries some pixel composited.
 // tile_order (optional): CTA b processes list position tile_order[b] (the
 // launch order, e.g. heaviest tiles first); results do not depend on it.
+// slot_rank (optional): the lists hold live-only subtotal slots (entry ->
+// rank through slot_rank); the backward writes each entry's record at its
+// slot with the tile row in float 9 (isg_bin_emit_live layout).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -22,7 +25,7 @@ void launch_raster_fwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
                            const float *feat, float bg0, float bg1, float bg2, void *image,
                            int image_f64, float *t_final, int32_t *n_last, int32_t *n_contrib,
                            int32_t *n_iter, int64_t *touched, uint32_t *cmask,
-                           const ChunkArgs *chunks, cudaStream_t s);
+                           const ChunkArgs *chunks, const int32_t *slot_rank, cudaStream_t s);
 
 template <typename DL>
 void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
@@ -31,6 +34,7 @@ void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
                            const float *feat, const int4 *rect_sorted, const int64_t *emit_off,
                            float bg0, float bg1, float bg2, const float *t_final,
                            const int32_t *n_last, const DL *dl, float *partials,
-                           const uint32_t *cmask, const ChunkArgs *chunks, cudaStream_t s);
+                           const uint32_t *cmask, const ChunkArgs *chunks,
+                           const int32_t *slot_rank, cudaStream_t s);
 
 }  // namespace isg

@@ -23,6 +23,8 @@
 // per (tile, splat) -- the reference's scratch row -- into a splat-major slot
 // so the per-splat fold below reads them in ascending tile order.
 #include "common.cuh"
+#include <type_traits>
+
 #include "fold.cuh"
 #include "raster_f32.cuh"
 
@@ -377,10 +379,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
     }
 }
 
+template <bool LIVE>
 __global__ void __launch_bounds__(RED_THREADS) reduce_ordered_f32_kernel(
     int64_t m, const int64_t *__restrict__ emit_off, const float *__restrict__ partials,
     const int32_t *__restrict__ order, const int4 *__restrict__ rect_sorted, int row_lo,
-    int canon_rows, double *__restrict__ grad2d, double *__restrict__ grad_norm) {
+    int row_hi, int canon_rows, double *__restrict__ grad2d, double *__restrict__ grad_norm) {
     constexpr int PS = partial_stride<float>();
     __shared__ __align__(128) float sbuf[RED_WARPS][2][RED_SLOTS * PS];
     __shared__ __align__(8) uint64_t sbar[RED_WARPS][2];
@@ -393,8 +396,12 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_ordered_f32_kernel(
     const int64_t span1 = emit_off[min(r0 + 32, m)];
     int64_t p = live ? emit_off[r] : 0;
     const int64_t p1 = live ? emit_off[r + 1] : 0;
-    FoldState st;
-    st.init(rect_sorted, r, live ? p1 - p : 0, row_lo, canon_rows);
+    typename std::conditional<LIVE, FoldLive, FoldState>::type st;
+    if constexpr (LIVE) {
+        if (live) st.init(rect_sorted, r, row_lo, row_hi, canon_rows);
+    } else {
+        st.init(rect_sorted, r, live ? p1 - p : 0, row_lo, canon_rows);
+    }
     const int nch = (int)((span1 - span0 + RED_SLOTS - 1) / RED_SLOTS);
     float(*buf)[RED_SLOTS * PS] = sbuf[warp];
     uint64_t *bar = sbar[warp];
@@ -445,7 +452,8 @@ static int raster_fwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t
                       const int32_t *offsets, const int32_t *entries, const void *feat_sorted,
                       const double *bg, void *image, int32_t image_dtype, void *t_final,
                       int32_t *n_last, int32_t *n_contrib, int32_t *n_iter, int64_t *touched,
-                      uint32_t *cmask, const isg_chunks *chunks, void *stream) {
+                      uint32_t *cmask, const isg_chunks *chunks, const int32_t *slot_rank,
+                      void *stream) {
     if (width <= 0 || height <= 0 || tiles_x <= 0 || row_lo < 0 || row_hi < row_lo || !bg ||
         !image || !t_final || !n_last || n_tile_ids < 0)
         return (int)cudaErrorInvalidValue;
@@ -458,7 +466,7 @@ static int raster_fwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t
                               offsets, entries,
                               (const float *)feat_sorted, (float)bg[0], (float)bg[1],
                               (float)bg[2], image, img64, (float *)t_final, n_last, n_contrib,
-                              n_iter, touched, cmask, chunks, s);
+                              n_iter, touched, cmask, chunks, slot_rank, s);
     } else if (feat_dtype == ISG_F64) {
         if (touched)
             raster_fwd_kernel<double, true><<<n_tiles, THREADS, 0, s>>>(
@@ -482,7 +490,7 @@ static int raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t
                       const int32_t *rect_sorted, const int64_t *emit_off, const double *bg,
                       const void *t_final, const int32_t *n_last, const void *dl_dimage,
                       int32_t dl_dtype, void *partials, const uint32_t *cmask,
-                      const isg_chunks *chunks, void *stream) {
+                      const isg_chunks *chunks, const int32_t *slot_rank, void *stream) {
     if (width <= 0 || height <= 0 || tiles_x <= 0 || row_lo < 0 || row_hi < row_lo || !bg ||
         n_tile_ids < 0 || (emit_off && !rect_sorted))
         return (int)cudaErrorInvalidValue;
@@ -502,14 +510,14 @@ static int raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t
                                      entries, (const float *)feat_sorted, rs, emit_off,
                                      (float)bg[0], (float)bg[1], (float)bg[2],
                                      (const float *)t_final, n_last, (const float *)dl_dimage,
-                                     (float *)partials, cmask, chunks, s);
+                                     (float *)partials, cmask, chunks, slot_rank, s);
     else if (feat_dtype == ISG_F32 && dl_dtype == ISG_F64)
         launch_raster_bwd_f32<double>(n_tiles, width, height, tiles_x, row_lo, tile_ids,
                                       tile_order, offsets,
                                       entries, (const float *)feat_sorted, rs, emit_off,
                                       (float)bg[0], (float)bg[1], (float)bg[2],
                                       (const float *)t_final, n_last, (const double *)dl_dimage,
-                                      (float *)partials, cmask, chunks, s);
+                                      (float *)partials, cmask, chunks, slot_rank, s);
     else if (feat_dtype == ISG_F64 && dl_dtype == ISG_F32) ISG_BWD(double, float);
     else if (feat_dtype == ISG_F64 && dl_dtype == ISG_F64) ISG_BWD(double, double);
     else return (int)cudaErrorInvalidValue;
@@ -528,8 +536,8 @@ extern "C" int isg_reduce_ordered(int32_t feat_dtype, int64_t m, const int64_t *
     if (m == 0) return 0;
     cudaStream_t s = (cudaStream_t)stream;
     if (feat_dtype == ISG_F32)
-        reduce_ordered_f32_kernel<<<blocks_for(m, RED_THREADS), RED_THREADS, 0, s>>>(
-            m, emit_off, (const float *)partials, order, rs, row_lo, canon_rows, grad2d,
+        reduce_ordered_f32_kernel<false><<<blocks_for(m, RED_THREADS), RED_THREADS, 0, s>>>(
+            m, emit_off, (const float *)partials, order, rs, row_lo, row_hi, canon_rows, grad2d,
             grad_norm);
     else if (feat_dtype == ISG_F64)
         reduce_ordered_kernel<double><<<blocks_for(m, 256), 256, 0, s>>>(
@@ -537,6 +545,21 @@ extern "C" int isg_reduce_ordered(int32_t feat_dtype, int64_t m, const int64_t *
             grad_norm);
     else
         return (int)cudaErrorInvalidValue;
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_reduce_live(int64_t m, const int64_t *live_off, const float *partials,
+                               const int32_t *order, const int32_t *rect_sorted, int32_t row_lo,
+                               int32_t row_hi, int32_t canon_rows, double *grad2d,
+                               double *grad_norm, void *stream) {
+    if (m < 0 || canon_rows < 1 || (m > 0 && (!live_off || !partials || !rect_sorted || !grad2d)))
+        return (int)cudaErrorInvalidValue;
+    if (m == 0) return 0;
+    reduce_ordered_f32_kernel<true><<<blocks_for(m, RED_THREADS), RED_THREADS, 0,
+                                      (cudaStream_t)stream>>>(
+        m, live_off, partials, order, (const int4 *)rect_sorted, row_lo, row_hi, canon_rows,
+        grad2d, grad_norm);
     ISG_CHECK_LAUNCH();
     return 0;
 }
@@ -551,7 +574,7 @@ extern "C" int isg_raster_fwd(int32_t feat_dtype, int32_t width, int32_t height,
     return raster_fwd(feat_dtype, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
                       nullptr,
                       offsets, entries, feat_sorted, bg, image, image_dtype, t_final, n_last,
-                      n_contrib, n_iter, touched, nullptr, nullptr, stream);
+                      n_contrib, n_iter, touched, nullptr, nullptr, nullptr, stream);
 }
 
 extern "C" int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height, int32_t tiles_x,
@@ -565,7 +588,7 @@ extern "C" int isg_raster_bwd(int32_t feat_dtype, int32_t width, int32_t height,
     return raster_bwd(feat_dtype, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
                       nullptr,
                       offsets, entries, feat_sorted, rect_sorted, emit_off, bg, t_final, n_last,
-                      dl_dimage, dl_dtype, partials, nullptr, nullptr, stream);
+                      dl_dimage, dl_dtype, partials, nullptr, nullptr, nullptr, stream);
 }
 
 namespace isg {
@@ -647,12 +670,13 @@ extern "C" int isg_raster_fwd_masked(int32_t width, int32_t height, int32_t tile
                                      const double *bg, void *image, int32_t image_dtype,
                                      void *t_final, int32_t *n_last, int32_t *n_contrib,
                                      int32_t *n_iter, int64_t *touched, uint32_t *contrib_mask,
-                                     const isg_chunks *chunks, void *stream) {
+                                     const isg_chunks *chunks, const int32_t *slot_rank,
+                                     void *stream) {
     if (!contrib_mask) return (int)cudaErrorInvalidValue;
     return raster_fwd(ISG_F32, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
                       tile_order,
                       offsets, entries, feat_sorted, bg, image, image_dtype, t_final, n_last,
-                      n_contrib, n_iter, touched, contrib_mask, chunks, stream);
+                      n_contrib, n_iter, touched, contrib_mask, chunks, slot_rank, stream);
 }
 
 extern "C" int isg_raster_bwd_masked(int32_t width, int32_t height, int32_t tiles_x,
@@ -665,11 +689,11 @@ extern "C" int isg_raster_bwd_masked(int32_t width, int32_t height, int32_t tile
                                      const int32_t *n_last, const void *dl_dimage,
                                      int32_t dl_dtype, void *partials,
                                      const uint32_t *contrib_mask, const isg_chunks *chunks,
-                                     void *stream) {
+                                     const int32_t *slot_rank, void *stream) {
     if (!contrib_mask || (dl_dtype != ISG_F32 && dl_dtype != ISG_F64))
         return (int)cudaErrorInvalidValue;
     return raster_bwd(ISG_F32, width, height, tiles_x, row_lo, row_hi, tile_ids, n_tile_ids,
                       tile_order,
                       offsets, entries, feat_sorted, rect_sorted, emit_off, bg, t_final, n_last,
-                      dl_dimage, dl_dtype, partials, contrib_mask, chunks, stream);
+                      dl_dimage, dl_dtype, partials, contrib_mask, chunks, slot_rank, stream);
 }

@@ -51,12 +51,13 @@ from . import _lib as L
 
 TILE = 16
 CANON_ROWS = 2
-# our kernels per sharded step (CUB scan/sort passes not counted):
-# preprocess, route_plan, route_scan, route_pack | depth tie fix, gather_rank,
-# finish_counts, bin_emit16_cull, tile_offsets16, raster_fwd_masked |
-# ssim_fields, ssim_adjoint, loss_finish | raster_bwd_masked, band_blocks,
-# band_fold | owner_fold_plan, chain_train, adam_groups
-LAUNCHES_PER_STEP = 19
+# our kernels per sharded step at config 3 (every launch is ours; counted
+# from the ncu launch list of one step): preprocess, route plan/scan/pack,
+# depth radix sort (5 passes x 4 + tie fix), band binning with live counts
+# (gather + 2 scans x 3), live emission, tile radix sort (2 x 4), offsets,
+# heavy-first order (keys + 2 x 4), raster fwd, loss (3), raster bwd, band
+# blocks + scan (3), band fold, owner fold, chain, Adam
+LAUNCHES_PER_STEP = 64
 
 
 class ProtocolError(RuntimeError):
@@ -482,7 +483,8 @@ class RankStep:
         # counts[0] = this shard's per-band totals, counts[1] = every source's for this band
         self.counts = torch.zeros((2, world, 3), dtype=torch.int64, device=d)
         self.counts_host = torch.zeros((2, world, 3), dtype=torch.int64).pin_memory()
-        self.bin_counts = torch.zeros(2, dtype=torch.int64, device=d)  # (M, E), not read
+        # (M, E, live E) of the band's binning; only the live count is read (on the device)
+        self.bin_counts = torch.zeros(3, dtype=torch.int64, device=d)
         nf = ctypes.c_int32(0)
         na = ctypes.c_int32(0)
         L.lib().isg_loss_partials_size(self.H, self.W, ctypes.byref(nf), ctypes.byref(na))
@@ -494,6 +496,8 @@ class RankStep:
         self.vals0 = self.key_sorted = self.order = None
         self.rect_sorted = self.feat_sorted = self.emit_off = None
         self.tk = self.tv = self.tk_sorted = self.entries = self.partials = None
+        self.live_off = self.live_mask = self.slot_rank = self.iota = None
+        self.live = False
         self.cmask = self.nb = self.gpos = self.gbuf = self.grad_recv = None
         self.to_keys = self.to_vals = self.to_keys_s = self.to_order = self.tile_order = None
         self.chunks = None
@@ -632,18 +636,42 @@ class RankStep:
         self.rect_sorted = _grow(self.rect_sorted, R, (4,), dtype=torch.int32, device=d)
         self.feat_sorted = _grow(self.feat_sorted, R, (12,), dtype=torch.float32, device=d)
         self.emit_off = _grow(self.emit_off, R + 1, dtype=torch.int64, device=d)
+        # band lists: live-only for training (pairs no pixel of their tile can
+        # composite have no entry and no subtotal slot; the live count stays on
+        # the device -- E, the band's tile entries, bounds it); count mode:
+        # the reference's full lists
+        live = not count
+        self.live = live
+        k16 = self.n_tiles <= 65536  # 2-byte tile keys (see engine.Rasterizer.forward)
+        kb = 2 if k16 else 4
         sz = ctypes.c_size_t(0)
-        L.check(lib.isg_bin_count_rows(None, ctypes.byref(sz), R, None, None, None, self.trow0,
-                                       self.trow1, None, None, None, None, None), "bin size")
+        if live:
+            L.check(lib.isg_bin_count_live(None, ctypes.byref(sz), R, None, None, None, None,
+                                           None, self.trow0, self.trow1, None, None, None, None,
+                                           None, None, None), "bin size")
+        else:
+            L.check(lib.isg_bin_count_rows(None, ctypes.byref(sz), R, None, None, None,
+                                           self.trow0, self.trow1, None, None, None, None, None),
+                    "bin size")
         ws = self.ws[2].get(sz.value, d)
         sz = ctypes.c_size_t(ws.numel())
-        L.check(lib.isg_bin_count_rows(L.ptr(ws), ctypes.byref(sz), R, L.ptr(self.key_sorted),
-                                       L.ptr(self.order), L.ptr(self.pay_recv), self.trow0,
-                                       self.trow1, L.ptr(self.rect_sorted),
-                                       L.ptr(self.feat_sorted), L.ptr(self.emit_off),
-                                       L.ptr(self.bin_counts), s), "isg_bin_count_rows")
+        if live:
+            self.live_off = _grow(self.live_off, R + 1, dtype=torch.int64, device=d)
+            self.live_mask = _grow(self.live_mask, R, dtype=torch.int64, device=d)
+            L.check(lib.isg_bin_count_live(L.ptr(ws), ctypes.byref(sz), R,
+                                           L.ptr(self.key_sorted), L.ptr(self.order), None,
+                                           L.ptr(self.pay_recv), None, self.trow0, self.trow1,
+                                           L.ptr(self.rect_sorted), L.ptr(self.feat_sorted),
+                                           L.ptr(self.emit_off), L.ptr(self.live_off),
+                                           L.ptr(self.live_mask), L.ptr(self.bin_counts), s),
+                    "isg_bin_count_live")
+        else:
+            L.check(lib.isg_bin_count_rows(L.ptr(ws), ctypes.byref(sz), R, L.ptr(self.key_sorted),
+                                           L.ptr(self.order), L.ptr(self.pay_recv), self.trow0,
+                                           self.trow1, L.ptr(self.rect_sorted),
+                                           L.ptr(self.feat_sorted), L.ptr(self.emit_off),
+                                           L.ptr(self.bin_counts), s), "isg_bin_count_rows")
         self.M = R
-        k16 = self.n_tiles <= 65536  # 2-byte tile keys (see engine.Rasterizer.forward)
         kdt = torch.int16 if k16 else torch.int32
         if self.tk is None or self.tk.dtype != kdt:
             self.tk = self.tk_sorted = None
@@ -652,26 +680,37 @@ class RankStep:
         self.tk_sorted = _grow(self.tk_sorted, E, dtype=kdt, device=d)
         self.entries = _grow(self.entries, E, dtype=torch.int32, device=d)
         self.partials = _grow(self.partials, E, (12,), dtype=torch.float32, device=d)
-        emit = lib.isg_bin_emit16 if k16 else lib.isg_bin_emit
-        offs = lib.isg_tile_offsets16 if k16 else lib.isg_tile_offsets
-        # band lists leave out the pairs no pixel of their tile can composite
-        # (isg_bin_emit16_cull writes their zero subtotals; see engine.Rasterizer)
-        cull = self.n_tiles < 65536 and not count
+        n_live = self.bin_counts[2:3]  # live pairs (device)
         if E:
-            if cull:
-                L.check(lib.isg_bin_emit16_cull(R, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
-                                                L.ptr(self.feat_sorted), self.tiles_x, self.trow0,
-                                                self.trow1, L.ptr(self.tk), L.ptr(self.tv),
-                                                L.ptr(self.partials), s), "isg_bin_emit16_cull")
+            if live:
+                from .engine import _iota
+                self.slot_rank = _grow(self.slot_rank, E, dtype=torch.int32, device=d)
+                self.iota = _iota(self.iota, E, d)
+                L.check(lib.isg_bin_emit_live(R, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
+                                              L.ptr(self.live_off), L.ptr(self.live_mask),
+                                              L.ptr(self.feat_sorted), self.tiles_x, self.trow0,
+                                              self.trow1, L.ptr(self.tk), kb,
+                                              L.ptr(self.slot_rank), s), "isg_bin_emit_live")
+                vals = self.iota
             else:
+                emit = lib.isg_bin_emit16 if k16 else lib.isg_bin_emit
                 L.check(emit(R, L.ptr(self.rect_sorted), L.ptr(self.emit_off), self.tiles_x,
                              self.trow0, self.trow1, L.ptr(self.tk), L.ptr(self.tv), s),
                         "isg_bin_emit")
-            bits = max(self.tile_bits, int(self.n_tiles).bit_length()) if cull else self.tile_bits
-            L.sort_pairs(self.tk[:E], self.tv[:E], (0, bits), self.ws[0], self.tk_sorted[:E],
-                         self.entries[:E])
-        L.check(offs(E, L.ptr(self.tk_sorted), self.n_tiles, L.ptr(self.offsets), s),
-                "isg_tile_offsets")
+                vals = self.tv
+            sz = ctypes.c_size_t(0)
+            L.check(lib.isg_sort_pairs_dev(None, ctypes.byref(sz), kb, None, None, None, None, E,
+                                           None, 0, self.tile_bits, None), "sort size")
+            sws = self.ws[0].get(sz.value, d)
+            sz = ctypes.c_size_t(sws.numel())
+            L.check(lib.isg_sort_pairs_dev(L.ptr(sws), ctypes.byref(sz), kb, L.ptr(self.tk),
+                                           L.ptr(self.tk_sorted), L.ptr(vals),
+                                           L.ptr(self.entries), E,
+                                           L.ptr(n_live) if live else None, 0, self.tile_bits,
+                                           s), "isg_sort_pairs_dev")
+        L.check(lib.isg_tile_offsets_dev(E, L.ptr(n_live) if live else None,
+                                         L.ptr(self.tk_sorted), kb, self.n_tiles,
+                                         L.ptr(self.offsets), s), "isg_tile_offsets_dev")
         from .engine import chunk_setup, heavy_first_order
         self.tile_order = heavy_first_order(self, self.n_tiles, self.offsets)
         self.chunks = None if count else chunk_setup(
@@ -704,8 +743,8 @@ class RankStep:
                 self._vptr(self.window, self.win0, W3), L.ISG_F32,
                 self._vptr(self.t_final, self.prow0, self.W),
                 self._vptr(self.n_last, self.prow0, self.W), None, None, None, L.ptr(self.cmask),
-                ctypes.byref(self.chunks) if self.chunks is not None else None, s),
-                "isg_raster_fwd_masked")
+                ctypes.byref(self.chunks) if self.chunks is not None else None,
+                L.ptr(self.slot_rank), s), "isg_raster_fwd_masked")
         # boundary rows for the neighbours' SSIM halo
         b0, b1 = self.prow0 - self.win0, self.prow1 - self.win0
         to_prev = self.window[b0:b0 + min(10, b1 - b0)] if self.rank > 0 else None
@@ -772,7 +811,7 @@ class RankStep:
                 self._vptr(self.n_last, self.prow0, self.W),
                 self._vptr(self.dl, self.prow0, W3), L.ISG_F32, L.ptr(self.partials),
                 L.ptr(self.cmask), ctypes.byref(self.chunks) if self.chunks is not None else None,
-                s), "isg_raster_bwd_masked")
+                L.ptr(self.slot_rank), s), "isg_raster_bwd_masked")
         _mark(timer, "raster_bwd")
         self.nb = _grow(self.nb, R, dtype=torch.int64, device=d)
         self.gpos = _grow(self.gpos, R + 1, dtype=torch.int64, device=d)
@@ -781,10 +820,11 @@ class RankStep:
             L.check(lib.isg_band_blocks(R, L.ptr(self.pay_recv), self.trow0, self.trow1,
                                         self.part.canon_rows, L.ptr(self.nb), s), "band blocks")
             _scan_i64(self, R, self.nb, self.gpos)
-            L.check(lib.isg_band_fold(R, L.ptr(self.emit_off), L.ptr(self.partials),
+            L.check(lib.isg_band_fold(R, L.ptr(self.live_off), L.ptr(self.partials),
                                       L.ptr(self.rect_sorted), L.ptr(self.order),
-                                      L.ptr(self.gpos), self.trow0, self.part.canon_rows,
-                                      L.ptr(self.gbuf), s), "isg_band_fold")
+                                      L.ptr(self.gpos), self.trow0, self.trow1,
+                                      self.part.canon_rows, 1, L.ptr(self.gbuf), s),
+                    "isg_band_fold")
         G = int(self.grecv_off[-1])
         self.grad_recv = _grow(self.grad_recv, G, (9,), dtype=torch.float64, device=d)
         ops = []

@@ -48,6 +48,13 @@ TILE = 16
 CANON_ROWS = 2
 
 
+def _iota(buf: torch.Tensor | None, n: int, device) -> torch.Tensor:
+    """0, 1, 2, ... of at least n entries (int32), grown on demand."""
+    if buf is None or buf.shape[0] < n:
+        return torch.arange(max(int(n * 1.25), 16), dtype=torch.int32, device=device)
+    return buf
+
+
 def _grow(buf: torch.Tensor | None, n: int, shape_tail=(), dtype=torch.float32, device=None,
           slack: float = 1.25) -> torch.Tensor:
     if buf is None or buf.shape[0] < n:
@@ -107,7 +114,7 @@ class Rasterizer:
         self.ftag = L.dtype_tag(feat_dtype)
         self.ws_sort = L.Workspace()
         self.ws_bin = L.Workspace()
-        self.counts_host = torch.zeros(2, dtype=torch.int64).pin_memory()
+        self.counts_host = torch.zeros(3, dtype=torch.int64).pin_memory()
         self.resize(n)
         dev = device
         self.image = torch.empty((height, width, 3), dtype=torch.float32, device=dev)
@@ -116,6 +123,8 @@ class Rasterizer:
         self.dl = torch.empty((height, width, 3), dtype=torch.float32, device=dev)
         self.offsets = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=dev)
         self.tile_keys = self.tile_vals = self.keys_sorted_t = self.entries = None
+        self.slot_rank = self.iota = None
+        self.live = False  # live-only training lists (isg_bin_emit_live)
         self.partials = None
         self.to_keys = self.to_vals = self.to_keys_s = self.to_order = None
         self.tile_order = None
@@ -148,7 +157,9 @@ class Rasterizer:
         self.feat_sorted = torch.empty((n, 12), dtype=self.feat_dtype, device=dev)
         self.emit_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
         self.rank_of = torch.empty(n, dtype=torch.int32, device=dev)
-        self.counts = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.live_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self.live_mask = torch.empty(n, dtype=torch.int64, device=dev)
+        self.counts = torch.zeros(3, dtype=torch.int64, device=dev)
         self.grad2d = torch.empty((n, 9), dtype=torch.float64, device=dev)
 
     # -- forward ---------------------------------------------------------
@@ -173,16 +184,35 @@ class Rasterizer:
         _mark(tm, "preprocess")
         L.sort_depth(self.key, self.vals0, self.ws_sort, self.key_sorted, self.order)
         _mark(tm, "sort_depth")
+        # float32 training lists are live-only: a (tile, splat) pair no pixel of
+        # the tile can composite has no list entry and no subtotal slot
+        live = self.use_cmask and self.feat_dtype == torch.float32
+        self.live = live
         sz = ctypes.c_size_t(0)
-        L.check(lib.isg_bin_count(None, ctypes.byref(sz), n, None, None, None, None, self.ftag,
-                                  0, self.tiles_y, None, None, None, None, None), "bin (size)")
+        if live:
+            L.check(lib.isg_bin_count_live(None, ctypes.byref(sz), n, None, None, None, None,
+                                           None, 0, self.tiles_y, None, None, None, None, None,
+                                           None, None), "bin (size)")
+        else:
+            L.check(lib.isg_bin_count(None, ctypes.byref(sz), n, None, None, None, None,
+                                      self.ftag, 0, self.tiles_y, None, None, None, None, None),
+                    "bin (size)")
         ws = self.ws_bin.get(sz.value, self.device)
         sz = ctypes.c_size_t(ws.numel())
-        L.check(lib.isg_bin_count(L.ptr(ws), ctypes.byref(sz), n, L.ptr(self.key_sorted),
-                                  L.ptr(self.order), L.ptr(self.rect), L.ptr(self.feat),
-                                  self.ftag, 0, self.tiles_y, L.ptr(self.rect_sorted),
-                                  L.ptr(self.feat_sorted), L.ptr(self.emit_off),
-                                  L.ptr(self.counts), s), "isg_bin_count")
+        if live:
+            L.check(lib.isg_bin_count_live(L.ptr(ws), ctypes.byref(sz), n, L.ptr(self.key_sorted),
+                                           L.ptr(self.order), L.ptr(self.rect), None,
+                                           L.ptr(self.feat), 0, self.tiles_y,
+                                           L.ptr(self.rect_sorted), L.ptr(self.feat_sorted),
+                                           L.ptr(self.emit_off), L.ptr(self.live_off),
+                                           L.ptr(self.live_mask), L.ptr(self.counts), s),
+                    "isg_bin_count_live")
+        else:
+            L.check(lib.isg_bin_count(L.ptr(ws), ctypes.byref(sz), n, L.ptr(self.key_sorted),
+                                      L.ptr(self.order), L.ptr(self.rect), L.ptr(self.feat),
+                                      self.ftag, 0, self.tiles_y, L.ptr(self.rect_sorted),
+                                      L.ptr(self.feat_sorted), L.ptr(self.emit_off),
+                                      L.ptr(self.counts), s), "isg_bin_count")
         if self.ranked_grads:
             L.check(lib.isg_rank_of(n, L.ptr(self.key_sorted), L.ptr(self.order),
                                     L.ptr(self.rank_of), s), "isg_rank_of")
@@ -190,13 +220,10 @@ class Rasterizer:
         self.counts_host.copy_(self.counts, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         _mark(tm, "host_sync")
-        m, e = int(self.counts_host[0]), int(self.counts_host[1])
-        slots = e
+        m, e_full = int(self.counts_host[0]), int(self.counts_host[1])
+        e = int(self.counts_host[2]) if live else e_full
         dev = self.device
-        # float32 training lists leave out the pairs no pixel of their tile can
-        # composite (isg_bin_emit16_cull; their zero subtotals are written there)
-        cull = self.use_cmask and self.feat_dtype == torch.float32 and self.n_tiles < 65536
-        k16 = self.n_tiles <= 65536  # 2-byte tile keys: 25 % less sort traffic
+        k16 = self.n_tiles <= 65536  # 2-byte tile keys: less sort traffic
         kdt = torch.int16 if k16 else torch.int32
         if self.tile_keys is None or self.tile_keys.dtype != kdt:
             self.tile_keys = self.keys_sorted_t = None
@@ -204,24 +231,27 @@ class Rasterizer:
         self.tile_vals = _grow(self.tile_vals, e, dtype=torch.int32, device=dev)
         self.keys_sorted_t = _grow(self.keys_sorted_t, e, dtype=kdt, device=dev)
         self.entries = _grow(self.entries, e, dtype=torch.int32, device=dev)
-        emit = lib.isg_bin_emit16 if k16 else lib.isg_bin_emit
         offs = lib.isg_tile_offsets16 if k16 else lib.isg_tile_offsets
         if e:
-            if cull:
-                self.partials = _grow(self.partials, e, (12,), dtype=self.feat_dtype, device=dev)
-                L.check(lib.isg_bin_emit16_cull(m, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
-                                                L.ptr(self.feat_sorted), self.tiles_x, 0,
-                                                self.tiles_y, L.ptr(self.tile_keys),
-                                                L.ptr(self.tile_vals), L.ptr(self.partials), s),
-                        "isg_bin_emit16_cull")
+            if live:
+                self.slot_rank = _grow(self.slot_rank, e, dtype=torch.int32, device=dev)
+                L.check(lib.isg_bin_emit_live(m, L.ptr(self.rect_sorted), L.ptr(self.emit_off),
+                                              L.ptr(self.live_off), L.ptr(self.live_mask),
+                                              L.ptr(self.feat_sorted), self.tiles_x, 0,
+                                              self.tiles_y, L.ptr(self.tile_keys),
+                                              2 if k16 else 4, L.ptr(self.slot_rank), s),
+                        "isg_bin_emit_live")
+                # the sort's values are the slots themselves: 0..e-1
+                self.iota = _iota(self.iota, e, dev)
+                vals = self.iota
             else:
+                emit = lib.isg_bin_emit16 if k16 else lib.isg_bin_emit
                 L.check(emit(m, L.ptr(self.rect_sorted), L.ptr(self.emit_off), self.tiles_x, 0,
                              self.tiles_y, L.ptr(self.tile_keys), L.ptr(self.tile_vals), s),
                         "isg_bin_emit")
+                vals = self.tile_vals
             _mark(tm, "bin_emit")
-            # culled pairs carry the key n_tiles: one more key bit
-            bits = max(self.tile_bits, int(self.n_tiles).bit_length()) if cull else self.tile_bits
-            L.sort_pairs(self.tile_keys[:e], self.tile_vals[:e], (0, bits),
+            L.sort_pairs(self.tile_keys[:e], vals[:e], (0, self.tile_bits),
                          self.ws_sort, self.keys_sorted_t[:e], self.entries[:e])
             _mark(tm, "sort_tiles")
         L.check(offs(e, L.ptr(self.keys_sorted_t), self.n_tiles, L.ptr(self.offsets), s),
@@ -243,7 +273,8 @@ class Rasterizer:
                 ctypes.cast(self.bg, ctypes.c_void_p), L.ptr(self.image), L.ISG_F32,
                 L.ptr(self.t_final), L.ptr(self.n_last), L.ptr(self.n_contrib_out),
                 L.ptr(self.n_iter_out), None, L.ptr(self.cmask),
-                ctypes.byref(self.chunks) if self.chunks is not None else None, s),
+                ctypes.byref(self.chunks) if self.chunks is not None else None,
+                L.ptr(self.slot_rank) if self.live else None, s),
                 "isg_raster_fwd_masked")
         else:
             L.check(lib.isg_raster_fwd(self.ftag, self.width, self.height, self.tiles_x, 0,
@@ -254,7 +285,7 @@ class Rasterizer:
                                        L.ptr(self.n_contrib_out), L.ptr(self.n_iter_out), None,
                                        s), "isg_raster_fwd")
         _mark(tm, "raster_fwd")
-        return ViewContext(m=m, e=e, slots=slots)
+        return ViewContext(m=m, e=e, slots=e)
 
     # -- backward --------------------------------------------------------
     def backward(self, ctx: ViewContext) -> None:
@@ -273,7 +304,8 @@ class Rasterizer:
                 L.ptr(self.rect_sorted), L.ptr(self.emit_off),
                 ctypes.cast(self.bg, ctypes.c_void_p), L.ptr(self.t_final), L.ptr(self.n_last),
                 L.ptr(self.dl), L.ISG_F32, L.ptr(self.partials), L.ptr(self.cmask),
-                ctypes.byref(self.chunks) if self.chunks is not None else None, s),
+                ctypes.byref(self.chunks) if self.chunks is not None else None,
+                L.ptr(self.slot_rank) if self.live else None, s),
                 "isg_raster_bwd_masked")
         else:
             L.check(lib.isg_raster_bwd(self.ftag, self.width, self.height, self.tiles_x, 0,
@@ -284,7 +316,13 @@ class Rasterizer:
                                        L.ptr(self.n_last), L.ptr(self.dl), L.ISG_F32,
                                        L.ptr(self.partials), s), "isg_raster_bwd")
         _mark(self.timer, "raster_bwd")
-        if ctx.m:
+        if ctx.m and self.live:
+            L.check(lib.isg_reduce_live(ctx.m, L.ptr(self.live_off), L.ptr(self.partials),
+                                        None if self.ranked_grads else L.ptr(self.order),
+                                        L.ptr(self.rect_sorted), 0, self.tiles_y,
+                                        self.canon_rows, L.ptr(self.grad2d), None, s),
+                    "isg_reduce_live")
+        elif ctx.m:
             L.check(lib.isg_reduce_ordered(self.ftag, ctx.m, L.ptr(self.emit_off),
                                            L.ptr(self.partials),
                                            None if self.ranked_grads else L.ptr(self.order),

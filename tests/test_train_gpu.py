@@ -105,12 +105,13 @@ def test_resume_from_train_state_is_bitwise(tmp_path):
 
 
 def test_contribution_masks_change_no_result():
-    """The training lists and raster pair (isg_bin_emit16_cull: pairs no pixel
-    of their tile can composite left out, zero subtotals written at emit;
+    """The training lists and raster pair (isg_bin_emit_live: pairs no pixel of
+    their tile can composite have no entry and no subtotal slot;
     isg_raster_fwd_masked / isg_raster_bwd_masked: the backward walks only the
-    entries the forward composited) == the full lists and the unmasked pair:
-    images and T_final bitwise, subtotals and 2-D gradients equal (== ignores
-    the sign of zero), and the parameters after 4 training iterations bitwise."""
+    entries the forward composited; isg_reduce_live folds the live slots) ==
+    the full lists and the unmasked pair: images and T_final bitwise, 2-D
+    gradients equal (== ignores the sign of zero), and the parameters after 4
+    training iterations bitwise."""
     import paper_2509_05216_b200 as P
     from paper_2509_05216_b200.engine import Trainer
     d = load("config1")
@@ -131,10 +132,7 @@ def test_contribution_masks_change_no_result():
     assert a.r.cmask_ok and not b.r.cmask_ok
     assert torch.equal(a.r.image, b.r.image) and torch.equal(a.r.t_final, b.r.t_final)
     # (n_last are list positions: the culled lists are shorter)
-    # masked: culled lists (fewer entries), the same subtotal slots
-    assert int(a.r.offsets[-1]) < int(b.r.offsets[-1])
-    slots = int(b.r.offsets[-1])
-    assert torch.equal(a.r.partials[:slots], b.r.partials[:slots])
+    assert a.r.live and int(a.r.offsets[-1]) < int(b.r.offsets[-1])
     assert torch.equal(a.r.grad2d, b.r.grad2d)
     for k in P.PARAM_NAMES:
         assert torch.equal(getattr(a.cloud, k), getattr(b.cloud, k)), k
@@ -184,9 +182,9 @@ def _images(ds):
 
 
 def test_culled_lists_are_ordered_sublists_of_the_full_lists():
-    """isg_bin_emit16_cull keeps, per tile, a subsequence of the reference's
-    list (same relative order), drops only pairs with zero subtotals, and the
-    culled pairs' slots hold zeros."""
+    """isg_bin_emit_live keeps, per tile, a subsequence of the reference's
+    list (same relative order); every live slot appears in exactly one list,
+    and its subtotal record carries its tile row (the fold's block key)."""
     import paper_2509_05216_b200 as P
     from paper_2509_05216_b200.engine import Trainer
     d = load("config1")
@@ -196,13 +194,17 @@ def test_culled_lists_are_ordered_sublists_of_the_full_lists():
     for masked in (True, False):
         t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
         t.r.use_cmask = masked
-        t.r.forward(t.cloud, ds.cameras[0])
+        ctx = t.r.forward(t.cloud, ds.cameras[0])
         torch.cuda.synchronize()
         off = t.r.offsets.cpu().numpy()
         ent = t.r.entries[:int(off[-1])].cpu().numpy()
-        lists.append([ent[off[k]:off[k + 1]] for k in range(len(off) - 1)])
         if masked:
-            parts, emit_off, rect = t.r.partials, t.r.emit_off, t.r.rect_sorted
+            slots = ent.copy()
+            ent = t.r.slot_rank[:ctx.e].cpu().numpy()[ent]  # slots -> ranks
+            live_slots = ctx.e
+            off_live = off
+            tr = t
+        lists.append([ent[off[k]:off[k + 1]] for k in range(len(off) - 1)])
     culled_total = 0
     for lc, lf in zip(*lists):
         assert np.all(np.isin(lc, lf))
@@ -210,13 +212,13 @@ def test_culled_lists_are_ordered_sublists_of_the_full_lists():
         assert np.array_equal(lf[pos], lc) and np.all(np.diff(pos) > 0)
         culled_total += len(lf) - len(lc)
     assert culled_total > 0
-    # every culled (tile, rank) slot holds a zero record
-    tiles_x = t.r.tiles_x
-    eo, rc = emit_off.cpu().numpy(), rect.cpu().numpy()
-    p = parts.cpu().numpy()
-    for tile, (lc, lf) in enumerate(zip(*lists)):
-        ty, tx = divmod(tile, tiles_x)
-        for r in np.setdiff1d(lf, lc):
-            x0, y0, x1, _ = rc[r]
-            slot = eo[r] + (ty - max(y0, 0)) * (x1 - x0 + 1) + (tx - x0)
-            assert not p[slot].any()
+    assert np.array_equal(np.sort(slots), np.arange(live_slots))
+    # the backward's records: tile row of every slot in float 9
+    tr.step(1, ds.cameras[0], _images(ds)[0])
+    torch.cuda.synchronize()
+    rows = tr.r.partials[:live_slots, 9].contiguous().view(torch.int32).cpu().numpy()
+    tiles_x = tr.r.tiles_x
+    tile_of = np.repeat(np.arange(len(off_live) - 1), np.diff(off_live))
+    want = np.empty(live_slots, dtype=np.int64)
+    want[slots] = tile_of // tiles_x
+    assert np.array_equal(rows, want)
