@@ -362,11 +362,13 @@ def run_ours(args, world, rank, local):
     cpu, parity = ((None, None) if args.no_cpu_baseline
                    else cpu_baseline(wl, args, schedule, cfg, scene_extent))
 
-    # our kernels per step (CUB sort/scan passes not counted): preprocess,
-    # depth_tie_fix, gather_rank, finish_counts, rank_of, emit_span,
-    # tile_offsets, raster fwd, ssim_fields, ssim_adjoint, loss_finish,
-    # raster bwd, ordered fold, chain (f32), Adam groups
-    launches_per_step = 15
+    # kernels per step, all ours (no library kernels on the path): the ncu
+    # launch list of one config-3 step (profiles/r02_v1/ncu_summary.md) --
+    # preprocess, depth radix sort (5 x 4) + tie fix, gather with live counts
+    # + 2 scans (3 each), rank_of, live emission, tile radix sort (2 x 4),
+    # offsets, heavy-first order (keys + 2 x 4), raster fwd, loss (3), raster
+    # bwd, live fold, chain, Adam
+    launches_per_step = 57
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
