@@ -366,6 +366,13 @@ int isg_route_pack(int64_t n, const uint8_t *flag, const int32_t *rect, const ui
                    uint64_t *keys_send, int32_t *pay_send, uint64_t *keys_self,
                    int32_t *pay_self, void *stream);
 
+/* The reference's round-robin routing mask (route_rows, distributed.py:127-136
+ * over _route_mask, _kernels.py:378-394): rects (n, 4) int32 (tile_min,
+ * tile_max); mask (n, workers) u8, 1 iff the rect touches a tile whose linear
+ * id is congruent to w.  workers <= 64. */
+int isg_route_mask(int64_t n, const int32_t *rects, int32_t tiles_x, int32_t workers,
+                   uint8_t *mask, void *stream);
+
 /* Canonical blocks (canon_rows tile rows) of each received splat's rect
  * inside the band [row_lo, row_hi) (payload rows as isg_route_pack). */
 int isg_band_blocks(int64_t r, const int32_t *payload, int32_t row_lo, int32_t row_hi,

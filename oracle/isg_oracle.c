@@ -13,8 +13,8 @@
  * linked against glibc libm so that exp/sqrt match what numba emits (numba
  * never contracts to FMA and lowers np.exp to libm exp).  Parity of this
  * restatement against the reference is pinned by tests/golden/ (fixtures
- * produced by importing the reference itself; tests/golden/make_golden.py)
- * and, when /root/reference is present, by tests/test_oracle_vs_reference.py.
+ * produced by importing the reference itself; tests/golden/make_golden.py and
+ * make_golden_dist.py), checked by tests/test_oracle_golden.py.
  *
  * Threading: OpenMP over independent units (Gaussians, tiles, image rows),
  * mirroring the reference's worker-thread parallelism.  Results do not

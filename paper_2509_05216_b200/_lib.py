@@ -114,6 +114,7 @@ SIGNATURES = {
     "isg_route_plan_size": [_I64, _I32, _P],
     "isg_route_plan": [_I64, _P, _P, _P, _I32, _I32, _P, _P, _P],
     "isg_route_pack": [_I64, _P, _P, _P, _P, _P, _I32, _P, _P, _I32, _P, _P, _P, _P, _P],
+    "isg_route_mask": [_I64, _P, _I32, _I32, _P, _P],
     "isg_band_blocks": [_I64, _P, _I32, _I32, _I32, _P, _P],
     "isg_band_fold": [_I64, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P, _P],
     "isg_reduce_live": [_I64, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P],

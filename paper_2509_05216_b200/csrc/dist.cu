@@ -282,6 +282,22 @@ __global__ void __launch_bounds__(PLAN_T) route_pack_kernel(
     }
 }
 
+// The reference's round-robin routing (_route_mask, _kernels.py:378-394):
+// row i reaches worker w iff its tile rect touches a tile whose linear id is
+// congruent to w modulo the worker count.
+__global__ void route_mask_kernel(int64_t n, const int4 *__restrict__ rects, int tiles_x,
+                                  int workers, uint8_t *__restrict__ mask) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 rc = rects[i];
+    const uint64_t full = workers == 64 ? ~0ull : (1ull << workers) - 1ull;
+    uint64_t seen = 0;
+    for (int ty = rc.y; ty <= rc.w && seen != full; ty++)
+        for (int tx = rc.x; tx <= rc.z && seen != full; tx++)
+            seen |= 1ull << (((int64_t)ty * tiles_x + tx) % workers);
+    for (int w = 0; w < workers; w++) mask[i * workers + w] = (uint8_t)((seen >> w) & 1ull);
+}
+
 // Canonical blocks of each received splat inside the band.
 __global__ void band_blocks_kernel(int64_t r, const int4 *__restrict__ pay, int row_lo,
                                    int row_hi, int canon, int64_t *__restrict__ nb) {
@@ -645,6 +661,17 @@ extern "C" int isg_route_pack(int64_t n, const uint8_t *flag, const int32_t *rec
     route_pack_kernel<<<(unsigned)nblk, PLAN_T, 0, (cudaStream_t)stream>>>(
         n, flag, (const int4 *)rect, key, (const int4 *)feat, b, plan, dst, keys_send,
         (int4 *)pay_send, keys_self, (int4 *)pay_self);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_route_mask(int64_t n, const int32_t *rects, int32_t tiles_x, int32_t workers,
+                              uint8_t *mask, void *stream) {
+    if (n < 0 || tiles_x <= 0 || workers < 1 || workers > 64 || (n > 0 && (!rects || !mask)))
+        return (int)cudaErrorInvalidValue;
+    if (n == 0) return 0;
+    route_mask_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+        n, (const int4 *)rects, tiles_x, workers, mask);
     ISG_CHECK_LAUNCH();
     return 0;
 }

@@ -231,17 +231,87 @@ def band_cost_ratio(weights: np.ndarray, band_rows: list, canon_rows: int) -> fl
     return float(sums.max() / max(sums.mean(), 1e-300))
 
 
-def route_rows(tile_min, tile_max, part: PixelPartition) -> np.ndarray:
-    """(n, W) membership mask: row i reaches worker w iff its tile rect
-    overlaps w's band (distributed.py:127-136 for row bands)."""
-    tmin = np.asarray(tile_min)
-    tmax = np.asarray(tile_max)
-    n = tmin.shape[0]
-    mask = np.zeros((n, part.workers), dtype=np.uint8)
-    for w in range(part.workers):
-        lo, hi = part.band_rows[w], part.band_rows[w + 1]
-        mask[:, w] = ((tmin[:, 1] < hi) & (tmax[:, 1] >= lo)).astype(np.uint8)
+def route_rows(tile_min, tile_max, part_or_workers, tiles_x: int | None = None):
+    """(n, W) u8 membership mask of rows over workers.
+
+    route_rows(tile_min, tile_max, workers, tiles_x): the reference's
+    round-robin routing (distributed.py:127-136): row i reaches worker w iff
+    its tile rect touches a tile whose linear id is congruent to w, on the
+    device (isg_route_mask); returns a device tensor.
+    route_rows(tile_min, tile_max, part): a PixelPartition of row bands: row i
+    reaches worker w iff its rect's tile rows overlap w's band (numpy)."""
+    if isinstance(part_or_workers, PixelPartition):
+        part = part_or_workers
+        tmin = np.asarray(tile_min.cpu() if isinstance(tile_min, torch.Tensor) else tile_min)
+        tmax = np.asarray(tile_max.cpu() if isinstance(tile_max, torch.Tensor) else tile_max)
+        n = tmin.shape[0]
+        mask = np.zeros((n, part.workers), dtype=np.uint8)
+        for w in range(part.workers):
+            lo, hi = part.band_rows[w], part.band_rows[w + 1]
+            mask[:, w] = ((tmin[:, 1] < hi) & (tmax[:, 1] >= lo)).astype(np.uint8)
+        return mask
+    workers = int(part_or_workers)
+    if tiles_x is None:
+        raise ValueError("route_rows(tile_min, tile_max, workers, tiles_x) needs tiles_x")
+    if workers < 1 or workers > 64:
+        raise ValueError("workers must be in 1..64")
+    dev = L.require_cuda()
+
+    def dev_i32(a):
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        return t.to(device=dev, dtype=torch.int32).reshape(-1, 2)
+
+    rects = torch.cat([dev_i32(tile_min), dev_i32(tile_max)], 1).contiguous()
+    n = rects.shape[0]
+    mask = torch.zeros((n, workers), dtype=torch.uint8, device=dev)
+    L.check(L.lib().isg_route_mask(n, L.ptr(rects), int(tiles_x), workers, L.ptr(mask),
+                                   L.stream_ptr()), "isg_route_mask")
     return mask
+
+
+def route_splats(splats, part) -> list:
+    """Per-destination splat lists, each in (depth, index) order
+    (distributed.py:139-154): a splat goes to every worker owning a tile of
+    its tile span (part.assignment: round-robin tiles or row bands)."""
+    assign = np.asarray(part.assignment)
+    out = [[] for _ in range(part.workers)]
+    for s in sorted(splats, key=lambda s: (s.depth, s.gaussian_index)):
+        (x0, y0), (x1, y1) = s.tile_span
+        owners = np.unique(assign[(np.arange(y0, y1 + 1)[:, None] * part.tiles_x
+                                   + np.arange(x0, x1 + 1)[None, :]).ravel()])
+        for d in owners.tolist():
+            out[d].append(s)
+    return out
+
+
+def rebalance(shard_map: ShardMap, counts: list) -> tuple:
+    """Migration plan that evens the shard sizes to within one row
+    (distributed.py:229-268): every over-full shard gives up its lowest-id
+    excess rows; the pooled rows, taken in ascending id, fill the under-full
+    shards in worker order.  Returns ((gaussian, from, to) moves in ascending
+    id within each destination, the resulting ShardMap)."""
+    if list(counts) != shard_map.sizes:
+        raise ValueError("counts disagree with the shard map")
+    w, n = shard_map.workers, shard_map.total
+    q, r = divmod(n, w)
+    target = [q + int(k < r) for k in range(w)]
+    sizes = shard_map.sizes
+    donated = sorted((int(g), src) for src in range(w)
+                     for g in shard_map.lists[src][:max(sizes[src] - target[src], 0)])
+    plan, it = [], iter(donated)
+    for dst in range(w):
+        for _ in range(max(target[dst] - sizes[dst], 0)):
+            g, src = next(it)
+            plan.append((g, src, dst))
+    leaving = {g for g, _, _ in plan}
+    arriving = [[] for _ in range(w)]
+    for g, _, dst in plan:
+        arriving[dst].append(g)
+    lists = [np.sort(np.concatenate([shard_map.lists[u][~np.isin(shard_map.lists[u],
+                                                                   list(leaving))],
+                                     np.asarray(arriving[u], dtype=np.int64)])).astype(np.int64)
+             for u in range(w)]
+    return plan, ShardMap.from_lists(lists, n)
 
 
 def estimate_min_workers(n_gaussians: int, per_worker_capacity: int) -> int:

@@ -252,3 +252,52 @@ def test_densify_exchange_world2_gloo_equals_single():
             assert np.array_equal(params[k], getattr(new, k)[a:b].numpy()), (rank, k)
             assert np.array_equal(mm[k], m1[k][a:b].numpy()), (rank, "m", k)
             assert np.array_equal(vv[k], v1[k][a:b].numpy()), (rank, "v", k)
+
+
+# ------------------------------------- reference data-plane helpers (fixtures) --
+
+def _dataplane():
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from golden_io import load
+    return load("dataplane")
+
+
+def test_rebalance_matches_reference():
+    """rebalance(shard_map, counts) == the reference's plan and resulting map
+    (distributed.py:229-268; tests/golden/make_golden_dist.py)."""
+    d = _dataplane()
+    for case in range(6):
+        owner = d[f"rb{case}_owner"]
+        w = int(owner.max()) + 1
+        smap = D.ShardMap.from_lists([np.nonzero(owner == k)[0] for k in range(w)], int(d[f"rb{case}_n"]))
+        plan, new = D.rebalance(smap, smap.sizes)
+        assert np.array_equal(np.array(plan, dtype=np.int64).reshape(-1, 3), d[f"rb{case}_plan"])
+        assert np.array_equal(new.owner, d[f"rb{case}_new_owner"])
+        sizes = new.sizes
+        assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        D.rebalance(smap, [1] * smap.workers)
+
+
+def test_route_splats_matches_reference():
+    """route_splats over the reference's round-robin tile assignment."""
+    from types import SimpleNamespace
+    from paper_2509_05216_b200.rasterizer import ProjectedSplat
+    d = _dataplane()
+    spl = [ProjectedSplat(gaussian_index=int(i), mean2d=np.zeros(2), cov2d=np.zeros(3),
+                          depth=float(z), color=np.zeros(3), opacity=0.5,
+                          tile_span=((int(s[0]), int(s[1])), (int(s[2]), int(s[3]))))
+           for s, z, i in zip(d["rs_spans"], d["rs_depth"], d["rs_index"])]
+    part = SimpleNamespace(workers=3, tiles_x=7, assignment=d["rs_assignment"])
+    lists = D.route_splats(spl, part)
+    for w in range(3):
+        assert [s.gaussian_index for s in lists[w]] == d[f"rs_list{w}"].tolist()
+    # row bands: a splat reaches exactly the bands its rows overlap
+    bands = D.partition_pixels(7 * 16, 8 * 16, 16, 2, canon_rows=2)
+    lists = D.route_splats(spl, bands)
+    for s in spl:
+        (_, y0), (_, y1) = s.tile_span
+        want = [w for w in range(2) if y0 < bands.band_rows[w + 1] and y1 >= bands.band_rows[w]]
+        got = [w for w in range(2) if any(t is s for t in lists[w])]
+        assert got == want

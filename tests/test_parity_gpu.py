@@ -311,6 +311,15 @@ def test_depth_sort_long_reversed_run_is_bounded():
     assert bool((k2[1:] >= k2[:-1]).all())
 
 
+def test_route_rows_round_robin_matches_reference():
+    """route_rows(tile_min, tile_max, workers, tiles_x) on the device
+    (isg_route_mask) == the reference's _route_mask output (route.npz)."""
+    from paper_2509_05216_b200 import distributed as D
+    d = load("route")
+    mask = D.route_rows(d["tile_min"], d["tile_max"], 3, int(d["tiles_x"]))
+    np.testing.assert_array_equal(np_(mask), d["mask"])
+
+
 def test_gpu_knn_init_matches_reference_bitwise():
     """init_log_scales on the GPU (isg_knn_mean_grid) reproduces the
     reference's init_from_points log-scales bit for bit (config 1: 20000
