@@ -287,9 +287,11 @@ int isg_tile_offsets_dev(int64_t e_max, const int64_t *e_dev, const void *sorted
 
 /* Heaviest-first launch order of n_tiles tile lists: keys16[t] = 65535 -
  * min(list length, 65535) and vals[t] = t, to be sorted ascending with
- * isg_sort_u16 (16 bits) into the tile_order of the raster pair. */
-int isg_tile_order_keys(int32_t n_tiles, const int32_t *offsets, uint16_t *keys16,
-                        int32_t *vals, void *stream);
+ * isg_sort_u16 (16 bits) into the tile_order of the raster pair.
+ * heavy_pct > 0: only lists of at least heavy_pct % of the mean length go
+ * first (by length); the rest follow in list order (spatial locality). */
+int isg_tile_order_keys(int32_t n_tiles, const int32_t *offsets, int32_t heavy_pct,
+                        uint16_t *keys16, int32_t *vals, void *stream);
 
 /* The ordered fold over the live-only layout (float32 records of
  * isg_raster_bwd_masked with slot_rank: rank r's slots live_off[r] ..

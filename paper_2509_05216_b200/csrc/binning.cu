@@ -278,11 +278,23 @@ __global__ void tile_offsets_kernel(int64_t e, const K *__restrict__ keys, int n
     offsets[t] = (int32_t)lo;
 }
 
+// heavy_pct > 0: only the lists at least heavy_pct % of the mean length are
+// ordered heaviest first; the others keep list (row-major) order after them,
+// so neighbouring tiles -- which share splats -- still run together (L2 reuse
+// of the staged features).  heavy_pct == 0: every list by length.
 __global__ void tile_order_keys_kernel(int n_tiles, const int32_t *__restrict__ offsets,
-                                       uint16_t *__restrict__ keys, int32_t *__restrict__ vals) {
+                                       int heavy_pct, uint16_t *__restrict__ keys,
+                                       int32_t *__restrict__ vals) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_tiles) return;
-    keys[t] = (uint16_t)(65535 - min(offsets[t + 1] - offsets[t], 65535));
+    const int len = offsets[t + 1] - offsets[t];
+    uint16_t k = (uint16_t)(65535 - min(len, 65535));
+    if (heavy_pct > 0) {
+        const int64_t total = offsets[n_tiles] - offsets[0];
+        const bool heavy = (int64_t)len * 100 * n_tiles >= (int64_t)heavy_pct * total;
+        k = heavy ? (uint16_t)(32767 - min(len, 32767)) : (uint16_t)65535;
+    }
+    keys[t] = k;
     vals[t] = t;
 }
 
@@ -411,13 +423,13 @@ extern "C" int isg_sort_u32(void *workspace, size_t *ws_bytes, const uint32_t *k
                                   begin_bit, end_bit, (cudaStream_t)stream);
 }
 
-extern "C" int isg_tile_order_keys(int32_t n_tiles, const int32_t *offsets, uint16_t *keys16,
-                                   int32_t *vals, void *stream) {
+extern "C" int isg_tile_order_keys(int32_t n_tiles, const int32_t *offsets, int32_t heavy_pct,
+                                   uint16_t *keys16, int32_t *vals, void *stream) {
     if (n_tiles < 0 || (n_tiles > 0 && (!offsets || !keys16 || !vals)))
         return (int)cudaErrorInvalidValue;
     if (n_tiles == 0) return 0;
     tile_order_keys_kernel<<<blocks_for(n_tiles, 256), 256, 0, (cudaStream_t)stream>>>(
-        n_tiles, offsets, keys16, vals);
+        n_tiles, offsets, heavy_pct, keys16, vals);
     ISG_CHECK_LAUNCH();
     return 0;
 }

@@ -334,6 +334,11 @@ class Rasterizer:
     LAUNCHES_PER_STEP = None  # filled by Trainer (documented count)
 
 
+# Tiles whose list is at least HEAVY_PCT % of the mean length launch first
+# (longest first); the rest keep row-major order (0: all by length).
+HEAVY_PCT = int(os.environ.get("ISOGS_HEAVY_PCT", "0"))
+
+
 def heavy_first_order(st, n_tiles: int, offsets: torch.Tensor):
     """Launch order of the raster pair, heaviest tile lists first
     (isg_tile_order_keys + a 16-bit stable sort): with one CTA per tile, a
@@ -348,7 +353,7 @@ def heavy_first_order(st, n_tiles: int, offsets: torch.Tensor):
     st.to_vals = _grow(st.to_vals, n_tiles, dtype=torch.int32, device=dev)
     st.to_keys_s = _grow(st.to_keys_s, n_tiles, dtype=torch.int16, device=dev)
     st.to_order = _grow(st.to_order, n_tiles, dtype=torch.int32, device=dev)
-    L.check(lib.isg_tile_order_keys(n_tiles, L.ptr(offsets), L.ptr(st.to_keys),
+    L.check(lib.isg_tile_order_keys(n_tiles, L.ptr(offsets), HEAVY_PCT, L.ptr(st.to_keys),
                                     L.ptr(st.to_vals), L.stream_ptr()), "isg_tile_order_keys")
     if not hasattr(st, "ws_order"):
         st.ws_order = L.Workspace()

@@ -91,3 +91,38 @@ def test_sharded_run_bitwise_equals_single_gpu_at_scale(name, workers):
     assert got.count == ref["cloud"].count
     for k in P.PARAM_NAMES:
         assert torch.equal(getattr(got, k), getattr(ref["cloud"], k)), k
+
+
+def test_sharded_config4_w4_bitwise_equals_single_gpu():
+    """BASELINE configs[3] (Miranda-scale, 18M Gaussians, 2048^2) on 4 ranks,
+    emulated: 5 iterations bitwise equal to the single-GPU engine."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200 import distributed as D
+    from paper_2509_05216_b200 import synthetic as S
+    from paper_2509_05216_b200.engine import Trainer
+    from paper_2509_05216_b200.training import TrainDataset, PointCloud, build_schedule
+    iters = 5
+    dev = torch.device("cuda", 0)
+    nv = S.CONFIGS["config4"][4]
+    sched = build_schedule(iters, nv, 0)
+    wl = S.make_workload("config4", dev, view_ids=sched)
+    ext = TrainDataset(wl.cameras, np.zeros((nv, 1, 1, 3)),
+                       PointCloud(wl.points, wl.normals)).scene_extent
+    cfg = P.TrainConfig(iterations=iters, densify=False, eval_interval=0)
+    cloud0 = P.cloud_from_points(wl.points, wl.log_scales, 1, dev)
+    tr = Trainer(cloud0.copy(), wl.resolution, wl.resolution, cfg, ext, dev)
+    for it in range(1, iters + 1):
+        tr.step(it, wl.cameras[sched[it - 1]], wl.images_u8[it - 1])
+    ref_losses = tr.loss_dev[1:iters + 1].tolist()
+    ref = tr.cloud
+    del tr
+    ranks, _, part = D.make_ranks(cloud0, wl.resolution, wl.resolution, cfg, ext, 4, dev)
+    del cloud0
+    losses = []
+    for it in range(1, iters + 1):
+        losses.append(float(D.emulated_step(ranks, wl.cameras[sched[it - 1]],
+                                            wl.images_u8[it - 1], it)[0]))
+    got = D.gather_cloud(ranks)
+    assert losses == ref_losses, (losses, ref_losses)
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(got, k), getattr(ref, k)), k
