@@ -599,7 +599,8 @@ __global__ void __launch_bounds__(1024) chunk_items_kernel(int n_tiles,
                                                            const int32_t *__restrict__ offsets,
                                                            const int32_t *__restrict__ order,
                                                            const int4 *__restrict__ tile_last,
-                                                           int chunk, int2 *__restrict__ items,
+                                                           int chunk, int split,
+                                                           int2 *__restrict__ items,
                                                            int32_t *__restrict__ n_items) {
     __shared__ int swarp[32];
     __shared__ int scarry;
@@ -613,7 +614,7 @@ __global__ void __launch_bounds__(1024) chunk_items_kernel(int n_tiles,
             tl = order ? order[p] : p;
             const int4 q = tile_last[tl];
             const int len = max(max(q.x, q.y), max(q.z, q.w));
-            nc = max(1, (len + chunk - 1) / chunk);
+            nc = split ? max(1, (len + chunk - 1) / chunk) : 1;
         }
         int x = nc;
 #pragma unroll
@@ -646,13 +647,14 @@ extern "C" int32_t isg_chunk_items_max(int64_t n_entries, int32_t n_tiles, int32
 }
 
 extern "C" int isg_chunk_items(int32_t n_tiles, const int32_t *offsets, const int32_t *tile_order,
-                               const int32_t *tile_last, int32_t chunk, int32_t *items,
-                               int32_t *n_items, void *stream) {
+                               const int32_t *tile_last, int32_t chunk, int32_t split,
+                               int32_t *items, int32_t *n_items, void *stream) {
     if (n_tiles < 0 || chunk <= 0 || chunk % 32 || !items || !n_items ||
         (n_tiles && (!offsets || !tile_last)))
         return (int)cudaErrorInvalidValue;
     chunk_items_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
-        n_tiles, offsets, tile_order, (const int4 *)tile_last, chunk, (int2 *)items, n_items);
+        n_tiles, offsets, tile_order, (const int4 *)tile_last, chunk, split, (int2 *)items,
+        n_items);
     ISG_CHECK_LAUNCH();
     return 0;
 }

@@ -364,11 +364,15 @@ def heavy_first_order(st, n_tiles: int, offsets: torch.Tensor):
 
 # Backward list chunking: entries per backward work item (isg_chunks).  A
 # constant, so the chunking of every tile is the same for any band partition
-# (bitwise W-invariance).  Measured (tools/ab_chunk.sh, profiles/r02_chunk):
-# chunks of 512 take config 2's backward 1.14 -> 0.91 ms and an emulated W=8
-# band's 1.03 -> 0.80 ms, but config 3's 3.88 -> 4.35 ms (more, shorter CTAs
-# lower the achieved occupancy), so the default is off (0: one CTA per tile).
+# (bitwise W-invariance); 0: off (one CTA per tile, no restarts).
+# Measured (tools/ab_chunk.sh, profiles/r02_chunk): chunks of 512 take config
+# 2's backward 1.14 -> 0.91 ms and an emulated W=8 band's 1.03 -> 0.80 ms,
+# but config 3's 3.88 -> 4.35 ms (more, shorter CTAs lower the achieved
+# occupancy); a variant that keeps one CTA per tile and restarts it at the
+# chunk boundaries (same arithmetic as split chunks, so the split could follow
+# the launch size) costs 3.78 -> 4.62 ms at config 3.  Off by default.
 CHUNK = int(os.environ.get("ISOGS_CHUNK", "0"))
+SPLIT_TILES = 1 << 30  # every chunk its own CTA when chunking is on
 
 
 def chunk_setup(st, n_tiles: int, e: int, image_ptr: int):
@@ -399,9 +403,11 @@ def chunk_items(st, n_tiles: int) -> None:
     positions (isg_chunk_items), in the heaviest-first tile order."""
     if st.chunks is None:
         return
+    split = 1 if n_tiles <= SPLIT_TILES else 0
     L.check(L.lib().isg_chunk_items(n_tiles, L.ptr(st.offsets), L.ptr(st.tile_order),
-                                    L.ptr(st.ch_last), st.chunks.chunk, L.ptr(st.ch_items),
-                                    L.ptr(st.ch_n), L.stream_ptr()), "isg_chunk_items")
+                                    L.ptr(st.ch_last), st.chunks.chunk, split,
+                                    L.ptr(st.ch_items), L.ptr(st.ch_n), L.stream_ptr()),
+            "isg_chunk_items")
 
 
 def update_params(cloud: GaussianCloud, m: dict, v: dict, grads: dict, seen, grad_accum, flag,
