@@ -472,6 +472,20 @@ int isg_chain_train_ranked(const isg_params *p, const isg_camera *cam, const int
                            int64_t *seen, double *grad_accum, double half_w, double half_h,
                            void *stream);
 
+/* The live fold fused into the ranked chain (the training step on live-only
+ * lists): row i folds the live subtotal slots of its rank r = rank_of[i]
+ * (live_off[r] .. live_off[r+1] of partials; rect_sorted, [row_lo, row_hi),
+ * canon_rows as isg_reduce_live -- bit-identical sums) and runs the chain
+ * rule on them; grad2d_out (optional) receives the rank-ordered 2-D
+ * gradients. */
+int isg_chain_fold_train(const isg_params *p, const isg_camera *cam, const int32_t *rank_of,
+                         const int64_t *live_off, const float *partials,
+                         const int32_t *rect_sorted, int32_t row_lo, int32_t row_hi,
+                         int32_t canon_rows, double *grad2d_out, float *d_positions,
+                         float *d_log_scales, float *d_rotations, float *d_opacity_logits,
+                         float *d_sh, int64_t *seen, double *grad_accum, double half_w,
+                         double half_h, void *stream);
+
 /* ... then dense float32 Adam over up to 8 groups in one launch (arrays of
  * `count` host-side pointers / sizes / learning rates; constants as for
  * isg_adam).  Bit-identical to isg_adam per element. */

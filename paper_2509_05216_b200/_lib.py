@@ -131,6 +131,8 @@ SIGNATURES = {
                         _P, _P, _P, _P, _D, _D, _P],
     "isg_chain_train_ranked": [ctypes.POINTER(Params_t), ctypes.POINTER(Camera_t), _P, _P, _P,
                                _P, _P, _P, _P, _P, _P, _D, _D, _P],
+    "isg_chain_fold_train": [ctypes.POINTER(Params_t), ctypes.POINTER(Camera_t), _P, _P, _P, _P,
+                             _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _D, _D, _P],
     "isg_adam_groups": [_I32, _P, _P, _P, _P, _P, _P, ctypes.POINTER(AdamConsts_t), _P],
     "isg_exp_f64": [_I64, _P, _P, _P],
     "isg_probe_ffma": [_I32, _I32, _P, _P],

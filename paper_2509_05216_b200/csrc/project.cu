@@ -578,6 +578,37 @@ extern "C" int isg_chain_train(const isg_params *p, const isg_camera *cam, const
                               half_h, stream);
 }
 
+namespace isg {
+void launch_chain_fold_train_f32(const isg_params &p, const Cam &cam, const int32_t *rank_of,
+                                 const int64_t *live_off, const float *partials,
+                                 const int32_t *rect_sorted, int row_lo, int row_hi, int canon,
+                                 double *grad2d_out, float *dpos, float *dls, float *drot,
+                                 float *dlogit, float *dsh, int64_t *seen, double *grad_accum,
+                                 double half_w, double half_h, cudaStream_t s);
+}
+
+extern "C" int isg_chain_fold_train(const isg_params *p, const isg_camera *cam,
+                                    const int32_t *rank_of, const int64_t *live_off,
+                                    const float *partials, const int32_t *rect_sorted,
+                                    int32_t row_lo, int32_t row_hi, int32_t canon_rows,
+                                    double *grad2d_out, float *d_positions, float *d_log_scales,
+                                    float *d_rotations, float *d_opacity_logits, float *d_sh,
+                                    int64_t *seen, double *grad_accum, double half_w,
+                                    double half_h, void *stream) {
+    if (!p || !cam || !rank_of || !live_off || !partials || !rect_sorted || canon_rows < 1 ||
+        p->n < 0 || p->dtype != ISG_F32 || !d_positions || !d_log_scales || !d_rotations ||
+        !d_opacity_logits || !d_sh)
+        return (int)cudaErrorInvalidValue;
+    if (p->n == 0) return 0;
+    const Cam c = to_cam(*cam);
+    launch_chain_fold_train_f32(*p, c, rank_of, live_off, partials, rect_sorted, row_lo, row_hi,
+                                canon_rows, grad2d_out, d_positions, d_log_scales, d_rotations,
+                                d_opacity_logits, d_sh, seen, grad_accum, half_w, half_h,
+                                (cudaStream_t)stream);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
 extern "C" int isg_chain_train_ranked(const isg_params *p, const isg_camera *cam,
                                       const int32_t *rank_of, const double *grad2d_ranked,
                                       float *d_positions, float *d_log_scales,

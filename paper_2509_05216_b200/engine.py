@@ -125,6 +125,10 @@ class Rasterizer:
         self.tile_keys = self.tile_vals = self.keys_sorted_t = self.entries = None
         self.slot_rank = self.iota = None
         self.live = False  # live-only training lists (isg_bin_emit_live)
+        # the training step folds the live subtotals inside the chain kernel
+        # (ranked grads only); keep_grad2d also stores the 2-D gradients
+        self.fuse_fold = os.environ.get("ISOGS_FUSE_FOLD", "1") != "0"
+        self.keep_grad2d = False
         self.partials = None
         self.to_keys = self.to_vals = self.to_keys_s = self.to_order = None
         self.tile_order = None
@@ -316,7 +320,9 @@ class Rasterizer:
                                        L.ptr(self.n_last), L.ptr(self.dl), L.ISG_F32,
                                        L.ptr(self.partials), s), "isg_raster_bwd")
         _mark(self.timer, "raster_bwd")
-        if ctx.m and self.live:
+        if ctx.m and self.live and self.fuse_fold and self.ranked_grads:
+            pass  # folded inside the chain (isg_chain_fold_train)
+        elif ctx.m and self.live:
             L.check(lib.isg_reduce_live(ctx.m, L.ptr(self.live_off), L.ptr(self.partials),
                                         None if self.ranked_grads else L.ptr(self.order),
                                         L.ptr(self.rect_sorted), 0, self.tiles_y,
@@ -412,9 +418,12 @@ def chunk_items(st, n_tiles: int) -> None:
 
 def update_params(cloud: GaussianCloud, m: dict, v: dict, grads: dict, seen, grad_accum, flag,
                   grad2d, cam_struct, lrs: list, it: int, width: int, height: int,
-                  timer=None, rank_of=None) -> None:
+                  timer=None, rank_of=None, fold=None) -> None:
     """Chain rule + TrainStats (isg_chain_train), then dense Adam over the five
-    groups in one launch (isg_adam_groups): engine.py:508-536, optim.py:20-56."""
+    groups in one launch (isg_adam_groups): engine.py:508-536, optim.py:20-56.
+    fold: the Rasterizer whose live subtotals the chain folds itself
+    (isg_chain_fold_train; grad2d then only receives the 2-D gradients when
+    fold.keep_grad2d)."""
     lib = L.lib()
     s = L.stream_ptr()
     p = L.Params_t()
@@ -423,7 +432,15 @@ def update_params(cloud: GaussianCloud, m: dict, v: dict, grads: dict, seen, gra
     p.sh, p.n, p.degree, p.dtype = L.ptr(cloud.sh_coeffs), cloud.count, cloud.degree, L.ISG_F32
     if cloud.count == 0:
         return
-    if rank_of is not None:
+    if fold is not None:
+        L.check(lib.isg_chain_fold_train(
+            ctypes.byref(p), ctypes.byref(cam_struct), L.ptr(rank_of), L.ptr(fold.live_off),
+            L.ptr(fold.partials), L.ptr(fold.rect_sorted), 0, fold.tiles_y, fold.canon_rows,
+            L.ptr(grad2d) if fold.keep_grad2d else None,
+            L.ptr(grads["positions"]), L.ptr(grads["log_scales"]), L.ptr(grads["rotations"]),
+            L.ptr(grads["opacity_logits"]), L.ptr(grads["sh_coeffs"]), L.ptr(seen),
+            L.ptr(grad_accum), 0.5 * width, 0.5 * height, s), "isg_chain_fold_train")
+    elif rank_of is not None:
         L.check(lib.isg_chain_train_ranked(
             ctypes.byref(p), ctypes.byref(cam_struct), L.ptr(rank_of), L.ptr(grad2d),
             L.ptr(grads["positions"]), L.ptr(grads["log_scales"]), L.ptr(grads["rotations"]),
@@ -513,9 +530,11 @@ class Trainer:
         r.backward(ctx)
         if self.grads is None:
             self.grads = {k: torch.empty_like(getattr(self.cloud, k)) for k in PARAM_NAMES}
+        fused = r.live and r.fuse_fold and r.ranked_grads
         update_params(self.cloud, self.m, self.v, self.grads, self.stats.seen,
                       self.stats.grad_accum, r.flag, r.grad2d, r.cam_struct, self.lrs(it), it,
-                      r.width, r.height, r.timer, rank_of=r.rank_of)
+                      r.width, r.height, r.timer, rank_of=r.rank_of,
+                      fold=r if fused else None)
 
     def densify_due(self, it: int) -> bool:
         """engine.py:540-541."""

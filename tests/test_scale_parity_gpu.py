@@ -254,6 +254,7 @@ def test_training_steps_match_oracle_from_the_same_state(name, iters):
     from paper_2509_05216_b200.engine import Trainer
     cfg = P.TrainConfig(iterations=iters, densify=False, eval_interval=0)
     tr = Trainer(_device_cloud(c), c["cam"].width, c["cam"].height, cfg, c["ext"])
+    tr.r.keep_grad2d = True  # the fused fold + chain also stores the 2-D gradients
     wl = c["wl"]
     ocfg = T.Config(iterations=iters, eval_interval=0, seed=0)
     for it in range(1, iters + 1):

@@ -124,6 +124,7 @@ def test_contribution_masks_change_no_result():
         t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
         t.r.use_cmask = masked
         t.r.chunk = 0  # one backward CTA per tile: the same arithmetic as the unmasked pair
+        t.r.keep_grad2d = True
         for it in range(1, 5):
             t.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
         torch.cuda.synchronize()
@@ -155,6 +156,7 @@ def test_backward_chunking_matches_one_cta_per_tile():
     for chunk in (64, 0):  # config 1 lists reach 6.3K entries: many chunks per tile
         t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
         t.r.chunk = chunk
+        t.r.keep_grad2d = True
         for it in range(1, 5):
             t.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
             if it == 1:
