@@ -288,6 +288,11 @@ int isg_sort_pairs_dev(void *workspace, size_t *ws_bytes, int32_t key_bytes, con
 int isg_tile_offsets_dev(int64_t e_max, const int64_t *e_dev, const void *sorted_keys,
                          int32_t key_bytes, int32_t n_tiles, int32_t *offsets, void *stream);
 
+/* Heaviest-first launch order in one launch: tiles bucketed by the bit length
+ * of their list, longest buckets first (order inside a bucket arbitrary; the
+ * raster results do not depend on the launch order). */
+int isg_tile_order(int32_t n_tiles, const int32_t *offsets, int32_t *order, void *stream);
+
 /* Heaviest-first launch order of n_tiles tile lists: keys16[t] = 65535 -
  * min(list length, 65535) and vals[t] = t, to be sorted ascending with
  * isg_sort_u16 (16 bits) into the tile_order of the raster pair.

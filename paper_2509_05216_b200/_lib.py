@@ -98,6 +98,7 @@ SIGNATURES = {
     "isg_chunk_items_max": [_I64, _I32, _I32],
     "isg_chunk_items": [_I32, _P, _P, _P, _I32, _I32, _P, _P, _P],
     "isg_tile_order_keys": [_I32, _P, _I32, _P, _P, _P],
+    "isg_tile_order": [_I32, _P, _P, _P],
     "isg_sort_pairs_dev": [_P, _SZ, _I32, _P, _P, _P, _P, _I64, _P, _I32, _I32, _P],
     "isg_tile_offsets_dev": [_I64, _P, _P, _I32, _I32, _P, _P],
     "isg_contrib_mask_words": [_I64, _I32],

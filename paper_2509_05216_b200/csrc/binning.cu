@@ -298,6 +298,53 @@ __global__ void tile_order_keys_kernel(int n_tiles, const int32_t *__restrict__ 
     vals[t] = t;
 }
 
+// Heaviest-first launch order in one CTA (any tile count): tiles bucketed by
+// list length into OB linear buckets of width max/OB (longest first), a
+// tile's place inside its bucket taken by a shared-memory atomic.  The order
+// inside a bucket is arbitrary -- it only schedules CTAs; no result depends
+// on it.
+constexpr int OB = 1024;
+__global__ void __launch_bounds__(1024) tile_order_kernel(int n_tiles,
+                                                          const int32_t *__restrict__ offsets,
+                                                          int32_t *__restrict__ order) {
+    __shared__ int cnt[OB];
+    __shared__ int smax;
+    if (threadIdx.x == 0) smax = 1;
+    for (int b = threadIdx.x; b < OB; b += blockDim.x) cnt[b] = 0;
+    __syncthreads();
+    int m = 0;
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
+        m = max(m, offsets[t + 1] - offsets[t]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&smax, m);
+    __syncthreads();
+    const int64_t mx = (int64_t)smax + 1;
+    auto bucket = [&](int len) { return OB - 1 - (int)((int64_t)len * OB / mx); };
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
+        atomicAdd(&cnt[bucket(offsets[t + 1] - offsets[t])], 1);
+    __syncthreads();
+    // exclusive scan of the bucket counts (OB == blockDim.x)
+    {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        __shared__ int sw[32];
+        const int v = cnt[threadIdx.x];
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) sw[warp] = x;
+        __syncthreads();
+        int before = 0;
+        for (int w = 0; w < warp; w++) before += sw[w];
+        __syncthreads();
+        cnt[threadIdx.x] = before + x - v;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
+        order[atomicAdd(&cnt[bucket(offsets[t + 1] - offsets[t])], 1)] = t;
+}
+
 inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace isg
@@ -421,6 +468,15 @@ extern "C" int isg_sort_u32(void *workspace, size_t *ws_bytes, const uint32_t *k
         return (int)cudaErrorInvalidValue;
     return radix::sort_pairs<uint32_t>(workspace, ws_bytes, keys_in, keys_out, vals_in, vals_out, n,
                                   begin_bit, end_bit, (cudaStream_t)stream);
+}
+
+extern "C" int isg_tile_order(int32_t n_tiles, const int32_t *offsets, int32_t *order,
+                              void *stream) {
+    if (n_tiles < 0 || (n_tiles > 0 && (!offsets || !order))) return (int)cudaErrorInvalidValue;
+    if (n_tiles == 0) return 0;
+    tile_order_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(n_tiles, offsets, order);
+    ISG_CHECK_LAUNCH();
+    return 0;
 }
 
 extern "C" int isg_tile_order_keys(int32_t n_tiles, const int32_t *offsets, int32_t heavy_pct,
