@@ -731,13 +731,13 @@ def run_dist(args, world: int, rank: int, local: int):
     from paper_2509_05216_b200.gaussians import cloud_from_points
     from paper_2509_05216_b200.training import TrainConfig, TrainDataset, PointCloud, build_schedule
     dev = torch.device("cuda", local)
-    comm = D.TorchComm()
     # torchrun pins OMP_NUM_THREADS=1; the host side of the step runs slower that way
     torch.set_num_threads(max(1, (os.cpu_count() or 1) // max(world, 1)))
     say = log if rank == 0 else (lambda *a: None)
     wl = S.make_workload(args.config, dev, log=say, resolution=args.res)
     n = wl.points.shape[0]
     res = wl.resolution
+    comm = D.TorchComm(peers=args.exchange == "peer", height=res, width=res, device=dev)
     cloud = cloud_from_points(wl.points, wl.log_scales, 1, dev)
     iters = args.warmup + args.steps
     cfg = TrainConfig(iterations=total_iterations(args), densify=False, eval_interval=0)
@@ -833,6 +833,7 @@ def run_dist(args, world: int, rank: int, local: int):
                     "h2d_bytes_per_step": int(gt.numel()), "d2h_bytes_per_step": 8},
             "clocks": clk.summary(), "gpu_launches": D.LAUNCHES_PER_STEP * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "parity": parity,
+            "exchange": args.exchange,
             "partition": {"bands_tile_rows": rs.part.band_rows, "initial": part.band_rows,
                           "canon_rows": part.canon_rows, "shard_sizes": smap.sizes,
                           "balance": rs.balance},
@@ -870,6 +871,11 @@ def main():
                          "iterations (0: skip)")
     ap.add_argument("--cpu-budget-s", type=float, default=120.0,
                     help="reference arm: stop timing iterations after this many seconds")
+    ap.add_argument("--exchange", default=os.environ.get("ISOGS_EXCHANGE", "peer"),
+                    choices=["peer", "nccl"],
+                    help="sharded step's exchange: peer = NVLink stores from the pack / band "
+                         "fold / forward kernels into symmetric-memory buffers; nccl = "
+                         "point-to-point NCCL copies")
     ap.add_argument("--dist", action="store_true",
                     help="run the sharded engine even at N=1 (world 1)")
     args = ap.parse_args()

@@ -376,6 +376,20 @@ int isg_route_pack(int64_t n, const uint8_t *flag, const int32_t *rect, const ui
                    uint64_t *keys_send, int32_t *pay_send, uint64_t *keys_self,
                    int32_t *pay_self, void *stream);
 
+/* Peer-store variant of isg_route_pack (the fused pack + exchange): band d's
+ * records go to keys_dst[d][j] / pay_dst[d][16 * j] (int32 units), j as
+ * above -- keys_dst/pay_dst are HOST arrays of n_bands DEVICE pointers, each
+ * already offset to where this shard's segment starts in band d's receive
+ * buffers.  For d != this rank they point into the peer GPU's memory mapped
+ * into this process (NVLink stores; e.g. torch symmetric memory), so the
+ * exchange is the pack kernel's own stores.  pay_dst entries 16-byte aligned.
+ * Replaces the mailbox put of engine.py:201-215 (the caller adds a barrier
+ * before the bands read). */
+int isg_route_pack_peer(int64_t n, const uint8_t *flag, const int32_t *rect, const uint64_t *key,
+                        const float *feat, const int32_t *band_rows, int32_t n_bands,
+                        const int64_t *plan, uint64_t *const *keys_dst, int32_t *const *pay_dst,
+                        void *stream);
+
 /* The reference's round-robin routing mask (route_rows, distributed.py:127-136
  * over _route_mask, _kernels.py:378-394): rects (n, 4) int32 (tile_min,
  * tile_max); mask (n, workers) u8, 1 iff the rect touches a tile whose linear
@@ -399,6 +413,22 @@ int isg_band_fold(int64_t m, const int64_t *emit_off, const float *partials,
                   const int32_t *rect_sorted, const int32_t *order, const int64_t *gpos,
                   int32_t row_lo, int32_t row_hi, int32_t canon_rows, int32_t live_layout,
                   double *gbuf, void *stream);
+
+/* Peer-store variant of isg_band_fold (the fused fold + gradient exchange,
+ * engine.py:256-284 / 499-507): receive indices [recv_end[s-1], recv_end[s])
+ * came from source rank s (recv_end HOST, n_src entries, last >= m), whose
+ * records go to dst_base[s] + 9 * gpos[...] -- dst_base a HOST array of
+ * DEVICE pointers (the owner's gradient receive buffer, on its GPU, offset so
+ * that its gpos range lands at this band's segment). */
+int isg_band_fold_peer(int64_t m, const int64_t *emit_off, const float *partials,
+                       const int32_t *rect_sorted, const int32_t *order, const int64_t *gpos,
+                       int32_t row_lo, int32_t row_hi, int32_t canon_rows, int32_t live_layout,
+                       int32_t n_src, const int64_t *recv_end, double *const *dst_base,
+                       void *stream);
+
+/* Device-to-device copy of `bytes` on `stream` (either side may be a peer
+ * GPU's memory mapped into this process): the halo rows of the peer exchange. */
+int isg_copy(void *dst, const void *src, int64_t bytes, void *stream);
 
 /* Band raster cost per canonical block (load balance of the row bands):
  * hist[(prow0 + y) / (16 * canon_rows)] += sum_x n_last[y][x] for the band's

@@ -229,20 +229,23 @@ __device__ __forceinline__ int64_t block_excl(int64_t v, int64_t *s_warp, int64_
     return before + x - v;
 }
 
+// Where band d's segment of this shard's records starts: a local send or
+// receive buffer, or -- the peer-store exchange -- band d's receive buffers
+// on its own GPU, mapped into this process (NVLink loads/stores).
 struct PackDest {
-    int64_t off[MAX_BANDS];  // base slot of each band's segment in its buffer
-    int self;                // the band whose records go to the self buffers
+    uint64_t *keys[MAX_BANDS];
+    int4 *pay[MAX_BANDS];  // 4 int4 per record
 };
 
 // Splat records of every visible shard row for each band it reaches, in
 // shard row order inside each band's segment: the depth key (8 B) and a
-// 64-byte payload (rect, 12 raster features).  The self band's segment is
-// written straight into this rank's receive buffers.
+// 64-byte payload (rect, 12 raster features), stored straight to the
+// segment's destination (own band: this rank's receive buffers; peer
+// exchange: the band's receive buffers on its GPU).
 __global__ void __launch_bounds__(PLAN_T) route_pack_kernel(
     int64_t n, const uint8_t *__restrict__ flag, const int4 *__restrict__ rect,
     const uint64_t *__restrict__ key, const int4 *__restrict__ feat, Bands bands,
-    const int64_t *__restrict__ plan, PackDest dst, uint64_t *__restrict__ keys_send,
-    int4 *__restrict__ pay_send, uint64_t *__restrict__ keys_self, int4 *__restrict__ pay_self) {
+    const int64_t *__restrict__ plan, PackDest dst) {
     __shared__ int64_t s_warp[PLAN_T / 32];
     __shared__ int s_lo, s_hi;
     const int nbands = bands.n;
@@ -270,10 +273,9 @@ __global__ void __launch_bounds__(PLAN_T) route_pack_kernel(
         int64_t tot;
         const int64_t ex = block_excl<PLAN_T>(on ? 1 : 0, s_warp, tot);
         if (on) {
-            const int64_t slot = dst.off[d] + pb[2 * d] + ex;
-            uint64_t *kk = d == dst.self ? keys_self : keys_send;
-            int4 *pp = (d == dst.self ? pay_self : pay_send) + 4 * slot;
-            kk[slot] = key[i];
+            const int64_t slot = pb[2 * d] + ex;
+            int4 *pp = dst.pay[d] + 4 * slot;
+            dst.keys[d][slot] = key[i];
             pp[0] = rc;
             pp[1] = feat[3 * i];
             pp[2] = feat[3 * i + 1];
@@ -427,12 +429,20 @@ struct BlockEmitLive {
     }
 };
 
+// Destination of the gradient records by source rank: receive indices
+// [recv_end[s-1], recv_end[s]) came from source s, whose records go to
+// base[s] + 9 * gpos (a local buffer, or -- the peer-store exchange -- the
+// owner's receive buffer on its GPU, base offset so gpos lands in place).
+struct GradDest {
+    double *base[MAX_BANDS];
+    int64_t recv_end[MAX_BANDS];
+};
+
 template <bool LIVE>
 __global__ void __launch_bounds__(BF_THREADS) band_fold_kernel(
     int64_t m, const int64_t *__restrict__ emit_off, const float *__restrict__ partials,
     const int4 *__restrict__ rect_sorted, const int32_t *__restrict__ order,
-    const int64_t *__restrict__ gpos, int row_lo, int row_hi, int canon,
-    double *__restrict__ gbuf) {
+    const int64_t *__restrict__ gpos, int row_lo, int row_hi, int canon, GradDest dst) {
     constexpr int PS = partial_stride<float>();
     __shared__ __align__(128) float sbuf[BF_WARPS][2][BF_SLOTS * PS];
     __shared__ __align__(8) uint64_t sbar[BF_WARPS][2];
@@ -445,13 +455,18 @@ __global__ void __launch_bounds__(BF_THREADS) band_fold_kernel(
     const int64_t span1 = emit_off[min(r0 + 32, m)];
     int64_t p = live ? emit_off[r] : 0;
     const int64_t p1 = live ? emit_off[r + 1] : 0;
+    double *out = dst.base[0];
+    if (live) {
+        const int32_t q = order[r];
+        int src = 0;
+        while (q >= dst.recv_end[src]) src++;
+        out = dst.base[src] + 9 * gpos[q];
+    }
     typename std::conditional<LIVE, BlockEmitLive, BlockEmit>::type st;
     if constexpr (LIVE) {
-        st.init(live ? rect_sorted[r] : make_int4(0, 0, -1, -1), row_lo, row_hi, canon,
-                live ? gbuf + 9 * gpos[order[r]] : gbuf);
+        st.init(live ? rect_sorted[r] : make_int4(0, 0, -1, -1), row_lo, row_hi, canon, out);
     } else {
-        st.init(live ? rect_sorted[r] : make_int4(0, 0, 0, 0), row_lo, canon,
-                live ? gbuf + 9 * gpos[order[r]] : gbuf);
+        st.init(live ? rect_sorted[r] : make_int4(0, 0, 0, 0), row_lo, canon, out);
     }
     const int nch = (int)((span1 - span0 + BF_SLOTS - 1) / BF_SLOTS);
     float(*buf)[BF_SLOTS * PS] = sbuf[warp];
@@ -656,11 +671,35 @@ extern "C" int isg_route_pack(int64_t n, const uint8_t *flag, const int32_t *rec
     const int64_t nblk = (n + PLAN_T - 1) / PLAN_T;
     if (nblk == 0) return 0;
     PackDest dst;
-    for (int d = 0; d < n_bands; d++) dst.off[d] = dest_off[d];
-    dst.self = self_band;
+    for (int d = 0; d < n_bands; d++) {
+        const bool self = d == self_band;
+        dst.keys[d] = (self ? keys_self : keys_send) + dest_off[d];
+        dst.pay[d] = (int4 *)(self ? pay_self : pay_send) + 4 * dest_off[d];
+    }
     route_pack_kernel<<<(unsigned)nblk, PLAN_T, 0, (cudaStream_t)stream>>>(
-        n, flag, (const int4 *)rect, key, (const int4 *)feat, b, plan, dst, keys_send,
-        (int4 *)pay_send, keys_self, (int4 *)pay_self);
+        n, flag, (const int4 *)rect, key, (const int4 *)feat, b, plan, dst);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_route_pack_peer(int64_t n, const uint8_t *flag, const int32_t *rect,
+                                   const uint64_t *key, const float *feat,
+                                   const int32_t *band_rows, int32_t n_bands, const int64_t *plan,
+                                   uint64_t *const *keys_dst, int32_t *const *pay_dst,
+                                   void *stream) {
+    Bands b;
+    if (n < 0 || fill_bands(b, band_rows, n_bands) || !keys_dst || !pay_dst)
+        return (int)cudaErrorInvalidValue;
+    const int64_t nblk = (n + PLAN_T - 1) / PLAN_T;
+    if (nblk == 0) return 0;
+    PackDest dst;
+    for (int d = 0; d < n_bands; d++) {
+        dst.keys[d] = keys_dst[d];
+        dst.pay[d] = (int4 *)pay_dst[d];
+        if ((reinterpret_cast<uintptr_t>(pay_dst[d]) & 15) != 0) return (int)cudaErrorInvalidValue;
+    }
+    route_pack_kernel<<<(unsigned)nblk, PLAN_T, 0, (cudaStream_t)stream>>>(
+        n, flag, (const int4 *)rect, key, (const int4 *)feat, b, plan, dst);
     ISG_CHECK_LAUNCH();
     return 0;
 }
@@ -686,23 +725,53 @@ extern "C" int isg_band_blocks(int64_t r, const int32_t *payload, int32_t row_lo
     return 0;
 }
 
+static int launch_band_fold(int64_t m, const int64_t *emit_off, const float *partials,
+                            const int32_t *rect_sorted, const int32_t *order, const int64_t *gpos,
+                            int row_lo, int row_hi, int canon, int live_layout,
+                            const GradDest &dst, cudaStream_t s) {
+    if (live_layout)
+        band_fold_kernel<true><<<blocks_for(m, BF_THREADS), BF_THREADS, 0, s>>>(
+            m, emit_off, partials, (const int4 *)rect_sorted, order, gpos, row_lo, row_hi, canon,
+            dst);
+    else
+        band_fold_kernel<false><<<blocks_for(m, BF_THREADS), BF_THREADS, 0, s>>>(
+            m, emit_off, partials, (const int4 *)rect_sorted, order, gpos, row_lo, row_hi, canon,
+            dst);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
 extern "C" int isg_band_fold(int64_t m, const int64_t *emit_off, const float *partials,
                              const int32_t *rect_sorted, const int32_t *order,
                              const int64_t *gpos, int32_t row_lo, int32_t row_hi,
                              int32_t canon_rows, int32_t live_layout, double *gbuf, void *stream) {
     if (m < 0 || canon_rows < 1) return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
-    if (live_layout)
-        band_fold_kernel<true><<<blocks_for(m, BF_THREADS), BF_THREADS, 0, (cudaStream_t)stream>>>(
-            m, emit_off, partials, (const int4 *)rect_sorted, order, gpos, row_lo, row_hi,
-            canon_rows, gbuf);
-    else
-        band_fold_kernel<false><<<blocks_for(m, BF_THREADS), BF_THREADS, 0,
-                                  (cudaStream_t)stream>>>(
-            m, emit_off, partials, (const int4 *)rect_sorted, order, gpos, row_lo, row_hi,
-            canon_rows, gbuf);
-    ISG_CHECK_LAUNCH();
-    return 0;
+    GradDest dst;
+    dst.base[0] = gbuf;
+    dst.recv_end[0] = INT64_MAX;
+    return launch_band_fold(m, emit_off, partials, rect_sorted, order, gpos, row_lo, row_hi,
+                            canon_rows, live_layout, dst, (cudaStream_t)stream);
+}
+
+extern "C" int isg_band_fold_peer(int64_t m, const int64_t *emit_off, const float *partials,
+                                  const int32_t *rect_sorted, const int32_t *order,
+                                  const int64_t *gpos, int32_t row_lo, int32_t row_hi,
+                                  int32_t canon_rows, int32_t live_layout, int32_t n_src,
+                                  const int64_t *recv_end, double *const *dst_base,
+                                  void *stream) {
+    if (m < 0 || canon_rows < 1 || n_src < 1 || n_src > MAX_BANDS || !recv_end || !dst_base)
+        return (int)cudaErrorInvalidValue;
+    if (m == 0) return 0;
+    if (recv_end[n_src - 1] < m) return (int)cudaErrorInvalidValue;
+    GradDest dst;
+    for (int s = 0; s < n_src; s++) {
+        dst.base[s] = dst_base[s];
+        dst.recv_end[s] = recv_end[s];
+    }
+    for (int s = n_src; s < MAX_BANDS; s++) dst.recv_end[s] = INT64_MAX;
+    return launch_band_fold(m, emit_off, partials, rect_sorted, order, gpos, row_lo, row_hi,
+                            canon_rows, live_layout, dst, (cudaStream_t)stream);
 }
 
 extern "C" int isg_band_cost(const int32_t *n_last, int32_t prow0, int32_t prow1, int32_t width,
@@ -750,4 +819,13 @@ extern "C" int isg_owner_fold(int64_t n_rows, const int32_t *seg_off, const int3
         n_rows, seg_off, perm, records, grad2d);
     ISG_CHECK_LAUNCH();
     return 0;
+}
+
+// Device-to-device copy on the stream; either side may be a peer GPU's
+// memory mapped into this process (the halo rows of the peer exchange).
+extern "C" int isg_copy(void *dst, const void *src, int64_t bytes, void *stream) {
+    if (bytes < 0 || (bytes > 0 && (!dst || !src))) return (int)cudaErrorInvalidValue;
+    if (bytes == 0) return 0;
+    return (int)cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                                (cudaStream_t)stream);
 }

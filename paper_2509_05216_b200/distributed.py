@@ -424,12 +424,16 @@ class TorchComm:
     """Collectives over a torch.distributed process group (NCCL on GPUs; gloo
     for the CPU tests of this layer)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, peers: bool = False, height: int = 0, width: int = 0,
+                 device=None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # peer-store exchange (PeerBuffers over symmetric memory) instead of
+        # point-to-point copies for the splat records, halo and gradients
+        self.peers = PeerBuffers(self.world, height, width, device, group) if peers else None
 
     def alltoallv(self, send: torch.Tensor, send_counts: list) -> tuple:
         """Rows of `send` (grouped by destination, counts per destination) ->
@@ -446,9 +450,12 @@ class TorchComm:
         return recv, recv_counts
 
     def counts(self, mine: torch.Tensor, out: torch.Tensor) -> None:
-        """(W, 3) per-destination counts -> out[s] = source s's row for this
-        rank (one all-to-all of 3 int64 per pair, on the device)."""
-        self.dist.all_to_all_single(out, mine.contiguous(), group=self.group)
+        """(W, 3) per-band counts of this shard -> out (W, W, 3), out[s] =
+        shard s's row (one all-gather of 3 int64 per pair, on the device):
+        every rank sees the whole count matrix, so every rank can place its
+        records directly in every other rank's buffers (peer exchange)."""
+        self.dist.all_gather_into_tensor(out.view(-1, *mine.shape[1:]), mine.contiguous(),
+                                         group=self.group)
 
     def exchange(self, ops: list) -> None:
         """Point-to-point segments: ops = [(peer, [send tensors], [recv
@@ -495,6 +502,130 @@ class TorchComm:
     def max_(self, t: torch.Tensor) -> torch.Tensor:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return t
+
+
+# ------------------------------------------------------- exchange layout --
+
+def exchange_layout(mat: np.ndarray, me: int) -> dict:
+    """Where every record of the iteration lives, from the all-gathered count
+    matrix mat (W, W, 3): mat[s, d] = shard s's (splat records, canonical
+    block records, tile entries) for band d.  Band d receives splat records
+    in source order, so shard me's segment starts at pack_at[d]; owner s
+    receives block records in band order, so band me's segment for owner s
+    starts at grad_at[s], and band b's segment of this rank's own receive
+    buffer at grad_seg[b].  need_r / need_g: the largest receive counts over
+    the ranks (the capacity of the peer buffers, the same on every rank)."""
+    mat = np.asarray(mat, dtype=np.int64)
+    rec, blk = mat[:, :, 0], mat[:, :, 1]
+    W = mat.shape[0]
+    return {
+        "pack_at": [int(rec[:me, d].sum()) for d in range(W)],
+        "grad_at": [int(blk[s, :me].sum()) for s in range(W)],
+        "grad_seg": [int(v) for v in np.concatenate([[0], np.cumsum(blk[me])])],
+        "need_r": int(rec.sum(axis=0).max()) if W else 0,
+        "need_g": int(blk.sum(axis=1).max()) if W else 0,
+    }
+
+
+class PeerBuffers:
+    """The peer-store exchange's receive buffers: every rank's
+    splat-record receive buffers (depth keys, 64-byte payloads), gradient
+    receive buffer and band image window live in torch symmetric memory, so
+    each rank maps every peer's buffers over NVLink and the producing kernels
+    store into them directly: the pack kernel writes each band's records into
+    that band's GPU (isg_route_pack_peer), the band fold writes each block
+    record into its owner's GPU (isg_band_fold_peer), the forward's boundary
+    rows go straight into the neighbours' windows.  A barrier (a signal-pad
+    kernel on the stream) follows each of the three; nothing is staged or
+    copied by NCCL.  The capacity is the max over the ranks of the receive
+    counts (exchange_layout), so every rank makes the same (collective)
+    growth decision."""
+
+    SLACK = 1.25
+
+    def __init__(self, world: int, height: int, width: int, device, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.symm = symm
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = world
+        self.H, self.W = height, width
+        self.dev = device
+        self.win = symm.empty(height * width * 3, dtype=torch.float32, device=device)
+        self.win.zero_()
+        self.win_h = symm.rendezvous(self.win, self.group)
+        self.win_ptrs = list(self.win_h.buffer_ptrs)
+        self.cap_r = self.cap_g = 0
+        self.buf = self.h = None
+        self.ptrs = [0] * world
+
+    def ensure(self, need_r: int, need_g: int) -> None:
+        if need_r <= self.cap_r and need_g <= self.cap_g and self.buf is not None:
+            return
+        cap_r = max(self.cap_r, int(need_r * self.SLACK) + 16)
+        cap_r += cap_r & 1                      # payloads 16-byte aligned
+        cap_g = max(self.cap_g, int(need_g * self.SLACK) + 16)
+        self.buf = self.h = None
+        self.buf = self.symm.empty(72 * cap_r + 72 * cap_g, dtype=torch.uint8, device=self.dev)
+        self.h = self.symm.rendezvous(self.buf, self.group)
+        self.ptrs = list(self.h.buffer_ptrs)
+        self.cap_r, self.cap_g = cap_r, cap_g
+
+    def bind(self, rs: "RankStep") -> None:
+        cr, cg = self.cap_r, self.cap_g
+        b = self.buf
+        rs.keys_recv = b[:8 * cr].view(torch.int64)
+        rs.pay_recv = b[8 * cr:72 * cr].view(torch.int32).view(cr, 16)
+        rs.grad_recv = b[72 * cr:72 * cr + 72 * cg].view(torch.float64).view(cg, 9)
+        rs.window = self.win.view(self.H, self.W, 3)
+
+    def keys_ptr(self, d: int) -> int:
+        return self.ptrs[d]
+
+    def pay_ptr(self, d: int) -> int:
+        return self.ptrs[d] + 8 * self.cap_r
+
+    def grad_ptr(self, d: int) -> int:
+        return self.ptrs[d] + 72 * self.cap_r
+
+    def window_ptr(self, d: int) -> int:
+        return self.win_ptrs[d]
+
+    def barrier(self) -> None:
+        self.win_h.barrier(channel=0)
+
+
+class EmulatedPeers:
+    """The same peer-store layout for W ranks held by one process on one GPU
+    (emulated_step): the 'peer' pointers are the other rank objects' own
+    buffers, and the phases run rank after rank, so no barrier is needed."""
+
+    def __init__(self, ranks: list):
+        self.ranks = ranks
+
+    def ensure(self, need_r: int, need_g: int) -> None:
+        for r in self.ranks:
+            r.keys_recv = _grow(r.keys_recv, need_r, dtype=torch.int64, device=r.dev)
+            r.pay_recv = _grow(r.pay_recv, need_r, (16,), dtype=torch.int32, device=r.dev)
+            r.grad_recv = _grow(r.grad_recv, need_g, (9,), dtype=torch.float64, device=r.dev)
+
+    def bind(self, rs: "RankStep") -> None:
+        pass
+
+    def keys_ptr(self, d: int) -> int:
+        return self.ranks[d].keys_recv.data_ptr()
+
+    def pay_ptr(self, d: int) -> int:
+        return self.ranks[d].pay_recv.data_ptr()
+
+    def grad_ptr(self, d: int) -> int:
+        return self.ranks[d].grad_recv.data_ptr()
+
+    def window_ptr(self, d: int) -> int:
+        return self.ranks[d].window.data_ptr()
+
+    def barrier(self) -> None:
+        pass
 
 
 # --------------------------------------------------------------- rank state --
@@ -550,9 +681,12 @@ class RankStep:
         pe = ctypes.c_int64(0)
         L.check(L.lib().isg_route_plan_size(n, world, ctypes.byref(pe)), "route plan size")
         self.plan = torch.empty(max(pe.value, 1), dtype=torch.int64, device=d)
-        # counts[0] = this shard's per-band totals, counts[1] = every source's for this band
-        self.counts = torch.zeros((2, world, 3), dtype=torch.int64, device=d)
-        self.counts_host = torch.zeros((2, world, 3), dtype=torch.int64).pin_memory()
+        # counts = this shard's per-band totals; cmat[s] = shard s's (all-gathered)
+        self.counts = torch.zeros((world, 3), dtype=torch.int64, device=d)
+        self.cmat = torch.zeros((world, world, 3), dtype=torch.int64, device=d)
+        self.cmat_host = torch.zeros((world, world, 3), dtype=torch.int64).pin_memory()
+        # peer-store exchange (PeerBuffers / EmulatedPeers) or None: point-to-point copies
+        self.peers = None
         # (M, E, live E) of the band's binning; only the live count is read (on the device)
         self.bin_counts = torch.zeros(3, dtype=torch.int64, device=d)
         nf = ctypes.c_int32(0)
@@ -630,20 +764,23 @@ class RankStep:
                                        ctypes.byref(out), s), "isg_preprocess")
         L.check(lib.isg_route_plan(self.n, L.ptr(self.flag), L.ptr(self.rect), self.band_host,
                                    self.world, self.part.canon_rows, L.ptr(self.plan),
-                                   L.ptr(self.counts[0]), s), "isg_route_plan")
-        return self.counts[0]
+                                   L.ptr(self.counts), s), "isg_route_plan")
+        return self.counts
 
     # -- the one host synchronisation --------------------------------------
     def phase_sizes(self) -> None:
-        """Read this shard's totals and every source's totals for this band
-        (counts[1], filled by the counts exchange) and size the iteration."""
-        self.counts_host.copy_(self.counts, non_blocking=True)
+        """Read the count matrix (cmat, filled by the counts all-gather) and
+        size the iteration."""
+        self.cmat_host.copy_(self.cmat, non_blocking=True)
         # the previous step's all-reduced band costs ride on the same sync
         self.cost_host.copy_(self.parts[self.n_ps + self.n_pl:], non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        h = self.counts_host.numpy()
-        mine, recv = h[0], h[1]
+        h = self.cmat_host.numpy()
         W, me = self.world, self.rank
+        mine, recv = h[me], h[:, me]
+        self.lay = exchange_layout(h, me)
+        if self.peers is not None:
+            self.peers.ensure(self.lay["need_r"], self.lay["need_g"])
         self.send_cnt = [int(x) for x in mine[:, 0]]
         self.recv_cnt = [int(x) for x in recv[:, 0]]
         self.gsend_cnt = [int(x) for x in recv[:, 1]]   # band -> owner s
@@ -664,6 +801,18 @@ class RankStep:
         Returns the exchange list [(peer, send tensors, recv tensors)]."""
         lib, s, d = L.lib(), L.stream_ptr(), self.dev
         me = self.rank
+        if self.peers is not None:
+            # peer-store exchange: each band's segment straight into its GPU
+            P, at, W = self.peers, self.lay["pack_at"], self.world
+            P.bind(self)
+            keys = (ctypes.c_void_p * W)(*[P.keys_ptr(k) + 8 * at[k] for k in range(W)])
+            pays = (ctypes.c_void_p * W)(*[P.pay_ptr(k) + 64 * at[k] for k in range(W)])
+            if self.n:
+                L.check(lib.isg_route_pack_peer(self.n, L.ptr(self.flag), L.ptr(self.rect),
+                                                L.ptr(self.key), L.ptr(self.feat), self.band_host,
+                                                W, L.ptr(self.plan), keys, pays, s),
+                        "isg_route_pack_peer")
+            return []
         R, S = self.R, int(self.send_off[-1])
         self.keys_recv = _grow(self.keys_recv, R, dtype=torch.int64, device=d)
         self.pay_recv = _grow(self.pay_recv, R, (16,), dtype=torch.int32, device=d)
@@ -817,8 +966,21 @@ class RankStep:
                 L.ptr(self.slot_rank), s), "isg_raster_fwd_masked")
         # boundary rows for the neighbours' SSIM halo
         b0, b1 = self.prow0 - self.win0, self.prow1 - self.win0
-        to_prev = self.window[b0:b0 + min(10, b1 - b0)] if self.rank > 0 else None
-        to_next = self.window[max(b0, b1 - 16):b1] if self.rank + 1 < self.world else None
+        n_prev = min(10, b1 - b0) if self.rank > 0 else 0
+        n_next = min(16, b1 - b0) if self.rank + 1 < self.world else 0
+        if self.peers is not None:
+            # straight into the neighbours' windows (their rows above / below their band)
+            row = self.W * 3 * 4
+            for nb, g0, cnt in ((self.rank - 1, self.prow0, n_prev),
+                                (self.rank + 1, self.prow1 - n_next, n_next)):
+                if cnt:
+                    w0 = max(0, self.part.pixel_rows(nb)[0] - 16)
+                    L.check(lib.isg_copy(self.peers.window_ptr(nb) + (g0 - w0) * row,
+                                         self.window.data_ptr() + (g0 - self.win0) * row,
+                                         cnt * row, s), "isg_copy")
+            return None, None
+        to_prev = self.window[b0:b0 + n_prev] if n_prev else None
+        to_next = self.window[b1 - n_next:b1] if n_next else None
         return to_prev, to_next
 
     def halo_shapes(self):
@@ -885,6 +1047,23 @@ class RankStep:
         _mark(timer, "raster_bwd")
         self.nb = _grow(self.nb, R, dtype=torch.int64, device=d)
         self.gpos = _grow(self.gpos, R + 1, dtype=torch.int64, device=d)
+        if self.peers is not None:
+            # peer-store exchange: each block record straight into its owner's GPU
+            P, at, W = self.peers, self.lay["grad_at"], self.world
+            if R:
+                L.check(lib.isg_band_blocks(R, L.ptr(self.pay_recv), self.trow0, self.trow1,
+                                            self.part.canon_rows, L.ptr(self.nb), s),
+                        "band blocks")
+                _scan_i64(self, R, self.nb, self.gpos)
+                ends = (ctypes.c_int64 * W)(*[int(v) for v in self.recv_off[1:]])
+                bases = (ctypes.c_void_p * W)(*[
+                    P.grad_ptr(k) + 72 * (at[k] - int(self.gpos_off[k])) for k in range(W)])
+                L.check(lib.isg_band_fold_peer(R, L.ptr(self.live_off), L.ptr(self.partials),
+                                               L.ptr(self.rect_sorted), L.ptr(self.order),
+                                               L.ptr(self.gpos), self.trow0, self.trow1,
+                                               self.part.canon_rows, 1, W, ends, bases, s),
+                        "isg_band_fold_peer")
+            return []
         self.gbuf = _grow(self.gbuf, self.NR, (9,), dtype=torch.float64, device=d)
         if R:
             L.check(lib.isg_band_blocks(R, L.ptr(self.pay_recv), self.trow0, self.trow1,
@@ -946,7 +1125,9 @@ class RankStep:
         me = self.rank
         segs = []
         for b in range(self.world):
-            if b == me:
+            if self.peers is not None:
+                segs.append(self.grad_recv.data_ptr() + 72 * self.lay["grad_seg"][b])
+            elif b == me:
                 segs.append(self.gbuf.data_ptr() + 72 * int(self.gpos_off[me]))
             else:
                 segs.append(self.grad_recv.data_ptr() + 72 * int(self.grecv_off[b]))
@@ -1152,20 +1333,25 @@ def comm_step(rs: RankStep, comm: TorchComm, cam, gt: torch.Tensor, it: int,
     host synchronisation (phase_sizes).  timer: optional engine.PhaseTimer
     (CUDA events between the phases)."""
     from .engine import _mark
+    P = rs.peers = comm.peers
     _mark(timer, "begin")
     mine = rs.phase_plan(cam)
     _mark(timer, "project_plan")
-    comm.counts(mine, rs.counts[1])
+    comm.counts(mine, rs.cmat)
     rs.phase_sizes()
     _mark(timer, "counts_sync")
     ops = rs.phase_pack()
     _mark(timer, "pack")
-    comm.exchange(ops)
+    P.barrier() if P is not None else comm.exchange(ops)
     _mark(timer, "exchange_splats")
     to_prev, to_next = rs.phase_render()
     _mark(timer, "bin_render")
-    sp, sn = rs.halo_shapes()
-    got_prev, got_next = comm.halo(to_prev, to_next, sp, sn, torch.float32, rs.dev)
+    if P is not None:
+        P.barrier()
+        got_prev = got_next = None
+    else:
+        sp, sn = rs.halo_shapes()
+        got_prev, got_next = comm.halo(to_prev, to_next, sp, sn, torch.float32, rs.dev)
     _mark(timer, "halo")
     parts = rs.phase_loss(got_prev, got_next, gt)
     comm.allreduce_sum_(parts)
@@ -1173,7 +1359,7 @@ def comm_step(rs: RankStep, comm: TorchComm, cam, gt: torch.Tensor, it: int,
     _mark(timer, "loss_allreduce")
     gops = rs.phase_backward(timer)
     _mark(timer, "band_fold")
-    comm.exchange(gops)
+    P.barrier() if P is not None else comm.exchange(gops)
     _mark(timer, "exchange_grads")
     rs.phase_update(it)
     _mark(timer, "owner_fold_chain_adam")
@@ -1185,9 +1371,11 @@ def comm_pair_counts(rs: RankStep, comm: TorchComm, cam) -> dict:
     """Roofline units of this rank's band for view `cam`: pairs
     iterated (I_f), contributing (C) and the backward's I_b (sum of the
     last-contributor index) over the reference's full lists; no state change."""
-    comm.counts(rs.phase_plan(cam), rs.counts[1])
+    P = rs.peers = comm.peers
+    comm.counts(rs.phase_plan(cam), rs.cmat)
     rs.phase_sizes()
-    comm.exchange(rs.phase_pack())
+    ops = rs.phase_pack()
+    P.barrier() if P is not None else comm.exchange(ops)
     rs.phase_render(count=True)
     return _band_pair_counts(rs)
 
@@ -1249,21 +1437,25 @@ def _emulated_exchange(ranks: list, ops: list) -> None:
 
 
 def emulated_step(ranks: list, cam, gt: torch.Tensor, it: int, timers=None,
-                  count: bool = False):
+                  count: bool = False, peers: bool = False):
     """The same phases for W ranks executed in sequence on ONE GPU with the
     exchanges done by in-process copies (no kernel waits on another rank).
     Used to check bitwise W-invariance on a single B200.  timers: optional
     per-rank SpanTimer list (each rank's device time per phase, i.e. what
     its own GPU would spend outside the exchanges).  count=True: stop after
-    the forward with the pair counters (returns the per-rank counts)."""
+    the forward with the pair counters (returns the per-rank counts).
+    peers=True: the peer-store exchange (EmulatedPeers) -- the pack, halo and
+    band-fold kernels store straight into the other ranks' buffers."""
     W = len(ranks)
     tm = timers or [_NoSpan()] * W
+    P = EmulatedPeers(ranks) if peers else None
     for r, t in zip(ranks, tm):
+        r.peers = P
         with t.span("project_plan"):
             r.phase_plan(cam)
     for dst in range(W):
         for src in range(W):
-            ranks[dst].counts[1, src].copy_(ranks[src].counts[0, dst])
+            ranks[dst].cmat[src].copy_(ranks[src].counts)
     for r in ranks:
         r.phase_sizes()
     ops = []
@@ -1278,8 +1470,8 @@ def emulated_step(ranks: list, cam, gt: torch.Tensor, it: int, timers=None,
     if count:
         return [_band_pair_counts(r) for r in ranks]
     for i, (r, t) in enumerate(zip(ranks, tm)):
-        got_prev = bounds[i - 1][1] if i > 0 else None
-        got_next = bounds[i + 1][0] if i + 1 < W else None
+        got_prev = bounds[i - 1][1] if i > 0 and P is None else None
+        got_next = bounds[i + 1][0] if i + 1 < W and P is None else None
         with t.span("loss"):
             r.phase_loss(got_prev, got_next, gt)
     total = torch.zeros_like(ranks[0].parts)

@@ -141,9 +141,10 @@ def _worker(rank, world, port, q):
         ok_red = torch.equal(parts, ref)
         # per-destination counts (3 int64 per pair) and point-to-point segments
         mine = torch.tensor([[10 * rank + d, rank, d] for d in range(world)], dtype=torch.int64)
-        got = torch.empty_like(mine)
+        got = torch.empty((world, world, 3), dtype=torch.int64)
         comm.counts(mine, got)
-        ok_counts = torch.equal(got, torch.tensor([[10 * s + rank, s, rank] for s in range(world)]))
+        ok_counts = torch.equal(got, torch.tensor(
+            [[[10 * s + d, s, d] for d in range(world)] for s in range(world)]))
         peer = 1 - rank
         keys = torch.arange(5, dtype=torch.int64) + 100 * rank
         pay = torch.full((5, 16), rank, dtype=torch.int32)
@@ -301,3 +302,30 @@ def test_route_splats_matches_reference():
         want = [w for w in range(2) if y0 < bands.band_rows[w + 1] and y1 >= bands.band_rows[w]]
         got = [w for w in range(2) if any(t is s for t in lists[w])]
         assert got == want
+
+
+def test_exchange_layout_places_every_segment_once():
+    """The peer-store exchange writes each shard's records straight into the
+    destination band's buffer at exchange_layout(...)["pack_at"], and each
+    band's block records into the owner's buffer at ["grad_at"]: those must be
+    exactly the segment starts the receiving side reads (source order for
+    splat records, band order for gradient records), every rank computing
+    them from the same all-gathered matrix, and the capacities must cover
+    every rank's receive totals."""
+    rng = np.random.default_rng(5)
+    for W in (1, 2, 3, 8):
+        mat = rng.integers(0, 50, size=(W, W, 3)).astype(np.int64)
+        mat[rng.random((W, W)) < 0.3] = 0
+        lays = [D.exchange_layout(mat, r) for r in range(W)]
+        for d in range(W):
+            recv = mat[:, d, 0]
+            starts = np.concatenate([[0], np.cumsum(recv)])
+            for s_ in range(W):
+                assert lays[s_]["pack_at"][d] == starts[s_]
+            assert starts[-1] <= lays[d]["need_r"]
+        for s_ in range(W):
+            # owner s receives band b's records at grad_seg[b]; band b writes at grad_at[s]
+            for b in range(W):
+                assert lays[b]["grad_at"][s_] == lays[s_]["grad_seg"][b]
+            assert lays[s_]["grad_seg"][-1] == mat[s_, :, 1].sum() <= lays[s_]["need_g"]
+        assert len({(l["need_r"], l["need_g"]) for l in lays}) == 1

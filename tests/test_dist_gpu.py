@@ -42,7 +42,7 @@ def _run_single(P, cams, gt, cloud, iters, canon):
     return tr.loss_dev[1:iters + 1].tolist(), tr.cloud
 
 
-def _run_emulated(P, cams, gt, cloud, iters, canon, workers, total=None):
+def _run_emulated(P, cams, gt, cloud, iters, canon, workers, total=None, peers=False):
     from paper_2509_05216_b200 import distributed as D
     cfg = P.TrainConfig(iterations=total or iters, densify=False)
     ranks, smap, part = D.make_ranks(cloud.copy(), cams[0].width, cams[0].height, cfg, _extent(cams),
@@ -50,18 +50,21 @@ def _run_emulated(P, cams, gt, cloud, iters, canon, workers, total=None):
     sched = P.build_schedule(total or iters, len(cams), 0)
     losses = []
     for it in range(1, iters + 1):
-        loss = D.emulated_step(ranks, cams[sched[it - 1]], gt[sched[it - 1]], it)
+        loss = D.emulated_step(ranks, cams[sched[it - 1]], gt[sched[it - 1]], it, peers=peers)
         losses.append(float(loss[0]))
     torch.cuda.synchronize()
     return losses, D.gather_cloud(ranks), part
 
 
+@pytest.mark.parametrize("peers", [False, True], ids=["p2p_copies", "peer_stores"])
 @pytest.mark.parametrize("workers", [1, 2, 3, 4])
-def test_sharded_step_bitwise_equals_single_gpu(workers):
+def test_sharded_step_bitwise_equals_single_gpu(workers, peers):
+    """peer_stores: the pack, forward-halo and band-fold kernels write straight
+    into the other ranks' buffers (the peer-store exchange's layout)."""
     P, d, cams, gt, cloud = _setup()
     iters, canon = 4, 1
     ref_losses, ref_cloud = _run_single(P, cams, gt, cloud, iters, canon)
-    losses, got, part = _run_emulated(P, cams, gt, cloud, iters, canon, workers)
+    losses, got, part = _run_emulated(P, cams, gt, cloud, iters, canon, workers, peers=peers)
     assert len(part.band_rows) == workers + 1
     assert losses == ref_losses, (losses, ref_losses)
     for k in P.PARAM_NAMES:
@@ -93,8 +96,9 @@ def _run_single_densify(P, cams, gt, cloud, iters, canon, cfg):
     return tr.loss_dev[1:iters + 1].tolist(), tr.cloud
 
 
+@pytest.mark.parametrize("peers", [False, True], ids=["p2p_copies", "peer_stores"])
 @pytest.mark.parametrize("workers", [2, 3])
-def test_sharded_densify_bitwise_equals_single_gpu(workers):
+def test_sharded_densify_bitwise_equals_single_gpu(workers, peers):
     """Densify + rebalance inside the sharded engine (emulated ranks) keeps
     the run bitwise equal to the single-GPU engine across the event."""
     from paper_2509_05216_b200 import distributed as D
@@ -109,7 +113,7 @@ def test_sharded_densify_bitwise_equals_single_gpu(workers):
     sched = P.build_schedule(iters, len(cams), 0)
     losses = []
     for it in range(1, iters + 1):
-        loss = D.emulated_step(ranks, cams[sched[it - 1]], gt[sched[it - 1]], it)
+        loss = D.emulated_step(ranks, cams[sched[it - 1]], gt[sched[it - 1]], it, peers=peers)
         losses.append(float(loss[0]))
         if D.densify_due(cfg, it):
             ranks = D.emulated_densify(ranks, it)

@@ -70,9 +70,13 @@ def _workload(name):
     return _CACHE[name]
 
 
-@pytest.mark.parametrize("name", ["config2", "config3"])
-@pytest.mark.parametrize("workers", [2, 4, 8])
-def test_sharded_run_bitwise_equals_single_gpu_at_scale(name, workers):
+@pytest.mark.parametrize("name,workers,peers", [
+    ("config2", 2, False), ("config2", 4, False), ("config2", 8, False),
+    ("config3", 2, False), ("config3", 4, False), ("config3", 8, False),
+    ("config2", 8, True), ("config3", 4, True), ("config3", 8, True)])
+def test_sharded_run_bitwise_equals_single_gpu_at_scale(name, workers, peers):
+    """peers: the peer-store exchange (pack / halo / band fold store straight
+    into the other ranks' buffers)."""
     from paper_2509_05216_b200 import distributed as D
     P, wl, sched, ext, cloud0, ref, cfg = _workload(name)
     ranks, smap, part = D.make_ranks(cloud0.copy(), wl.resolution, wl.resolution, cfg, ext,
@@ -80,7 +84,8 @@ def test_sharded_run_bitwise_equals_single_gpu_at_scale(name, workers):
     assert part.canon_rows == D.CANON_ROWS
     losses = []
     for it in range(1, ITERS + 1):
-        loss = D.emulated_step(ranks, wl.cameras[sched[it - 1]], wl.images_u8[it - 1], it)
+        loss = D.emulated_step(ranks, wl.cameras[sched[it - 1]], wl.images_u8[it - 1], it,
+                               peers=peers)
         losses.append(float(loss[0]))
         if D.densify_due(cfg, it):
             ranks = D.emulated_densify(ranks, it)
