@@ -427,7 +427,8 @@ int isg_band_fold_peer(int64_t m, const int64_t *emit_off, const float *partials
                        void *stream);
 
 /* Device-to-device copy of `bytes` on `stream` (either side may be a peer
- * GPU's memory mapped into this process): the halo rows of the peer exchange. */
+ * GPU's memory mapped into this process): the halo rows of the peer exchange,
+ * which replace the reference's full-canvas `frag` exchange (engine.py:229-237). */
 int isg_copy(void *dst, const void *src, int64_t bytes, void *stream);
 
 /* Band raster cost per canonical block (load balance of the row bands):
