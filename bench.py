@@ -658,6 +658,7 @@ def step_parity(wl, v, cfg, scene_extent, pre, post, oloss, det):
         dev = wl.images_u8.device
         cloud = P.cloud_from_points(wl.points, wl.log_scales, 1, dev)
         tr = Trainer(cloud, wl.resolution, wl.resolution, cfg, scene_extent, dev)
+        tr.r.keep_grads = True  # the parameter gradients, for the comparison below
         tr.step(1, wl.cameras[v], wl.images_u8[v])
         torch.cuda.synchronize()
         PN = P.PARAM_NAMES

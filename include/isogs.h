@@ -522,6 +522,26 @@ int isg_chain_fold_train(const isg_params *p, const isg_camera *cam, const int32
                          float *d_sh, int64_t *seen, double *grad_accum, double half_w,
                          double half_h, void *stream);
 
+/* The whole per-Gaussian tail of a training step in one pass: the live fold
+ * and chain rule of isg_chain_fold_train, TrainStats, then the dense Adam
+ * update of every row's 23 parameters (isg_adam_groups' arithmetic, bit for
+ * bit: engine.py:508-536, optim.py:20-56) without the parameter gradients
+ * leaving registers.  grads_out: NULL, or 5 float32 arrays (PARAM_NAMES order)
+ * that also receive the gradients; lr5 HOST, PARAM_NAMES order. */
+int isg_chain_fold_adam(const isg_train_state *s, const isg_camera *cam, const int32_t *rank_of,
+                        const int64_t *live_off, const float *partials, const int32_t *rect_sorted,
+                        int32_t row_lo, int32_t row_hi, int32_t canon_rows, double *grad2d_out,
+                        float *const *grads_out, const float *lr5, const isg_adam_consts *c,
+                        double half_w, double half_h, void *stream);
+
+/* The same single pass from row-ordered 2-D gradients (rows with flag set;
+ * the sharded step's owner fold, isg_owner_fold_plan): float32 chain rule +
+ * TrainStats + dense Adam, the gradients kept in registers (grads_out
+ * optional as above).  The float32 training counterpart of isg_chain_adam. */
+int isg_chain_adam_train(const isg_train_state *s, const isg_camera *cam, const uint8_t *flag,
+                         const double *grad2d, float *const *grads_out, const float *lr5,
+                         const isg_adam_consts *c, double half_w, double half_h, void *stream);
+
 /* ... then dense float32 Adam over up to 8 groups in one launch (arrays of
  * `count` host-side pointers / sizes / learning rates; constants as for
  * isg_adam).  Bit-identical to isg_adam per element. */

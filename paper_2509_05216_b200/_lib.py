@@ -131,6 +131,11 @@ SIGNATURES = {
     "isg_adam": [_I32, _I64, _P, _P, _P, _P, ctypes.POINTER(AdamConsts_t), _P],
     "isg_chain_adam": [ctypes.POINTER(TrainState_t), ctypes.POINTER(Camera_t), _P, _P, _P,
                        ctypes.POINTER(AdamConsts_t), _D, _D, _P],
+    "isg_chain_fold_adam": [ctypes.POINTER(TrainState_t), ctypes.POINTER(Camera_t), _P, _P, _P,
+                            _P, _I32, _I32, _I32, _P, _P, _P, ctypes.POINTER(AdamConsts_t), _D,
+                            _D, _P],
+    "isg_chain_adam_train": [ctypes.POINTER(TrainState_t), ctypes.POINTER(Camera_t), _P, _P, _P,
+                             _P, ctypes.POINTER(AdamConsts_t), _D, _D, _P],
     "isg_chain_train": [ctypes.POINTER(Params_t), ctypes.POINTER(Camera_t), _P, _P, _P, _P, _P,
                         _P, _P, _P, _P, _D, _D, _P],
     "isg_chain_train_ranked": [ctypes.POINTER(Params_t), ctypes.POINTER(Camera_t), _P, _P, _P,

@@ -8,6 +8,7 @@
 // ~450 for the chain) stays well under the B200's FP64 rate.
 #include <math.h>
 
+#include "adam.cuh"
 #include "common.cuh"
 
 namespace isg {
@@ -288,26 +289,6 @@ __global__ void __launch_bounds__(256) chain_kernel(isg_params p, Cam cam, const
     }
 }
 
-struct AdamF {
-    float b1, omb1, b2, omb2, bc1, bc2, eps;
-};
-
-// optim.py:49-55 in float32 with numpy's operation order (no FMA).
-__device__ __forceinline__ void adam_f32(float &p, float &m, float &v, float g, float lr,
-                                         const AdamF &c) {
-    float mi = m * c.b1;
-    mi = mi + c.omb1 * g;
-    float vi = v * c.b2;
-    float gg = g * g;
-    vi = vi + c.omb2 * gg;
-    float mhat = mi / c.bc1;
-    float vhat = vi / c.bc2;
-    float den = sqrtf(vhat) + c.eps;
-    float step = (lr * mhat) / den;
-    p = p - step;
-    m = mi;
-    v = vi;
-}
 
 // Fused: chain (flagged rows) + TrainStats (engine.py:508-515) + dense Adam
 // over the five groups (engine.py:524-536, optim.py:20-56).  K3 = 3 (SH
@@ -585,6 +566,68 @@ void launch_chain_fold_train_f32(const isg_params &p, const Cam &cam, const int3
                                  double *grad2d_out, float *dpos, float *dls, float *drot,
                                  float *dlogit, float *dsh, int64_t *seen, double *grad_accum,
                                  double half_w, double half_h, cudaStream_t s);
+}
+
+namespace isg {
+void launch_chain_fold_adam_f32(const isg_train_state &st, const Cam &cam, const uint8_t *flag,
+                                const double *grad2d, const int32_t *rank_of,
+                                const int64_t *live_off, const float *partials,
+                                const int32_t *rect_sorted, int row_lo, int row_hi, int canon,
+                                double *grad2d_out, float *const *grads_out, const float *lr5,
+                                const isg_adam_consts &ac, double half_w, double half_h,
+                                cudaStream_t s);
+}
+
+// The fused Adam updates each CTA's rows with 16-byte accesses.
+static bool state_aligned16(const isg_train_state &s) {
+    const void *ptrs[15] = {s.positions,   s.log_scales,       s.rotations,     s.opacity_logits,
+                            s.sh,          s.m_positions,      s.m_log_scales,  s.m_rotations,
+                            s.m_opacity_logits, s.m_sh,        s.v_positions,   s.v_log_scales,
+                            s.v_rotations, s.v_opacity_logits, s.v_sh};
+    for (const void *q : ptrs)
+        if (!q || (reinterpret_cast<uintptr_t>(q) & 15) != 0) return false;
+    return true;
+}
+
+extern "C" int isg_chain_fold_adam(const isg_train_state *st, const isg_camera *cam,
+                                   const int32_t *rank_of, const int64_t *live_off,
+                                   const float *partials, const int32_t *rect_sorted,
+                                   int32_t row_lo, int32_t row_hi, int32_t canon_rows,
+                                   double *grad2d_out, float *const *grads_out, const float *lr5,
+                                   const isg_adam_consts *c, double half_w, double half_h,
+                                   void *stream) {
+    if (!st || !cam || !rank_of || !live_off || !partials || !rect_sorted || canon_rows < 1 ||
+        st->n < 0 || !lr5 || !c)
+        return (int)cudaErrorInvalidValue;
+    if (grads_out)
+        for (int k = 0; k < 5; k++)
+            if (!grads_out[k]) return (int)cudaErrorInvalidValue;
+    if (!state_aligned16(*st)) return (int)cudaErrorInvalidValue;
+    if (st->n == 0) return 0;
+    launch_chain_fold_adam_f32(*st, to_cam(*cam), nullptr, nullptr, rank_of, live_off, partials,
+                               rect_sorted, row_lo, row_hi, canon_rows, grad2d_out, grads_out, lr5,
+                               *c, half_w, half_h, (cudaStream_t)stream);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_chain_adam_train(const isg_train_state *st, const isg_camera *cam,
+                                    const uint8_t *flag, const double *grad2d,
+                                    float *const *grads_out, const float *lr5,
+                                    const isg_adam_consts *c, double half_w, double half_h,
+                                    void *stream) {
+    if (!st || !cam || !flag || !grad2d || st->n < 0 || !lr5 || !c)
+        return (int)cudaErrorInvalidValue;
+    if (grads_out)
+        for (int k = 0; k < 5; k++)
+            if (!grads_out[k]) return (int)cudaErrorInvalidValue;
+    if (!state_aligned16(*st)) return (int)cudaErrorInvalidValue;
+    if (st->n == 0) return 0;
+    launch_chain_fold_adam_f32(*st, to_cam(*cam), flag, grad2d, nullptr, nullptr, nullptr, nullptr,
+                               0, 0, 1, nullptr, grads_out, lr5, *c, half_w, half_h,
+                               (cudaStream_t)stream);
+    ISG_CHECK_LAUNCH();
+    return 0;
 }
 
 extern "C" int isg_chain_fold_train(const isg_params *p, const isg_camera *cam,

@@ -129,6 +129,7 @@ class Rasterizer:
         # (ranked grads only); keep_grad2d also stores the 2-D gradients
         self.fuse_fold = os.environ.get("ISOGS_FUSE_FOLD", "1") != "0"
         self.keep_grad2d = False
+        self.keep_grads = False  # store the parameter gradients (fused Adam)
         self.partials = None
         self.to_keys = self.to_vals = self.to_keys_s = self.to_order = None
         self.tile_order = None
@@ -343,6 +344,12 @@ class Rasterizer:
 # Tiles whose list is at least HEAVY_PCT % of the mean length launch first
 # (longest first); the rest keep row-major order (0: all by length).
 HEAVY_PCT = int(os.environ.get("ISOGS_HEAVY_PCT", "0"))
+# chain rule + stats + Adam in one pass (the gradients stay in registers;
+# isg_chain_fold_adam).  Off by default: measured slower at config 3 (1.14 ms
+# against 0.63 + 0.39 ms for the fold-chain and the dense Adam launches) --
+# the fused kernel's register footprint costs the latency-bound fold more
+# occupancy than the 0.74 GB of gradient traffic it saves.
+FUSE_ADAM = os.environ.get("ISOGS_FUSE_ADAM", "0") != "0"
 # exact longest-first order (a 16-bit radix sort of the lengths; default) or
 # the one-launch bucketed order (isg_tile_order, 1024 linear buckets): the
 # same raster times and 0.04 ms less GPU time, but config 2 measured 412 ->
@@ -428,12 +435,14 @@ def chunk_items(st, n_tiles: int) -> None:
 
 def update_params(cloud: GaussianCloud, m: dict, v: dict, grads: dict, seen, grad_accum, flag,
                   grad2d, cam_struct, lrs: list, it: int, width: int, height: int,
-                  timer=None, rank_of=None, fold=None) -> None:
+                  timer=None, rank_of=None, fold=None, keep_grads: bool = False) -> None:
     """Chain rule + TrainStats (isg_chain_train), then dense Adam over the five
     groups in one launch (isg_adam_groups): engine.py:508-536, optim.py:20-56.
     fold: the Rasterizer whose live subtotals the chain folds itself
     (isg_chain_fold_train; grad2d then only receives the 2-D gradients when
-    fold.keep_grad2d)."""
+    fold.keep_grad2d).  FUSE_ADAM: the chain and Adam in one pass
+    (isg_chain_fold_adam / isg_chain_adam_train); the parameter gradients are
+    then only stored when asked for (fold.keep_grads / keep_grad2d, keep_grads)."""
     lib = L.lib()
     s = L.stream_ptr()
     p = L.Params_t()
@@ -441,6 +450,33 @@ def update_params(cloud: GaussianCloud, m: dict, v: dict, grads: dict, seen, gra
     p.rotations, p.opacity_logits = L.ptr(cloud.rotations), L.ptr(cloud.opacity_logits)
     p.sh, p.n, p.degree, p.dtype = L.ptr(cloud.sh_coeffs), cloud.count, cloud.degree, L.ISG_F32
     if cloud.count == 0:
+        return
+    if FUSE_ADAM and (fold is not None or rank_of is None):
+        # one pass: (fold +) chain + stats + Adam, gradients kept in registers
+        st = L.TrainState_t()
+        for k, f in zip(PARAM_NAMES, ("positions", "log_scales", "rotations", "opacity_logits",
+                                      "sh")):
+            setattr(st, f, L.ptr(getattr(cloud, k)))
+            setattr(st, "m_" + f, L.ptr(m[k]))
+            setattr(st, "v_" + f, L.ptr(v[k]))
+        st.seen, st.grad_accum = L.ptr(seen), L.ptr(grad_accum)
+        st.n, st.degree = cloud.count, cloud.degree
+        keep = fold.keep_grad2d or fold.keep_grads if fold is not None else keep_grads
+        go = (ctypes.c_void_p * 5)(*(L.ptr(grads[k]) for k in PARAM_NAMES)) if keep else None
+        ll = (ctypes.c_float * 5)(*(float(np.float32(x)) for x in lrs))
+        c = adam_consts(torch.float32, it, 0.0)
+        if fold is not None:
+            L.check(lib.isg_chain_fold_adam(
+                ctypes.byref(st), ctypes.byref(cam_struct), L.ptr(rank_of), L.ptr(fold.live_off),
+                L.ptr(fold.partials), L.ptr(fold.rect_sorted), 0, fold.tiles_y, fold.canon_rows,
+                L.ptr(grad2d) if fold.keep_grad2d else None, go, ll, ctypes.byref(c),
+                0.5 * width, 0.5 * height, s), "isg_chain_fold_adam")
+        else:
+            L.check(lib.isg_chain_adam_train(
+                ctypes.byref(st), ctypes.byref(cam_struct), L.ptr(flag), L.ptr(grad2d), go, ll,
+                ctypes.byref(c), 0.5 * width, 0.5 * height, s), "isg_chain_adam_train")
+        _mark(timer, "chain")
+        _mark(timer, "adam")
         return
     if fold is not None:
         L.check(lib.isg_chain_fold_train(

@@ -224,3 +224,41 @@ def test_culled_lists_are_ordered_sublists_of_the_full_lists():
     want = np.empty(live_slots, dtype=np.int64)
     want[slots] = tile_of // tiles_x
     assert np.array_equal(rows, want)
+
+
+@pytest.mark.parametrize("densify", [False, True])
+def test_fused_chain_adam_is_bitwise_the_separate_launches(densify):
+    """isg_chain_fold_adam (fold + chain + stats + Adam in one pass, gradients
+    kept in registers) == isg_chain_fold_train + isg_adam_groups: parameters,
+    moments and statistics bitwise after 6 iterations (with a densify event,
+    which reads the statistics)."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200 import engine as E
+    from paper_2509_05216_b200.engine import Trainer
+    d = load("config1")
+    ds = _dataset(d, "images_u8", d["images_u8"].shape[0])
+    cfg = P.TrainConfig(iterations=6, densify=densify, densify_start=2, densify_interval=2,
+                        densify_stop=5, seed=0)
+    gt = _images(ds)
+    sched = P.build_schedule(6, ds.view_count, 0)
+    runs = []
+    saved = E.FUSE_ADAM
+    try:
+        for fused in (True, False):
+            E.FUSE_ADAM = fused
+            t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
+            for it in range(1, 7):
+                t.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
+                if t.densify_due(it):
+                    t.densify(it)
+            torch.cuda.synchronize()
+            runs.append(t)
+    finally:
+        E.FUSE_ADAM = saved
+    a, b = runs
+    assert torch.equal(a.loss_dev, b.loss_dev)
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(a.cloud, k), getattr(b.cloud, k)), k
+        assert torch.equal(a.m[k], b.m[k]) and torch.equal(a.v[k], b.v[k]), k
+    assert torch.equal(a.stats.seen, b.stats.seen)
+    assert torch.equal(a.stats.grad_accum, b.stats.grad_accum)
