@@ -738,7 +738,14 @@ def run_dist(args, world: int, rank: int, local: int):
     wl = S.make_workload(args.config, dev, log=say, resolution=args.res)
     n = wl.points.shape[0]
     res = wl.resolution
-    comm = D.TorchComm(peers=args.exchange == "peer", height=res, width=res, device=dev)
+    exchange = args.exchange
+    try:
+        comm = D.TorchComm(peers=exchange == "peer", height=res, width=res, device=dev)
+    except Exception as exc:  # no symmetric memory / peer mapping on this box
+        say(f"[dist] peer-store exchange unavailable ({type(exc).__name__}: {exc}); "
+            "using point-to-point NCCL copies")
+        exchange = f"nccl (peer unavailable: {type(exc).__name__})"
+        comm = D.TorchComm(peers=False)
     cloud = cloud_from_points(wl.points, wl.log_scales, 1, dev)
     iters = args.warmup + args.steps
     cfg = TrainConfig(iterations=total_iterations(args), densify=False, eval_interval=0)
@@ -834,7 +841,7 @@ def run_dist(args, world: int, rank: int, local: int):
                     "h2d_bytes_per_step": int(gt.numel()), "d2h_bytes_per_step": 8},
             "clocks": clk.summary(), "gpu_launches": D.LAUNCHES_PER_STEP * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "parity": parity,
-            "exchange": args.exchange,
+            "exchange": exchange,
             "partition": {"bands_tile_rows": rs.part.band_rows, "initial": part.band_rows,
                           "canon_rows": part.canon_rows, "shard_sizes": smap.sizes,
                           "balance": rs.balance},
