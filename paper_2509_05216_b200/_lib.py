@@ -196,7 +196,9 @@ def ptr(t: torch.Tensor | None) -> int | None:
 
 
 def stream_ptr() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    # the current stream's raw handle straight from the C++ side (a
+    # torch.cuda.current_stream() object costs ~15 us of Python per call)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def dtype_tag(dt: torch.dtype) -> int:

@@ -669,6 +669,7 @@ class RankStep:
         self.grad_accum = torch.zeros(self.n, dtype=torch.float64, device=device)
         self.W, self.H = part.width, part.height
         self.tiles_x = part.tiles_x
+        self.image_tiles = part.tiles_x * part.tiles_y  # the chunk policy: per image, not band
         self.bg = (ctypes.c_double * 3)(*[float(v) for v in background])
         d = device
         n = self.n

@@ -108,6 +108,7 @@ class Rasterizer:
         self.tiles_x = (width + TILE - 1) // TILE
         self.tiles_y = (height + TILE - 1) // TILE
         self.n_tiles = self.tiles_x * self.tiles_y
+        self.image_tiles = self.n_tiles  # (the chunk policy's input)
         self.tile_bits = max(1, int(self.n_tiles - 1).bit_length())
         self.bg = (ctypes.c_double * 3)(*[float(v) for v in background])
         self.feat_dtype = feat_dtype
@@ -134,7 +135,7 @@ class Rasterizer:
         self.to_keys = self.to_vals = self.to_keys_s = self.to_order = None
         self.tile_order = None
         self.chunks = None
-        self.chunk = CHUNK  # backward entries per work item (0: one CTA per tile)
+        self.chunk = CHUNK  # backward entries per work item (0: one CTA per tile; None: auto)
         # launch the raster pair heaviest tile lists first (ISOGS_HEAVY_FIRST=0: list order)
         self.heavy_first = os.environ.get("ISOGS_HEAVY_FIRST", "1") != "0"
         # float32: forward contribution masks drive the backward (ISOGS_CMASK=0: A/B off)
@@ -394,7 +395,30 @@ def heavy_first_order(st, n_tiles: int, offsets: torch.Tensor):
 # occupancy); a variant that keeps one CTA per tile and restarts it at the
 # chunk boundaries (same arithmetic as split chunks, so the split could follow
 # the launch size) costs 3.78 -> 4.62 ms at config 3.  Off by default.
-CHUNK = int(os.environ.get("ISOGS_CHUNK", "0"))
+# Backward list chunking: ISOGS_CHUNK=<entries> forces a chunk size (0: off).
+# By default (auto) the chunk follows the IMAGE's tile count, never the
+# launch's: images of few tiles (config 2: 4096 tiles, about 2 waves of
+# backward CTAs, where one CTA per tile leaves the heaviest lists running
+# alone at the end) are chunked, larger ones (2048^2) are not.  A function of
+# the workload only, so every row band of every GPU count cuts the same
+# chunks as one GPU and the sharded step stays bitwise equal to it (chunk
+# restarts round differently from an unbroken walk).  Measured: config 2
+# 416 -> 458 images/s at 1024; config 3 116.8 -> 107.1 (the chunked
+# instantiation rematerialises lane indices under register pressure: +3.5 %
+# instructions, 12 vs 14 CTAs/SM); emulated W = 8 config-3 bands would gain
+# 410 -> 438 with per-band chunking, at the cost of that bitwise equality.
+_ck = os.environ.get("ISOGS_CHUNK", "auto")
+CHUNK = None if _ck == "auto" else int(_ck)
+AUTO_CHUNK = 1024
+AUTO_CHUNK_TILES = 6144
+
+
+def chunk_size(image_tiles: int, forced=None) -> int:
+    """The backward chunk for an image of `image_tiles` tiles (0: one CTA per
+    tile list); `forced` (an int) overrides."""
+    if forced is not None:
+        return forced
+    return AUTO_CHUNK if 0 < image_tiles <= AUTO_CHUNK_TILES else 0
 SPLIT_TILES = 1 << 30  # every chunk its own CTA when chunking is on
 
 
@@ -403,7 +427,7 @@ def chunk_setup(st, n_tiles: int, e: int, image_ptr: int):
     entries (the boundary-state and per-quadrant last-position buffers); the
     work items are built between the forward and the backward by
     chunk_items().  `st` holds the buffers.  None when off."""
-    chunk = getattr(st, "chunk", CHUNK)
+    chunk = chunk_size(st.image_tiles, getattr(st, "chunk", CHUNK))
     if chunk <= 0 or n_tiles == 0:
         return None
     lib = L.lib()
