@@ -160,105 +160,46 @@ __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
     }
 }
 
-// Live-only emission (the float32 training lists): the same entry-parallel
-// walk over the full rect span, but only the pairs some pixel of their tile
-// can composite are written, compacted in walk order: pair p (its subtotal
-// slot) gets key[p] = tile and slot_rank[p] = rank, p = live_off[rank] +
-// live index.  Live decisions come from gather's mask (rects of <= 64 tiles)
-// or are recomputed.  No zero records: an uncomposited pair has no slot.
+// Thread-per-rank emission of the live lists: each rank writes its live
+// (tile, slot) pairs into its own span [live_off[r], live_off[r + 1]) in
+// row-major rect order (consecutive ranks' spans are adjacent, so a warp's
+// stores stay within one small region).  Rects of <= 64 tiles walk the set
+// bits of the rank's live mask; larger ones repeat the box test.
 template <typename K>
-__global__ void __launch_bounds__(256) emit_live_kernel(
-    int64_t m, const int4 *__restrict__ rect_sorted, const int64_t *__restrict__ emit_off,
-    const int64_t *__restrict__ live_off, const uint64_t *__restrict__ live_mask,
-    const float *__restrict__ feat_sorted, int tiles_x, int row_lo, K *__restrict__ tile_keys,
-    int32_t *__restrict__ slot_rank) {
-    __shared__ int64_t soff[EMIT_R + 1];
-    __shared__ int4 srect[EMIT_R];
-    __shared__ uint64_t smask[EMIT_R];
-    __shared__ f32::CullForm scf[EMIT_R];
-    __shared__ int srk[ECH];
-    __shared__ int swarp[8];
-    __shared__ int scnt[8];
-    const int64_t r0 = (int64_t)blockIdx.x * EMIT_R;
-    const int nr = (int)min((int64_t)EMIT_R, m - r0);
-    for (int i = threadIdx.x; i <= nr; i += blockDim.x) soff[i] = emit_off[r0 + i];
-    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
-        int4 rc = rect_sorted[r0 + i];
-        rc.y = max(rc.y, row_lo);
-        rc.w = rc.z - rc.x + 1;
-        srect[i] = rc;
-        smask[i] = live_mask[r0 + i];
-        scf[i] = f32::cull_form(f32::stage(feat_sorted, (int)(r0 + i)));
-    }
-    __syncthreads();
-    const int64_t s0 = soff[0], s1 = soff[nr];
-    const uint32_t base_tile = (uint32_t)row_lo * (uint32_t)tiles_x;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    int carry = -1;
-    int64_t out = live_off[r0];  // this block's first live slot
-    for (int64_t c = s0; c < s1; c += ECH) {
-        const int n = (int)min((int64_t)ECH, s1 - c);
-        for (int i = t; i < ECH; i += 256) srk[i] = -1;
-        __syncthreads();
-        for (int i = t; i < nr; i += 256) {
-            const int64_t a = soff[i];
-            if (soff[i + 1] > a && a >= c && a < c + ECH) srk[a - c] = i;
+__global__ void __launch_bounds__(256) emit_live_thread_kernel(
+    int64_t m, const int4 *__restrict__ rect_sorted, const int64_t *__restrict__ live_off,
+    const uint64_t *__restrict__ live_mask, const float *__restrict__ feat_sorted, int tiles_x,
+    int row_lo, int row_hi, K *__restrict__ tile_keys, int32_t *__restrict__ slot_rank) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    int64_t out = live_off[r];
+    const int64_t end = live_off[r + 1];
+    if (out == end) return;
+    const int4 rc = rect_sorted[r];
+    const int y0 = max(rc.y, row_lo), y1 = min(rc.w, row_hi - 1);
+    const int w = rc.z - rc.x + 1;
+    const int n = (y1 - y0 + 1) * w;
+    const uint32_t base = (uint32_t)(y0 - row_lo) * (uint32_t)tiles_x + (uint32_t)rc.x;
+    if (n <= 64) {
+        uint64_t mk = live_mask[r];
+        while (mk) {
+            const int k = __ffsll((long long)mk) - 1;
+            mk &= mk - 1;
+            const int dy = k / w, dx = k - dy * w;
+            tile_keys[out] = (K)(base + (uint32_t)dy * (uint32_t)tiles_x + (uint32_t)dx);
+            slot_rank[out] = (int32_t)r;
+            out++;
         }
-        __syncthreads();
-        int v0 = srk[4 * t], v1 = max(v0, srk[4 * t + 1]), v2 = max(v1, srk[4 * t + 2]),
-            v3 = max(v2, srk[4 * t + 3]);
-        int x = v3;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x = max(x, y);
-        }
-        if (lane == 31) swarp[warp] = x;
-        __syncthreads();
-        int ex = max(carry, __shfl_up_sync(0xffffffffu, x, 1));
-        if (lane == 0) ex = carry;
-        for (int w = 0; w < warp; w++) ex = max(ex, swarp[w]);
-        srk[4 * t] = max(ex, v0);
-        srk[4 * t + 1] = max(ex, v1);
-        srk[4 * t + 2] = max(ex, v2);
-        srk[4 * t + 3] = max(ex, v3);
-        __syncthreads();
-        // rounds of 256 consecutive slots: live flags -> block prefix -> slots
-        for (int i0 = 0; i0 < n; i0 += 256) {
-            const int i = i0 + t;
-            bool live = false;
-            int lo = 0, dx = 0, dy = 0;
-            if (i < n) {
-                lo = srk[i];
-                const int4 rc = srect[lo];
-                const int k = (int)(c + i - soff[lo]);
-                dy = k / rc.w;
-                dx = k - dy * rc.w;
-                live = k < 64 ? ((smask[lo] >> k) & 1ull)
-                              : !f32::box_dead_cf(scf[lo], (float)(16 * (rc.x + dx)),
-                                                  (float)(16 * (rc.y + dy)), 15.0f);
-            }
-            const unsigned bal = __ballot_sync(0xffffffffu, live);
-            if (lane == 0) scnt[warp] = __popc(bal);
-            __syncthreads();
-            int before = 0, tot = 0;
-#pragma unroll
-            for (int w = 0; w < 8; w++) {
-                if (w < warp) before += scnt[w];
-                tot += scnt[w];
-            }
-            if (live) {
-                const int64_t p = out + before + __popc(bal & ((1u << lane) - 1u));
-                const int4 rc = srect[lo];
-                tile_keys[p] = (K)((uint32_t)(rc.y + dy) * (uint32_t)tiles_x - base_tile +
-                                   (uint32_t)(rc.x + dx));
-                slot_rank[p] = (int32_t)(r0 + lo);
-            }
-            out += tot;
-            __syncthreads();  // scnt is rewritten next round
-        }
-        carry = srk[n - 1];
-        __syncthreads();  // srk is rewritten by the next chunk
+    } else {
+        const f32::CullForm cf = f32::cull_form(f32::stage(feat_sorted, (int)r));
+        for (int ty = y0; ty <= y1; ty++)
+            for (int tx = rc.x; tx <= rc.z; tx++)
+                if (!f32::box_dead_cf(cf, (float)(16 * tx), (float)(16 * ty), 15.0f)) {
+                    tile_keys[out] = (K)((uint32_t)(ty - row_lo) * (uint32_t)tiles_x +
+                                         (uint32_t)tx);
+                    slot_rank[out] = (int32_t)r;
+                    out++;
+                }
     }
 }
 
@@ -570,13 +511,14 @@ extern "C" int isg_bin_emit_live(int64_t m, const int32_t *rect_sorted, const in
         return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
     if (key_bytes == 2)
-        emit_live_kernel<uint16_t><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
-            m, (const int4 *)rect_sorted, emit_off, live_off, live_mask, feat_sorted, tiles_x,
-            row_lo, (uint16_t *)tile_keys, slot_rank);
+        emit_live_thread_kernel<uint16_t><<<blocks_for(m, 256), 256, 0, (cudaStream_t)stream>>>(
+            m, (const int4 *)rect_sorted, live_off, live_mask, feat_sorted, tiles_x, row_lo,
+            row_hi, (uint16_t *)tile_keys, slot_rank);
     else
-        emit_live_kernel<uint32_t><<<blocks_for(m, EMIT_R), 256, 0, (cudaStream_t)stream>>>(
-            m, (const int4 *)rect_sorted, emit_off, live_off, live_mask, feat_sorted, tiles_x,
-            row_lo, (uint32_t *)tile_keys, slot_rank);
+        emit_live_thread_kernel<uint32_t><<<blocks_for(m, 256), 256, 0, (cudaStream_t)stream>>>(
+            m, (const int4 *)rect_sorted, live_off, live_mask, feat_sorted, tiles_x, row_lo,
+            row_hi, (uint32_t *)tile_keys, slot_rank);
+
     ISG_CHECK_LAUNCH();
     return 0;
 }

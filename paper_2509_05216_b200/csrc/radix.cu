@@ -107,21 +107,25 @@ template <typename T>
 __global__ void __launch_bounds__(RT) scan_chunks_kernel(const T *in, T *out, int64_t n,
                                                          T *__restrict__ sums) {
     constexpr int PER = SC / RT;  // elements per thread (contiguous in shared memory)
-    __shared__ T sm[SC];
+    // one pad element per PER: thread t's run starts t * (PER + 1) elements in,
+    // so a warp's lanes read different banks (unpadded, every lane of the
+    // warp hit the same bank at each step)
+    __shared__ T sm[SC + SC / PER];
     __shared__ T swarp[NWARP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t cb = (int64_t)blockIdx.x * SC;
+    auto at = [](int i) { return i + i / PER; };
 #pragma unroll
     for (int k = 0; k < PER; k++) {
         const int64_t i = cb + k * RT + threadIdx.x;
-        sm[k * RT + threadIdx.x] = i < n ? in[i] : (T)0;
+        sm[at(k * RT + threadIdx.x)] = i < n ? in[i] : (T)0;
     }
     __syncthreads();
     T v[PER];
     T s = 0;
 #pragma unroll
     for (int k = 0; k < PER; k++) {
-        v[k] = sm[threadIdx.x * PER + k];
+        v[k] = sm[at(threadIdx.x * PER + k)];
         s += v[k];
     }
     T x = s;
@@ -141,14 +145,14 @@ __global__ void __launch_bounds__(RT) scan_chunks_kernel(const T *in, T *out, in
     T run = before + x - s;
 #pragma unroll
     for (int k = 0; k < PER; k++) {
-        sm[threadIdx.x * PER + k] = run;
+        sm[at(threadIdx.x * PER + k)] = run;
         run += v[k];
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < PER; k++) {
         const int64_t i = cb + k * RT + threadIdx.x;
-        if (i < n) out[i] = sm[k * RT + threadIdx.x];
+        if (i < n) out[i] = sm[at(k * RT + threadIdx.x)];
     }
     if (threadIdx.x == 0) sums[blockIdx.x] = total;
 }
