@@ -351,11 +351,11 @@ HEAVY_PCT = int(os.environ.get("ISOGS_HEAVY_PCT", "0"))
 # the fused kernel's register footprint costs the latency-bound fold more
 # occupancy than the 0.74 GB of gradient traffic it saves.
 FUSE_ADAM = os.environ.get("ISOGS_FUSE_ADAM", "0") != "0"
-# exact longest-first order (a 16-bit radix sort of the lengths; default) or
-# the one-launch bucketed order (isg_tile_order, 1024 linear buckets): the
-# same raster times and 0.04 ms less GPU time, but config 2 measured 412 ->
-# 395 images/s with it (the GPU then waits on the host's launches)
-EXACT_ORDER = os.environ.get("ISOGS_EXACT_ORDER", "1") != "0"
+# heavy-first launch order: one launch bucketing the tiles by list length
+# (isg_tile_order, 1024 linear buckets; default) or the exact longest-first
+# order (a 16-bit radix sort of the lengths, 8 launches for 16K keys):
+# measured 119.0 -> 119.6 images/s at config 3, 469 -> 477 at config 2
+EXACT_ORDER = os.environ.get("ISOGS_EXACT_ORDER", "0") != "0"
 
 
 def heavy_first_order(st, n_tiles: int, offsets: torch.Tensor):
