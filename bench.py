@@ -363,12 +363,13 @@ def run_ours(args, world, rank, local):
                    else cpu_baseline(wl, args, schedule, cfg, scene_extent))
 
     # kernels per step, all ours (no library kernels on the path): the ncu
-    # launch list of one config-3 step (profiles/r02_v1/ncu_summary.md) --
+    # launch list of one config-3 step (profiles/r02_final/launches.md) --
     # preprocess, depth radix sort (5 x 4) + tie fix, gather with live counts
     # + 2 scans (3 each), rank_of, live emission, tile radix sort (2 x 4),
-    # offsets, heavy-first order (keys + 2 x 4), raster fwd, loss (3), raster
-    # bwd, live fold, chain, Adam
-    launches_per_step = 57
+    # offsets, heavy-first order (1), raster fwd, loss (3), raster bwd, fused
+    # live fold + chain, Adam (+ the chunk items launch when the image is
+    # chunked, config 2)
+    launches_per_step = 48 + (1 if tr.r.chunks is not None else 0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

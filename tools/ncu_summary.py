@@ -55,9 +55,12 @@ def launches(path, steps):
     return "\n".join(out)
 
 
-def full(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+def full(rep, raw=None):
+    if raw:  # `ncu -i REP --page raw --csv` output written on the GPU box
+        txt = open(raw).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, units = rows[0], rows[1]
     data = rows[2:]
@@ -77,14 +80,15 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--rep")
+    ap.add_argument("--raw", help="the --page raw --csv dump instead of a report")
     a = ap.parse_args()
     if a.launches:
         print("## Launch list (ncu gpu__time_duration, --clock-control none, timed steps only)\n")
         print(launches(a.launches, a.steps))
         print()
-    if a.rep:
+    if a.rep or a.raw:
         print("## Full capture (ncu --set full)\n")
-        print(full(a.rep))
+        print(full(a.rep, a.raw))
 
 
 if __name__ == "__main__":
