@@ -488,6 +488,16 @@ typedef struct isg_train_state {
     int32_t degree;
 } isg_train_state;
 
+/* densify_and_prune's row classification (training.py:334-347) on the device,
+ * float64 with the glibc-exact exp like the reference's numpy: per row cls =
+ * 0 keep, 1 clone, 2 split, 3 prune.  log_scales (n, 3) and logits (n)
+ * float32; seen int64, grad_accum float64 (TrainStats); scale_prune applies
+ * when scale_prune_on. */
+int isg_densify_classify(int64_t n, const float *log_scales, const float *logits,
+                         const int64_t *seen, const double *grad_accum, double opacity_prune,
+                         double scale_prune, int32_t scale_prune_on, double grad_threshold,
+                         double split_threshold, uint8_t *cls, void *stream);
+
 int isg_chain_adam(const isg_train_state *s, const isg_camera *cam, const uint8_t *flag,
                    const double *grad2d, const float *lr5, const isg_adam_consts *c,
                    double half_w, double half_h, void *stream);

@@ -456,6 +456,35 @@ __global__ void exp_kernel(int64_t n, const double *x, double *y) {
     if (i < n) y[i] = exp_glibc(x[i]);
 }
 
+// densify_and_prune's classification (training.py:334-347), statement for
+// statement in float64 with the glibc-exact exp (the reference's numpy):
+//   avg = grad_accum / max(seen, 1); scales = exp(log_scales); opacity =
+//   1 / (1 + exp(-logit)); prune = opacity < opacity_prune (| max scale >
+//   scale_prune when finite); hot = avg > grad_thr & !prune; split = hot &
+//   max scale > split_thr; clone = hot & !split.  cls: 0 keep, 1 clone,
+//   2 split, 3 prune.
+__global__ void densify_classify_kernel(int64_t n, const float *__restrict__ log_scales,
+                                        const float *__restrict__ logits,
+                                        const int64_t *__restrict__ seen,
+                                        const double *__restrict__ grad_accum,
+                                        double opacity_prune, double scale_prune,
+                                        int scale_prune_on, double grad_thr, double split_thr,
+                                        uint8_t *__restrict__ cls) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t s = seen[i];
+    const double avg = grad_accum[i] / (double)(s > 1 ? s : 1);
+    double mx = exp_glibc((double)log_scales[3 * i]);
+    mx = fmax(mx, exp_glibc((double)log_scales[3 * i + 1]));
+    mx = fmax(mx, exp_glibc((double)log_scales[3 * i + 2]));
+    const double opacity = 1.0 / (1.0 + exp_glibc(-(double)logits[i]));
+    bool prune = opacity < opacity_prune;
+    if (scale_prune_on) prune = prune || mx > scale_prune;
+    const bool hot = avg > grad_thr && !prune;
+    const bool split = hot && mx > split_thr;
+    cls[i] = prune ? 3 : split ? 2 : hot ? 1 : 0;
+}
+
 }  // namespace isg
 
 using namespace isg;
@@ -730,6 +759,21 @@ extern "C" int isg_chain_adam(const isg_train_state *st, const isg_camera *cam,
     else
         chain_adam_kernel<3><<<blocks_for(st->n, 128), 128, 0, s>>>(
             *st, k, flag, grad2d, lr5[0], lr5[1], lr5[2], lr5[3], lr5[4], a, half_w, half_h);
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int isg_densify_classify(int64_t n, const float *log_scales, const float *logits,
+                                    const int64_t *seen, const double *grad_accum,
+                                    double opacity_prune, double scale_prune,
+                                    int32_t scale_prune_on, double grad_threshold,
+                                    double split_threshold, uint8_t *cls, void *stream) {
+    if (n < 0 || (n > 0 && (!log_scales || !logits || !seen || !grad_accum || !cls)))
+        return (int)cudaErrorInvalidValue;
+    if (n == 0) return 0;
+    densify_classify_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+        n, log_scales, logits, seen, grad_accum, opacity_prune, scale_prune, scale_prune_on,
+        grad_threshold, split_threshold, cls);
     ISG_CHECK_LAUNCH();
     return 0;
 }

@@ -8,9 +8,9 @@ parent), then the two children of every split parent; kept rows carry their
 Adam moments, new rows start cold, and the statistics restart at zero.
 
 The reference classifies with numpy (np.exp of the log-scales and logits,
-float64), so the classification here runs with the same numpy on the host
-over the rows' 20 bytes of state, and the row gather / concatenation runs on
-the device.  Split children are drawn exactly as the reference draws them:
+float64); here the classification runs on the device in float64 with the
+glibc-exact exp (isg_densify_classify, the same bits), and only the split
+parents' rows go to the host.  Split children are drawn exactly as the reference draws them:
 one numpy Generator per parent seeded by (seed, iteration, global id), for
 the split rows only.  Densify runs every densify_interval steps; it is not
 on the per-iteration path.
@@ -92,22 +92,35 @@ def densify_and_prune(cloud: GaussianCloud, stats: TrainStats, config, iteration
                           else global_ids, dtype=np.int64)
         if gids.shape != (n,):
             raise ValueError("global_ids must have one id per row")
-    keep, clone, split, prune, scales = classify(
-        cloud.log_scales.cpu().numpy(), cloud.opacity_logits.cpu().numpy(),
-        _host(stats.seen, np.int64), _host(stats.grad_accum, np.float64),
-        config.opacity_prune, config.scale_prune, grad_threshold, split_threshold)
-    rows = {}
-    for name, mask in (("kept", keep), ("clone", clone), ("split", split), ("prune", prune)):
-        rows[name] = torch.from_numpy(np.nonzero(mask)[0].astype(np.int64)).to(dev)
-    kept_rows, clone_rows, split_rows, prune_rows = (rows["kept"], rows["clone"],
-                                                     rows["split"], rows["prune"])
+    if dev.type == "cuda" and cloud.positions.dtype == torch.float32:
+        # classification on the device (isg_densify_classify: float64, the
+        # glibc-exact exp); only the split parents' rows come to the host
+        cls = _classify_device(cloud, stats, config, grad_threshold, split_threshold)
+        kept_rows = torch.nonzero(cls <= 1).flatten()
+        clone_rows = torch.nonzero(cls == 1).flatten()
+        split_rows = torch.nonzero(cls == 2).flatten()
+        prune_rows = torch.nonzero(cls == 3).flatten()
+        rows_h = split_rows.cpu().numpy()
+        scales = None
+    else:  # host tensors (the gloo tests of the sharded bookkeeping)
+        keep, clone, split, prune, scales = classify(
+            cloud.log_scales.cpu().numpy(), cloud.opacity_logits.cpu().numpy(),
+            _host(stats.seen, np.int64), _host(stats.grad_accum, np.float64),
+            config.opacity_prune, config.scale_prune, grad_threshold, split_threshold)
+        rows = {}
+        for name, mask in (("kept", keep), ("clone", clone), ("split", split),
+                           ("prune", prune)):
+            rows[name] = torch.from_numpy(np.nonzero(mask)[0].astype(np.int64)).to(dev)
+        kept_rows, clone_rows, split_rows, prune_rows = (rows["kept"], rows["clone"],
+                                                         rows["split"], rows["prune"])
+        rows_h = np.nonzero(split)[0]
     parts = {k: [getattr(cloud, k)[kept_rows], getattr(cloud, k)[clone_rows]]
              for k in PARAM_NAMES}
     ns = int(split_rows.numel())
     if ns:
         dt = cloud.positions.dtype
-        rows_h = np.nonzero(split)[0]
-        sc_h = scales[rows_h]
+        sc_h = (scales[rows_h] if scales is not None else
+                np.exp(cloud.log_scales[split_rows].cpu().numpy().astype(np.float64)))
         rot_h = cloud.rotations[split_rows].cpu().numpy().astype(np.float64)
         pos_h = cloud.positions[split_rows].cpu().numpy().astype(np.float64)
         child = np.empty((2 * ns, 3), dtype=np.float64)
@@ -129,6 +142,24 @@ def densify_and_prune(cloud: GaussianCloud, stats: TrainStats, config, iteration
                         degree=cloud.degree)
     return new, DensifyMapping(kept=kept_rows, cloned=clone_rows, split=split_rows,
                                pruned=prune_rows)
+
+
+def _classify_device(cloud: GaussianCloud, stats: TrainStats, config, grad_threshold: float,
+                     split_threshold: float) -> torch.Tensor:
+    """Per-row class (0 keep, 1 clone, 2 split, 3 prune) by isg_densify_classify."""
+    import ctypes
+    from . import _lib as L
+    n = cloud.count
+    cls = torch.empty(n, dtype=torch.uint8, device=cloud.positions.device)
+    seen = stats.seen.to(device=cls.device, dtype=torch.int64).contiguous()
+    acc = stats.grad_accum.to(device=cls.device, dtype=torch.float64).contiguous()
+    sp = float(config.scale_prune)
+    on = 1 if math.isfinite(sp) else 0
+    L.check(L.lib().isg_densify_classify(
+        n, L.ptr(cloud.log_scales), L.ptr(cloud.opacity_logits), L.ptr(seen), L.ptr(acc),
+        float(config.opacity_prune), sp if on else 0.0, on, float(grad_threshold),
+        float(split_threshold), L.ptr(cls), L.stream_ptr()), "isg_densify_classify")
+    return cls
 
 
 def _host(x, dtype) -> np.ndarray:

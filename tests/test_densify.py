@@ -91,3 +91,37 @@ def test_train_with_densify_matches_reference():
     assert np.max(np.abs(got - ref) / ref) <= 2e-3, (got, ref)
     for r, p, s in zip(rep.records, d["rec_psnr"], d["rec_ssim"]):
         assert abs(r.psnr - p) <= 0.05 and abs(r.ssim - s) <= 2e-3, (r.psnr, p, r.ssim, s)
+
+
+@pytest.mark.gpu
+def test_device_classification_equals_numpy():
+    """isg_densify_classify (float64, glibc-exact exp, on the device) == the
+    reference's numpy classification (training.py:334-347) on 200K rows with
+    thresholds placed inside the data's range, never-seen rows, and both
+    with and without scale pruning."""
+    from paper_2509_05216_b200.densify import _classify_device, classify
+    from paper_2509_05216_b200.gaussians import GaussianCloud
+    from paper_2509_05216_b200.training import TrainStats
+    import paper_2509_05216_b200 as P
+    rng = np.random.default_rng(11)
+    n = 200_000
+    ls = rng.normal(-4.0, 1.5, (n, 3)).astype(np.float32)
+    lg = rng.normal(-2.0, 3.0, n).astype(np.float32)
+    seen = rng.integers(0, 40, n).astype(np.int64)
+    acc = np.abs(rng.normal(0.0, 2e-3, n)) * seen
+    dev = torch.device("cuda", 0)
+    z = lambda k: torch.zeros((n, k) if k > 1 else n, dtype=torch.float32, device=dev)
+    cloud = GaussianCloud(z(3), torch.from_numpy(ls).to(dev), z(4), torch.from_numpy(lg).to(dev),
+                          torch.zeros((n, 4, 3), dtype=torch.float32, device=dev), degree=1)
+    stats = TrainStats(grad_accum=torch.from_numpy(acc).to(dev), seen=torch.from_numpy(seen).to(dev))
+    gthr = float(np.median(acc / np.maximum(seen, 1)))
+    sthr = float(np.median(np.exp(ls.astype(np.float64)).max(axis=1)))
+    for scale_prune in (float("inf"), float(np.quantile(np.exp(ls.astype(np.float64)), 0.99))):
+        cfg = P.TrainConfig(opacity_prune=0.005, scale_prune=scale_prune)
+        keep, clone, split, prune, _ = classify(ls, lg, seen, acc, cfg.opacity_prune,
+                                                cfg.scale_prune, gthr, sthr)
+        cls = _classify_device(cloud, stats, cfg, gthr, sthr).cpu().numpy()
+        ref = np.where(prune, 3, np.where(split, 2, np.where(clone, 1, 0)))
+        assert (keep == (ref <= 1)).all()
+        assert np.array_equal(cls, ref), (scale_prune, int((cls != ref).sum()))
+        assert 0 < (ref == 2).sum() and 0 < (ref == 1).sum() and 0 < (ref == 3).sum()
