@@ -255,11 +255,10 @@ int32_t isg_chunk_items_max(int64_t n_entries, int32_t n_tiles, int32_t chunk);
  * for every list position of tile_order (NULL: 0..n_tiles-1) with tile_last
  * maximum L over its quadrants, split != 0: ceil(L / chunk) chunks (at least
  * one; the last one runs to the end of the list, whose entries past L
- * contribute nothing); split == 0: one item for the whole list, which
- * restarts at every internal chunk boundary from the same state -- the same
- * arithmetic either way, so the split can follow the launch size.  Written
- * as (position, chunk | 1 << 30 for the last) pairs; *n_items (device) =
- * their number. */
+ * contribute nothing); split == 0: one item for the whole list.  Written as
+ * (position, chunk | 1 << 30 for the last) pairs; *n_items (device) = their
+ * number.  A chunk restart rounds differently from an unbroken walk, so the
+ * chunking is part of the arithmetic (engine.py: it follows the image). */
 int isg_chunk_items(int32_t n_tiles, const int32_t *offsets, const int32_t *tile_order,
                     const int32_t *tile_last, int32_t chunk, int32_t split, int32_t *items,
                     int32_t *n_items, void *stream);
