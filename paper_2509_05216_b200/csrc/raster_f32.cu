@@ -192,7 +192,7 @@ __device__ __forceinline__ bool composite_pr(float a, bool on, const float4 &c, 
 // composites them.  "All pixels done" is tested every FCHK entries (a
 // finished pixel only skips work, so the late test changes no result).
 #ifndef FWD_FCHK
-#define FWD_FCHK 16
+#define FWD_FCHK 32
 #endif
 constexpr int FCHK = FWD_FCHK;
 constexpr int WB = 32;  // per-warp staging batch
