@@ -6,7 +6,7 @@
 // HBM-bound integer work, written for the B200 SM (no library code):
 //
 //   per 8-bit digit pass (reduce-then-scan, deterministic):
-//     upsweep  : each CTA counts the digits of its 4096 keys (2048 for 64-bit
+//     upsweep  : each CTA counts the digits of its 2048 keys (1024 for 64-bit
 //                keys) in warp-private shared-memory counters -> counts[digit][cta]
 //     scan     : digit-major exclusive scan of the counts (4096-element
 //                chunks in shared memory + one CTA over the chunk sums)
@@ -32,8 +32,14 @@ namespace radix {
 constexpr int RT = 256;        // threads per CTA
 constexpr int NWARP = RT / 32;
 // items per CTA (shared-memory staging: 64-bit keys take half as many)
+#ifndef RADIX_IPC8
+#define RADIX_IPC8 1024
+#endif
+#ifndef RADIX_IPC_SMALL
+#define RADIX_IPC_SMALL 2048
+#endif
 template <typename K>
-constexpr int ipc() { return sizeof(K) == 8 ? 2048 : 4096; }
+constexpr int ipc() { return sizeof(K) == 8 ? RADIX_IPC8 : RADIX_IPC_SMALL; }
 constexpr int BINS = 256;
 constexpr int SC = 4096;       // scan chunk (elements per CTA)
 
