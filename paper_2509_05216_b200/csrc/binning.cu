@@ -15,7 +15,13 @@
 
 namespace isg {
 
-__global__ void __launch_bounds__(256) gather_rank_kernel(
+#ifndef GATHER_T
+#define GATHER_T 256
+#endif
+#ifndef EMIT_T
+#define EMIT_T 256
+#endif
+__global__ void __launch_bounds__(GATHER_T) gather_rank_kernel(
     int64_t n, const uint64_t *__restrict__ sorted_keys, const int32_t *__restrict__ order,
     const int4 *__restrict__ rect, int rect_stride4, const float4 *__restrict__ feat,
     int feat_stride4, int feat_vec4, int row_lo, int row_hi, int4 *__restrict__ rect_sorted,
@@ -166,7 +172,7 @@ __global__ void __launch_bounds__(256) emit_span_kernel(int64_t m,
 // stores stay within one small region).  Rects of <= 64 tiles walk the set
 // bits of the rank's live mask; larger ones repeat the box test.
 template <typename K>
-__global__ void __launch_bounds__(256) emit_live_thread_kernel(
+__global__ void __launch_bounds__(EMIT_T) emit_live_thread_kernel(
     int64_t m, const int4 *__restrict__ rect_sorted, const int64_t *__restrict__ live_off,
     const uint64_t *__restrict__ live_mask, const float *__restrict__ feat_sorted, int tiles_x,
     int row_lo, int row_hi, K *__restrict__ tile_keys, int32_t *__restrict__ slot_rank) {
@@ -457,7 +463,7 @@ static int bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_
     int64_t *cnt = (int64_t *)workspace;
     int64_t *cnt_live = live_off ? (int64_t *)((char *)workspace + cnt_bytes) : nullptr;
     void *scan_ws = (char *)workspace + (live_off ? 2 : 1) * cnt_bytes;
-    gather_rank_kernel<<<blocks_for(n, 256), 256, 0, s>>>(
+    gather_rank_kernel<<<blocks_for(n, GATHER_T), GATHER_T, 0, s>>>(
         n, sorted_keys, order, rect, rect_stride4, feat, feat_stride4, vec4, row_lo, row_hi,
         (int4 *)rect_sorted, (float4 *)feat_sorted, cnt, counts, cnt_live, live_mask);
     ISG_CHECK_LAUNCH();
@@ -511,11 +517,11 @@ extern "C" int isg_bin_emit_live(int64_t m, const int32_t *rect_sorted, const in
         return (int)cudaErrorInvalidValue;
     if (m == 0) return 0;
     if (key_bytes == 2)
-        emit_live_thread_kernel<uint16_t><<<blocks_for(m, 256), 256, 0, (cudaStream_t)stream>>>(
+        emit_live_thread_kernel<uint16_t><<<blocks_for(m, EMIT_T), EMIT_T, 0, (cudaStream_t)stream>>>(
             m, (const int4 *)rect_sorted, live_off, live_mask, feat_sorted, tiles_x, row_lo,
             row_hi, (uint16_t *)tile_keys, slot_rank);
     else
-        emit_live_thread_kernel<uint32_t><<<blocks_for(m, 256), 256, 0, (cudaStream_t)stream>>>(
+        emit_live_thread_kernel<uint32_t><<<blocks_for(m, EMIT_T), EMIT_T, 0, (cudaStream_t)stream>>>(
             m, (const int4 *)rect_sorted, live_off, live_mask, feat_sorted, tiles_x, row_lo,
             row_hi, (uint32_t *)tile_keys, slot_rank);
 
