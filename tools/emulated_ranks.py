@@ -93,10 +93,12 @@ def main():
         "exchange_ms": {"splats": float(np.mean(xs)), "grads": float(np.mean(xg)),
                         "link_gbs": a.link_gbs},
         "host_sync_ms": a.sync_us * 1e-3,
-        "projected_step_ms": float(np.mean(proj)),
-        "projected_images_per_s": 1000.0 / float(np.mean(proj)),
+        "projected_step_ms_mean": float(np.mean(proj)),
+        "projected_step_ms": float(np.median(proj)),
+        "projected_images_per_s": 1000.0 / float(np.median(proj)),
         "note": "emulated on one B200: each rank's phases timed alone (CUDA events); exchanges "
-                "projected from their byte counts",
+                "projected from their byte counts; the projection is the median step (a step "
+                "that grows a buffer pays a one-off allocation inside a timed phase)",
     }
     print(json.dumps(out))
 
