@@ -352,6 +352,10 @@ def run_ours(args, world, rank, local):
     roof = roofline(phases, counts, n, args.config if args.res is None else f"{args.config}_{args.res}")
     log("[ours] phases (ms): " + ", ".join(f"{k} {v:.3f}" for k, v in phases.items()))
 
+    # ---- the reference's precision: the float64 raster build through the
+    # public render API (not the training step; reported beside it)
+    api64 = api_render_timing(tr, wl, schedule[0], torch.float64)
+
     # ---- end-to-end through the public API: GT H2D from pinned host + loss D2H
     e2e = end_to_end(tr, wl, schedule, args)
 
@@ -379,6 +383,7 @@ def run_ours(args, world, rank, local):
         "roofline": roof, "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "clocks": clocks,
         "gpu_launches": launches_per_step * args.steps,
         "phases_ms": {k: round(v, 4) for k, v in phases.items()},
+        "render_api_f64": api64,
         "pairs": counts,
         "warm": warm,
     }
@@ -509,6 +514,43 @@ def fp32_peak_source() -> str:
         return ("measured in this run: isg_probe_ffma, mean of 200 back-to-back launches "
                 f"(burst {_FP32['burst_tflops']:.2f} TFLOP/s)")
     return "FP32 FFMA peak 148 SM x 128 lanes x 2 x max SM clock (not measured)"
+
+
+def api_render_timing(tr, wl, view, dtype, reps: int = 3):
+    """Device time of one forward + backward render of `view` through the
+    public API (project, sort_order, tile lists, raster forward / backward in
+    `dtype`, the scratch fold and chain rule; rasterizer.render_forward /
+    render_backward) on the trainer's current Gaussians."""
+    import torch
+    import paper_2509_05216_b200 as P
+    cam = wl.cameras[view]
+    res = wl.resolution
+    cloud = tr.cloud
+    dl = torch.full((res, res, 3), 1e-3, dtype=dtype, device=cloud.positions.device)
+
+    def once():
+        batch = P.project(cloud, cam)
+        img, aux, order = P.render_forward(batch, res, res, dtype=dtype)
+        return batch, aux, order
+
+    batch, aux, order = once()
+    P.render_backward(cloud, cam, batch, order, aux, dl)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    f = b = 0.0
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        ev[0].record()
+        batch, aux, order = once()
+        ev[1].record()
+        P.render_backward(cloud, cam, batch, order, aux, dl)
+        ev[2].record()
+        torch.cuda.synchronize()
+        f += ev[0].elapsed_time(ev[1]) / reps
+        b += ev[1].elapsed_time(ev[2]) / reps
+    return {"dtype": str(dtype).replace("torch.", ""), "forward_ms": round(f, 3),
+            "backward_ms": round(b, 3), "images_per_s": round(1000.0 / (f + b), 2),
+            "view": int(view), "note": "public render API (full lists, unmasked raster pair, "
+            "host-synchronised sizes), no optimiser step: a precision reference, not the metric"}
 
 
 def end_to_end(tr, wl, schedule, args):
