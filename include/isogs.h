@@ -375,6 +375,26 @@ int isg_route_pack(int64_t n, const uint8_t *flag, const int32_t *rect, const ui
                    uint64_t *keys_send, int32_t *pay_send, uint64_t *keys_self,
                    int32_t *pay_self, void *stream);
 
+/* Render-API glue (rasterizer.py's SplatBatch columns).  isg_compact_count:
+ * pos[0..n] = exclusive scan of the keep flags (pos[n] = kept rows, device;
+ * two-phase workspace).  isg_compact_batch: each kept row i of
+ * isg_preprocess's full64 / rect (indices optional: NULL = row id) to column
+ * position pos[i] of mean2d (m,2), cov2d (m,3), conic (m,3), depth, colour
+ * (m,3), opacity, tile_min / tile_max (m,2) int32, indices int64 -- the
+ * reference's stable `keep` compaction (rasterizer.py:142-158).
+ * isg_gather_batch: sorted row r <- column row order[r]: the 12 raster
+ * features in feat_dtype and the int32 tile rect (rasterizer.py:294-345). */
+int isg_compact_count(void *workspace, size_t *ws_bytes, int64_t n, const uint8_t *flag,
+                      int64_t *pos, void *stream);
+int isg_compact_batch(int64_t n, const uint8_t *flag, const int64_t *pos, const double *full64,
+                      const int32_t *rect, const int64_t *indices, double *mean2d, double *cov2d,
+                      double *conic, double *depth, double *color, double *opacity,
+                      int32_t *tile_min, int32_t *tile_max, int64_t *indices_out, void *stream);
+int isg_gather_batch(int64_t m, const int64_t *order, const double *mean2d, const double *conic,
+                     const double *color, const double *opacity, const int32_t *tile_min,
+                     const int32_t *tile_max, int32_t feat_dtype, void *feat, int32_t *rect,
+                     void *stream);
+
 /* Peer-store variant of isg_route_pack (the fused pack + exchange): band d's
  * records go to keys_dst[d][j] / pay_dst[d][16 * j] (int32 units), j as
  * above -- keys_dst/pay_dst are HOST arrays of n_bands DEVICE pointers, each

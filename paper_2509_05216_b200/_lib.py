@@ -121,6 +121,9 @@ SIGNATURES = {
     "isg_band_fold_peer": [_I64, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P],
     "isg_route_pack_peer": [_I64, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P],
     "isg_copy": [_P, _P, _I64, _P],
+    "isg_compact_count": [_P, _SZ, _I64, _P, _P, _P],
+    "isg_compact_batch": [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "isg_gather_batch": [_I64, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _P],
     "isg_densify_classify": [_I64, _P, _P, _P, _P, _D, _D, _I32, _D, _D, _P, _P],
     "isg_reduce_live": [_I64, _P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P],
     "isg_band_cost": [_P, _I32, _I32, _I32, _I32, _P, _P],

@@ -36,6 +36,7 @@ SOURCES = {
     "volume.cu": ["-fmad=false"],
     "probe.cu": [],
     "radix.cu": [],
+    "api.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

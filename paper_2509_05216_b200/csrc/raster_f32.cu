@@ -136,16 +136,15 @@ constexpr int F_TOUCH = 1, F_STATS = 2;
 // carried.  CHECK re-tests that sentinel for an alpha computed before the
 // pixel finished (the second entry of a step).
 template <int MODE, bool CHECK>
-__device__ __forceinline__ void composite(float a, bool on, int slot, int base, uint32_t a_col,
-                                          int64_t *touched, const int *srank, float &fpy,
-                                          int &it, float &t, float &r, float &g, float &b,
-                                          int &last, int &cnt, unsigned &cm) {
-    if (!on || (CHECK && fpy == FINF)) return;
+__device__ __forceinline__ bool composite(float a, bool on, int slot, int base, uint32_t a_col,
+                                          float &fpy, int &it, float &t, float &r, float &g,
+                                          float &b, int &last, int &cnt, unsigned &cm) {
+    if (!on || (CHECK && fpy == FINF)) return false;
     const float test = t * (1.0f - a);
     if (test < 1e-4f) {
         fpy = FINF;
         if (MODE & F_STATS) it = base + slot + 1;
-        return;
+        return false;
     }
     const float4 c = lds4(a_col + 16 * slot);
     const float w = a * t;
@@ -156,7 +155,16 @@ __device__ __forceinline__ void composite(float a, bool on, int slot, int base, 
     last = base + slot + 1;
     cm |= 1u << slot;
     if (MODE & F_STATS) cnt++;
-    if (MODE & F_TOUCH) atomicAdd((unsigned long long *)&touched[srank[slot]], 1ull);
+    return true;
+}
+
+// Touch counts (the reference's `touched`): the pixels of the warp's quadrant
+// that composited a slot, added with one atomic per (quadrant, entry).
+__device__ __forceinline__ void touch_add(bool c0, bool c1, int slot, int64_t *touched,
+                                          const int *srank) {
+    const unsigned n = __popc(__ballot_sync(FULL, c0)) + __popc(__ballot_sync(FULL, c1));
+    if (n && (threadIdx.x & 31) == 0)
+        atomicAdd((unsigned long long *)&touched[srank[slot]], (unsigned long long)n);
 }
 
 // composite() for the training launch (no touch / stats counters), written so
@@ -302,14 +310,18 @@ __global__ void __launch_bounds__(NT, FWD_MINB) fwd_kernel(
                     if (ca0 || ca1) cm |= 1u << sa;
                     if (cb0 || cb1) cm |= 1u << sb;
                 } else {
-                    composite<MODE, false>(aa0, oa0, sa, base, a_col, touched, srank, fpy0, it0,
-                                           t0, r0, g0, b0, last0, cnt0, cm);
-                    composite<MODE, false>(aa1, oa1, sa, base, a_col, touched, srank, fpy1, it1,
-                                           t1, r1, g1, b1, last1, cnt1, cm);
-                    composite<MODE, true>(ab0, ob0, sb, base, a_col, touched, srank, fpy0, it0,
-                                          t0, r0, g0, b0, last0, cnt0, cm);
-                    composite<MODE, true>(ab1, ob1, sb, base, a_col, touched, srank, fpy1, it1,
-                                          t1, r1, g1, b1, last1, cnt1, cm);
+                    const bool ca0 = composite<MODE, false>(aa0, oa0, sa, base, a_col, fpy0, it0,
+                                                            t0, r0, g0, b0, last0, cnt0, cm);
+                    const bool ca1 = composite<MODE, false>(aa1, oa1, sa, base, a_col, fpy1, it1,
+                                                            t1, r1, g1, b1, last1, cnt1, cm);
+                    const bool cb0 = composite<MODE, true>(ab0, ob0, sb, base, a_col, fpy0, it0,
+                                                           t0, r0, g0, b0, last0, cnt0, cm);
+                    const bool cb1 = composite<MODE, true>(ab1, ob1, sb, base, a_col, fpy1, it1,
+                                                           t1, r1, g1, b1, last1, cnt1, cm);
+                    if (TOUCH) {
+                        touch_add(ca0, ca1, sa, touched, srank);
+                        touch_add(cb0, cb1, sb, touched, srank);
+                    }
                 }
             }
         }

@@ -121,6 +121,7 @@ def _sortable_f64(x: torch.Tensor) -> torch.Tensor:
 
 
 _WS = L.Workspace()
+_WS_COMPACT = L.Workspace()
 
 
 def _stable_argsort_u64(keys: torch.Tensor) -> torch.Tensor:
@@ -163,15 +164,30 @@ def project(cloud, cam, tile_size: int = TILE_SIZE, indices=None) -> SplatBatch:
         cs = L.camera_struct(cam)
         L.check(L.lib().isg_preprocess(ctypes.byref(p), ctypes.byref(cs), tile_size,
                                        ctypes.byref(out), L.stream_ptr()), "isg_preprocess")
-    keep = flag.bool()
-    f = full[keep]
-    r = rect[keep]
-    return SplatBatch(
-        indices=indices[keep], mean2d=f[:, 0:2].contiguous(), cov2d=f[:, 2:5].contiguous(),
-        conic=f[:, 5:8].contiguous(), depth=f[:, 8].contiguous(), color=f[:, 9:12].contiguous(),
-        opacity=f[:, 12].contiguous(), tile_min=r[:, 0:2].contiguous(),
-        tile_max=r[:, 2:4].contiguous(), width=cam.width, height=cam.height,
-        tile_size=tile_size, tiles_x=tiles_x, tiles_y=tiles_y)
+    # the stable keep compaction straight into the batch columns
+    lib = L.lib()
+    pos = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    sz = ctypes.c_size_t(0)
+    L.check(lib.isg_compact_count(None, ctypes.byref(sz), n, None, None, None), "compact size")
+    ws = _WS_COMPACT.get(sz.value, dev)
+    sz = ctypes.c_size_t(ws.numel())
+    L.check(lib.isg_compact_count(L.ptr(ws), ctypes.byref(sz), n, L.ptr(flag) if n else None,
+                                  L.ptr(pos), L.stream_ptr()), "isg_compact_count")
+    m = int(pos[n].item())
+    f64 = lambda *shape: torch.empty(shape, dtype=torch.float64, device=dev)
+    cols = {"mean2d": f64(m, 2), "cov2d": f64(m, 3), "conic": f64(m, 3), "depth": f64(m),
+            "color": f64(m, 3), "opacity": f64(m),
+            "tile_min": torch.empty((m, 2), dtype=torch.int32, device=dev),
+            "tile_max": torch.empty((m, 2), dtype=torch.int32, device=dev),
+            "indices": torch.empty(m, dtype=torch.int64, device=dev)}
+    if m:
+        L.check(lib.isg_compact_batch(n, L.ptr(flag), L.ptr(pos), L.ptr(full), L.ptr(rect),
+                                      L.ptr(indices), *(L.ptr(cols[k]) for k in (
+                                          "mean2d", "cov2d", "conic", "depth", "color",
+                                          "opacity", "tile_min", "tile_max", "indices")),
+                                      L.stream_ptr()), "isg_compact_batch")
+    return SplatBatch(width=cam.width, height=cam.height, tile_size=tile_size, tiles_x=tiles_x,
+                      tiles_y=tiles_y, **cols)
 
 
 def sort_order(batch: SplatBatch) -> torch.Tensor:
@@ -392,10 +408,15 @@ def render_forward(batch: SplatBatch, width: int, height: int,
     dev = L.require_cuda()
     m = len(batch)
     order = sort_order(batch)
-    rect = torch.cat([batch.tile_min, batch.tile_max], 1).to(torch.int32)[order].contiguous()
-    sa = {"mean2d": batch.mean2d[order], "conic": batch.conic[order],
-          "color": batch.color[order], "opacity": batch.opacity[order]}
-    feat = _feat_from(sa, dt)
+    rect = torch.empty((m, 4), dtype=torch.int32, device=dev)
+    feat = torch.empty((m, 12), dtype=dt, device=dev)
+    if m:
+        cols = [_dev(getattr(batch, k), torch.float64) for k in ("mean2d", "conic", "color",
+                                                                 "opacity")]
+        tmin, tmax = _dev(batch.tile_min, torch.int32), _dev(batch.tile_max, torch.int32)
+        L.check(L.lib().isg_gather_batch(m, L.ptr(order), *(L.ptr(c) for c in cols),
+                                         L.ptr(tmin), L.ptr(tmax), L.dtype_tag(dt), L.ptr(feat),
+                                         L.ptr(rect), L.stream_ptr()), "isg_gather_batch")
     emit_off = _emit_offsets(rect, 0, batch.tiles_y)
     offsets, entries = _bin_all_tiles(rect, emit_off, batch.tiles_x, batch.tiles_y)
     image = torch.empty((height, width, 3), dtype=dt, device=dev)

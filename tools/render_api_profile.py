@@ -1,0 +1,42 @@
+"""Where the public render_forward's time goes (CUDA events around each of
+its steps, config from argv)."""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, '.')
+import paper_2509_05216_b200 as P
+from paper_2509_05216_b200 import rasterizer as R
+from paper_2509_05216_b200 import synthetic as S
+
+name = sys.argv[1] if len(sys.argv) > 1 else "config3"
+dev = torch.device("cuda", 0)
+wl = S.make_workload(name, dev, view_ids=[0, 1])
+cloud = P.cloud_from_points(wl.points, wl.log_scales, 1, dev)
+cam = wl.cameras[0]
+res = wl.resolution
+for rep in range(3):
+    ev = []
+    def mark(tag):
+        e = torch.cuda.Event(enable_timing=True); e.record(); ev.append((tag, e))
+    torch.cuda.synchronize(); mark("start")
+    batch = P.project(cloud, cam); mark("project")
+    order = R.sort_order(batch); mark("sort_order")
+    rect = torch.cat([batch.tile_min, batch.tile_max], 1).to(torch.int32)[order].contiguous()
+    sa = {"mean2d": batch.mean2d[order], "conic": batch.conic[order],
+          "color": batch.color[order], "opacity": batch.opacity[order]}
+    feat = R._feat_from(sa, torch.float32); mark("gather+feat")
+    emit_off = R._emit_offsets(rect, 0, batch.tiles_y); mark("emit_offsets")
+    offsets, entries = R._bin_all_tiles(rect, emit_off, batch.tiles_x, batch.tiles_y); mark("bin_all_tiles")
+    m = len(batch)
+    image = torch.empty((res, res, 3), dtype=torch.float32, device=dev)
+    t_final = torch.empty((res, res), dtype=torch.float32, device=dev)
+    n_last = torch.empty((res, res), dtype=torch.int32, device=dev)
+    n_contrib = torch.empty((res, res), dtype=torch.int32, device=dev)
+    touched_sorted = torch.zeros(m, dtype=torch.int64, device=dev)
+    R._raster_fwd(feat, offsets, entries, res, res, batch.tiles_x, None, (1.0, 1.0, 1.0), image,
+                  t_final, n_last, n_contrib, touched_sorted); mark("raster_fwd")
+    touched = torch.zeros(m, dtype=torch.int64, device=dev); touched[order] = touched_sorted
+    t64 = t_final.to(torch.float64); idx = batch.indices.clone(); mark("aux")
+    torch.cuda.synchronize()
+    print({tag: round(ev[i - 1][1].elapsed_time(e), 3) for i, (tag, e) in enumerate(ev) if i},
+          "m", m, "e", int(entries.numel()))
