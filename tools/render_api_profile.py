@@ -21,10 +21,15 @@ for rep in range(3):
     torch.cuda.synchronize(); mark("start")
     batch = P.project(cloud, cam); mark("project")
     order = R.sort_order(batch); mark("sort_order")
-    rect = torch.cat([batch.tile_min, batch.tile_max], 1).to(torch.int32)[order].contiguous()
-    sa = {"mean2d": batch.mean2d[order], "conic": batch.conic[order],
-          "color": batch.color[order], "opacity": batch.opacity[order]}
-    feat = R._feat_from(sa, torch.float32); mark("gather+feat")
+    m = len(batch)
+    rect = torch.empty((m, 4), dtype=torch.int32, device=dev)
+    feat = torch.empty((m, 12), dtype=torch.float32, device=dev)
+    R.L.check(R.L.lib().isg_gather_batch(m, R.L.ptr(order), R.L.ptr(batch.mean2d),
+                                         R.L.ptr(batch.conic), R.L.ptr(batch.color),
+                                         R.L.ptr(batch.opacity), R.L.ptr(batch.tile_min),
+                                         R.L.ptr(batch.tile_max), R.L.ISG_F32, R.L.ptr(feat),
+                                         R.L.ptr(rect), R.L.stream_ptr()), "gather")
+    mark("gather+feat")
     emit_off = R._emit_offsets(rect, 0, batch.tiles_y); mark("emit_offsets")
     offsets, entries = R._bin_all_tiles(rect, emit_off, batch.tiles_x, batch.tiles_y); mark("bin_all_tiles")
     m = len(batch)
