@@ -45,3 +45,31 @@ for rep in range(3):
     torch.cuda.synchronize()
     print({tag: round(ev[i - 1][1].elapsed_time(e), 3) for i, (tag, e) in enumerate(ev) if i},
           "m", m, "e", int(entries.numel()))
+
+# render_backward's steps
+img, aux, order = P.render_forward(P.project(cloud, cam), res, res)
+batch = P.project(cloud, cam)
+dl = torch.full((res, res, 3), 1e-3, dtype=torch.float32, device=dev)
+import ctypes
+for rep in range(2):
+    ev = []
+    def mark(tag):
+        e = torch.cuda.Event(enable_timing=True); e.record(); ev.append((tag, e))
+    torch.cuda.synchronize(); mark("start")
+    cache = aux.cache
+    o = R._dev(order, torch.int64)
+    ok = o.shape == cache["order"].shape and torch.equal(o, cache["order"])
+    ok2 = torch.equal(R._dev(aux.indices), R._dev(batch.indices)); mark("checks")
+    feat = cache["feat"]; e_ = int(cache["entries"].numel()); m = len(batch)
+    partials = torch.empty((max(e_, 1), 12), dtype=feat.dtype, device=dev)
+    bgc = (ctypes.c_double * 3)(*cache["background"])
+    R.L.check(R.L.lib().isg_raster_bwd(R.L.dtype_tag(feat.dtype), aux.width, aux.height, cache["tiles_x"], 0, cache["tiles_y"], None, 0, R.L.ptr(cache["offsets"]), R.L.ptr(cache["entries"]), R.L.ptr(feat), R.L.ptr(cache["rect"]), R.L.ptr(cache["emit_off"]), ctypes.cast(bgc, ctypes.c_void_p), R.L.ptr(cache["t_final"]), R.L.ptr(cache["n_last"]), R.L.ptr(dl), R.L.dtype_tag(dl.dtype), R.L.ptr(partials), R.L.stream_ptr()), "bwd"); mark("raster_bwd")
+    g2d = torch.zeros((m, 9), dtype=torch.float64, device=dev); gn = torch.zeros(m, dtype=torch.float64, device=dev)
+    R.L.check(R.L.lib().isg_reduce_ordered(R.L.dtype_tag(feat.dtype), m, R.L.ptr(cache["emit_off"]), R.L.ptr(partials), R.L.ptr(o.to(torch.int32)), None, 0, 0, 0, R.L.ptr(g2d), R.L.ptr(gn), R.L.stream_ptr()), "reduce"); mark("reduce")
+    n = cloud.count
+    rows = R._dev(batch.indices, torch.int64)
+    flags = torch.zeros(n, dtype=torch.uint8, device=dev); flags[rows] = 1
+    full = torch.zeros((n, 9), dtype=torch.float64, device=dev); full[rows] = g2d; mark("scatter")
+    R._chain(cloud, cam, flags, full); mark("chain")
+    torch.cuda.synchronize()
+    print({tag: round(ev[i - 1][1].elapsed_time(e), 3) for i, (tag, e) in enumerate(ev) if i})
