@@ -316,7 +316,9 @@ int isg_reduce_live(int64_t m, const int64_t *live_off, const float *partials,
  * clipped rect in row-major order, rects of <= 64 tiles) and counts[2] = live
  * total.  rect/feat (float32 SoA) or payload (64-byte rows).  isg_bin_emit_live
  * then writes the live (tile, slot) pairs compacted in rank order: keys[p] =
- * band tile, slot_rank[p] = rank for slot p in [0, live total). */
+ * band tile, slot_rank[p] = rank for slot p in [0, live total) (one thread
+ * per rank; emit_off is not read, kept for the call's symmetry with
+ * isg_bin_emit). */
 int isg_bin_count_live(void *workspace, size_t *ws_bytes, int64_t n, const uint64_t *sorted_keys,
                        const int32_t *order, const int32_t *rect, const int32_t *payload,
                        const float *feat, int32_t row_lo, int32_t row_hi, int32_t *rect_sorted,
