@@ -262,3 +262,30 @@ def test_fused_chain_adam_is_bitwise_the_separate_launches(densify):
         assert torch.equal(a.m[k], b.m[k]) and torch.equal(a.v[k], b.v[k]), k
     assert torch.equal(a.stats.seen, b.stats.seen)
     assert torch.equal(a.stats.grad_accum, b.stats.grad_accum)
+
+
+def test_training_step_beyond_65536_tiles():
+    """An 8192^2 image (262144 tiles): 4-byte tile keys through the live
+    emission, the tile sort, the offsets and the bucketed launch order; three
+    training steps run with finite losses."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200 import synthetic as S
+    from paper_2509_05216_b200.engine import Trainer
+    from paper_2509_05216_b200.training import TrainConfig, TrainDataset, PointCloud, build_schedule
+    dev = torch.device("cuda", 0)
+    res = 8192
+    nv = S.CONFIGS["config2"][4]
+    sched = build_schedule(3, nv, 0)
+    wl = S.make_workload("config2", dev, view_ids=sched, resolution=res)
+    ext = TrainDataset(wl.cameras, np.zeros((nv, 1, 1, 3)),
+                       PointCloud(wl.points, wl.normals)).scene_extent
+    tr = Trainer(P.cloud_from_points(wl.points, wl.log_scales, 1, dev), res, res,
+                 TrainConfig(iterations=3, densify=False), ext, dev)
+    for it in range(1, 4):
+        tr.step(it, wl.cameras[sched[it - 1]], wl.images_u8[it - 1])
+    torch.cuda.synchronize()
+    assert tr.r.n_tiles == 262144 and tr.r.live
+    losses = tr.loss_dev[1:4].cpu().numpy()
+    assert np.isfinite(losses).all() and (losses > 0).all()
+    off = tr.r.offsets.cpu().numpy()
+    assert off[0] == 0 and (np.diff(off) >= 0).all() and off[-1] > 0
