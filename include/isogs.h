@@ -324,6 +324,16 @@ int isg_bin_count_live(void *workspace, size_t *ws_bytes, int64_t n, const uint6
                        const float *feat, int32_t row_lo, int32_t row_hi, int32_t *rect_sorted,
                        float *feat_sorted, int64_t *emit_off, int64_t *live_off,
                        uint64_t *live_mask, int64_t *counts, void *stream);
+
+/* The training variant of isg_bin_count_live (float32 SoA rect/feat): no
+ * full-layout offsets (emit_off is not produced and counts[1] stays 0: the
+ * live lists never read them) and, when rank_of is given, the row -> rank
+ * inverse of isg_rank_of in the same pass. */
+int isg_bin_count_train(void *workspace, size_t *ws_bytes, int64_t n, const uint64_t *sorted_keys,
+                        const int32_t *order, const int32_t *rect, const float *feat,
+                        int32_t row_lo, int32_t row_hi, int32_t *rect_sorted, float *feat_sorted,
+                        int64_t *live_off, uint64_t *live_mask, int32_t *rank_of, int64_t *counts,
+                        void *stream);
 int isg_bin_emit_live(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,
                       const int64_t *live_off, const uint64_t *live_mask, const float *feat_sorted,
                       int32_t tiles_x, int32_t row_lo, int32_t row_hi, void *tile_keys,

@@ -26,11 +26,14 @@ __global__ void __launch_bounds__(GATHER_T) gather_rank_kernel(
     const int4 *__restrict__ rect, int rect_stride4, const float4 *__restrict__ feat,
     int feat_stride4, int feat_vec4, int row_lo, int row_hi, int4 *__restrict__ rect_sorted,
     float4 *__restrict__ feat_sorted, int64_t *__restrict__ cnt, int64_t *__restrict__ counts,
-    int64_t *__restrict__ cnt_live, uint64_t *__restrict__ live_mask) {
+    int64_t *__restrict__ cnt_live, uint64_t *__restrict__ live_mask,
+    int32_t *__restrict__ rank_of) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const uint64_t key = sorted_keys[r];
     const bool vis = key != ~0ull;
+    // the row -> rank inverse (isg_rank_of) while order[r] is at hand
+    if (rank_of) rank_of[order[r]] = vis ? (int32_t)r : -1;
     int64_t c = 0, cl = 0;
     uint64_t lm = 0;
     if (vis) {
@@ -59,7 +62,7 @@ __global__ void __launch_bounds__(GATHER_T) gather_rank_kernel(
     } else {
         rect_sorted[r] = make_int4(0, 0, -1, -1);
     }
-    cnt[r] = c;
+    if (cnt) cnt[r] = c;
     if (cnt_live) {
         cnt_live[r] = cl;
         if (live_mask) live_mask[r] = lm;
@@ -442,7 +445,8 @@ static int bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_
                      const float4 *feat, int feat_stride4, int vec4, int32_t row_lo,
                      int32_t row_hi, int32_t *rect_sorted, void *feat_sorted, int64_t *emit_off,
                      int64_t *counts, void *stream, bool live = false,
-                     int64_t *live_off = nullptr, uint64_t *live_mask = nullptr) {
+                     int64_t *live_off = nullptr, uint64_t *live_mask = nullptr,
+                     bool full_offsets = true, int32_t *rank_of = nullptr) {
     if (!ws_bytes || n < 0 || n > INT32_MAX || row_lo < 0 || row_hi < row_lo)
         return (int)cudaErrorInvalidValue;
     const size_t scan_bytes = scan_i64_ws_bytes(n > 0 ? n : 1);
@@ -456,7 +460,7 @@ static int bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(counts, 0, (live ? 3 : 2) * sizeof(int64_t), s);
     if (e != cudaSuccess) return (int)e;
-    e = cudaMemsetAsync(emit_off, 0, sizeof(int64_t), s);
+    if (full_offsets) e = cudaMemsetAsync(emit_off, 0, sizeof(int64_t), s);
     if (e == cudaSuccess && live_off) e = cudaMemsetAsync(live_off, 0, sizeof(int64_t), s);
     if (e != cudaSuccess) return (int)e;
     if (n == 0) return 0;
@@ -465,10 +469,14 @@ static int bin_count(void *workspace, size_t *ws_bytes, int64_t n, const uint64_
     void *scan_ws = (char *)workspace + (live_off ? 2 : 1) * cnt_bytes;
     gather_rank_kernel<<<blocks_for(n, GATHER_T), GATHER_T, 0, s>>>(
         n, sorted_keys, order, rect, rect_stride4, feat, feat_stride4, vec4, row_lo, row_hi,
-        (int4 *)rect_sorted, (float4 *)feat_sorted, cnt, counts, cnt_live, live_mask);
+        (int4 *)rect_sorted, (float4 *)feat_sorted, full_offsets ? cnt : nullptr, counts,
+        cnt_live, live_mask, rank_of);
     ISG_CHECK_LAUNCH();
-    int se = scan_i64(scan_ws, scan_bytes, n, cnt, emit_off, counts + 1, s);
-    if (se != 0) return se;
+    int se = 0;
+    if (full_offsets) {
+        se = scan_i64(scan_ws, scan_bytes, n, cnt, emit_off, counts + 1, s);
+        if (se != 0) return se;
+    }
     if (live_off) {
         se = scan_i64(scan_ws, scan_bytes, n, cnt_live, live_off, counts + 2, s);
         if (se != 0) return se;
@@ -502,6 +510,18 @@ extern "C" int isg_bin_count_live(void *workspace, size_t *ws_bytes, int64_t n,
     return bin_count(workspace, ws_bytes, n, sorted_keys, order, (const int4 *)rect, 1,
                      (const float4 *)feat, 3, 3, row_lo, row_hi, rect_sorted, feat_sorted,
                      emit_off, counts, stream, true, live_off, live_mask);
+}
+
+extern "C" int isg_bin_count_train(void *workspace, size_t *ws_bytes, int64_t n,
+                                   const uint64_t *sorted_keys, const int32_t *order,
+                                   const int32_t *rect, const float *feat, int32_t row_lo,
+                                   int32_t row_hi, int32_t *rect_sorted, float *feat_sorted,
+                                   int64_t *live_off, uint64_t *live_mask, int32_t *rank_of,
+                                   int64_t *counts, void *stream) {
+    if (workspace && (!live_off || !live_mask)) return (int)cudaErrorInvalidValue;
+    return bin_count(workspace, ws_bytes, n, sorted_keys, order, (const int4 *)rect, 1,
+                     (const float4 *)feat, 3, 3, row_lo, row_hi, rect_sorted, feat_sorted, nullptr,
+                     counts, stream, true, live_off, live_mask, false, rank_of);
 }
 
 extern "C" int isg_bin_emit_live(int64_t m, const int32_t *rect_sorted, const int64_t *emit_off,

@@ -196,9 +196,9 @@ class Rasterizer:
         self.live = live
         sz = ctypes.c_size_t(0)
         if live:
-            L.check(lib.isg_bin_count_live(None, ctypes.byref(sz), n, None, None, None, None,
-                                           None, 0, self.tiles_y, None, None, None, None, None,
-                                           None, None), "bin (size)")
+            L.check(lib.isg_bin_count_train(None, ctypes.byref(sz), n, None, None, None, None, 0,
+                                            self.tiles_y, None, None, None, None, None, None,
+                                            None), "bin (size)")
         else:
             L.check(lib.isg_bin_count(None, ctypes.byref(sz), n, None, None, None, None,
                                       self.ftag, 0, self.tiles_y, None, None, None, None, None),
@@ -206,20 +206,21 @@ class Rasterizer:
         ws = self.ws_bin.get(sz.value, self.device)
         sz = ctypes.c_size_t(ws.numel())
         if live:
-            L.check(lib.isg_bin_count_live(L.ptr(ws), ctypes.byref(sz), n, L.ptr(self.key_sorted),
-                                           L.ptr(self.order), L.ptr(self.rect), None,
-                                           L.ptr(self.feat), 0, self.tiles_y,
-                                           L.ptr(self.rect_sorted), L.ptr(self.feat_sorted),
-                                           L.ptr(self.emit_off), L.ptr(self.live_off),
-                                           L.ptr(self.live_mask), L.ptr(self.counts), s),
-                    "isg_bin_count_live")
+            # live lists only (no full-layout offsets), the rank inverse fused
+            L.check(lib.isg_bin_count_train(L.ptr(ws), ctypes.byref(sz), n,
+                                            L.ptr(self.key_sorted), L.ptr(self.order),
+                                            L.ptr(self.rect), L.ptr(self.feat), 0, self.tiles_y,
+                                            L.ptr(self.rect_sorted), L.ptr(self.feat_sorted),
+                                            L.ptr(self.live_off), L.ptr(self.live_mask),
+                                            L.ptr(self.rank_of) if self.ranked_grads else None,
+                                            L.ptr(self.counts), s), "isg_bin_count_train")
         else:
             L.check(lib.isg_bin_count(L.ptr(ws), ctypes.byref(sz), n, L.ptr(self.key_sorted),
                                       L.ptr(self.order), L.ptr(self.rect), L.ptr(self.feat),
                                       self.ftag, 0, self.tiles_y, L.ptr(self.rect_sorted),
                                       L.ptr(self.feat_sorted), L.ptr(self.emit_off),
                                       L.ptr(self.counts), s), "isg_bin_count")
-        if self.ranked_grads:
+        if self.ranked_grads and not live:
             L.check(lib.isg_rank_of(n, L.ptr(self.key_sorted), L.ptr(self.order),
                                     L.ptr(self.rank_of), s), "isg_rank_of")
         _mark(tm, "bin_count")
