@@ -368,12 +368,13 @@ def run_ours(args, world, rank, local):
 
     # kernels per step, all ours (no library kernels on the path): the ncu
     # launch list of one config-3 step (profiles/r02_final/launches.md) --
-    # preprocess, depth radix sort (5 x 4) + tie fix, gather with live counts
-    # + one scan (3; the rank inverse fused into the gather), live emission,
-    # tile radix sort (2 x 4), offsets, heavy-first order (1), raster fwd,
-    # loss (3), raster bwd, fused live fold + chain, Adam (+ the chunk items
-    # launch when the image is chunked, config 2)
-    launches_per_step = 44 + (1 if tr.r.chunks is not None else 0)
+    # preprocess, depth radix sort (5 passes x 3: upsweep, chunk scan with the
+    # sums scanned by its last CTA, scatter) + tie fix, gather with live
+    # counts and the rank inverse + one scan (2), live emission, tile radix
+    # sort (2 x 3), offsets, heavy-first order (1), raster fwd, loss (3),
+    # raster bwd, fused live fold + chain, Adam (+ the chunk items launch when
+    # the image is chunked, config 2)
+    launches_per_step = 36 + (1 if tr.r.chunks is not None else 0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

@@ -74,8 +74,10 @@ template <typename K, bool VEC>
 __global__ void __launch_bounds__(RT) upsweep_kernel(const K *__restrict__ keys, int64_t n,
                                                      int shift, unsigned mask, int nblk,
                                                      uint32_t *__restrict__ counts,
-                                                     const int64_t *__restrict__ n_dev) {
+                                                     const int64_t *__restrict__ n_dev,
+                                                     unsigned *__restrict__ done) {
     constexpr int IPC = ipc<K>(), IPT = ipt<K>();
+    if (done && blockIdx.x == 0 && threadIdx.x == 0) *done = 0u;  // the scan's arrival counter
     if (n_dev) n = min(n, *n_dev);  // device-side item count (upper bound n)
     __shared__ uint32_t h[NWARP][BINS];
     const int warp = threadIdx.x >> 5;
@@ -111,7 +113,8 @@ __global__ void __launch_bounds__(RT) upsweep_kernel(const K *__restrict__ keys,
 // chunk total to sums.  Coalesced through shared memory.
 template <typename T>
 __global__ void __launch_bounds__(RT) scan_chunks_kernel(const T *in, T *out, int64_t n,
-                                                         T *__restrict__ sums) {
+                                                         T *__restrict__ sums,
+                                                         unsigned *__restrict__ done) {
     constexpr int PER = SC / RT;  // elements per thread (contiguous in shared memory)
     // one pad element per PER: thread t's run starts t * (PER + 1) elements in,
     // so a warp's lanes read different banks (unpadded, every lane of the
@@ -160,41 +163,44 @@ __global__ void __launch_bounds__(RT) scan_chunks_kernel(const T *in, T *out, in
         const int64_t i = cb + k * RT + threadIdx.x;
         if (i < n) out[i] = sm[at(k * RT + threadIdx.x)];
     }
-    if (threadIdx.x == 0) sums[blockIdx.x] = total;
-}
-
-// One CTA: exclusive scan of the chunk sums in place (any count), optional total.
-template <typename T>
-__global__ void __launch_bounds__(1024) scan_sums_kernel(T *__restrict__ sums, int64_t m,
-                                                         T *__restrict__ total) {
-    __shared__ T swarp[32];
-    __shared__ T scarry;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) scarry = 0;
+    // the last CTA to finish scans the chunk sums in place (no separate
+    // launch); done: an arrival counter that starts at 0 and is left at 0
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+        sums[blockIdx.x] = total;
+        if (done) {
+            __threadfence();
+            s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+        }
+    }
+    if (!done) return;
     __syncthreads();
-    for (int64_t c0 = 0; c0 < m; c0 += 1024) {
-        const int64_t i = c0 + threadIdx.x;
-        const T v = i < m ? sums[i] : (T)0;
-        T x = v;
+    if (!s_last) return;
+    __threadfence();
+    const int m = (int)gridDim.x;
+    T carry = 0;
+    for (int c0 = 0; c0 < m; c0 += RT) {
+        const int i = c0 + threadIdx.x;
+        const T v = i < m ? reinterpret_cast<volatile T *>(sums)[i] : (T)0;
+        T y = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const T y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+            const T z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z;
         }
-        if (lane == 31) swarp[warp] = x;
+        if (lane == 31) swarp[warp] = y;
         __syncthreads();
-        T before = scarry;
-        T tot = 0;
-        for (int w = 0; w < 32; w++) {
-            if (w < warp) before += swarp[w];
+        T pre = carry, tot = 0;
+#pragma unroll
+        for (int w = 0; w < NWARP; w++) {
+            if (w < warp) pre += swarp[w];
             tot += swarp[w];
         }
-        if (i < m) sums[i] = before + x - v;
-        __syncthreads();
-        if (threadIdx.x == 0) scarry += tot;
+        if (i < m) sums[i] = pre + y - v;
+        carry += tot;
         __syncthreads();
     }
-    if (total && threadIdx.x == 0) *total = scarry;
+    if (threadIdx.x == 0) *done = 0u;
 }
 
 template <typename K, bool VEC>
@@ -428,7 +434,8 @@ size_t sort_ws_bytes(int64_t n) {
     const int64_t nc = (int64_t)BINS * nblk;
     const int64_t nch = (nc + SC - 1) / SC;
     return al(sizeof(K) * (size_t)n) + al(sizeof(int32_t) * (size_t)n) +
-           al(sizeof(uint32_t) * (size_t)nc) + al(sizeof(uint32_t) * (size_t)(nch + 1));
+           al(sizeof(uint32_t) * (size_t)nc) + al(sizeof(uint32_t) * (size_t)(nch + 1)) +
+           al(sizeof(unsigned));
 }
 
 template <typename K>
@@ -455,6 +462,8 @@ int sort_pairs(void *ws, size_t *ws_bytes, const K *keys_in, K *keys_out,
     uint32_t *counts = (uint32_t *)p;
     p += al(sizeof(uint32_t) * (size_t)nc);
     uint32_t *csum = (uint32_t *)p;
+    p += al(sizeof(uint32_t) * (size_t)(nch + 1));
+    unsigned *done = (unsigned *)p;  // zeroed by the first upsweep CTA each pass
     const int passes = (b1 - b0 + 7) / 8;
     for (auto fn : {scatter_kernel<K, true>, scatter_kernel<K, false>,
                     scatter_staged_kernel<K, true>, scatter_staged_kernel<K, false>}) {
@@ -478,14 +487,12 @@ int sort_pairs(void *ws, size_t *ws_bytes, const K *keys_in, K *keys_out,
         const bool vec = ((uintptr_t)src_k % 16 == 0) && ((uintptr_t)src_v % 16 == 0);
         if (vec)
             upsweep_kernel<K, true><<<(unsigned)nblk, RT, 0, s>>>(src_k, n, shift, mask,
-                                                                  (int)nblk, counts, n_dev);
+                                                                  (int)nblk, counts, n_dev, done);
         else
             upsweep_kernel<K, false><<<(unsigned)nblk, RT, 0, s>>>(src_k, n, shift, mask,
-                                                                   (int)nblk, counts, n_dev);
+                                                                   (int)nblk, counts, n_dev, done);
         ISG_CHECK_LAUNCH();
-        scan_chunks_kernel<uint32_t><<<(unsigned)nch, RT, 0, s>>>(counts, counts, nc, csum);
-        ISG_CHECK_LAUNCH();
-        scan_sums_kernel<uint32_t><<<1, 1024, 0, s>>>(csum, nch, nullptr);
+        scan_chunks_kernel<uint32_t><<<(unsigned)nch, RT, 0, s>>>(counts, counts, nc, csum, done);
         ISG_CHECK_LAUNCH();
         if (!staged<K>())
             scatter_kernel<K, true><<<(unsigned)nblk, RT, scatter_smem<K>(), s>>>(
@@ -508,7 +515,8 @@ int sort_pairs(void *ws, size_t *ws_bytes, const K *keys_in, K *keys_out,
 // Exclusive int64 scan: off[0] = 0, off[i + 1] = cnt[0] + ... + cnt[i]; total
 // (device, optional) = off[n].  Workspace: the chunk sums.
 size_t scan_i64_ws_bytes(int64_t n) {
-    return radix::al(sizeof(int64_t) * (size_t)((n + radix::SC - 1) / radix::SC + 1));
+    return radix::al(sizeof(int64_t) * (size_t)((n + radix::SC - 1) / radix::SC + 1)) +
+           radix::al(sizeof(unsigned));
 }
 
 
@@ -536,9 +544,11 @@ int scan_i64(void *ws, size_t ws_bytes, int64_t n, const int64_t *cnt, int64_t *
     }
     const int64_t nch = (n + radix::SC - 1) / radix::SC;
     int64_t *csum = (int64_t *)ws;
-    radix::scan_chunks_kernel<int64_t><<<(unsigned)nch, radix::RT, 0, s>>>(cnt, off, n, csum);
-    ISG_CHECK_LAUNCH();
-    radix::scan_sums_kernel<int64_t><<<1, 1024, 0, s>>>(csum, nch, nullptr);
+    unsigned *done = (unsigned *)((char *)ws + radix::al(sizeof(int64_t) * (size_t)(nch + 1)));
+    cudaError_t e = cudaMemsetAsync(done, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return (int)e;
+    radix::scan_chunks_kernel<int64_t><<<(unsigned)nch, radix::RT, 0, s>>>(cnt, off, n, csum,
+                                                                            done);
     ISG_CHECK_LAUNCH();
     scan_tail_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, off, csum, cnt, total);
     ISG_CHECK_LAUNCH();

@@ -53,13 +53,13 @@ TILE = 16
 CANON_ROWS = 2
 # our kernels per sharded step at config 3 (every launch is ours; counted
 # from the code path, as the single-GPU count is from its ncu launch list):
-# preprocess, route plan + scan, pack, depth radix sort (5 passes x 4 + tie
-# fix), band binning with live counts (gather + 2 scans x 3), live emission,
-# tile radix sort (2 x 4), offsets, heavy-first order (1), raster fwd, loss
-# (3) + band cost, raster bwd, band blocks + scan (3), band fold, owner
+# preprocess, route plan + scan, pack, depth radix sort (5 passes x 3 + tie
+# fix), band binning with live counts (gather + 2 scans x 2), live emission,
+# tile radix sort (2 x 3), offsets, heavy-first order (1), raster fwd, loss
+# (3) + band cost, raster bwd, band blocks + scan (2), band fold, owner
 # fold, chain, Adam.  The exchange barriers / halo copies / NCCL collectives
-# are not counted.
-LAUNCHES_PER_STEP = 57
+# and memsets are not counted.
+LAUNCHES_PER_STEP = 47
 
 
 class ProtocolError(RuntimeError):
