@@ -428,6 +428,9 @@ __device__ __forceinline__ float rcpa(float x) {
 // s1 = sum dp d1, s2 = sum dp d1^2; d0 is shared), turned into linear moments
 // by moment_terms; s0 also carries the opacity term (dopacity = sum dalpha g
 // = s0 / o, divided once per (tile, entry) in the fold).
+#ifndef BWD_FLAT_CLAMP
+#define BWD_FLAT_CLAMP 0
+#endif
 __device__ __forceinline__ void pair_grad(float a, float og, float d1, float wc, float wr,
                                           float wg, float wb, float &T, float &Q, float (&v)[9],
                                           float &s0, float &s1, float &s2) {
@@ -439,6 +442,14 @@ __device__ __forceinline__ void pair_grad(float a, float og, float d1, float wc,
     v[7] = fmaf(wb, at, v[7]);
     const float dalpha = fmaf(wc, ti, -(Q * inv));
     Q = fmaf(wc, at, Q);
+#if BWD_FLAT_CLAMP
+    // clamped alpha: zero sub-gradient, as a select instead of a branch
+    const float dp = og > 0.99f ? 0.0f : dalpha * og;
+    const float t = dp * d1;
+    s0 += dp;
+    s1 += t;
+    s2 = fmaf(t, d1, s2);
+#else
     if (!(og > 0.99f)) {  // clamped alpha: zero sub-gradient
         const float dp = dalpha * og;
         const float t = dp * d1;
@@ -446,6 +457,7 @@ __device__ __forceinline__ void pair_grad(float a, float og, float d1, float wc,
         s1 += t;
         s2 = fmaf(t, d1, s2);
     }
+#endif
     T = ti;
 }
 
@@ -480,6 +492,9 @@ __device__ __forceinline__ void moment_terms(float d0, float s0, float s1, float
 // of the other; it waits only when its ring slot has not been folded yet.
 #ifndef BWD_RING
 #define BWD_RING 4
+#endif
+#ifndef BWD_FLAT_ALPHA
+#define BWD_FLAT_ALPHA 1
 #endif
 constexpr int RING = BWD_RING;
 
@@ -638,6 +653,18 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
             const float4 col = lds4(a_col + 16 * slot);
 #pragma unroll
             for (int q = 0; q < 4; q++) {
+#if BWD_FLAT_ALPHA
+                // the exponent for every pixel (no early-exit branch), one
+                // branch per pixel on the forward's exact decision
+                const float d1 = fpy[q] - g4.y;
+                const float power = __fmaf_rn(d1, __fmaf_rn(h4.x, d1, B), A);
+                const float og = __fmul_rn(h4.z, ex2a(power));
+                const float a = fminf(og, 0.99f);
+                if (jj < last[q] && !(power > 0.0f) && a >= (1.0f / 255.0f)) {
+                    const float wc = fmaf(wb[q], col.z, fmaf(wg[q], col.y, wr[q] * col.x));
+                    pair_grad(a, og, d1, wc, wr[q], wg[q], wb[q], T[q], Q[q], v, s0, s1, s2);
+                }
+#else
                 if (jj < last[q]) {
                     float og;
                     const float d1 = fpy[q] - g4.y;
@@ -647,6 +674,7 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
                         pair_grad(a, og, d1, wc, wr[q], wg[q], wb[q], T[q], Q[q], v, s0, s1, s2);
                     }
                 }
+#endif
             }
             moment_terms(d0, s0, s1, s2, v);
             const float y = bfly9(v, lane);
