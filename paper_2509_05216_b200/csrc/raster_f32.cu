@@ -491,7 +491,7 @@ __device__ __forceinline__ void moment_terms(float d0, float s0, float s1, float
 // padded record per (tile, entry).  A warp may run up to RING-1 batches ahead
 // of the other; it waits only when its ring slot has not been folded yet.
 #ifndef BWD_RING
-#define BWD_RING 4
+#define BWD_RING 3
 #endif
 #ifndef BWD_FLAT_ALPHA
 #define BWD_FLAT_ALPHA 1
