@@ -18,7 +18,11 @@
 //
 // Backward: one 64-thread CTA per tile, warp h owns 16x8 half h, four pixels
 // per lane; contributors walked back to front (T recovered by division from
-// T_final).  The 9 gradient terms of an entry are reduced over the warp with a
+// T_final).  Each pixel's exponent and alpha are computed unconditionally and
+// a single branch on the forward's exact decision guards its gradient update
+// (an early exit on the exponent would nest a second divergent branch per
+// pixel, whose reconvergence costs more than the exp it saves).  The 9
+// gradient terms of an entry are reduced over the warp with a
 // butterfly reduce-scatter; the last warp to finish a batch folds both halves'
 // sums in fixed order into the entry's (tile, splat) subtotal.  Deterministic
 // throughout, no atomics on the data path.
