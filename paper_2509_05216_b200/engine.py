@@ -360,11 +360,13 @@ EXACT_ORDER = os.environ.get("ISOGS_EXACT_ORDER", "0") != "0"
 
 
 def heavy_first_order(st, n_tiles: int, offsets: torch.Tensor):
-    """Launch order of the raster pair, heaviest tile lists first
-    (isg_tile_order_keys + a 16-bit stable sort): with one CTA per tile, a
-    long list launched last runs alone at the end of the kernel; launched
-    first it overlaps the light ones.  `st` holds the scratch buffers and the
-    heavy_first switch.  Returns None (list order) when off."""
+    """Launch order of the raster pair, heaviest tile lists first (one launch,
+    isg_tile_order: tiles bucketed by list length; EXACT_ORDER / HEAVY_PCT:
+    isg_tile_order_keys + a 16-bit stable sort): with one CTA per tile, a long
+    list launched last runs alone at the end of the kernel; launched first it
+    overlaps the light ones.  The order is the launch order only -- results
+    do not depend on it.  `st` holds the scratch buffers and the heavy_first
+    switch.  Returns None (list order) when off."""
     if not st.heavy_first or n_tiles < 2:
         return None
     lib = L.lib()
@@ -387,15 +389,6 @@ def heavy_first_order(st, n_tiles: int, offsets: torch.Tensor):
     return st.to_order
 
 
-# Backward list chunking: entries per backward work item (isg_chunks).  A
-# constant, so the chunking of every tile is the same for any band partition
-# (bitwise W-invariance); 0: off (one CTA per tile, no restarts).
-# Measured (tools/ab_chunk.sh, profiles/r02_chunk): chunks of 512 take config
-# 2's backward 1.14 -> 0.91 ms and an emulated W=8 band's 1.03 -> 0.80 ms,
-# but config 3's 3.88 -> 4.35 ms (more, shorter CTAs lower the achieved
-# occupancy); a variant that keeps one CTA per tile and restarts it at the
-# chunk boundaries (same arithmetic as split chunks, so the split could follow
-# the launch size) costs 3.78 -> 4.62 ms at config 3.  Off by default.
 # Backward list chunking: ISOGS_CHUNK=<entries> forces a chunk size (0: off).
 # By default (auto) the chunk follows the IMAGE's tile count, never the
 # launch's: images of few tiles (config 2: 4096 tiles, about 2 waves of

@@ -289,3 +289,39 @@ def test_training_step_beyond_65536_tiles():
     assert np.isfinite(losses).all() and (losses > 0).all()
     off = tr.r.offsets.cpu().numpy()
     assert off[0] == 0 and (np.diff(off) >= 0).all() and off[-1] > 0
+
+
+def test_launch_order_changes_no_result():
+    """The raster pair's launch order (heaviest lists first: the one-launch
+    bucketed order, the exact 16-bit sort, or plain list order) is the launch
+    order only: losses and parameters after 4 iterations are bitwise equal."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200 import engine as E
+    from paper_2509_05216_b200.engine import Trainer
+    d = load("config1")
+    ds = _dataset(d, "images_u8", d["images_u8"].shape[0])
+    cfg = P.TrainConfig(iterations=4, densify=False, seed=0)
+    gt = _images(ds)
+    sched = P.build_schedule(4, ds.view_count, 0)
+    saved = E.EXACT_ORDER
+    runs = []
+    try:
+        for heavy, exact in ((True, False), (True, True), (False, False)):
+            E.EXACT_ORDER = exact
+            t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
+            t.r.heavy_first = heavy
+            for it in range(1, 5):
+                t.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
+            torch.cuda.synchronize()
+            order = t.r.tile_order.clone() if t.r.tile_order is not None else None
+            runs.append((t, order))
+    finally:
+        E.EXACT_ORDER = saved
+    (a, oa), (b, ob), (c, oc) = runs
+    n = a.r.n_tiles
+    assert oc is None and sorted(oa[:n].tolist()) == list(range(n))
+    assert sorted(ob[:n].tolist()) == list(range(n))
+    for t in (b, c):
+        assert torch.equal(a.loss_dev, t.loss_dev)
+        for k in P.PARAM_NAMES:
+            assert torch.equal(getattr(a.cloud, k), getattr(t.cloud, k)), k
