@@ -560,6 +560,10 @@ class PeerBuffers:
         self.cap_r = self.cap_g = 0
         self.buf = self.h = None
         self.ptrs = [0] * world
+        # a first buffer now, so a box without peer mappings fails here (where
+        # the caller can fall back to the point-to-point exchange), not mid-step
+        self.ensure(1 << 16, 1 << 16)
+        self.barrier()
 
     def ensure(self, need_r: int, need_g: int) -> None:
         if need_r <= self.cap_r and need_g <= self.cap_g and self.buf is not None:
