@@ -1536,10 +1536,15 @@ def run_training_distributed(dataset, config, workers: int, init_cloud=None, eva
     if not dist.is_initialized():
         raise RuntimeError("workers > 1 needs torch.distributed (launch with torchrun, one "
                            "process per GPU)")
-    comm = TorchComm()
+    dev = L.require_cuda()
+    exchange = getattr(config, "exchange", "peer")
+    try:
+        comm = TorchComm(peers=exchange == "peer", height=dataset.height, width=dataset.width,
+                         device=dev)
+    except Exception:  # no symmetric memory / peer mappings: point-to-point copies
+        comm = TorchComm(peers=False)
     if comm.world != workers:
         raise ValueError(f"workers={workers} but WORLD_SIZE={comm.world}")
-    dev = L.require_cuda()
     if init_cloud is None:
         pts = np.asarray(dataset.points.positions, dtype=np.float64)
         cloud = cloud_from_points(pts, init_log_scales(pts), config.sh_degree, dev)
