@@ -78,6 +78,13 @@ typedef struct isg_preprocess_out {
 int isg_preprocess(const isg_params *p, const isg_camera *cam, int32_t tile_size,
                    const isg_preprocess_out *out, void *stream);
 
+/* isg_preprocess with the camera in DEVICE memory (an isg_camera the caller
+ * uploads before the launch), float32 parameters and features: a launch that
+ * can be captured into a CUDA graph and replayed for every view. */
+int isg_preprocess_devcam(const isg_params *p, const isg_camera *cam_dev, int32_t width,
+                          int32_t height, int32_t tile_size, const isg_preprocess_out *out,
+                          void *stream);
+
 /* Stable radix sort of (uint64 key, int32 value) pairs over key bits
  * [begin_bit, end_bit).  Replaces np.lexsort((indices, depth))
  * (rasterizer.py:161-163, engine.py:214) when values are in index order.

@@ -121,6 +121,8 @@ SIGNATURES = {
     "isg_band_fold_peer": [_I64, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P],
     "isg_route_pack_peer": [_I64, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P],
     "isg_copy": [_P, _P, _I64, _P],
+    "isg_preprocess_devcam": [ctypes.POINTER(Params_t), _P, _I32, _I32, _I32,
+                              ctypes.POINTER(PreprocessOut_t), _P],
     "isg_bin_count_train": [_P, _SZ, _I64, _P, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P,
                             _P],
     "isg_compact_count": [_P, _SZ, _I64, _P, _P, _P],

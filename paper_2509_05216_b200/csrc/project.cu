@@ -36,12 +36,16 @@ template <typename P, typename F>
 #ifndef PRE_MINB
 #define PRE_MINB 8
 #endif
-__global__ void __launch_bounds__(128, PRE_MINB) preprocess_kernel(isg_params p, Cam cam, int tile,
+__global__ void __launch_bounds__(128, PRE_MINB) preprocess_kernel(isg_params p, Cam cam_val, int tile,
                                                          int tiles_x, int tiles_y, uint64_t *key,
                                                          int4 *rect, F *feat, uint8_t *flag,
-                                                         double *full64) {
+                                                         double *full64,
+                                                         const Cam *__restrict__ cam_dev) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= p.n) return;
+    // the camera by value, or from device memory (a graph-captured launch
+    // whose camera is uploaded before each replay)
+    const Cam cam = cam_dev ? *cam_dev : cam_val;
     Row<P> row;
     load_row<P>(p, i, row);
     Proj o;
@@ -503,21 +507,43 @@ extern "C" int isg_preprocess(const isg_params *p, const isg_camera *cam, int32_
     if (p->dtype == ISG_F32 && out->feat_dtype == ISG_F32)
         preprocess_kernel<float, float><<<grid, 128, 0, s>>>(*p, c, tile_size, tiles_x, tiles_y,
                                                              out->key, rect, (float *)out->feat,
-                                                             out->flag, out->full64);
+                                                             out->flag, out->full64, nullptr);
     else if (p->dtype == ISG_F32 && out->feat_dtype == ISG_F64)
         preprocess_kernel<float, double><<<grid, 128, 0, s>>>(*p, c, tile_size, tiles_x, tiles_y,
                                                               out->key, rect, (double *)out->feat,
-                                                              out->flag, out->full64);
+                                                              out->flag, out->full64, nullptr);
     else if (p->dtype == ISG_F64 && out->feat_dtype == ISG_F32)
         preprocess_kernel<double, float><<<grid, 128, 0, s>>>(*p, c, tile_size, tiles_x, tiles_y,
                                                               out->key, rect, (float *)out->feat,
-                                                              out->flag, out->full64);
+                                                              out->flag, out->full64, nullptr);
     else if (p->dtype == ISG_F64 && out->feat_dtype == ISG_F64)
         preprocess_kernel<double, double><<<grid, 128, 0, s>>>(
             *p, c, tile_size, tiles_x, tiles_y, out->key, rect, (double *)out->feat, out->flag,
-            out->full64);
+            out->full64, nullptr);
     else
         return (int)cudaErrorInvalidValue;
+    ISG_CHECK_LAUNCH();
+    return 0;
+}
+
+// isg_preprocess with the camera read from device memory (an isg_camera
+// there, uploaded by the caller before the launch): the launch can be
+// captured into a CUDA graph and replayed for any view.  Float32 parameters
+// and features.
+extern "C" int isg_preprocess_devcam(const isg_params *p, const isg_camera *cam_dev,
+                                     int32_t width, int32_t height, int32_t tile_size,
+                                     const isg_preprocess_out *out, void *stream) {
+    static_assert(sizeof(Cam) == sizeof(isg_camera), "Cam mirrors isg_camera");
+    if (!p || !cam_dev || !out || tile_size != TILE || p->n < 0 || width <= 0 || height <= 0 ||
+        p->dtype != ISG_F32 || out->feat_dtype != ISG_F32)
+        return (int)cudaErrorInvalidValue;
+    if (p->n == 0) return 0;
+    if (!out->key || !out->rect || !out->flag || !out->feat) return (int)cudaErrorInvalidValue;
+    const int tiles_x = (width + tile_size - 1) / tile_size;
+    const int tiles_y = (height + tile_size - 1) / tile_size;
+    preprocess_kernel<float, float><<<dim3(blocks_for(p->n, 128)), 128, 0, (cudaStream_t)stream>>>(
+        *p, Cam{}, tile_size, tiles_x, tiles_y, out->key, reinterpret_cast<int4 *>(out->rect),
+        (float *)out->feat, out->flag, out->full64, reinterpret_cast<const Cam *>(cam_dev));
     ISG_CHECK_LAUNCH();
     return 0;
 }

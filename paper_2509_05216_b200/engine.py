@@ -131,6 +131,7 @@ class Rasterizer:
         self.fuse_fold = os.environ.get("ISOGS_FUSE_FOLD", "1") != "0"
         self.keep_grad2d = False
         self.keep_grads = False  # store the parameter gradients (fused Adam)
+        self.graph = self.graph_key = None  # the captured pre-sync launches
         self.partials = None
         self.to_keys = self.to_vals = self.to_keys_s = self.to_order = None
         self.tile_order = None
@@ -168,32 +169,21 @@ class Rasterizer:
         self.counts = torch.zeros(3, dtype=torch.int64, device=dev)
         self.grad2d = torch.empty((n, 9), dtype=torch.float64, device=dev)
 
-    # -- forward ---------------------------------------------------------
-    def forward(self, cloud: GaussianCloud, cam) -> ViewContext:
+    def _presync(self, p, out, live: bool, n: int, tm, cam_dev=None) -> None:
+        """The step's launches before its one host read: preprocess, depth
+        sort, binning (live counts, the rank inverse)."""
         lib = L.lib()
         s = L.stream_ptr()
-        n = cloud.count
-        if n != self.n:
-            self.resize(n)
-        out = L.PreprocessOut_t()
-        out.key, out.rect, out.feat = L.ptr(self.key), L.ptr(self.rect), L.ptr(self.feat)
-        out.flag, out.full64, out.feat_dtype = L.ptr(self.flag), None, self.ftag
-        p = L.Params_t()
-        p.positions, p.log_scales = L.ptr(cloud.positions), L.ptr(cloud.log_scales)
-        p.rotations, p.opacity_logits = L.ptr(cloud.rotations), L.ptr(cloud.opacity_logits)
-        p.sh, p.n, p.degree, p.dtype = L.ptr(cloud.sh_coeffs), n, cloud.degree, L.ISG_F32
-        self.cam_struct = L.camera_struct(cam)
-        tm = self.timer
-        _mark(tm, "begin")
-        L.check(lib.isg_preprocess(ctypes.byref(p), ctypes.byref(self.cam_struct), TILE,
-                                   ctypes.byref(out), s), "isg_preprocess")
+        if cam_dev is not None:
+            L.check(lib.isg_preprocess_devcam(ctypes.byref(p), L.ptr(cam_dev), self.width,
+                                              self.height, TILE, ctypes.byref(out), s),
+                    "isg_preprocess_devcam")
+        else:
+            L.check(lib.isg_preprocess(ctypes.byref(p), ctypes.byref(self.cam_struct), TILE,
+                                       ctypes.byref(out), s), "isg_preprocess")
         _mark(tm, "preprocess")
         L.sort_depth(self.key, self.vals0, self.ws_sort, self.key_sorted, self.order)
         _mark(tm, "sort_depth")
-        # float32 training lists are live-only: a (tile, splat) pair no pixel of
-        # the tile can composite has no list entry and no subtotal slot
-        live = self.use_cmask and self.feat_dtype == torch.float32
-        self.live = live
         sz = ctypes.c_size_t(0)
         if live:
             L.check(lib.isg_bin_count_train(None, ctypes.byref(sz), n, None, None, None, None, 0,
@@ -223,6 +213,59 @@ class Rasterizer:
         if self.ranked_grads and not live:
             L.check(lib.isg_rank_of(n, L.ptr(self.key_sorted), L.ptr(self.order),
                                     L.ptr(self.rank_of), s), "isg_rank_of")
+
+    def _presync_graph(self, cloud, p, out) -> None:
+        """_presync as one CUDA graph replay: the launches depend only on the
+        Gaussian count and the buffers, the camera is uploaded to device
+        memory before each replay.  Captured after one eager run (which
+        sizes every workspace) and re-captured when the cloud changes."""
+        n = cloud.count
+        key = (n, cloud.degree, L.ptr(cloud.positions), L.ptr(cloud.log_scales),
+               L.ptr(cloud.rotations), L.ptr(cloud.opacity_logits), L.ptr(cloud.sh_coeffs),
+               L.ptr(self.key), self.ranked_grads)
+        nb = ctypes.sizeof(L.Camera_t)
+        if getattr(self, "cam_dev", None) is None:
+            self.cam_dev = torch.empty(nb, dtype=torch.uint8, device=self.device)
+            self.cam_pin = torch.empty(nb, dtype=torch.uint8).pin_memory()
+        ctypes.memmove(self.cam_pin.data_ptr(), ctypes.addressof(self.cam_struct), nb)
+        self.cam_dev.copy_(self.cam_pin, non_blocking=True)
+        if self.graph is not None and self.graph_key == key:
+            self.graph.replay()
+            return
+        # eager run for this step (sizes the workspaces), then capture
+        self._presync(p, out, True, n, None, self.cam_dev)
+        self.graph = None
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            self._presync(p, out, True, n, None, self.cam_dev)
+        self.graph, self.graph_key = g, key
+
+    # -- forward ---------------------------------------------------------
+    def forward(self, cloud: GaussianCloud, cam) -> ViewContext:
+        lib = L.lib()
+        s = L.stream_ptr()
+        n = cloud.count
+        if n != self.n:
+            self.resize(n)
+        out = L.PreprocessOut_t()
+        out.key, out.rect, out.feat = L.ptr(self.key), L.ptr(self.rect), L.ptr(self.feat)
+        out.flag, out.full64, out.feat_dtype = L.ptr(self.flag), None, self.ftag
+        p = L.Params_t()
+        p.positions, p.log_scales = L.ptr(cloud.positions), L.ptr(cloud.log_scales)
+        p.rotations, p.opacity_logits = L.ptr(cloud.rotations), L.ptr(cloud.opacity_logits)
+        p.sh, p.n, p.degree, p.dtype = L.ptr(cloud.sh_coeffs), n, cloud.degree, L.ISG_F32
+        self.cam_struct = L.camera_struct(cam)
+        tm = self.timer
+        _mark(tm, "begin")
+        # float32 training lists are live-only: a (tile, splat) pair no pixel of
+        # the tile can composite has no list entry and no subtotal slot
+        live = self.use_cmask and self.feat_dtype == torch.float32
+        self.live = live
+        if GRAPH and live and tm is None and n:
+            self._presync_graph(cloud, p, out)
+        else:
+            self._presync(p, out, live, n, tm)
         _mark(tm, "bin_count")
         self.counts_host.copy_(self.counts, non_blocking=True)
         torch.cuda.current_stream().synchronize()
@@ -346,6 +389,9 @@ class Rasterizer:
 # Tiles whose list is at least HEAVY_PCT % of the mean length launch first
 # (longest first); the rest keep row-major order (0: all by length).
 HEAVY_PCT = int(os.environ.get("ISOGS_HEAVY_PCT", "0"))
+# the step's launches before its host read (preprocess, depth sort, binning)
+# as one CUDA graph replay (ISOGS_GRAPH=0: eager launches)
+GRAPH = os.environ.get("ISOGS_GRAPH", "1") != "0"
 # chain rule + stats + Adam in one pass (the gradients stay in registers;
 # isg_chain_fold_adam).  Off by default: measured slower at config 3 (1.14 ms
 # against 0.63 + 0.39 ms for the fold-chain and the dense Adam launches) --

@@ -325,3 +325,37 @@ def test_launch_order_changes_no_result():
         assert torch.equal(a.loss_dev, t.loss_dev)
         for k in P.PARAM_NAMES:
             assert torch.equal(getattr(a.cloud, k), getattr(t.cloud, k)), k
+
+
+def test_graph_captured_presync_equals_eager():
+    """The pre-sync launches as a CUDA graph replay (camera uploaded to device
+    memory, re-captured when densify replaces the cloud) == eager launches:
+    losses, parameters and statistics bitwise over 6 iterations."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200 import engine as E
+    from paper_2509_05216_b200.engine import Trainer
+    d = load("config1")
+    ds = _dataset(d, "images_u8", d["images_u8"].shape[0])
+    cfg = P.TrainConfig(iterations=6, densify_start=2, densify_interval=2, densify_stop=5, seed=0)
+    gt = _images(ds)
+    sched = P.build_schedule(6, ds.view_count, 0)
+    saved = E.GRAPH
+    runs = []
+    try:
+        for graph in (True, False):
+            E.GRAPH = graph
+            t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
+            for it in range(1, 7):
+                t.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
+                if t.densify_due(it):
+                    t.densify(it)
+            torch.cuda.synchronize()
+            runs.append(t)
+    finally:
+        E.GRAPH = saved
+    a, b = runs
+    assert a.r.graph is not None and b.r.graph is None
+    assert torch.equal(a.loss_dev, b.loss_dev)
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(a.cloud, k), getattr(b.cloud, k)), k
+    assert torch.equal(a.stats.seen, b.stats.seen)
