@@ -121,3 +121,34 @@ def test_sharded_densify_bitwise_equals_single_gpu(workers, peers):
     assert losses == ref_losses, (losses, ref_losses)
     for k in P.PARAM_NAMES:
         assert torch.equal(getattr(got, k), getattr(ref_cloud, k)), k
+
+
+@pytest.mark.parametrize("peers", [False, True], ids=["p2p_copies", "peer_stores"])
+def test_sharded_step_with_nothing_visible(peers):
+    """A view that sees no Gaussian (camera turned 180 degrees about its y
+    axis) between ordinary ones: every rank routes, packs and renders nothing,
+    and the W=3 run stays bitwise the single-GPU run."""
+    from paper_2509_05216_b200 import distributed as D
+    from paper_2509_05216_b200.engine import Trainer
+    P, d, cams, gt, cloud = _setup()
+    iters, canon = 4, 1
+    sched = P.build_schedule(iters, len(cams), 0)
+    c0 = cams[sched[1]]
+    flip = np.diag([-1.0, 1.0, -1.0])
+    away = P.Camera(flip @ np.asarray(c0.rotation), flip @ np.asarray(c0.translation),
+                    c0.fx, c0.fy, c0.cx, c0.cy, c0.width, c0.height)
+    views = [cams[sched[0]], away, cams[sched[2]], away]
+    cfg = P.TrainConfig(iterations=iters, densify=False)
+    tr = Trainer(cloud.copy(), c0.width, c0.height, cfg, _extent(cams), canon_rows=canon)
+    for it in range(1, iters + 1):
+        tr.step(it, views[it - 1], gt[sched[it - 1]])
+    torch.cuda.synchronize()
+    ref_losses = tr.loss_dev[1:iters + 1].tolist()
+    ranks, smap, part = D.make_ranks(cloud.copy(), c0.width, c0.height, cfg, _extent(cams), 3,
+                                     torch.device("cuda", 0), canon_rows=canon)
+    losses = [float(D.emulated_step(ranks, views[it - 1], gt[sched[it - 1]], it, peers=peers)[0])
+              for it in range(1, iters + 1)]
+    got = D.gather_cloud(ranks)
+    assert losses == ref_losses, (losses, ref_losses)
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(got, k), getattr(tr.cloud, k)), k

@@ -359,3 +359,49 @@ def test_graph_captured_presync_equals_eager():
     for k in P.PARAM_NAMES:
         assert torch.equal(getattr(a.cloud, k), getattr(b.cloud, k)), k
     assert torch.equal(a.stats.seen, b.stats.seen)
+
+
+def test_step_on_a_view_with_nothing_visible():
+    """A view that sees no Gaussian (the camera turned 180 degrees about its y
+    axis) between two ordinary ones: zero visible splats, zero entries and zero
+    live slots through the graph-captured binning, the sort, the raster pair
+    and the fold.  The image is the background, no statistics move, and the
+    run is bitwise the same with eager pre-sync launches."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200 import engine as E
+    from paper_2509_05216_b200.engine import Trainer
+    d = load("config1")
+    ds = _dataset(d, "images_u8", d["images_u8"].shape[0])
+    cfg = P.TrainConfig(iterations=4, densify=False, seed=0)
+    gt = _images(ds)
+    sched = P.build_schedule(4, ds.view_count, 0)
+    c0 = ds.cameras[sched[1]]
+    flip = np.diag([-1.0, 1.0, -1.0])
+    away = P.Camera(flip @ np.asarray(c0.rotation), flip @ np.asarray(c0.translation),
+                    c0.fx, c0.fy, c0.cx, c0.cy, c0.width, c0.height)
+    views = [ds.cameras[sched[0]], away, ds.cameras[sched[2]], away]
+    saved = E.GRAPH
+    runs = []
+    try:
+        for graph in (True, False):
+            E.GRAPH = graph
+            t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
+            seen = []
+            for it in range(1, 5):
+                t.step(it, views[it - 1], gt[sched[it - 1]])
+                torch.cuda.synchronize()
+                seen.append(t.stats.seen.clone())
+                if it == 2:
+                    img = t.r.image.float().cpu().numpy()
+                    assert (img == 1.0).all()  # background (1, 1, 1)
+            runs.append((t, seen))
+    finally:
+        E.GRAPH = saved
+    (a, sa), (b, sb) = runs
+    assert torch.equal(sa[1], sa[0]) and torch.equal(sa[3], sa[2])
+    assert int(sa[0].sum()) > 0
+    losses = a.loss_dev[1:5].cpu().numpy()
+    assert np.isfinite(losses).all()
+    assert torch.equal(a.loss_dev, b.loss_dev)
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(a.cloud, k), getattr(b.cloud, k)), k
