@@ -405,3 +405,59 @@ def test_step_on_a_view_with_nothing_visible():
     assert torch.equal(a.loss_dev, b.loss_dev)
     for k in P.PARAM_NAMES:
         assert torch.equal(getattr(a.cloud, k), getattr(b.cloud, k)), k
+
+
+@pytest.mark.parametrize("wh", [(70, 45), (33, 97)])
+def test_ragged_image_step_matches_oracle(wh):
+    """Image sizes that are not multiples of the 16-pixel tile (partial tiles on
+    the right and bottom edges): two training iterations against the oracle's
+    iteration (src/engine.py:481-537) from the same pre-step state -- loss rel
+    <= 2e-5, 2-D and parameter gradients within the scale-parity bars, and the
+    post-step parameters bitwise the reference's Adam on the GPU's gradients."""
+    import paper_2509_05216_b200 as P
+    from oracle import oracle as O
+    from oracle import train as T
+    from paper_2509_05216_b200.engine import Trainer
+    O.build()
+    W, H = wh
+    d = load("config1")
+    ds = _dataset(d, "images_u8", d["images_u8"].shape[0])
+    cams = [P.Camera(c.rotation, c.translation, c.fx * W / c.width, c.fx * W / c.width,
+                     0.5 * W, 0.5 * H, W, H) for c in ds.cameras[:2]]
+    rng = np.random.default_rng(11)
+    gt = (rng.integers(0, 256, (2, H, W, 3)).astype(np.float64) / 255.0).astype(np.float32)
+    init = _init(d)
+    cfg = P.TrainConfig(iterations=2, densify=False, eval_interval=0)
+    tr = Trainer(P.to_device_cloud(init), W, H, cfg, ds.scene_extent)
+    tr.r.keep_grad2d = True
+    ocfg = T.Config(iterations=2, eval_interval=0, seed=0)
+    names = P.PARAM_NAMES
+    for it in (1, 2):
+        params = {k: getattr(tr.cloud, k).cpu().numpy().copy() for k in names}
+        state = {k: {"m": tr.m[k].cpu().numpy().copy(), "v": tr.v[k].cpu().numpy().copy()}
+                 for k in names}
+        pre = {k: params[k].copy() for k in names}
+        pre_state = {k: {"m": state[k]["m"].copy(), "v": state[k]["v"].copy()} for k in names}
+        tr.step(it, cams[it - 1], torch.from_numpy(gt[it - 1]).cuda())
+        torch.cuda.synchronize()
+        n = params["positions"].shape[0]
+        oloss, det = T.iteration(params, state, np.zeros(n, np.int64), np.zeros(n), 1, it,
+                                 cams[it - 1], gt[it - 1], ocfg, ds.scene_extent)
+        got = float(tr.loss_dev[it])
+        assert abs(got - oloss) / oloss <= 2e-5, (got, oloss)
+        vis = det["visible"]
+        assert vis.shape[0] > 1000
+        rank_of = tr.r.rank_of.cpu().numpy()
+        assert int((rank_of >= 0).sum()) == vis.shape[0] and np.all(rank_of[vis] >= 0)
+        g2d = tr.r.grad2d.cpu().numpy()[rank_of[vis]]
+        for k, cols in (("dmean", slice(0, 2)), ("dconic", slice(2, 5)),
+                        ("dcolor", slice(5, 8)), ("dopac", slice(8, 9))):
+            a = g2d[:, cols].ravel()
+            b = det["grad2d"][k][vis].reshape(vis.shape[0], -1).ravel()
+            assert np.linalg.norm(a - b) <= 1e-3 * max(np.linalg.norm(b), 1e-300), k
+        for k in names:
+            a, b = tr.grads[k].cpu().numpy().ravel(), det["param_grads"][k].ravel()
+            assert np.linalg.norm(a - b) <= 1e-3 * max(np.linalg.norm(b), 1e-300), k
+        O.adam_step(pre, {k: tr.grads[k].cpu().numpy() for k in names}, pre_state, it, det["lrs"])
+        for k in names:
+            np.testing.assert_array_equal(getattr(tr.cloud, k).cpu().numpy(), pre[k], err_msg=k)
