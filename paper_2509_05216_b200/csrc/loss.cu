@@ -34,6 +34,47 @@ template <typename T> __device__ __forceinline__ T wt(int i);
 template <> __device__ __forceinline__ float wt<float>(int i) { return c_w1f[i]; }
 template <> __device__ __forceinline__ double wt<double>(int i) { return c_w1d[i]; }
 
+// float32 instantiation: two consecutive outputs of a stencil row accumulate
+// as one packed pair (fma.rn.f32x2 -> FFMA2, each component the scalar FMA):
+// output pair (o, o + 1) takes input i with the weight pair (w[i - o],
+// w[i - o - 1]), zero past either end of the 11 taps.  Every accumulator is a
+// sum of products whose exact value is never a negative zero, so the extra
+// zero-weight FMA at a pair's edge (acc + 0 * v) leaves it bit for bit, and
+// each output still sums its taps in ascending order.
+#ifndef LOSS_PACK2
+#define LOSS_PACK2 1
+#endif
+typedef unsigned long long lf2_t;
+__device__ __forceinline__ lf2_t lpk(float a, float b) {
+    lf2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void lup(lf2_t r, float &a, float &b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ lf2_t lfma2(lf2_t a, lf2_t b, lf2_t c) {
+    lf2_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+// weight pair for tap t of the pair's first output (t in [0, 11]):
+// (w[t], w[t - 1]), 64-bit constants the FFMA2 reads from the constant bank
+#define W1F(i) ((float)c_w1d_host[i])
+constexpr double c_w1d_host[11] = {
+    0x1.0d956b52a1d70p-10, 0x1.f1fe01ae5a5b8p-8, 0x1.26eb175d83f67p-5,
+    0x1.bff0fe8e98418p-4,  0x1.b43c3f52b19f2p-3, 0x1.106560aa892c0p-2,
+    0x1.b43c3f52b19f2p-3,  0x1.bff0fe8e98418p-4, 0x1.26eb175d83f67p-5,
+    0x1.f1fe01ae5a5b8p-8,  0x1.0d956b52a1d70p-10};
+__constant__ float2 c_w2f[12] = {
+    {W1F(0), 0.0f},    {W1F(1), W1F(0)}, {W1F(2), W1F(1)}, {W1F(3), W1F(2)},
+    {W1F(4), W1F(3)},  {W1F(5), W1F(4)}, {W1F(6), W1F(5)}, {W1F(7), W1F(6)},
+    {W1F(8), W1F(7)},  {W1F(9), W1F(8)}, {W1F(10), W1F(9)}, {0.0f, W1F(10)}};
+#undef W1F
+__device__ __forceinline__ lf2_t wpair(int t) {
+    return *reinterpret_cast<const lf2_t *>(&c_w2f[t]);
+}
+
 // Ground-truth sample: float/double as stored, or an 8-bit code k read as
 // float(k / 255.0) -- the value the reference's PNG load + astype produces.
 template <typename T, typename R>
@@ -168,6 +209,41 @@ __global__ void __launch_bounds__(LTHREADS, LF_MINB) ssim_fields_kernel(
             }
         }
         __syncthreads();
+#if LOSS_PACK2
+        if (sizeof(T) == 4 && threadIdx.x < HTASKS) {
+            lf2_t a[5][HK / 2];
+#pragma unroll
+            for (int o = 0; o < HK / 2; o++)
+#pragma unroll
+                for (int f = 0; f < 5; f++) a[f][o] = lpk(0.0f, 0.0f);
+#pragma unroll
+            for (int i = 0; i < HK + 10; i++) {
+                const float x = (float)sx[hr][hu * HK + i], y = (float)sy[hr][hu * HK + i];
+                const float xx = x * x, yy = y * y, xy = x * y;
+#pragma unroll
+                for (int o = 0; o < HK / 2; o++) {
+                    const int t = i - 2 * o;
+                    if (t >= 0 && t <= 11) {
+                        const lf2_t w = wpair(t);
+                        a[0][o] = lfma2(w, lpk(x, x), a[0][o]);
+                        a[1][o] = lfma2(w, lpk(y, y), a[1][o]);
+                        a[2][o] = lfma2(w, lpk(xx, xx), a[2][o]);
+                        a[3][o] = lfma2(w, lpk(yy, yy), a[3][o]);
+                        a[4][o] = lfma2(w, lpk(xy, xy), a[4][o]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int f = 0; f < 5; f++)
+#pragma unroll
+                for (int o = 0; o < HK / 2; o++) {
+                    float u, v;
+                    lup(a[f][o], u, v);
+                    hs[f][hr][hu * HK + 2 * o] = (T)u;
+                    hs[f][hr][hu * HK + 2 * o + 1] = (T)v;
+                }
+        } else
+#endif
         if (threadIdx.x < HTASKS) {
             T a[5][HK];
 #pragma unroll
@@ -199,6 +275,40 @@ __global__ void __launch_bounds__(LTHREADS, LF_MINB) ssim_fields_kernel(
         __syncthreads();
         {
             T m[5][VK];
+#if LOSS_PACK2
+            if (sizeof(T) == 4) {
+                lf2_t m2[5][VK / 2];
+#pragma unroll
+                for (int k = 0; k < VK / 2; k++)
+#pragma unroll
+                    for (int f = 0; f < 5; f++) m2[f][k] = lpk(0.0f, 0.0f);
+#pragma unroll
+                for (int t = 0; t < VK + 10; t++) {
+                    float h[5];
+#pragma unroll
+                    for (int f = 0; f < 5; f++) h[f] = (float)hs[f][rr * VK + t][col];
+#pragma unroll
+                    for (int k = 0; k < VK / 2; k++) {
+                        const int i = t - 2 * k;
+                        if (i >= 0 && i <= 11) {
+                            const lf2_t w = wpair(i);
+#pragma unroll
+                            for (int f = 0; f < 5; f++) m2[f][k] = lfma2(w, lpk(h[f], h[f]), m2[f][k]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int f = 0; f < 5; f++)
+#pragma unroll
+                    for (int k = 0; k < VK / 2; k++) {
+                        float u, v;
+                        lup(m2[f][k], u, v);
+                        m[f][2 * k] = (T)u;
+                        m[f][2 * k + 1] = (T)v;
+                    }
+            } else
+#endif
+            {
 #pragma unroll
             for (int k = 0; k < VK; k++)
 #pragma unroll
@@ -217,6 +327,7 @@ __global__ void __launch_bounds__(LTHREADS, LF_MINB) ssim_fields_kernel(
                         for (int f = 0; f < 5; f++) m[f][k] += w * h[f];
                     }
                 }
+            }
             }
 #pragma unroll
             for (int k = 0; k < VK; k++) {
@@ -316,6 +427,32 @@ __global__ void __launch_bounds__(LTHREADS, LA_MINB) ssim_adjoint_kernel(
             }
         }
         __syncthreads();
+#if LOSS_PACK2
+        if (sizeof(T) == 4 && threadIdx.x < HTASKS) {
+#pragma unroll
+            for (int f = 0; f < 3; f++) {
+                lf2_t a[HK / 2];
+#pragma unroll
+                for (int o = 0; o < HK / 2; o++) a[o] = lpk(0.0f, 0.0f);
+#pragma unroll
+                for (int i = 0; i < HK + 10; i++) {
+                    const float v = (float)sf[f][hr][hu * HK + i];
+#pragma unroll
+                    for (int o = 0; o < HK / 2; o++) {
+                        const int t = i - 2 * o;
+                        if (t >= 0 && t <= 11) a[o] = lfma2(wpair(t), lpk(v, v), a[o]);
+                    }
+                }
+#pragma unroll
+                for (int o = 0; o < HK / 2; o++) {
+                    float u, w;
+                    lup(a[o], u, w);
+                    hs[f][hr][hu * HK + 2 * o] = (T)u;
+                    hs[f][hr][hu * HK + 2 * o + 1] = (T)w;
+                }
+            }
+        } else
+#endif
         if (threadIdx.x < HTASKS) {
 #pragma unroll
             for (int f = 0; f < 3; f++) {
@@ -338,6 +475,38 @@ __global__ void __launch_bounds__(LTHREADS, LA_MINB) ssim_adjoint_kernel(
         __syncthreads();
         {
             T g[3][VK];
+#if LOSS_PACK2
+            if (sizeof(T) == 4) {
+                lf2_t g2[3][VK / 2];
+#pragma unroll
+                for (int k = 0; k < VK / 2; k++) g2[0][k] = g2[1][k] = g2[2][k] = lpk(0.0f, 0.0f);
+#pragma unroll
+                for (int t = 0; t < VK + 10; t++) {
+                    const float h0 = (float)hs[0][rr * VK + t][col], h1 = (float)hs[1][rr * VK + t][col],
+                                h2 = (float)hs[2][rr * VK + t][col];
+#pragma unroll
+                    for (int k = 0; k < VK / 2; k++) {
+                        const int i = t - 2 * k;
+                        if (i >= 0 && i <= 11) {
+                            const lf2_t w = wpair(i);
+                            g2[0][k] = lfma2(w, lpk(h0, h0), g2[0][k]);
+                            g2[1][k] = lfma2(w, lpk(h1, h1), g2[1][k]);
+                            g2[2][k] = lfma2(w, lpk(h2, h2), g2[2][k]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int f = 0; f < 3; f++)
+#pragma unroll
+                    for (int k = 0; k < VK / 2; k++) {
+                        float u, v;
+                        lup(g2[f][k], u, v);
+                        g[f][2 * k] = (T)u;
+                        g[f][2 * k + 1] = (T)v;
+                    }
+            } else
+#endif
+            {
 #pragma unroll
             for (int k = 0; k < VK; k++) g[0][k] = g[1][k] = g[2][k] = 0;
 #pragma unroll
@@ -354,6 +523,7 @@ __global__ void __launch_bounds__(LTHREADS, LA_MINB) ssim_adjoint_kernel(
                         g[2][k] += w * h2;
                     }
                 }
+            }
             }
 #pragma unroll
             for (int k = 0; k < VK; k++) {
