@@ -374,7 +374,7 @@ def run_ours(args, world, rank, local):
     # sort (2 x 3), offsets, heavy-first order (1), raster fwd, loss (3),
     # raster bwd, fused live fold + chain, Adam (+ the chunk items launch when
     # the image is chunked, config 2)
-    launches_per_step = 36 + (1 if tr.r.chunks is not None else 0)
+    launches_per_step = 36 + (1 if tr.r.chunks is not None and tr.r.chunks.chunk else 0)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

@@ -54,7 +54,7 @@ class Chunks_t(ctypes.Structure):
     _fields_ = [("chunk", ctypes.c_int32), ("state", ctypes.c_void_p),
                 ("items", ctypes.c_void_p), ("n_items", ctypes.c_void_p),
                 ("max_items", ctypes.c_int32), ("image", ctypes.c_void_p),
-                ("tile_last", ctypes.c_void_p)]
+                ("tile_last", ctypes.c_void_p), ("unroll2", ctypes.c_int32)]
 
 
 class TrainState_t(ctypes.Structure):

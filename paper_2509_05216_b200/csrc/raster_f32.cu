@@ -578,8 +578,16 @@ __device__ __forceinline__ int ld_volatile(const int *p) {
 
 constexpr int BNT = 64;  // backward threads per tile (two 16x8 halves)
 
-template <typename DL, bool MASK, bool CHUNKED>
-__global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
+// UNR = 2: the entry loop takes two entries per step (the exponents and the
+// butterflies of both are independent, so a warp that runs alone on its SM --
+// the tail of a one-wave launch -- has twice the instruction-level
+// parallelism); every pixel still walks its entries in list order, so the
+// results are the bits of UNR = 1.
+#ifndef BWD_MINB2
+#define BWD_MINB2 10
+#endif
+template <typename DL, bool MASK, bool CHUNKED, int UNR = 1>
+__global__ void __launch_bounds__(BNT, UNR == 1 ? BWD_MINB : BWD_MINB2) bwd_kernel(
     int W, int H, int tiles_x, int row_lo, const int32_t *__restrict__ tile_ids,
     const int32_t *__restrict__ tile_order, const int32_t *__restrict__ offsets,
     const int32_t *__restrict__ entries, const float *__restrict__ feat,
@@ -709,7 +717,53 @@ __global__ void __launch_bounds__(BNT, BWD_MINB) bwd_kernel(
         if (alive) slist_all[warp][__popc(bal & lt)] = (unsigned char)lane;
         __syncwarp();
         const uint32_t a_red = smem_addr(&sred[rs][warp][0][0]) + 4u * (uint32_t)max(my_slot, 0);
-        for (int k = __popc(bal) - 1; k >= 0; k--) {
+        int k = __popc(bal) - 1;
+        if (UNR == 2) {
+            for (; k >= 1; k -= 2) {
+                // entries sa (later in the list, walked first) and sb
+                const int sl[2] = {ldsu8(a_list + k), ldsu8(a_list + k - 1)};
+                float4 g4[2], h4[2], col[2];
+                float d0[2], pw[2][4], ogv[2][4], dv[2][4];
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    const uint32_t ag = a_gh + 32 * sl[e];
+                    g4[e] = lds4(ag);
+                    h4[e] = lds4(ag + 16);
+                    col[e] = lds4(a_col + 16 * sl[e]);
+                    d0[e] = fpx - g4[e].x;
+                    float A, B;
+                    col_terms(d0[e], g4[e], A, B);
+                    pair_alpha_bl2(fpy[0], fpy[1], g4[e].y, A, B, h4[e], pw[e][0], pw[e][1],
+                                   ogv[e][0], ogv[e][1], dv[e][0], dv[e][1]);
+                    pair_alpha_bl2(fpy[2], fpy[3], g4[e].y, A, B, h4[e], pw[e][2], pw[e][3],
+                                   ogv[e][2], ogv[e][3], dv[e][2], dv[e][3]);
+                }
+                float v[2][9], sm[2][3];
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+#pragma unroll
+                    for (int q = 0; q < 9; q++) v[e][q] = 0.0f;
+                    sm[e][0] = sm[e][1] = sm[e][2] = 0.0f;
+                    const int jj = start + sl[e];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const float a = fminf(ogv[e][q], 0.99f);
+                        if (jj < last[q] && !(pw[e][q] > 0.0f) && a >= (1.0f / 255.0f)) {
+                            const float wc = fmaf(wb[q], col[e].z, fmaf(wg[q], col[e].y, wr[q] * col[e].x));
+                            pair_grad(a, ogv[e][q], dv[e][q], wc, wr[q], wg[q], wb[q], T[q], Q[q],
+                                      v[e], sm[e][0], sm[e][1], sm[e][2]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    moment_terms(d0[e], sm[e][0], sm[e][1], sm[e][2], v[e]);
+                    const float y = bfly9(v[e], lane);
+                    if (my_slot >= 0) sts(a_red + 36u * (uint32_t)sl[e], y);
+                }
+            }
+        }
+        for (; k >= 0; k--) {
             const int slot = ldsu8(a_list + k);
             const uint32_t ag = a_gh + 32 * slot;
             const float4 g4 = lds4(ag), h4 = lds4(ag + 16);
@@ -876,16 +930,17 @@ void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
     const int chunk = chunked ? ch->chunk : 0;
     const float4 *cstate = chunked ? (const float4 *)ch->state : nullptr;
     const float *image = chunked ? ch->image : nullptr;
-#define ISG_BWD32(MASK, CH)                                                                  \
-    f32::bwd_kernel<DL, MASK, CH><<<grid, f32::BNT, 0, s>>>(                                     \
+#define ISG_BWD32(MASK, CH, U)                                                               \
+    f32::bwd_kernel<DL, MASK, CH, U><<<grid, f32::BNT, 0, s>>>(                                  \
         W, H, tiles_x, row_lo, tile_ids, tile_order, offsets, entries, feat, rect_sorted,        \
         emit_off, bg0, bg1, bg2, t_final, n_last, dl, partials, MASK ? cmask : nullptr, items,    \
         n_items, chunk, cstate, image, slot_rank)
     if (cmask) {
-        if (chunked) ISG_BWD32(true, true);
-        else ISG_BWD32(true, false);
+        if (chunked) ISG_BWD32(true, true, 1);
+        else if (ch && ch->unroll2) ISG_BWD32(true, false, 2);
+        else ISG_BWD32(true, false, 1);
     } else {
-        ISG_BWD32(false, false);  // the unmasked launch is never chunked
+        ISG_BWD32(false, false, 1);  // the unmasked launch is never chunked
     }
 #undef ISG_BWD32
 }

@@ -460,6 +460,19 @@ def chunk_size(image_tiles: int, forced=None) -> int:
         return forced
     return AUTO_CHUNK if 0 < image_tiles <= AUTO_CHUNK_TILES else 0
 SPLIT_TILES = 1 << 30  # every chunk its own CTA when chunking is on
+# Unchunked backward launches of at most UNROLL2_TILES lists take two entries
+# per step (bwd_kernel<..., 2>: the same bits, more instruction-level
+# parallelism for the heaviest lists that finish alone on their SMs; a
+# per-launch choice, so any band split keeps its results).
+# Measured (emulated config-3 ranks): W = 8 bands of 2048 lists 470 -> 490
+# images/s; W = 4 bands of 4096 lists 311 -> 305; one GPU (16384 lists) 126 ->
+# 115.  Default: launches of at most 2560 lists.
+_u2 = os.environ.get("ISOGS_BWD_UNROLL2", "2560")
+UNROLL2_TILES = 0 if _u2 == "0" else (1 << 30 if _u2 == "1" else int(_u2))
+
+
+def unroll2(n_tiles: int) -> bool:
+    return 0 < n_tiles <= UNROLL2_TILES
 
 
 def chunk_setup(st, n_tiles: int, e: int, image_ptr: int):
@@ -468,8 +481,14 @@ def chunk_setup(st, n_tiles: int, e: int, image_ptr: int):
     work items are built between the forward and the backward by
     chunk_items().  `st` holds the buffers.  None when off."""
     chunk = chunk_size(st.image_tiles, getattr(st, "chunk", CHUNK))
-    if chunk <= 0 or n_tiles == 0:
+    if n_tiles == 0:
         return None
+    if chunk <= 0:
+        if not unroll2(n_tiles):
+            return None
+        c = L.Chunks_t()  # unchunked, two entries per backward step
+        c.unroll2 = 1
+        return c
     lib = L.lib()
     dev = st.offsets.device
     nst = int(lib.isg_chunk_state_floats(e, n_tiles, chunk))
@@ -488,7 +507,7 @@ def chunk_setup(st, n_tiles: int, e: int, image_ptr: int):
 def chunk_items(st, n_tiles: int) -> None:
     """The backward's work items from the forward's per-quadrant last
     positions (isg_chunk_items), in the heaviest-first tile order."""
-    if st.chunks is None:
+    if st.chunks is None or st.chunks.chunk == 0:
         return
     split = 1 if n_tiles <= SPLIT_TILES else 0
     L.check(L.lib().isg_chunk_items(n_tiles, L.ptr(st.offsets), L.ptr(st.tile_order),

@@ -165,7 +165,8 @@ def test_backward_chunking_matches_one_cta_per_tile():
         torch.cuda.synchronize()
         runs.append((t, g1, img1))
     (a, ga, ia), (b, gb, ib) = runs
-    assert a.r.chunks is not None and b.r.chunks is None
+    assert a.r.chunks is not None and a.r.chunks.chunk == 64
+    assert b.r.chunks is None or b.r.chunks.chunk == 0  # (unchunked; maybe two entries per step)
     assert torch.equal(ia, ib)
     rel = float((ga - gb).abs().max() / gb.abs().max())
     assert rel <= 1e-4, rel
@@ -461,3 +462,35 @@ def test_ragged_image_step_matches_oracle(wh):
         O.adam_step(pre, {k: tr.grads[k].cpu().numpy() for k in names}, pre_state, it, det["lrs"])
         for k in names:
             np.testing.assert_array_equal(getattr(tr.cloud, k).cpu().numpy(), pre[k], err_msg=k)
+
+
+def test_backward_two_entries_per_step_is_bitwise():
+    """bwd_kernel<..., 2> (two list entries per step, chosen per launch for
+    launches of about one wave) == one entry per step: losses, parameters and
+    Adam moments bitwise over 4 iterations."""
+    import paper_2509_05216_b200 as P
+    from paper_2509_05216_b200 import engine as E
+    from paper_2509_05216_b200.engine import Trainer
+    d = load("config1")
+    ds = _dataset(d, "images_u8", d["images_u8"].shape[0])
+    cfg = P.TrainConfig(iterations=4, densify=False, seed=0)
+    gt = _images(ds)
+    sched = P.build_schedule(4, ds.view_count, 0)
+    saved = E.UNROLL2_TILES, E.CHUNK
+    runs = []
+    try:
+        for u in (1 << 30, 0):
+            E.UNROLL2_TILES, E.CHUNK = u, 0  # unchunked launches (config 1 chunks by default)
+            t = Trainer(P.to_device_cloud(_init(d)), ds.width, ds.height, cfg, ds.scene_extent)
+            for it in range(1, 5):
+                t.step(it, ds.cameras[sched[it - 1]], gt[sched[it - 1]])
+            torch.cuda.synchronize()
+            assert (t.r.chunks is not None and t.r.chunks.unroll2 == 1) == bool(u)
+            runs.append(t)
+    finally:
+        E.UNROLL2_TILES, E.CHUNK = saved
+    a, b = runs
+    assert torch.equal(a.loss_dev, b.loss_dev)
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(a.cloud, k), getattr(b.cloud, k)), k
+        assert torch.equal(a.m[k], b.m[k]) and torch.equal(a.v[k], b.v[k]), k
