@@ -255,7 +255,7 @@ typedef struct isg_chunks {
     int32_t max_items;      /* grid of the backward launch */
     const float *image;     /* the forward's float32 image (same pixels as t_final) */
     int32_t *tile_last;     /* forward -> items: last composited position per (tile, quadrant), 4 x n_tiles */
-    int32_t unroll2;        /* unchunked backward: two entries per step (same results; for
+    int32_t unroll2;        /* unchunked backward: several entries per step (same results; for
                                launches of about one wave, whose tails run one warp per SM) */
 } isg_chunks;
 int64_t isg_chunk_state_floats(int64_t n_entries, int32_t n_tiles, int32_t chunk);

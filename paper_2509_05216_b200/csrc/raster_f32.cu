@@ -578,13 +578,17 @@ __device__ __forceinline__ int ld_volatile(const int *p) {
 
 constexpr int BNT = 64;  // backward threads per tile (two 16x8 halves)
 
-// UNR = 2: the entry loop takes two entries per step (the exponents and the
-// butterflies of both are independent, so a warp that runs alone on its SM --
-// the tail of a one-wave launch -- has twice the instruction-level
-// parallelism); every pixel still walks its entries in list order, so the
-// results are the bits of UNR = 1.
+// UNR > 1: the entry loop takes UNR entries per step (their exponents and
+// butterflies are independent, so a warp that runs alone on its SM -- the tail
+// of a one-wave launch -- has UNR times the instruction-level parallelism);
+// every pixel still walks its entries in list order, so the results are the
+// bits of UNR = 1.  Measured on emulated W = 8 bands (config 3): UNR 2 491,
+// 3 496, 4 474 images/s.
+#ifndef BWD_UNR
+#define BWD_UNR 3
+#endif
 #ifndef BWD_MINB2
-#define BWD_MINB2 10
+#define BWD_MINB2 1
 #endif
 template <typename DL, bool MASK, bool CHUNKED, int UNR = 1>
 __global__ void __launch_bounds__(BNT, UNR == 1 ? BWD_MINB : BWD_MINB2) bwd_kernel(
@@ -718,14 +722,16 @@ __global__ void __launch_bounds__(BNT, UNR == 1 ? BWD_MINB : BWD_MINB2) bwd_kern
         __syncwarp();
         const uint32_t a_red = smem_addr(&sred[rs][warp][0][0]) + 4u * (uint32_t)max(my_slot, 0);
         int k = __popc(bal) - 1;
-        if (UNR == 2) {
-            for (; k >= 1; k -= 2) {
+        if (UNR > 1) {
+            for (; k >= UNR - 1; k -= UNR) {
                 // entries sa (later in the list, walked first) and sb
-                const int sl[2] = {ldsu8(a_list + k), ldsu8(a_list + k - 1)};
-                float4 g4[2], h4[2], col[2];
-                float d0[2], pw[2][4], ogv[2][4], dv[2][4];
+                int sl[UNR];
 #pragma unroll
-                for (int e = 0; e < 2; e++) {
+                for (int e = 0; e < UNR; e++) sl[e] = ldsu8(a_list + k - e);
+                float4 g4[UNR], h4[UNR], col[UNR];
+                float d0[UNR], pw[UNR][4], ogv[UNR][4], dv[UNR][4];
+#pragma unroll
+                for (int e = 0; e < UNR; e++) {
                     const uint32_t ag = a_gh + 32 * sl[e];
                     g4[e] = lds4(ag);
                     h4[e] = lds4(ag + 16);
@@ -738,9 +744,9 @@ __global__ void __launch_bounds__(BNT, UNR == 1 ? BWD_MINB : BWD_MINB2) bwd_kern
                     pair_alpha_bl2(fpy[2], fpy[3], g4[e].y, A, B, h4[e], pw[e][2], pw[e][3],
                                    ogv[e][2], ogv[e][3], dv[e][2], dv[e][3]);
                 }
-                float v[2][9], sm[2][3];
+                float v[UNR][9], sm[UNR][3];
 #pragma unroll
-                for (int e = 0; e < 2; e++) {
+                for (int e = 0; e < UNR; e++) {
 #pragma unroll
                     for (int q = 0; q < 9; q++) v[e][q] = 0.0f;
                     sm[e][0] = sm[e][1] = sm[e][2] = 0.0f;
@@ -756,7 +762,7 @@ __global__ void __launch_bounds__(BNT, UNR == 1 ? BWD_MINB : BWD_MINB2) bwd_kern
                     }
                 }
 #pragma unroll
-                for (int e = 0; e < 2; e++) {
+                for (int e = 0; e < UNR; e++) {
                     moment_terms(d0[e], sm[e][0], sm[e][1], sm[e][2], v[e]);
                     const float y = bfly9(v[e], lane);
                     if (my_slot >= 0) sts(a_red + 36u * (uint32_t)sl[e], y);
@@ -937,7 +943,7 @@ void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
         n_items, chunk, cstate, image, slot_rank)
     if (cmask) {
         if (chunked) ISG_BWD32(true, true, 1);
-        else if (ch && ch->unroll2) ISG_BWD32(true, false, 2);
+        else if (ch && ch->unroll2) ISG_BWD32(true, false, BWD_UNR);
         else ISG_BWD32(true, false, 1);
     } else {
         ISG_BWD32(false, false, 1);  // the unmasked launch is never chunked

@@ -460,8 +460,8 @@ def chunk_size(image_tiles: int, forced=None) -> int:
         return forced
     return AUTO_CHUNK if 0 < image_tiles <= AUTO_CHUNK_TILES else 0
 SPLIT_TILES = 1 << 30  # every chunk its own CTA when chunking is on
-# Unchunked backward launches of at most UNROLL2_TILES lists take two entries
-# per step (bwd_kernel<..., 2>: the same bits, more instruction-level
+# Unchunked backward launches of at most UNROLL2_TILES lists take three entries
+# per step (bwd_kernel<..., 3>: the same bits, more instruction-level
 # parallelism for the heaviest lists that finish alone on their SMs; a
 # per-launch choice, so any band split keeps its results).
 # Measured (emulated config-3 ranks): W = 8 bands of 2048 lists 470 -> 490

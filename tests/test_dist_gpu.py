@@ -178,7 +178,7 @@ def test_sharded_ragged_image_bitwise_equals_single_gpu(wh, peers):
 
 @pytest.mark.parametrize("peers", [False, True], ids=["p2p_copies", "peer_stores"])
 def test_sharded_two_entry_backward_bitwise_equals_single_gpu(peers):
-    """Band launches small enough for the two-entries-per-step backward
+    """Band launches small enough for the several-entries-per-step backward
     (engine.UNROLL2_TILES) while the single-GPU launch walks one entry per
     step: the W=2 run is still bitwise the single-GPU run."""
     from paper_2509_05216_b200 import engine as E

@@ -465,7 +465,7 @@ def test_ragged_image_step_matches_oracle(wh):
 
 
 def test_backward_two_entries_per_step_is_bitwise():
-    """bwd_kernel<..., 2> (two list entries per step, chosen per launch for
+    """bwd_kernel<..., 3> (three list entries per step, chosen per launch for
     launches of about one wave) == one entry per step: losses, parameters and
     Adam moments bitwise over 4 iterations."""
     import paper_2509_05216_b200 as P
