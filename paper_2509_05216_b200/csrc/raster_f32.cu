@@ -942,7 +942,8 @@ void launch_raster_bwd_f32(int n_tiles, int W, int H, int tiles_x, int row_lo,
         emit_off, bg0, bg1, bg2, t_final, n_last, dl, partials, MASK ? cmask : nullptr, items,    \
         n_items, chunk, cstate, image, slot_rank)
     if (cmask) {
-        if (chunked) ISG_BWD32(true, true, 1);
+        if (chunked && ch->unroll2) ISG_BWD32(true, true, BWD_UNR);
+        else if (chunked) ISG_BWD32(true, true, 1);
         else if (ch && ch->unroll2) ISG_BWD32(true, false, BWD_UNR);
         else ISG_BWD32(true, false, 1);
     } else {

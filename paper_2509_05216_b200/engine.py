@@ -501,6 +501,7 @@ def chunk_setup(st, n_tiles: int, e: int, image_ptr: int):
     c = L.Chunks_t()
     c.chunk, c.state, c.items, c.n_items = chunk, L.ptr(st.ch_state), L.ptr(st.ch_items), L.ptr(st.ch_n)
     c.max_items, c.image, c.tile_last = mx, image_ptr, L.ptr(st.ch_last)
+    c.unroll2 = 1 if unroll2(n_tiles) else 0
     return c
 
 

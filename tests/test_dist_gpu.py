@@ -194,3 +194,22 @@ def test_sharded_two_entry_backward_bitwise_equals_single_gpu(peers):
     assert losses == ref_losses, (losses, ref_losses)
     for k in P.PARAM_NAMES:
         assert torch.equal(getattr(got, k), getattr(ref_cloud, k)), k
+
+
+@pytest.mark.parametrize("peers", [False, True], ids=["p2p_copies", "peer_stores"])
+def test_sharded_chunked_multi_entry_backward_bitwise_equals_single_gpu(peers):
+    """Chunked backward (config 1 chunks its lists) with the several-entries-
+    per-step instantiation in the W=2 bands only: still bitwise one GPU."""
+    from paper_2509_05216_b200 import engine as E
+    P, d, cams, gt, cloud = _setup()
+    iters, canon = 4, 1
+    saved = E.UNROLL2_TILES
+    try:
+        E.UNROLL2_TILES = 15  # 16 tiles on one GPU, fewer per band at W = 2
+        ref_losses, ref_cloud = _run_single(P, cams, gt, cloud, iters, canon)
+        losses, got, part = _run_emulated(P, cams, gt, cloud, iters, canon, 2, peers=peers)
+    finally:
+        E.UNROLL2_TILES = saved
+    assert losses == ref_losses, (losses, ref_losses)
+    for k in P.PARAM_NAMES:
+        assert torch.equal(getattr(got, k), getattr(ref_cloud, k)), k
